@@ -1,0 +1,175 @@
+/* ensemble_b200.h -- C ABI of the B200-native ensemble forward path.
+ *
+ * This library replaces the compute behind ensemblegate's forward boundary:
+ *
+ *   ensemblegate.ensemble.forward(ensemble, raw) -> EnsembleOutput
+ *       (pkg/src/ensemblegate/ensemble.py:232-250)
+ *     = validation (ensemble.py:238-247)
+ *     + preprocess once                (models.py:238-260)      -> K1
+ *     + every member in manifest order (models.py:263-279)      -> K2/K3/K4 (CNN), K6 (LIN1)
+ *   followed, in the gateway, by
+ *     votes_from_output + apply_policy (policy.py:53-92)        -> K5
+ *
+ * The reference has no FFI of its own (it is pure Python/NumPy);
+ * these entry points are what a ctypes binding of that boundary needs, and are
+ * bound by paper_2003_01538_b200/_lib.py.
+ *
+ * Conventions: every function returns an eb_status; on failure a thread-local
+ * message is available from eb_last_error().  No C++ exception crosses the ABI.
+ * Pointers named host_* are host memory (pageable or pinned); pointers named
+ * dev_* are device memory on the engine's GPU.
+ */
+#ifndef ENSEMBLE_B200_H
+#define ENSEMBLE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The Python wrapper maps them onto ensemblegate.errors:
+ *   EB_E_EMPTY      -> EmptyBatch        (ensemble.py:239-240)
+ *   EB_E_TOO_LARGE  -> BatchTooLarge     (ensemble.py:241-242)
+ *   EB_E_SHAPE      -> ShapeMismatch     (ensemble.py:243-247)
+ *   EB_E_POLICY     -> PolicyUnavailable (policy.py:88-91)
+ *   EB_E_BAD_K      -> BadK              (policy.py:74-75)
+ *   anything else   -> a generic internal error (gateway.py:85-88: never leaked) */
+typedef enum {
+  EB_OK = 0,
+  EB_E_INVALID = 1,
+  EB_E_CUDA = 2,
+  EB_E_SHAPE = 3,
+  EB_E_EMPTY = 4,
+  EB_E_TOO_LARGE = 5,
+  EB_E_POLICY = 6,
+  EB_E_BAD_K = 7,
+  EB_E_NOMEM = 8,
+  EB_E_STATE = 9
+} eb_status;
+
+/* Input encodings accepted by eb_forward. */
+enum {
+  EB_IN_F32_CHW = 0, /* SampleBatch.data: (B, C*H*W) float32, already /pixel_scale (wire.py:71) */
+  EB_IN_U8_HWC = 1   /* raw pixels, (B, H, W, C) uint8; /pixel_scale fused into K1 */
+};
+
+/* Tensor element types. */
+enum { EB_BF16 = 0, EB_F32 = 1, EB_F64 = 2 };
+
+/* Reserved tensor ids created by eb_engine_create. */
+enum {
+  EB_T_IMAGE_NHWC8 = 0, /* bf16 (H, W, 8): preprocessed image, channels >= C are zero */
+  EB_T_IMAGE_F32 = 1    /* f32 (C, H, W): preprocessed image in the reference layout */
+};
+
+/* Operation kinds. */
+enum {
+  EB_OP_CONV = 0,   /* implicit-GEMM conv / FC on tcgen05; bias, residual, ReLU fused */
+  EB_OP_POOL = 1,   /* max / avg pooling, optional per-channel BN-ReLU on the input */
+  EB_OP_BNRELU = 2, /* y = relu(x * scale + shift) per channel */
+  EB_OP_GAP = 3,    /* global average pool (optional BN-ReLU first) -> (1, 1, C) */
+  EB_OP_LIN1 = 4    /* fp64 linear scores of all LIN1 members: (C*H*W) -> (sum K) */
+};
+
+enum { EB_POOL_MAX = 0, EB_POOL_AVG = 1, EB_POOL_AVG_EXCL_PAD = 2 };
+
+enum { EB_POLICY_NONE = 0, EB_POLICY_ANY = 1, EB_POLICY_ALL = 2, EB_POLICY_AT_LEAST = 3 };
+
+enum { EB_MEMBER_CNN = 0, EB_MEMBER_LIN1 = 1 };
+
+#define EB_NO_OFFSET UINT64_MAX
+
+/* One node of a member's network.  Offsets are byte offsets into the engine's
+ * weight pool.  Activations are NHWC; an op reads channels
+ * [src_c_off, src_c_off + src_c) of `src` and writes channels
+ * [dst_c_off, dst_c_off + cout) of `dst` (this is how concatenation is done). */
+typedef struct {
+  int32_t kind;
+  int32_t src, dst, res; /* tensor ids; res = -1 for none */
+  int32_t src_c_off, src_c;
+  int32_t dst_c_off, cout;
+  int32_t kh, kw, sh, sw, ph, pw;
+  int32_t relu;
+  int32_t pool_mode;
+  int32_t flatten; /* CONV: treat src (H, W, C) as one row of H*W*C features */
+  int32_t stream;  /* concurrency lane (0..3); ops on different lanes may overlap */
+  uint64_t w_off, b_off, scale_off, shift_off;
+} eb_op_desc;
+
+typedef struct eb_engine eb_engine;
+
+const char* eb_last_error(void);
+int eb_abi_version(void);
+
+/* Engine lifecycle.  The image geometry is the ensemble's shared input shape
+ * (ensemble.py:202-208). */
+int eb_engine_create(int device, int max_batch, int in_c, int in_h, int in_w, eb_engine** out);
+int eb_engine_destroy(eb_engine* e);
+
+/* Normalisation: mean/std have 1 or C entries (models.py:247-253).  lut_u8 is
+ * C*256 floats: the reference's fp32 value of ((v / pixel_scale) - mean) / std
+ * for every byte v, computed on the host by the caller (exact by construction). */
+int eb_set_preprocess(eb_engine* e, const float* host_mean, const float* host_std, int n,
+                      const float* host_lut_u8);
+
+/* One device allocation holds every member's weights (the shared pool of
+ * ensemble.py:215-220, here in real device bytes). */
+int eb_pool_reserve(eb_engine* e, uint64_t bytes);
+int eb_pool_write(eb_engine* e, uint64_t offset, const void* host_src, uint64_t bytes);
+int eb_pool_bytes(eb_engine* e, uint64_t* bytes);
+
+/* Activation tensor of per-sample shape (h, w, c); storage is max_batch deep. */
+int eb_tensor(eb_engine* e, int h, int w, int c, int dtype, int* id_out);
+int eb_add_op(eb_engine* e, const eb_op_desc* op);
+/* Register an output member: its logits are columns [k_off, k_off + k) of
+ * `logits_tensor` (fp32 for CNN members, fp64 for LIN1). Manifest order. */
+int eb_add_member(eb_engine* e, int kind, int logits_tensor, int k_off, int k);
+int eb_finalize(eb_engine* e);
+
+/* The forward boundary.  host_labels: int32 [N][batch] (EnsembleOutput.per_model
+ * layout).  Optional outputs (NULL to skip): host_logits fp32 [N][batch][Kmax]
+ * (zero padded), top-k indices/probabilities [N][batch][topk], combined policy
+ * output [batch].  Host<->device copies are inside this call. */
+int eb_forward(eb_engine* e, const void* host_input, int input_kind, int batch,
+               int32_t* host_labels, float* host_logits, int topk, int32_t* host_topk_idx,
+               float* host_topk_prob, int policy, int policy_k, int32_t* host_combined);
+
+/* Device-resident variant used for kernel-only timing: the input is already in
+ * the engine's device staging buffer (see eb_input_buffer) and outputs stay on
+ * the device (see eb_output_labels). */
+int eb_forward_device(eb_engine* e, int input_kind, int batch, int topk, int policy, int policy_k);
+int eb_input_buffer(eb_engine* e, int input_kind, void** dev_ptr);
+int eb_output_labels(eb_engine* e, int32_t** dev_labels);
+int eb_tensor_ptr(eb_engine* e, int id, void** dev_ptr, int* h, int* w, int* c, int* dtype);
+int eb_engine_stream(eb_engine* e, void** stream);
+/* Number of kernels one eb_forward_device launches for this batch size. */
+int eb_launch_count(eb_engine* e, int input_kind, int batch, int* count);
+
+/* Kernel-level entry points on caller-owned device memory (used by the parity
+ * tests; `stream` is a cudaStream_t, NULL = legacy default stream). */
+int eb_k_preprocess_f32(const float* dev_x, float* dev_y, int batch, int c, int64_t plane,
+                        const float* dev_mean, const float* dev_std, int n, void* stream);
+int eb_k_preprocess_u8_nhwc8(const uint8_t* dev_x, void* dev_y_bf16, int batch, int c,
+                             int64_t plane, const float* dev_lut, void* stream);
+int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, const void* dev_w,
+              const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
+              int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
+              int out_f32, int c8_stem, int split_k, int block_n, void* dev_workspace,
+              void* stream);
+int eb_k_pool(const void* dev_x, int ldx, void* dev_y, int ldy, int y_off, int batch, int h,
+              int w, int c, int k, int s, int pad, int mode, const float* dev_scale,
+              const float* dev_shift, void* stream);
+int eb_k_gap(const void* dev_x, int ldx, void* dev_y, int batch, int hw, int c,
+             const float* dev_scale, const float* dev_shift, void* stream);
+int eb_k_lin1(const float* dev_x, const float* dev_w, const float* dev_bias, double* dev_part,
+              double* dev_logits, int batch, int k, int64_t d, int nsplit, void* stream);
+int eb_k_combine(const float* dev_l32, int ld32, const double* dev_l64, int ld64,
+                 const int* dev_kind, const int* dev_koff, const int* dev_kcnt, int n, int batch,
+                 int32_t* dev_labels, int topk, int32_t* dev_topk_idx, float* dev_topk_prob,
+                 int policy, int policy_k, int32_t* dev_combined, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENSEMBLE_B200_H */

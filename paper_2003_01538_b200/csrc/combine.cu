@@ -1,0 +1,222 @@
+// combine.cu -- K5 (per-member argmax / softmax / top-k + ensemble policy) and
+// K6 (LIN1 members: fp64 linear scores).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "eb_kernels.h"
+
+namespace eb {
+
+// ------------------------------------------------------------------ K5 combine
+//
+// One CTA per sample, one warp per member (looping when N > warps).  Per member:
+//   label  = argmax over the member's K logits, lowest index on ties
+//            (np.argmax semantics, eg/models.py:279)
+//   top-k  = indices ordered by (logit desc, index asc), with softmax
+//            probabilities computed in fp32 from the logits
+// Then thread 0 applies the sensitivity policy over the N binary votes
+// (eg/policy.py:66-76): any = max, all = min, at_least = count >= k.
+
+template <typename T>
+__device__ __forceinline__ bool better(T v, int i, T bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+template <typename T>
+__device__ void warp_argmax_excluding(const T* row, int K, bool have_prev, T pv, int pi, T* out_v,
+                                      int* out_i) {
+  T bv = 0;
+  int bi = -1;
+  for (int i = threadIdx.x & 31; i < K; i += 32) {
+    const T v = row[i];
+    // candidates strictly after (pv, pi) in (value desc, index asc) order
+    if (have_prev && !(v < pv || (v == pv && i > pi))) continue;
+    if (bi < 0 || better(v, i, bv, bi)) {
+      bv = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const T ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    if (oi >= 0 && (bi < 0 || better(ov, oi, bv, bi))) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  *out_v = bv;
+  *out_i = bi;
+}
+
+template <typename T>
+__device__ void member_outputs(const T* row, int K, int lane, int mem, int B, int b,
+                               int32_t* labels, int* s_lab, int topk, int32_t* topk_idx,
+                               float* topk_prob) {
+  T bv;
+  int bi;
+  warp_argmax_excluding(row, K, false, T(0), 0, &bv, &bi);
+  if (lane == 0) {
+    labels[static_cast<int64_t>(mem) * B + b] = bi;
+    s_lab[mem] = bi;
+  }
+  if (topk > 0) {
+    // softmax denominator in fp32, max-subtracted
+    const float mx = static_cast<float>(bv);
+    float sum = 0.f;
+    for (int i = lane; i < K; i += 32) sum += __expf(static_cast<float>(row[i]) - mx);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    const float inv = 1.f / sum;
+    T pv = bv;
+    int pi = bi;
+    const int64_t base = (static_cast<int64_t>(mem) * B + b) * topk;
+    for (int j = 0; j < topk; ++j) {
+      T v = pv;
+      int idx = pi;
+      if (j > 0) warp_argmax_excluding(row, K, true, pv, pi, &v, &idx);
+      if (lane == 0) {
+        topk_idx[base + j] = idx;
+        topk_prob[base + j] = (idx >= 0) ? __expf(static_cast<float>(v) - mx) * inv : 0.f;
+      }
+      pv = v;
+      pi = idx;
+    }
+  }
+}
+
+// Member m reads logits from the fp32 buffer (CNN members) when kind[m] == 0,
+// else from the fp64 buffer (LIN1 members); koff[m] is its column offset.
+__global__ void combine_kernel(const float* __restrict__ l32, int ld32,
+                               const double* __restrict__ l64, int ld64,
+                               const int* __restrict__ kind, const int* __restrict__ koff,
+                               const int* __restrict__ kcnt, int N, int B, int32_t* labels,
+                               int topk, int32_t* topk_idx, float* topk_prob, int policy,
+                               int policy_k, int32_t* combined) {
+  extern __shared__ int s_lab[];
+  const int b = blockIdx.x;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int mem = warp; mem < N; mem += nwarps) {
+    if (kind[mem] == 0)
+      member_outputs(l32 + static_cast<int64_t>(b) * ld32 + koff[mem], kcnt[mem], lane, mem, B, b,
+                     labels, s_lab, topk, topk_idx, topk_prob);
+    else
+      member_outputs(l64 + static_cast<int64_t>(b) * ld64 + koff[mem], kcnt[mem], lane, mem, B, b,
+                     labels, s_lab, topk, topk_idx, topk_prob);
+  }
+  if (policy > 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int lo = 1, hi = 0, sum = 0;
+      for (int mem = 0; mem < N; ++mem) {
+        const int v = s_lab[mem];
+        lo = min(lo, v);
+        hi = max(hi, v);
+        sum += v;
+      }
+      int out = 0;
+      if (policy == 1) out = hi;             // any
+      else if (policy == 2) out = lo;        // all
+      else out = (sum >= policy_k) ? 1 : 0;  // at_least
+      combined[b] = out;
+    }
+  }
+}
+
+cudaError_t k_combine(const float* l32, int ld32, const double* l64, int ld64, const int* kind,
+                      const int* koff, const int* kcnt, int N, int B, int32_t* labels, int topk,
+                      int32_t* topk_idx, float* topk_prob, int policy, int policy_k,
+                      int32_t* combined, cudaStream_t s) {
+  if (B == 0 || N == 0) return cudaSuccess;
+  const int warps = N < 8 ? N : 8;
+  combine_kernel<<<B, 32 * warps, sizeof(int) * N, s>>>(l32, ld32, l64, ld64, kind, koff, kcnt, N,
+                                                        B, labels, topk, topk_idx, topk_prob,
+                                                        policy, policy_k, combined);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K6 LIN1 scores
+//
+// logits[b, k] = sum_d f64(x[b, d]) * f64(W[k, d])  (+ bias[k] afterwards),
+// eg/models.py:275-278.  Products of two fp32 values are exact in fp64, so the
+// only rounding is in the summation.  The d range is cut into `nsplit` fixed
+// slices that depend on D only; each slice is summed in ascending d by one
+// thread, and slices are added in ascending order by the reduce kernel.  A
+// sample's logits are therefore bitwise independent of the batch it arrives in
+// (the reference's batch == concatenated singles property, eg/models.py:273-274).
+
+constexpr int kLinTile = 32;
+constexpr int kLinChunk = 32;
+
+__global__ void lin1_partial_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                    double* __restrict__ part, int B, int K, int64_t D,
+                                    int64_t dslice) {
+  __shared__ float sx[kLinTile][kLinChunk + 1];
+  __shared__ float sw[kLinTile][kLinChunk + 1];
+  const int tx = threadIdx.x & 15;  // k direction
+  const int ty = threadIdx.x >> 4;  // b direction
+  const int b0 = blockIdx.x * kLinTile;
+  const int k0 = blockIdx.y * kLinTile;
+  const int64_t d0 = blockIdx.z * dslice;
+  int64_t d1 = d0 + dslice;
+  if (d1 > D) d1 = D;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int64_t dc = d0; dc < d1; dc += kLinChunk) {
+    for (int i = threadIdx.x; i < kLinTile * kLinChunk; i += blockDim.x) {
+      const int r = i / kLinChunk;
+      const int c = i % kLinChunk;
+      const int64_t d = dc + c;
+      const bool dok = d < d1;
+      sx[r][c] = (dok && b0 + r < B) ? x[static_cast<int64_t>(b0 + r) * D + d] : 0.f;
+      sw[r][c] = (dok && k0 + r < K) ? w[static_cast<int64_t>(k0 + r) * D + d] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int c = 0; c < kLinChunk; ++c) {
+      const double xa = sx[ty][c], xb = sx[ty + 16][c];
+      const double wa = sw[tx][c], wb = sw[tx + 16][c];
+      acc[0][0] = fma(xa, wa, acc[0][0]);
+      acc[0][1] = fma(xa, wb, acc[0][1]);
+      acc[1][0] = fma(xb, wa, acc[1][0]);
+      acc[1][1] = fma(xb, wb, acc[1][1]);
+    }
+    __syncthreads();
+  }
+  for (int i = 0; i < 2; ++i)
+    for (int j = 0; j < 2; ++j) {
+      const int b = b0 + ty + 16 * i;
+      const int k = k0 + tx + 16 * j;
+      if (b < B && k < K) part[(static_cast<int64_t>(blockIdx.z) * B + b) * K + k] = acc[i][j];
+    }
+}
+
+__global__ void lin1_reduce_kernel(const double* __restrict__ part, const float* __restrict__ bias,
+                                   double* __restrict__ logits, int B, int K, int nsplit) {
+  const int64_t total = static_cast<int64_t>(B) * K;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < nsplit; ++z) s += part[z * total + i];
+    logits[i] = s + static_cast<double>(bias[i % K]);
+  }
+}
+
+cudaError_t k_lin1(const float* x, const float* w, const float* bias, double* part,
+                   double* logits, int B, int K, int64_t D, int nsplit, cudaStream_t s) {
+  if (B == 0 || K == 0) return cudaSuccess;
+  const int64_t dslice = (D + nsplit - 1) / nsplit;
+  dim3 grid((B + kLinTile - 1) / kLinTile, (K + kLinTile - 1) / kLinTile, nsplit);
+  lin1_partial_kernel<<<grid, 256, 0, s>>>(x, w, part, B, K, D, dslice);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t total = static_cast<int64_t>(B) * K;
+  int g = static_cast<int>((total + 255) / 256);
+  if (g > 148 * 16) g = 148 * 16;
+  lin1_reduce_kernel<<<g, 256, 0, s>>>(part, bias, logits, B, K, nsplit);
+  return cudaGetLastError();
+}
+
+}  // namespace eb

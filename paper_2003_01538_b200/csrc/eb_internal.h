@@ -1,0 +1,52 @@
+// eb_internal.h -- types shared by the kernels and the native runtime.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+namespace eb {
+
+enum AMode : int {
+  kAModeTiled = 0,     // A is a plain [M, K] matrix (1x1 stride-1 conv, FC)
+  kAModeIm2col = 1,    // TMA im2col, 64-channel chunks, 128B swizzle
+  kAModeIm2colC8 = 2,  // TMA im2col, 8-channel taps (stem), no swizzle
+};
+
+enum OutMode : int {
+  kOutBF16 = 0,       // bf16 NHWC slice, bias/residual/ReLU fused
+  kOutF32 = 1,        // fp32 (logits), bias/ReLU fused
+  kOutAtomicF32 = 2,  // fp32 split-K partials, accumulated with atomics
+};
+
+struct ConvParams {
+  int M, N;
+  int num_kb, kb_per_split;
+  int a_mode;
+  int Ho, Wo, sh, sw, ph, pw, kw, taps, cchunks;
+  void* out;
+  int ldo, out_off;
+  const __nv_bfloat16* res;
+  int ldr;
+  const float* bias;
+  int relu;
+  int out_mode;
+};
+
+cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const ConvParams& p,
+                             int block_n, dim3 grid, cudaStream_t stream);
+
+// Driver entry point for tensor-map encoding (resolved through the runtime so the
+// library does not link libcuda directly).
+bool encode_tiled_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                          uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer,
+                          std::string* err);
+bool encode_im2col_bf16(CUtensorMap* map, const void* base, int n, int h, int w, int c, int ldc,
+                        int kh, int kw, int sh, int sw, int ph, int pw, int chans_per_pixel,
+                        int pixels, bool swizzle128, std::string* err);
+
+void set_error(const std::string& msg);
+
+}  // namespace eb

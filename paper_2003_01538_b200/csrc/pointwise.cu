@@ -1,0 +1,302 @@
+// pointwise.cu -- K1 (shared preprocess) and K4 (pooling / BN-ReLU) kernels.
+//
+// All activation tensors are NHWC bf16 with a row (pixel) stride `ld` that may
+// exceed the channel count (channel slices of a concat buffer).  Channel work is
+// vectorised by 8 (16-byte loads/stores); every channel count used by the
+// supported model families is a multiple of 8.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "eb_kernels.h"
+
+namespace eb {
+
+static inline int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+// ------------------------------------------------------------------ K1 preprocess
+
+// Reference semantics (eg/models.py:254-259): y = (x - mean_c) / std_c in fp32,
+// each op correctly rounded, same (B, C, H*W) layout.  No FMA can form here
+// (there is no multiply), and '/' compiles to the IEEE divide without fast-math.
+__global__ void preprocess_f32_kernel(const float* __restrict__ x, float* __restrict__ y,
+                                      int64_t total, int C, int64_t plane,
+                                      const float* __restrict__ mean,
+                                      const float* __restrict__ stdv, int nms) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = (nms == 1) ? 0 : static_cast<int>((i / plane) % C);
+    y[i] = __fdiv_rn(__fsub_rn(x[i], mean[c]), stdv[c]);
+  }
+}
+
+// f32 CHW (already divided by pixel_scale on the wire, eg/wire.py:71) ->
+// normalised fp32 -> bf16 NHWC with channels zero-padded to `cpad` (8).
+__global__ void preprocess_f32chw_to_nhwc_kernel(const float* __restrict__ x,
+                                                 __nv_bfloat16* __restrict__ y, int64_t pixels,
+                                                 int C, int64_t plane, int cpad,
+                                                 const float* __restrict__ mean,
+                                                 const float* __restrict__ stdv, int nms) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < pixels;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = p / plane;
+    const int64_t q = p - b * plane;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float f = 0.f;
+      if (c < C) {
+        const int mc = (nms == 1) ? 0 : c;
+        f = __fdiv_rn(__fsub_rn(x[(b * C + c) * plane + q], mean[mc]), stdv[mc]);
+      }
+      v[c] = __float2bfloat16_rn(f);
+    }
+    *reinterpret_cast<uint4*>(y + p * cpad) = *reinterpret_cast<uint4*>(v);
+  }
+}
+
+// u8 HWC -> bf16 NHWC8 through a per-channel 256-entry LUT.  The LUT holds the
+// reference's fp32 value ((u8 / pixel_scale) - mean_c) / std_c for every byte,
+// computed on the host with numpy's own fp32 ops, so the kernel is exact by
+// construction (no divides on the device).
+__global__ void preprocess_u8hwc_to_nhwc_kernel(const uint8_t* __restrict__ x,
+                                                __nv_bfloat16* __restrict__ y, int64_t pixels,
+                                                int C, int cpad, const float* __restrict__ lut) {
+  __shared__ float s_lut[8 * 256];
+  for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
+  __syncthreads();
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < pixels;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float f = (c < C) ? s_lut[c * 256 + x[p * C + c]] : 0.f;
+      v[c] = __float2bfloat16_rn(f);
+    }
+    *reinterpret_cast<uint4*>(y + p * cpad) = *reinterpret_cast<uint4*>(v);
+  }
+}
+
+// u8 HWC -> fp32 CHW normalised (LIN1 members fed from u8 requests).
+__global__ void preprocess_u8hwc_to_f32chw_kernel(const uint8_t* __restrict__ x,
+                                                  float* __restrict__ y, int64_t pixels, int C,
+                                                  int64_t plane, const float* __restrict__ lut) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < pixels;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = p / plane;
+    const int64_t q = p - b * plane;
+    for (int c = 0; c < C; ++c) y[(b * C + c) * plane + q] = lut[c * 256 + x[p * C + c]];
+  }
+}
+
+cudaError_t k_preprocess_f32(const float* x, float* y, int B, int C, int64_t plane,
+                             const float* mean, const float* stdv, int nms, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(B) * C * plane;
+  if (total == 0) return cudaSuccess;
+  preprocess_f32_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, y, total, C, plane, mean, stdv,
+                                                             nms);
+  return cudaGetLastError();
+}
+
+cudaError_t k_preprocess_f32chw_to_nhwc(const float* x, __nv_bfloat16* y, int B, int C,
+                                        int64_t plane, int cpad, const float* mean,
+                                        const float* stdv, int nms, cudaStream_t s) {
+  const int64_t pixels = static_cast<int64_t>(B) * plane;
+  if (pixels == 0) return cudaSuccess;
+  preprocess_f32chw_to_nhwc_kernel<<<grid_for(pixels, 256), 256, 0, s>>>(x, y, pixels, C, plane,
+                                                                         cpad, mean, stdv, nms);
+  return cudaGetLastError();
+}
+
+cudaError_t k_preprocess_u8hwc_to_nhwc(const uint8_t* x, __nv_bfloat16* y, int B, int C,
+                                       int64_t plane, int cpad, const float* lut,
+                                       cudaStream_t s) {
+  const int64_t pixels = static_cast<int64_t>(B) * plane;
+  if (pixels == 0) return cudaSuccess;
+  preprocess_u8hwc_to_nhwc_kernel<<<grid_for(pixels, 256), 256, 0, s>>>(x, y, pixels, C, cpad,
+                                                                        lut);
+  return cudaGetLastError();
+}
+
+cudaError_t k_preprocess_u8hwc_to_f32chw(const uint8_t* x, float* y, int B, int C,
+                                         int64_t plane, const float* lut, cudaStream_t s) {
+  const int64_t pixels = static_cast<int64_t>(B) * plane;
+  if (pixels == 0) return cudaSuccess;
+  preprocess_u8hwc_to_f32chw_kernel<<<grid_for(pixels, 256), 256, 0, s>>>(x, y, pixels, C,
+                                                                          plane, lut);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K4 pooling / BN-ReLU
+
+struct Vec8 {
+  float v[8];
+};
+
+__device__ __forceinline__ Vec8 load8(const __nv_bfloat16* p) {
+  uint4 q = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+  Vec8 r;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r.v[j] = __bfloat162float(h[j]);
+  return r;
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const Vec8& r) {
+  __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) h[j] = __float2bfloat16_rn(r.v[j]);
+  *reinterpret_cast<uint4*>(p) = *reinterpret_cast<uint4*>(h);
+}
+__device__ __forceinline__ void bnrelu8(Vec8& r, const float* scale, const float* shift, int c) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r.v[j] = fmaxf(fmaf(r.v[j], __ldg(scale + c + j), __ldg(shift + c + j)), 0.f);
+}
+
+// mode 0 = max (padding ignored), 1 = avg count_include_pad, 2 = avg exclude pad.
+// Optional per-channel BN-ReLU applied to every input element before pooling.
+__global__ void pool_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
+                            __nv_bfloat16* __restrict__ y, int ldy, int y_off, int B, int H,
+                            int W, int C, int Ho, int Wo, int k, int s, int pad, int mode,
+                            const float* __restrict__ scale, const float* __restrict__ shift) {
+  const int cg = C / 8;
+  const int64_t total = static_cast<int64_t>(B) * Ho * Wo * cg;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % cg) * 8;
+    int64_t t = i / cg;
+    const int ow = static_cast<int>(t % Wo);
+    t /= Wo;
+    const int oh = static_cast<int>(t % Ho);
+    const int b = static_cast<int>(t / Ho);
+    Vec8 acc;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc.v[j] = (mode == 0) ? -INFINITY : 0.f;
+    int cnt = 0;
+    for (int dh = 0; dh < k; ++dh) {
+      const int ih = oh * s - pad + dh;
+      if (ih < 0 || ih >= H) continue;
+      for (int dw = 0; dw < k; ++dw) {
+        const int iw = ow * s - pad + dw;
+        if (iw < 0 || iw >= W) continue;
+        Vec8 v = load8(x + (static_cast<int64_t>(b) * H * W + static_cast<int64_t>(ih) * W + iw) * ldx + c);
+        if (scale) bnrelu8(v, scale, shift, c);
+        ++cnt;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc.v[j] = (mode == 0) ? fmaxf(acc.v[j], v.v[j]) : acc.v[j] + v.v[j];
+      }
+    }
+    if (mode == 1) {
+      const float inv = 1.f / static_cast<float>(k * k);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc.v[j] *= inv;
+    } else if (mode == 2) {
+      const float inv = 1.f / static_cast<float>(cnt > 0 ? cnt : 1);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc.v[j] *= inv;
+    }
+    store8(y + (static_cast<int64_t>(b) * Ho * Wo + static_cast<int64_t>(oh) * Wo + ow) * ldy + y_off + c, acc);
+  }
+}
+
+cudaError_t k_pool(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, int y_off, int B,
+                   int H, int W, int C, int Ho, int Wo, int k, int s, int pad, int mode,
+                   const float* scale, const float* shift, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(B) * Ho * Wo * (C / 8);
+  if (total == 0) return cudaSuccess;
+  pool_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, ldx, y, ldy, y_off, B, H, W, C, Ho, Wo, k,
+                                                    s, pad, mode, scale, shift);
+  return cudaGetLastError();
+}
+
+// y[m, c] = relu(x[m, c] * scale[c] + shift[c]) for c < C (DenseNet pre-activation).
+__global__ void bnrelu_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
+                              __nv_bfloat16* __restrict__ y, int ldy, int64_t M, int C,
+                              const float* __restrict__ scale, const float* __restrict__ shift) {
+  const int cg = C / 8;
+  const int64_t total = M * cg;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % cg) * 8;
+    const int64_t m = i / cg;
+    Vec8 v = load8(x + m * ldx + c);
+    bnrelu8(v, scale, shift, c);
+    store8(y + m * ldy + c, v);
+  }
+}
+
+cudaError_t k_bnrelu(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, int64_t M, int C,
+                     const float* scale, const float* shift, cudaStream_t st) {
+  const int64_t total = M * (C / 8);
+  if (total == 0) return cudaSuccess;
+  bnrelu_kernel<<<grid_for(total, 256), 256, 0, st>>>(x, ldx, y, ldy, M, C, scale, shift);
+  return cudaGetLastError();
+}
+
+// Global average pool over H*W (optionally BN-ReLU first) -> bf16 [B, C].
+__global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
+                           __nv_bfloat16* __restrict__ y, int B, int HW, int C,
+                           const float* __restrict__ scale, const float* __restrict__ shift) {
+  const int cg = C / 8;
+  const int64_t total = static_cast<int64_t>(B) * cg;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % cg) * 8;
+    const int64_t b = i / cg;
+    Vec8 acc;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc.v[j] = 0.f;
+    for (int p = 0; p < HW; ++p) {
+      Vec8 v = load8(x + (b * HW + p) * ldx + c);
+      if (scale) bnrelu8(v, scale, shift, c);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc.v[j] += v.v[j];
+    }
+    const float inv = 1.f / static_cast<float>(HW);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc.v[j] *= inv;
+    store8(y + b * C + c, acc);
+  }
+}
+
+cudaError_t k_gap(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int B, int HW, int C,
+                  const float* scale, const float* shift, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(B) * (C / 8);
+  if (total == 0) return cudaSuccess;
+  gap_kernel<<<grid_for(total, 128), 128, 0, st>>>(x, ldx, y, B, HW, C, scale, shift);
+  return cudaGetLastError();
+}
+
+// Split-K finalisation: y = act(ws + bias) -> bf16 slice or fp32.
+__global__ void splitk_finalize_kernel(const float* __restrict__ ws, int64_t M, int N,
+                                       const float* __restrict__ bias, int relu, void* out,
+                                       int ldo, int out_off, int out_f32) {
+  const int64_t total = M * N;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(i % N);
+    const int64_t m = i / N;
+    float v = ws[i] + (bias ? bias[n] : 0.f);
+    if (relu) v = fmaxf(v, 0.f);
+    if (out_f32)
+      reinterpret_cast<float*>(out)[m * ldo + out_off + n] = v;
+    else
+      reinterpret_cast<__nv_bfloat16*>(out)[m * ldo + out_off + n] = __float2bfloat16_rn(v);
+  }
+}
+
+cudaError_t k_splitk_finalize(const float* ws, int64_t M, int N, const float* bias, int relu,
+                              void* out, int ldo, int out_off, int out_f32, cudaStream_t st) {
+  const int64_t total = M * N;
+  if (total == 0) return cudaSuccess;
+  splitk_finalize_kernel<<<grid_for(total, 256), 256, 0, st>>>(ws, M, N, bias, relu, out, ldo,
+                                                               out_off, out_f32);
+  return cudaGetLastError();
+}
+
+}  // namespace eb

@@ -1,0 +1,902 @@
+// runtime.cu -- the native engine behind include/ensemble_b200.h.
+//
+// An engine owns, for one GPU: the weight pool (one allocation for every
+// member), the activation arena (one buffer per plan tensor, max_batch deep),
+// the op list of every member, and a cache of instantiated CUDA graphs keyed by
+// (batch size, input encoding).  eb_forward = H2D input copy -> graph replay
+// (K1 preprocess, every member's layers on its own concurrency lane) -> K5
+// combine -> D2H copy of labels / top-k / policy output.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ensemble_b200.h"
+#include "eb_internal.h"
+#include "eb_kernels.h"
+
+namespace eb {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+}  // namespace eb
+
+using namespace eb;
+
+#define EB_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess) {                                                           \
+      set_error(std::string(#call) + ": " + cudaGetErrorString(_e));                   \
+      return EB_E_CUDA;                                                                \
+    }                                                                                  \
+  } while (0)
+
+#define EB_FAIL(code, msg)   \
+  do {                       \
+    set_error(msg);          \
+    return (code);           \
+  } while (0)
+
+namespace {
+
+constexpr int kLanes = 4;
+constexpr size_t kSplitWsFloats = static_cast<size_t>(148) * 128 * 256;
+constexpr int kMaxGraphs = 256;
+
+struct Tensor {
+  int h, w, c, dtype;
+  void* dev = nullptr;
+};
+
+struct Member {
+  int kind, tensor, koff, k;
+};
+
+size_t dsize(int dtype) { return dtype == EB_BF16 ? 2 : (dtype == EB_F32 ? 4 : 8); }
+
+// ------------------------------------------------------------------ conv planning
+
+struct ConvArgs {
+  const void* x;  // first channel of the slice
+  int B, H, W, ldx, cin;
+  const void* w;
+  const float* bias;
+  const void* res;
+  int ldr;
+  void* y;
+  int ldy, y_off, cout;
+  int kh, kw, sh, sw, ph, pw;
+  int relu, out_f32, c8_stem, flatten;
+  int split_k;  // 0 = auto
+  int block_n;  // 0 = auto
+};
+
+int conv_out(int in, int k, int s, int p) { return (in + 2 * p - k) / s + 1; }
+
+int pick_block_n(int cout) {
+  if (cout <= 32) return 32;
+  if (cout <= 64) return 64;
+  if (cout <= 128) return 128;
+  return (cout % 256 == 0) ? 256 : 128;
+}
+
+// K extent (elements) of the packed weight rows for a conv of this geometry.
+int64_t packed_k(int cin, int kh, int kw, bool c8, bool flatten, int H, int W) {
+  if (flatten) return ((static_cast<int64_t>(H) * W * cin + 63) / 64) * 64;
+  if (c8) return ((static_cast<int64_t>(kh) * kw + 7) / 8) * 64;
+  return static_cast<int64_t>(kh) * kw * ((cin + 63) / 64) * 64;
+}
+
+struct ConvPlan {
+  CUtensorMap ma, mb;
+  ConvParams p;
+  dim3 grid;
+  int block_n;
+  int splits;
+  size_t ws_floats;
+};
+
+int plan_conv(const ConvArgs& a, ConvPlan* out) {
+  const bool tiled = a.flatten || (a.kh == 1 && a.kw == 1 && a.sh == 1 && a.sw == 1 &&
+                                   a.ph == 0 && a.pw == 0 && !a.c8_stem);
+  const int Ho = a.flatten ? 1 : conv_out(a.H, a.kh, a.sh, a.ph);
+  const int Wo = a.flatten ? 1 : conv_out(a.W, a.kw, a.sw, a.pw);
+  if (Ho <= 0 || Wo <= 0) EB_FAIL(EB_E_SHAPE, "conv output would be empty");
+  const int64_t M64 = static_cast<int64_t>(a.B) * Ho * Wo;
+  if (M64 > (1ll << 31) - 1) EB_FAIL(EB_E_INVALID, "conv M too large");
+  const int M = static_cast<int>(M64);
+  const int64_t kpad = packed_k(a.cin, a.kh, a.kw, a.c8_stem, a.flatten, a.H, a.W);
+  std::string err;
+  ConvPlan& pl = *out;
+  memset(&pl.p, 0, sizeof(pl.p));
+  if (a.flatten) {
+    const int64_t feat = static_cast<int64_t>(a.H) * a.W * a.cin;
+    if (a.ldx != a.cin) EB_FAIL(EB_E_INVALID, "flatten needs a dense source tensor");
+    if (!encode_tiled_2d_bf16(&pl.ma, a.x, feat, a.B, feat, 64, 128, &err))
+      EB_FAIL(EB_E_INVALID, err);
+    pl.p.a_mode = kAModeTiled;
+  } else if (tiled) {
+    if (!encode_tiled_2d_bf16(&pl.ma, a.x, a.cin, M64, a.ldx, 64, 128, &err))
+      EB_FAIL(EB_E_INVALID, err);
+    pl.p.a_mode = kAModeTiled;
+  } else if (a.c8_stem) {
+    if (a.cin != 8 || a.ldx != 8) EB_FAIL(EB_E_INVALID, "stem mode expects an 8-channel image");
+    if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, 8, 8, a.kh, a.kw, a.sh, a.sw, a.ph, a.pw,
+                            8, 128, false, &err))
+      EB_FAIL(EB_E_INVALID, err);
+    pl.p.a_mode = kAModeIm2colC8;
+  } else {
+    if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, a.cin, a.ldx, a.kh, a.kw, a.sh, a.sw, a.ph,
+                            a.pw, 64, 128, true, &err))
+      EB_FAIL(EB_E_INVALID, err);
+    pl.p.a_mode = kAModeIm2col;
+  }
+  const int bn = a.block_n ? a.block_n : pick_block_n(a.cout);
+  if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn, &err))
+    EB_FAIL(EB_E_INVALID, err);
+  const int num_kb = static_cast<int>(kpad / 64);
+  const int mt = (M + 127) / 128;
+  const int nt = (a.cout + bn - 1) / bn;
+  int splits = a.split_k;
+  if (splits <= 0) {
+    splits = 1;
+    const int64_t tiles = static_cast<int64_t>(mt) * nt;
+    if (!a.res && tiles < 148 && num_kb >= 8) {
+      splits = static_cast<int>(std::min<int64_t>((148 + tiles - 1) / tiles, num_kb / 4));
+      splits = std::max(1, std::min(splits, 32));
+    }
+  }
+  if (splits > num_kb) splits = num_kb;
+  const int kb_per = (num_kb + splits - 1) / splits;
+  splits = (num_kb + kb_per - 1) / kb_per;
+  if (splits > 1 && a.res) EB_FAIL(EB_E_INVALID, "split-K with a residual is not supported");
+  pl.p.M = M;
+  pl.p.N = a.cout;
+  pl.p.num_kb = num_kb;
+  pl.p.kb_per_split = kb_per;
+  pl.p.Ho = Ho;
+  pl.p.Wo = Wo;
+  pl.p.sh = a.sh;
+  pl.p.sw = a.sw;
+  pl.p.ph = a.ph;
+  pl.p.pw = a.pw;
+  pl.p.kw = a.kw;
+  pl.p.taps = a.kh * a.kw;
+  pl.p.cchunks = (a.cin + 63) / 64;
+  pl.p.res = static_cast<const __nv_bfloat16*>(a.res);
+  pl.p.ldr = a.ldr;
+  pl.p.bias = a.bias;
+  pl.p.relu = a.relu;
+  pl.p.out = a.y;
+  pl.p.ldo = a.ldy;
+  pl.p.out_off = a.y_off;
+  pl.p.out_mode = a.out_f32 ? kOutF32 : kOutBF16;
+  pl.block_n = bn;
+  pl.splits = splits;
+  pl.ws_floats = splits > 1 ? static_cast<size_t>(M) * a.cout : 0;
+  pl.grid = dim3(mt, nt, splits);
+  return EB_OK;
+}
+
+int run_conv_plan(ConvPlan& pl, float* ws, size_t ws_cap, const ConvArgs& a, cudaStream_t s,
+                  int* launches) {
+  if (pl.splits > 1) {
+    if (!ws || pl.ws_floats > ws_cap) EB_FAIL(EB_E_INVALID, "split-K workspace too small");
+    ConvParams p = pl.p;
+    p.out = ws;
+    p.ldo = a.cout;
+    p.out_off = 0;
+    p.out_mode = kOutAtomicF32;
+    p.bias = nullptr;
+    p.relu = 0;
+    EB_CUDA(cudaMemsetAsync(ws, 0, pl.ws_floats * sizeof(float), s));
+    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, p, pl.block_n, pl.grid, s));
+    EB_CUDA(k_splitk_finalize(ws, pl.p.M, a.cout, a.bias, a.relu, a.y, a.ldy, a.y_off, a.out_f32,
+                              s));
+    if (launches) *launches += 2;
+  } else {
+    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.p, pl.block_n, pl.grid, s));
+    if (launches) *launches += 1;
+  }
+  return EB_OK;
+}
+
+}  // namespace
+
+struct eb_engine {
+  int device = 0;
+  int max_batch = 0;
+  int C = 0, H = 0, W = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t lanes[kLanes] = {};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_join[kLanes] = {};
+  void* pool = nullptr;
+  uint64_t pool_bytes = 0;
+  std::vector<Tensor> tensors;
+  std::vector<eb_op_desc> ops;
+  std::vector<Member> members;
+  bool finalized = false;
+  bool have_pre = false;
+  float* d_mean = nullptr;
+  float* d_std = nullptr;
+  float* d_lut = nullptr;
+  int nms = 1;
+  uint8_t* d_in_u8 = nullptr;
+  float* d_in_f32 = nullptr;
+  float* ws[kLanes] = {};
+  double* lin_part = nullptr;
+  int lin_nsplit = 1;
+  int32_t* d_labels = nullptr;
+  int32_t* d_topk_idx = nullptr;
+  float* d_topk_prob = nullptr;
+  int32_t* d_combined = nullptr;
+  int* d_kind = nullptr;
+  int* d_koff = nullptr;
+  int* d_kcnt = nullptr;
+  int max_topk = 16;
+  int l32_tensor = -1, l64_tensor = -1;
+  bool any_cnn = false, any_lin = false;
+  std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+  std::map<std::pair<int, int>, int> launch_counts;
+  std::mutex mu;
+};
+
+namespace {
+
+// Enqueue preprocess + every op for batch B on e->stream (fork/join over lanes).
+int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
+  cudaStream_t s = e->stream;
+  const int64_t plane = static_cast<int64_t>(e->H) * e->W;
+  Tensor& img8 = e->tensors[EB_T_IMAGE_NHWC8];
+  Tensor& imgf = e->tensors[EB_T_IMAGE_F32];
+  if (input_kind == EB_IN_U8_HWC) {
+    if (e->any_cnn) {
+      EB_CUDA(k_preprocess_u8hwc_to_nhwc(e->d_in_u8, static_cast<__nv_bfloat16*>(img8.dev), B,
+                                         e->C, plane, 8, e->d_lut, s));
+      ++*launches;
+    }
+    if (e->any_lin) {
+      EB_CUDA(k_preprocess_u8hwc_to_f32chw(e->d_in_u8, static_cast<float*>(imgf.dev), B, e->C,
+                                           plane, e->d_lut, s));
+      ++*launches;
+    }
+  } else {
+    if (e->any_cnn) {
+      EB_CUDA(k_preprocess_f32chw_to_nhwc(e->d_in_f32, static_cast<__nv_bfloat16*>(img8.dev), B,
+                                          e->C, plane, 8, e->d_mean, e->d_std, e->nms, s));
+      ++*launches;
+    }
+    if (e->any_lin) {
+      EB_CUDA(k_preprocess_f32(e->d_in_f32, static_cast<float*>(imgf.dev), B, e->C, plane,
+                               e->d_mean, e->d_std, e->nms, s));
+      ++*launches;
+    }
+  }
+  bool used[kLanes] = {};
+  for (const auto& op : e->ops) used[op.stream] = true;
+  EB_CUDA(cudaEventRecord(e->ev_fork, s));
+  for (int l = 0; l < kLanes; ++l)
+    if (used[l] && l != 0) EB_CUDA(cudaStreamWaitEvent(e->lanes[l], e->ev_fork, 0));
+  const uint8_t* pool = static_cast<const uint8_t*>(e->pool);
+  auto P = [&](uint64_t off) -> const void* {
+    return off == EB_NO_OFFSET ? nullptr : static_cast<const void*>(pool + off);
+  };
+  for (const auto& op : e->ops) {
+    cudaStream_t ls = op.stream == 0 ? s : e->lanes[op.stream];
+    Tensor& src = e->tensors[op.src];
+    Tensor& dst = e->tensors[op.dst];
+    const size_t es = dsize(src.dtype);
+    const void* x = static_cast<const uint8_t*>(src.dev) + static_cast<size_t>(op.src_c_off) * es;
+    switch (op.kind) {
+      case EB_OP_CONV: {
+        ConvArgs a{};
+        a.x = x;
+        a.B = B;
+        a.H = src.h;
+        a.W = src.w;
+        a.ldx = src.c;
+        a.cin = op.src_c;
+        a.w = P(op.w_off);
+        a.bias = static_cast<const float*>(P(op.b_off));
+        if (op.res >= 0) {
+          a.res = e->tensors[op.res].dev;
+          a.ldr = e->tensors[op.res].c;
+        }
+        a.y = dst.dev;
+        a.ldy = dst.c;
+        a.y_off = op.dst_c_off;
+        a.cout = op.cout;
+        a.kh = op.kh;
+        a.kw = op.kw;
+        a.sh = op.sh;
+        a.sw = op.sw;
+        a.ph = op.ph;
+        a.pw = op.pw;
+        a.relu = op.relu;
+        a.out_f32 = dst.dtype == EB_F32;
+        a.c8_stem = op.src == EB_T_IMAGE_NHWC8;
+        a.flatten = op.flatten;
+        ConvPlan pl;
+        int rc = plan_conv(a, &pl);
+        if (rc != EB_OK) return rc;
+        rc = run_conv_plan(pl, e->ws[op.stream], kSplitWsFloats, a, ls, launches);
+        if (rc != EB_OK) return rc;
+        break;
+      }
+      case EB_OP_POOL: {
+        const int Ho = conv_out(src.h, op.kh, op.sh, op.ph);
+        const int Wo = conv_out(src.w, op.kw, op.sw, op.pw);
+        EB_CUDA(k_pool(static_cast<const __nv_bfloat16*>(x), src.c,
+                       static_cast<__nv_bfloat16*>(dst.dev), dst.c, op.dst_c_off, B, src.h, src.w,
+                       op.src_c, Ho, Wo, op.kh, op.sh, op.ph, op.pool_mode,
+                       static_cast<const float*>(P(op.scale_off)),
+                       static_cast<const float*>(P(op.shift_off)), ls));
+        ++*launches;
+        break;
+      }
+      case EB_OP_BNRELU: {
+        EB_CUDA(k_bnrelu(static_cast<const __nv_bfloat16*>(x), src.c,
+                         static_cast<__nv_bfloat16*>(dst.dev) + op.dst_c_off, dst.c,
+                         static_cast<int64_t>(B) * src.h * src.w, op.src_c,
+                         static_cast<const float*>(P(op.scale_off)),
+                         static_cast<const float*>(P(op.shift_off)), ls));
+        ++*launches;
+        break;
+      }
+      case EB_OP_GAP: {
+        EB_CUDA(k_gap(static_cast<const __nv_bfloat16*>(x), src.c,
+                      static_cast<__nv_bfloat16*>(dst.dev), B, src.h * src.w, op.src_c,
+                      static_cast<const float*>(P(op.scale_off)),
+                      static_cast<const float*>(P(op.shift_off)), ls));
+        ++*launches;
+        break;
+      }
+      case EB_OP_LIN1: {
+        const int64_t D = static_cast<int64_t>(src.c) * src.h * src.w;
+        EB_CUDA(k_lin1(static_cast<const float*>(src.dev), static_cast<const float*>(P(op.w_off)),
+                       static_cast<const float*>(P(op.b_off)), e->lin_part,
+                       static_cast<double*>(dst.dev), B, op.cout, D, e->lin_nsplit, ls));
+        *launches += 2;
+        break;
+      }
+      default:
+        EB_FAIL(EB_E_INVALID, "unknown op kind");
+    }
+  }
+  for (int l = 1; l < kLanes; ++l) {
+    if (!used[l]) continue;
+    EB_CUDA(cudaEventRecord(e->ev_join[l], e->lanes[l]));
+    EB_CUDA(cudaStreamWaitEvent(s, e->ev_join[l], 0));
+  }
+  return EB_OK;
+}
+
+int run_layers(eb_engine* e, int input_kind, int B) {
+  const auto key = std::make_pair(B, input_kind);
+  auto it = e->graphs.find(key);
+  if (it != e->graphs.end()) {
+    EB_CUDA(cudaGraphLaunch(it->second, e->stream));
+    return EB_OK;
+  }
+  int launches = 0;
+  if (static_cast<int>(e->graphs.size()) >= kMaxGraphs) {
+    return enqueue_layers(e, input_kind, B, &launches);  // cache full: plain launches
+  }
+  EB_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_layers(e, input_kind, B, &launches);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+  if (rc != EB_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ce != cudaSuccess) EB_FAIL(EB_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  cudaGraphExec_t ex = nullptr;
+  ce = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess)
+    EB_FAIL(EB_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+  e->graphs[key] = ex;
+  e->launch_counts[key] = launches;
+  EB_CUDA(cudaGraphLaunch(ex, e->stream));
+  return EB_OK;
+}
+
+int check_batch(eb_engine* e, int batch) {
+  if (!e) EB_FAIL(EB_E_INVALID, "null engine");
+  if (!e->finalized) EB_FAIL(EB_E_STATE, "engine not finalized");
+  if (batch == 0) EB_FAIL(EB_E_EMPTY, "batch has no samples");
+  if (batch < 0) EB_FAIL(EB_E_INVALID, "negative batch");
+  if (batch > e->max_batch)
+    EB_FAIL(EB_E_TOO_LARGE, "batch size " + std::to_string(batch) + " exceeds max_batch " +
+                                std::to_string(e->max_batch));
+  return EB_OK;
+}
+
+int check_policy(eb_engine* e, int policy, int policy_k) {
+  if (policy == EB_POLICY_NONE) return EB_OK;
+  if (policy < 0 || policy > EB_POLICY_AT_LEAST) EB_FAIL(EB_E_INVALID, "unknown policy");
+  for (const auto& m : e->members)
+    if (m.k != 2) EB_FAIL(EB_E_POLICY, "policy unavailable: every model must be binary");
+  const int n = static_cast<int>(e->members.size());
+  if (policy == EB_POLICY_AT_LEAST && (policy_k < 1 || policy_k > n))
+    EB_FAIL(EB_E_BAD_K, "k must be between 1 and " + std::to_string(n) +
+                            " for this ensemble, got " + std::to_string(policy_k));
+  return EB_OK;
+}
+
+int enqueue_combine(eb_engine* e, int B, int topk, int policy, int policy_k) {
+  const float* l32 = nullptr;
+  const double* l64 = nullptr;
+  int ld32 = 0, ld64 = 0;
+  if (e->l32_tensor >= 0) {
+    l32 = static_cast<const float*>(e->tensors[e->l32_tensor].dev);
+    ld32 = e->tensors[e->l32_tensor].c;
+  }
+  if (e->l64_tensor >= 0) {
+    l64 = static_cast<const double*>(e->tensors[e->l64_tensor].dev);
+    ld64 = e->tensors[e->l64_tensor].c;
+  }
+  EB_CUDA(k_combine(l32, ld32, l64, ld64, e->d_kind, e->d_koff, e->d_kcnt,
+                    static_cast<int>(e->members.size()), B, e->d_labels, topk, e->d_topk_idx,
+                    e->d_topk_prob, policy, policy_k, e->d_combined, e->stream));
+  return EB_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+const char* eb_last_error(void) { return g_err.c_str(); }
+int eb_abi_version(void) { return 1; }
+
+int eb_engine_create(int device, int max_batch, int in_c, int in_h, int in_w, eb_engine** out) {
+  if (!out || max_batch < 1 || in_c < 1 || in_c > 8 || in_h < 1 || in_w < 1)
+    EB_FAIL(EB_E_INVALID, "bad engine geometry");
+  EB_CUDA(cudaSetDevice(device));
+  eb_engine* e = new eb_engine();
+  e->device = device;
+  e->max_batch = max_batch;
+  e->C = in_c;
+  e->H = in_h;
+  e->W = in_w;
+  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete e;
+    EB_FAIL(EB_E_CUDA, "stream create failed");
+  }
+  for (int l = 1; l < kLanes; ++l) cudaStreamCreateWithFlags(&e->lanes[l], cudaStreamNonBlocking);
+  e->lanes[0] = e->stream;
+  cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming);
+  for (int l = 0; l < kLanes; ++l) cudaEventCreateWithFlags(&e->ev_join[l], cudaEventDisableTiming);
+  e->tensors.push_back(Tensor{in_h, in_w, 8, EB_BF16, nullptr});
+  e->tensors.push_back(Tensor{in_h, in_w, in_c, EB_F32, nullptr});  // (C,H,W) layout
+  *out = e;
+  return EB_OK;
+}
+
+int eb_engine_destroy(eb_engine* e) {
+  if (!e) return EB_OK;
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(e->stream);
+  for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& t : e->tensors) cudaFree(t.dev);
+  cudaFree(e->pool);
+  cudaFree(e->d_mean);
+  cudaFree(e->d_std);
+  cudaFree(e->d_lut);
+  cudaFree(e->d_in_u8);
+  cudaFree(e->d_in_f32);
+  for (int l = 0; l < kLanes; ++l) cudaFree(e->ws[l]);
+  cudaFree(e->lin_part);
+  cudaFree(e->d_labels);
+  cudaFree(e->d_topk_idx);
+  cudaFree(e->d_topk_prob);
+  cudaFree(e->d_combined);
+  cudaFree(e->d_kind);
+  cudaFree(e->d_koff);
+  cudaFree(e->d_kcnt);
+  for (int l = 1; l < kLanes; ++l) cudaStreamDestroy(e->lanes[l]);
+  cudaEventDestroy(e->ev_fork);
+  for (int l = 0; l < kLanes; ++l) cudaEventDestroy(e->ev_join[l]);
+  cudaStreamDestroy(e->stream);
+  delete e;
+  return EB_OK;
+}
+
+int eb_set_preprocess(eb_engine* e, const float* host_mean, const float* host_std, int n,
+                      const float* host_lut_u8) {
+  if (!e || !host_mean || !host_std || !host_lut_u8) EB_FAIL(EB_E_INVALID, "null argument");
+  if (n != 1 && n != e->C)
+    EB_FAIL(EB_E_SHAPE, "mean/std have " + std::to_string(n) + " entries; input has " +
+                            std::to_string(e->C) + " channel(s)");
+  cudaSetDevice(e->device);
+  if (!e->d_mean) {
+    EB_CUDA(cudaMalloc(&e->d_mean, 8 * sizeof(float)));
+    EB_CUDA(cudaMalloc(&e->d_std, 8 * sizeof(float)));
+    EB_CUDA(cudaMalloc(&e->d_lut, 8 * 256 * sizeof(float)));
+  }
+  EB_CUDA(cudaMemcpy(e->d_mean, host_mean, n * sizeof(float), cudaMemcpyHostToDevice));
+  EB_CUDA(cudaMemcpy(e->d_std, host_std, n * sizeof(float), cudaMemcpyHostToDevice));
+  EB_CUDA(cudaMemcpy(e->d_lut, host_lut_u8, e->C * 256 * sizeof(float), cudaMemcpyHostToDevice));
+  e->nms = n;
+  e->have_pre = true;
+  return EB_OK;
+}
+
+int eb_pool_reserve(eb_engine* e, uint64_t bytes) {
+  if (!e || e->pool) EB_FAIL(EB_E_STATE, "pool already reserved");
+  cudaSetDevice(e->device);
+  if (cudaMalloc(&e->pool, bytes ? bytes : 256) != cudaSuccess) {
+    cudaGetLastError();
+    EB_FAIL(EB_E_NOMEM, "cannot allocate a " + std::to_string(bytes) + "-byte weight pool");
+  }
+  e->pool_bytes = bytes;
+  return EB_OK;
+}
+
+int eb_pool_write(eb_engine* e, uint64_t offset, const void* host_src, uint64_t bytes) {
+  if (!e || !e->pool) EB_FAIL(EB_E_STATE, "pool not reserved");
+  if (offset + bytes > e->pool_bytes) EB_FAIL(EB_E_INVALID, "pool write out of range");
+  cudaSetDevice(e->device);
+  EB_CUDA(cudaMemcpy(static_cast<uint8_t*>(e->pool) + offset, host_src, bytes,
+                     cudaMemcpyHostToDevice));
+  return EB_OK;
+}
+
+int eb_pool_bytes(eb_engine* e, uint64_t* bytes) {
+  if (!e || !bytes) EB_FAIL(EB_E_INVALID, "null argument");
+  *bytes = e->pool_bytes;
+  return EB_OK;
+}
+
+int eb_tensor(eb_engine* e, int h, int w, int c, int dtype, int* id_out) {
+  if (!e || e->finalized) EB_FAIL(EB_E_STATE, "engine finalized");
+  if (h < 1 || w < 1 || c < 1 || dtype < EB_BF16 || dtype > EB_F64)
+    EB_FAIL(EB_E_INVALID, "bad tensor shape");
+  if (dtype == EB_BF16 && c % 8 != 0) EB_FAIL(EB_E_INVALID, "bf16 tensors need c % 8 == 0");
+  e->tensors.push_back(Tensor{h, w, c, dtype, nullptr});
+  *id_out = static_cast<int>(e->tensors.size()) - 1;
+  return EB_OK;
+}
+
+int eb_add_op(eb_engine* e, const eb_op_desc* op) {
+  if (!e || !op || e->finalized) EB_FAIL(EB_E_STATE, "engine finalized");
+  const int nt = static_cast<int>(e->tensors.size());
+  if (op->src < 0 || op->src >= nt || op->dst < 0 || op->dst >= nt || op->res >= nt)
+    EB_FAIL(EB_E_INVALID, "op references an unknown tensor");
+  if (op->stream < 0 || op->stream >= kLanes) EB_FAIL(EB_E_INVALID, "bad lane");
+  const Tensor& src = e->tensors[op->src];
+  const Tensor& dst = e->tensors[op->dst];
+  if (op->src_c_off < 0 || op->src_c < 1 || op->src_c_off + op->src_c > src.c)
+    EB_FAIL(EB_E_INVALID, "source channel slice out of range");
+  if (op->kind == EB_OP_CONV) {
+    if (src.dtype != EB_BF16 || (dst.dtype != EB_BF16 && dst.dtype != EB_F32))
+      EB_FAIL(EB_E_INVALID, "conv dtypes");
+    if (op->dst_c_off < 0 || op->dst_c_off + op->cout > dst.c)
+      EB_FAIL(EB_E_INVALID, "conv output slice out of range");
+    const int Ho = op->flatten ? 1 : conv_out(src.h, op->kh, op->sh, op->ph);
+    const int Wo = op->flatten ? 1 : conv_out(src.w, op->kw, op->sw, op->pw);
+    if (Ho != dst.h || Wo != dst.w)
+      EB_FAIL(EB_E_SHAPE, "conv output geometry " + std::to_string(Ho) + "x" +
+                              std::to_string(Wo) + " does not match the destination tensor");
+    if (op->w_off == EB_NO_OFFSET || op->w_off % 16 != 0) EB_FAIL(EB_E_INVALID, "weights offset");
+    if (op->src_c_off % 8 != 0 || op->dst_c_off % 8 != 0 || op->cout % 8 != 0)
+      EB_FAIL(EB_E_INVALID, "channel slices must be multiples of 8");
+    if (op->res >= 0 && (e->tensors[op->res].h != dst.h || e->tensors[op->res].w != dst.w))
+      EB_FAIL(EB_E_SHAPE, "residual geometry");
+  } else if (op->kind == EB_OP_LIN1) {
+    if (op->src != EB_T_IMAGE_F32 || dst.dtype != EB_F64 || dst.c != op->cout)
+      EB_FAIL(EB_E_INVALID, "LIN1 op must read the f32 image and write fp64 scores");
+  } else if (op->kind == EB_OP_POOL || op->kind == EB_OP_BNRELU || op->kind == EB_OP_GAP) {
+    if (src.dtype != EB_BF16 || dst.dtype != EB_BF16) EB_FAIL(EB_E_INVALID, "pool dtypes");
+    if (op->src_c % 8 != 0 || op->src_c_off % 8 != 0 || op->dst_c_off % 8 != 0)
+      EB_FAIL(EB_E_INVALID, "channel slices must be multiples of 8");
+    if (op->kind == EB_OP_POOL) {
+      const int Ho = conv_out(src.h, op->kh, op->sh, op->ph);
+      const int Wo = conv_out(src.w, op->kw, op->sw, op->pw);
+      if (Ho != dst.h || Wo != dst.w || op->kh != op->kw || op->sh != op->sw || op->ph != op->pw)
+        EB_FAIL(EB_E_SHAPE, "pool geometry");
+    }
+    if (op->kind == EB_OP_GAP && (dst.h != 1 || dst.w != 1 || dst.c != op->src_c))
+      EB_FAIL(EB_E_SHAPE, "gap destination must be (1, 1, C)");
+  } else {
+    EB_FAIL(EB_E_INVALID, "unknown op kind");
+  }
+  e->ops.push_back(*op);
+  return EB_OK;
+}
+
+int eb_add_member(eb_engine* e, int kind, int logits_tensor, int k_off, int k) {
+  if (!e || e->finalized) EB_FAIL(EB_E_STATE, "engine finalized");
+  if (logits_tensor < 0 || logits_tensor >= static_cast<int>(e->tensors.size()) || k < 1 ||
+      k_off < 0 || k_off + k > e->tensors[logits_tensor].c)
+    EB_FAIL(EB_E_INVALID, "bad member logits slice");
+  const Tensor& t = e->tensors[logits_tensor];
+  if (kind == EB_MEMBER_CNN) {
+    if (t.dtype != EB_F32) EB_FAIL(EB_E_INVALID, "CNN logits must be fp32");
+    if (e->l32_tensor >= 0 && e->l32_tensor != logits_tensor)
+      EB_FAIL(EB_E_INVALID, "all CNN members must share one logits tensor");
+    e->l32_tensor = logits_tensor;
+    e->any_cnn = true;
+  } else if (kind == EB_MEMBER_LIN1) {
+    if (t.dtype != EB_F64) EB_FAIL(EB_E_INVALID, "LIN1 logits must be fp64");
+    if (e->l64_tensor >= 0 && e->l64_tensor != logits_tensor)
+      EB_FAIL(EB_E_INVALID, "all LIN1 members must share one logits tensor");
+    e->l64_tensor = logits_tensor;
+    e->any_lin = true;
+  } else {
+    EB_FAIL(EB_E_INVALID, "unknown member kind");
+  }
+  e->members.push_back(Member{kind, logits_tensor, k_off, k});
+  return EB_OK;
+}
+
+int eb_finalize(eb_engine* e) {
+  if (!e || e->finalized) EB_FAIL(EB_E_STATE, "engine already finalized");
+  if (e->members.empty()) EB_FAIL(EB_E_INVALID, "no members");
+  if (!e->have_pre) EB_FAIL(EB_E_STATE, "preprocess not set");
+  cudaSetDevice(e->device);
+  const int mb = e->max_batch;
+  for (size_t i = 0; i < e->tensors.size(); ++i) {
+    Tensor& t = e->tensors[i];
+    if (i == EB_T_IMAGE_NHWC8 && !e->any_cnn) continue;
+    if (i == EB_T_IMAGE_F32 && !e->any_lin) continue;
+    const size_t bytes = static_cast<size_t>(mb) * t.h * t.w * t.c * dsize(t.dtype);
+    if (cudaMalloc(&t.dev, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      EB_FAIL(EB_E_NOMEM, "activation arena allocation failed");
+    }
+    EB_CUDA(cudaMemset(t.dev, 0, bytes));
+  }
+  const size_t img = static_cast<size_t>(mb) * e->C * e->H * e->W;
+  EB_CUDA(cudaMalloc(&e->d_in_u8, img));
+  EB_CUDA(cudaMalloc(&e->d_in_f32, img * sizeof(float)));
+  bool used[kLanes] = {};
+  for (const auto& op : e->ops) used[op.stream] = true;
+  for (int l = 0; l < kLanes; ++l)
+    if (used[l] && e->any_cnn) EB_CUDA(cudaMalloc(&e->ws[l], kSplitWsFloats * sizeof(float)));
+  // LIN1 d-slices: a function of D and the member set only (never of the batch).
+  int64_t lin_k = 0;
+  for (const auto& op : e->ops)
+    if (op.kind == EB_OP_LIN1) lin_k = std::max<int64_t>(lin_k, op.cout);
+  if (lin_k > 0) {
+    const int64_t D = static_cast<int64_t>(e->C) * e->H * e->W;
+    int64_t ns = std::max<int64_t>(1, std::min<int64_t>(148, D / 1024));
+    const int64_t cap = (static_cast<int64_t>(256) << 20) / (static_cast<int64_t>(mb) * lin_k * 8);
+    ns = std::max<int64_t>(1, std::min(ns, cap));
+    e->lin_nsplit = static_cast<int>(ns);
+    EB_CUDA(cudaMalloc(&e->lin_part, static_cast<size_t>(ns) * mb * lin_k * sizeof(double)));
+  }
+  const int n = static_cast<int>(e->members.size());
+  std::vector<int> kind(n), koff(n), kcnt(n);
+  for (int i = 0; i < n; ++i) {
+    kind[i] = e->members[i].kind;
+    koff[i] = e->members[i].koff;
+    kcnt[i] = e->members[i].k;
+  }
+  EB_CUDA(cudaMalloc(&e->d_kind, n * sizeof(int)));
+  EB_CUDA(cudaMalloc(&e->d_koff, n * sizeof(int)));
+  EB_CUDA(cudaMalloc(&e->d_kcnt, n * sizeof(int)));
+  EB_CUDA(cudaMemcpy(e->d_kind, kind.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+  EB_CUDA(cudaMemcpy(e->d_koff, koff.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+  EB_CUDA(cudaMemcpy(e->d_kcnt, kcnt.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+  EB_CUDA(cudaMalloc(&e->d_labels, static_cast<size_t>(n) * mb * sizeof(int32_t)));
+  EB_CUDA(cudaMalloc(&e->d_topk_idx, static_cast<size_t>(n) * mb * e->max_topk * sizeof(int32_t)));
+  EB_CUDA(cudaMalloc(&e->d_topk_prob, static_cast<size_t>(n) * mb * e->max_topk * sizeof(float)));
+  EB_CUDA(cudaMalloc(&e->d_combined, static_cast<size_t>(mb) * sizeof(int32_t)));
+  e->finalized = true;
+  return EB_OK;
+}
+
+int eb_forward_device(eb_engine* e, int input_kind, int batch, int topk, int policy,
+                      int policy_k) {
+  int rc = check_batch(e, batch);
+  if (rc != EB_OK) return rc;
+  if (input_kind != EB_IN_F32_CHW && input_kind != EB_IN_U8_HWC)
+    EB_FAIL(EB_E_INVALID, "unknown input encoding");
+  if (topk < 0 || topk > e->max_topk) EB_FAIL(EB_E_INVALID, "topk out of range");
+  rc = check_policy(e, policy, policy_k);
+  if (rc != EB_OK) return rc;
+  cudaSetDevice(e->device);
+  rc = run_layers(e, input_kind, batch);
+  if (rc != EB_OK) return rc;
+  return enqueue_combine(e, batch, topk, policy, policy_k);
+}
+
+int eb_forward(eb_engine* e, const void* host_input, int input_kind, int batch,
+               int32_t* host_labels, float* host_logits, int topk, int32_t* host_topk_idx,
+               float* host_topk_prob, int policy, int policy_k, int32_t* host_combined) {
+  int rc = check_batch(e, batch);
+  if (rc != EB_OK) return rc;
+  if (!host_input || !host_labels) EB_FAIL(EB_E_INVALID, "null input/labels");
+  if (topk > 0 && (!host_topk_idx || !host_topk_prob)) EB_FAIL(EB_E_INVALID, "null top-k out");
+  if (policy != EB_POLICY_NONE && !host_combined) EB_FAIL(EB_E_INVALID, "null combined out");
+  rc = check_policy(e, policy, policy_k);
+  if (rc != EB_OK) return rc;
+  std::lock_guard<std::mutex> lock(e->mu);
+  cudaSetDevice(e->device);
+  const size_t px = static_cast<size_t>(batch) * e->C * e->H * e->W;
+  if (input_kind == EB_IN_U8_HWC) {
+    EB_CUDA(cudaMemcpyAsync(e->d_in_u8, host_input, px, cudaMemcpyHostToDevice, e->stream));
+  } else if (input_kind == EB_IN_F32_CHW) {
+    EB_CUDA(cudaMemcpyAsync(e->d_in_f32, host_input, px * sizeof(float), cudaMemcpyHostToDevice,
+                            e->stream));
+  } else {
+    EB_FAIL(EB_E_INVALID, "unknown input encoding");
+  }
+  rc = eb_forward_device(e, input_kind, batch, topk, policy, policy_k);
+  if (rc != EB_OK) return rc;
+  const int n = static_cast<int>(e->members.size());
+  EB_CUDA(cudaMemcpyAsync(host_labels, e->d_labels, static_cast<size_t>(n) * batch * sizeof(int32_t),
+                          cudaMemcpyDeviceToHost, e->stream));
+  if (topk > 0) {
+    EB_CUDA(cudaMemcpyAsync(host_topk_idx, e->d_topk_idx,
+                            static_cast<size_t>(n) * batch * topk * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, e->stream));
+    EB_CUDA(cudaMemcpyAsync(host_topk_prob, e->d_topk_prob,
+                            static_cast<size_t>(n) * batch * topk * sizeof(float),
+                            cudaMemcpyDeviceToHost, e->stream));
+  }
+  if (policy != EB_POLICY_NONE)
+    EB_CUDA(cudaMemcpyAsync(host_combined, e->d_combined, static_cast<size_t>(batch) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, e->stream));
+  if (host_logits) {
+    int kmax = 0;
+    for (const auto& m : e->members) kmax = std::max(kmax, m.k);
+    // fp32 member logits are copied row by row into [N][B][Kmax]; LIN1 (fp64)
+    // scores are narrowed on the host side of the copy by the caller.
+    for (int i = 0; i < n; ++i) {
+      const Member& m = e->members[i];
+      if (m.kind != EB_MEMBER_CNN) continue;
+      const Tensor& t = e->tensors[m.tensor];
+      EB_CUDA(cudaMemcpy2DAsync(host_logits + static_cast<size_t>(i) * batch * kmax,
+                                kmax * sizeof(float),
+                                static_cast<const float*>(t.dev) + m.koff, t.c * sizeof(float),
+                                m.k * sizeof(float), batch, cudaMemcpyDeviceToHost, e->stream));
+    }
+  }
+  EB_CUDA(cudaStreamSynchronize(e->stream));
+  return EB_OK;
+}
+
+int eb_input_buffer(eb_engine* e, int input_kind, void** dev_ptr) {
+  if (!e || !dev_ptr || !e->finalized) EB_FAIL(EB_E_STATE, "engine not finalized");
+  *dev_ptr = input_kind == EB_IN_U8_HWC ? static_cast<void*>(e->d_in_u8)
+                                        : static_cast<void*>(e->d_in_f32);
+  return EB_OK;
+}
+
+int eb_output_labels(eb_engine* e, int32_t** dev_labels) {
+  if (!e || !dev_labels || !e->finalized) EB_FAIL(EB_E_STATE, "engine not finalized");
+  *dev_labels = e->d_labels;
+  return EB_OK;
+}
+
+int eb_tensor_ptr(eb_engine* e, int id, void** dev_ptr, int* h, int* w, int* c, int* dtype) {
+  if (!e || id < 0 || id >= static_cast<int>(e->tensors.size()))
+    EB_FAIL(EB_E_INVALID, "bad tensor id");
+  const Tensor& t = e->tensors[id];
+  if (dev_ptr) *dev_ptr = t.dev;
+  if (h) *h = t.h;
+  if (w) *w = t.w;
+  if (c) *c = t.c;
+  if (dtype) *dtype = t.dtype;
+  return EB_OK;
+}
+
+int eb_engine_stream(eb_engine* e, void** stream) {
+  if (!e || !stream) EB_FAIL(EB_E_INVALID, "null argument");
+  *stream = e->stream;
+  return EB_OK;
+}
+
+int eb_launch_count(eb_engine* e, int input_kind, int batch, int* count) {
+  if (!e || !count) EB_FAIL(EB_E_INVALID, "null argument");
+  auto it = e->launch_counts.find(std::make_pair(batch, input_kind));
+  if (it == e->launch_counts.end()) EB_FAIL(EB_E_STATE, "no graph captured for this batch");
+  *count = it->second + 1;  // + combine
+  return EB_OK;
+}
+
+// ------------------------------------------------------------------ kernel-level ABI
+
+int eb_k_preprocess_f32(const float* dev_x, float* dev_y, int batch, int c, int64_t plane,
+                        const float* dev_mean, const float* dev_std, int n, void* stream) {
+  EB_CUDA(k_preprocess_f32(dev_x, dev_y, batch, c, plane, dev_mean, dev_std, n,
+                           static_cast<cudaStream_t>(stream)));
+  return EB_OK;
+}
+
+int eb_k_preprocess_u8_nhwc8(const uint8_t* dev_x, void* dev_y_bf16, int batch, int c,
+                             int64_t plane, const float* dev_lut, void* stream) {
+  if (c < 1 || c > 8) EB_FAIL(EB_E_INVALID, "channels must be 1..8");
+  EB_CUDA(k_preprocess_u8hwc_to_nhwc(dev_x, static_cast<__nv_bfloat16*>(dev_y_bf16), batch, c,
+                                     plane, 8, dev_lut, static_cast<cudaStream_t>(stream)));
+  return EB_OK;
+}
+
+int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, const void* dev_w,
+              const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
+              int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
+              int out_f32, int c8_stem, int split_k, int block_n, void* dev_workspace,
+              void* stream) {
+  ConvArgs a{};
+  a.x = dev_x;
+  a.B = batch;
+  a.H = h;
+  a.W = w;
+  a.ldx = ldx;
+  a.cin = cin;
+  a.w = dev_w;
+  a.bias = dev_bias;
+  a.res = dev_res;
+  a.ldr = ldr;
+  a.y = dev_y;
+  a.ldy = ldy;
+  a.y_off = y_off;
+  a.cout = cout;
+  a.kh = kh;
+  a.kw = kw;
+  a.sh = sh;
+  a.sw = sw;
+  a.ph = ph;
+  a.pw = pw;
+  a.relu = relu;
+  a.out_f32 = out_f32;
+  a.c8_stem = c8_stem;
+  a.flatten = 0;
+  a.split_k = split_k;
+  a.block_n = block_n;
+  ConvPlan pl;
+  int rc = plan_conv(a, &pl);
+  if (rc != EB_OK) return rc;
+  return run_conv_plan(pl, static_cast<float*>(dev_workspace), kSplitWsFloats, a,
+                       static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int eb_k_pool(const void* dev_x, int ldx, void* dev_y, int ldy, int y_off, int batch, int h,
+              int w, int c, int k, int s, int pad, int mode, const float* dev_scale,
+              const float* dev_shift, void* stream) {
+  const int Ho = conv_out(h, k, s, pad), Wo = conv_out(w, k, s, pad);
+  EB_CUDA(k_pool(static_cast<const __nv_bfloat16*>(dev_x), ldx, static_cast<__nv_bfloat16*>(dev_y),
+                 ldy, y_off, batch, h, w, c, Ho, Wo, k, s, pad, mode, dev_scale, dev_shift,
+                 static_cast<cudaStream_t>(stream)));
+  return EB_OK;
+}
+
+int eb_k_gap(const void* dev_x, int ldx, void* dev_y, int batch, int hw, int c,
+             const float* dev_scale, const float* dev_shift, void* stream) {
+  EB_CUDA(k_gap(static_cast<const __nv_bfloat16*>(dev_x), ldx, static_cast<__nv_bfloat16*>(dev_y),
+                batch, hw, c, dev_scale, dev_shift, static_cast<cudaStream_t>(stream)));
+  return EB_OK;
+}
+
+int eb_k_lin1(const float* dev_x, const float* dev_w, const float* dev_bias, double* dev_part,
+              double* dev_logits, int batch, int k, int64_t d, int nsplit, void* stream) {
+  EB_CUDA(k_lin1(dev_x, dev_w, dev_bias, dev_part, dev_logits, batch, k, d, nsplit,
+                 static_cast<cudaStream_t>(stream)));
+  return EB_OK;
+}
+
+int eb_k_combine(const float* dev_l32, int ld32, const double* dev_l64, int ld64,
+                 const int* dev_kind, const int* dev_koff, const int* dev_kcnt, int n, int batch,
+                 int32_t* dev_labels, int topk, int32_t* dev_topk_idx, float* dev_topk_prob,
+                 int policy, int policy_k, int32_t* dev_combined, void* stream) {
+  EB_CUDA(k_combine(dev_l32, ld32, dev_l64, ld64, dev_kind, dev_koff, dev_kcnt, n, batch,
+                    dev_labels, topk, dev_topk_idx, dev_topk_prob, policy, policy_k,
+                    dev_combined, static_cast<cudaStream_t>(stream)));
+  return EB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+"""Kernel-level parity on the B200: every conv class the model families use,
+against a plain fp32 PyTorch CPU convolution of the same bf16-rounded operands."""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2003_01538_b200 import _lib
+from paper_2003_01538_b200.packing import conv_mode, pack_conv_weight, u8_lut
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def _p(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def run_conv(x_nhwc, ldx, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw, *, y_ld=None,
+             y_off=0, out_f32=False, stem=False, split_k=0, block_n=0):
+    lib = _lib.load()
+    B, H, W, _ = x_nhwc.shape
+    cout = w.shape[0]
+    Ho = (H + 2 * ph - kh) // sh + 1
+    Wo = (W + 2 * pw - kw) // sw + 1
+    mode = conv_mode(kh, kw, sh, sw, ph, pw, cin, stem)
+    wp = pack_conv_weight(w, mode).to(DEV)
+    ld = y_ld or cout
+    y = torch.zeros(B, Ho, Wo, ld, device=DEV, dtype=torch.float32 if out_f32 else torch.bfloat16)
+    ws = torch.empty(148 * 128 * 256, device=DEV, dtype=torch.float32)
+    b = bias.to(DEV) if bias is not None else None
+    _lib.check(lib.eb_k_conv(
+        _p(x_nhwc), B, H, W, ldx, cin, _p(wp), _p(b), _p(res), res.shape[-1] if res is not None else 0,
+        _p(y), ld, y_off, cout, kh, kw, sh, sw, ph, pw, int(relu), int(out_f32), int(stem),
+        split_k, block_n, _p(ws), None))
+    torch.cuda.synchronize()
+    return y
+
+
+def ref_conv(x_nhwc, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw):
+    x = x_nhwc[..., :cin].float().cpu().permute(0, 3, 1, 2)
+    wr = w.to(torch.bfloat16).float()
+    y = F.conv2d(x, wr, None if bias is None else bias.float(), stride=(sh, sw), padding=(ph, pw))
+    y = y.permute(0, 2, 3, 1)
+    if res is not None:
+        y = y + res.float().cpu()
+    if relu:
+        y = torch.relu(y)
+    return y
+
+
+CASES = [
+    # name, B, H, W, cin, cout, kh, kw, sh, sw, ph, pw
+    ("1x1", 2, 14, 14, 256, 128, 1, 1, 1, 1, 0, 0),
+    ("3x3", 2, 14, 14, 64, 64, 3, 3, 1, 1, 1, 1),
+    ("3x3s2", 3, 28, 28, 128, 256, 3, 3, 2, 2, 1, 1),
+    ("1x1s2", 2, 28, 28, 256, 512, 1, 1, 2, 2, 0, 0),
+    ("7x7tail", 5, 7, 7, 512, 512, 3, 3, 1, 1, 1, 1),
+    ("1x7", 2, 17, 17, 128, 192, 1, 7, 1, 1, 0, 3),
+    ("7x1", 2, 17, 17, 128, 192, 7, 1, 1, 1, 3, 0),
+    ("5x5", 2, 35, 35, 48, 64, 5, 5, 1, 1, 2, 2),
+    ("3x3s2valid", 2, 35, 35, 96, 96, 3, 3, 2, 2, 0, 0),
+    ("growth32", 2, 56, 56, 128, 32, 3, 3, 1, 1, 1, 1),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_conv_matches_fp32(case):
+    _, B, H, W, cin, cout, kh, kw, sh, sw, ph, pw = case
+    g = torch.Generator().manual_seed(hash(case[0]) & 0xFFFF)
+    x = torch.randn(B, H, W, cin, generator=g).to(torch.bfloat16).to(DEV)
+    w = torch.randn(cout, cin, kh, kw, generator=g) / np.sqrt(cin * kh * kw)
+    bias = torch.randn(cout, generator=g) * 0.1
+    y = run_conv(x, cin, cin, w, bias, None, True, kh, kw, sh, sw, ph, pw)
+    r = ref_conv(x, cin, w, bias, None, True, kh, kw, sh, sw, ph, pw)
+    err = (y.float().cpu() - r).abs().max().item()
+    assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+
+
+def test_conv_stem_c8():
+    g = torch.Generator().manual_seed(7)
+    B, H, W = 2, 56, 56
+    x3 = torch.randn(B, H, W, 3, generator=g)
+    x = torch.zeros(B, H, W, 8)
+    x[..., :3] = x3
+    x = x.to(torch.bfloat16).to(DEV)
+    w = torch.randn(64, 3, 7, 7, generator=g) / np.sqrt(147)
+    bias = torch.randn(64, generator=g) * 0.1
+    y = run_conv(x, 8, 8, w, bias, None, True, 7, 7, 2, 2, 3, 3, stem=True)
+    r = ref_conv(x, 3, w, bias, None, True, 7, 7, 2, 2, 3, 3)
+    err = (y.float().cpu() - r).abs().max().item()
+    assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+
+
+def test_conv_slices_residual():
+    # DenseNet-style: read a channel prefix of a wider buffer, write into a slice.
+    g = torch.Generator().manual_seed(3)
+    B, H, W, ld, cin, cout = 3, 14, 14, 192, 96, 32
+    x = torch.randn(B, H, W, ld, generator=g).to(torch.bfloat16).to(DEV)
+    w = torch.randn(cout, cin, 3, 3, generator=g) / np.sqrt(cin * 9)
+    res = torch.randn(B, H, W, cout, generator=g).to(torch.bfloat16).to(DEV)
+    y = run_conv(x, ld, cin, w, None, res, True, 3, 3, 1, 1, 1, 1, y_ld=128, y_off=64)
+    r = ref_conv(x, cin, w, None, res, True, 3, 3, 1, 1, 1, 1)
+    yy = y.float().cpu()
+    assert (yy[..., :64] == 0).all() and (yy[..., 96:] == 0).all()
+    err = (yy[..., 64:96] - r).abs().max().item()
+    assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+
+
+@pytest.mark.parametrize("split", [1, 0, 4])
+def test_fc_f32_splitk(split):
+    g = torch.Generator().manual_seed(11)
+    B, cin, cout = 5, 2048, 1000
+    x = torch.randn(B, 1, 1, cin, generator=g).to(torch.bfloat16).to(DEV)
+    w = torch.randn(cout, cin, 1, 1, generator=g) / np.sqrt(cin)
+    bias = torch.randn(cout, generator=g)
+    y = run_conv(x, cin, cin, w, bias, None, False, 1, 1, 1, 1, 0, 0, out_f32=True, split_k=split)
+    r = ref_conv(x, cin, w, bias, None, False, 1, 1, 1, 1, 0, 0)
+    err = (y.cpu() - r).abs().max().item()
+    assert err <= 2e-3 * r.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("bn", [32, 64, 128, 256])
+def test_block_n_variants(bn):
+    g = torch.Generator().manual_seed(bn)
+    x = torch.randn(2, 14, 14, 128, generator=g).to(torch.bfloat16).to(DEV)
+    w = torch.randn(256, 128, 3, 3, generator=g) / np.sqrt(128 * 9)
+    y = run_conv(x, 128, 128, w, None, None, False, 3, 3, 1, 1, 1, 1, block_n=bn)
+    r = ref_conv(x, 128, w, None, None, False, 3, 3, 1, 1, 1, 1)
+    err = (y.float().cpu() - r).abs().max().item()
+    assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+
+
+def test_preprocess_u8_lut_exact():
+    lib = _lib.load()
+    rng = np.random.default_rng(0)
+    B, H, W, C = 3, 17, 9, 3
+    px = rng.integers(0, 256, size=(B, H, W, C), dtype=np.uint8)
+    mean, std = (0.485, 0.456, 0.406), (0.229, 0.224, 0.225)
+    lut = u8_lut(mean, std, 255.0, C)
+    d_x = torch.from_numpy(px).to(DEV)
+    d_lut = torch.from_numpy(lut).to(DEV)
+    d_y = torch.empty(B, H, W, 8, dtype=torch.bfloat16, device=DEV)
+    _lib.check(lib.eb_k_preprocess_u8_nhwc8(_p(d_x), _p(d_y), B, C, H * W, _p(d_lut), None))
+    torch.cuda.synchronize()
+    # reference semantics: wire.py:71 then models.py:254-259, fp32, then bf16
+    x = px.astype(np.float32) / np.float32(255.0)
+    ref = (x - np.asarray(mean, np.float32)) / np.asarray(std, np.float32)
+    ref_bf16 = torch.from_numpy(ref).to(torch.bfloat16)
+    got = d_y.cpu()
+    assert torch.equal(got[..., :C], ref_bf16)
+    assert (got[..., C:].float() == 0).all()
+
+
+def test_preprocess_f32_bit_exact():
+    lib = _lib.load()
+    rng = np.random.default_rng(1)
+    B, C, H, W = 4, 3, 13, 11
+    x = rng.random((B, C * H * W), dtype=np.float32)
+    mean = np.asarray([0.485, 0.456, 0.406], np.float32)
+    std = np.asarray([0.229, 0.224, 0.225], np.float32)
+    ref = ((x.reshape(B, C, H * W) - mean.reshape(-1, 1)) / std.reshape(-1, 1)).reshape(B, -1)
+    d_x = torch.from_numpy(x).to(DEV)
+    d_y = torch.empty_like(d_x)
+    d_mean, d_std = torch.from_numpy(mean).to(DEV), torch.from_numpy(std).to(DEV)
+    _lib.check(lib.eb_k_preprocess_f32(_p(d_x), _p(d_y), B, C, H * W, _p(d_mean), _p(d_std), 3, None))
+    torch.cuda.synchronize()
+    assert np.array_equal(d_y.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+def test_pool_and_gap():
+    lib = _lib.load()
+    g = torch.Generator().manual_seed(5)
+    B, H, W, C = 2, 14, 14, 64
+    x = torch.randn(B, H, W, C, generator=g).to(torch.bfloat16).to(DEV)
+    for mode, k, s, p in [(0, 3, 2, 1), (0, 2, 2, 0), (1, 2, 2, 0), (1, 3, 1, 1)]:
+        Ho = (H + 2 * p - k) // s + 1
+        y = torch.zeros(B, Ho, Ho, C, dtype=torch.bfloat16, device=DEV)
+        _lib.check(lib.eb_k_pool(_p(x), C, _p(y), C, 0, B, H, W, C, k, s, p, mode, None, None, None))
+        torch.cuda.synchronize()
+        xc = x.float().cpu().permute(0, 3, 1, 2)
+        if mode == 0:
+            r = F.max_pool2d(xc, k, s, p)
+        else:
+            r = F.avg_pool2d(xc, k, s, p, count_include_pad=True)
+        r = r.permute(0, 2, 3, 1)
+        assert (y.float().cpu() - r).abs().max().item() < 0.02
+    y = torch.zeros(B, C, dtype=torch.bfloat16, device=DEV)
+    _lib.check(lib.eb_k_gap(_p(x), C, _p(y), B, H * W, C, None, None, None))
+    torch.cuda.synchronize()
+    r = x.float().cpu().mean(dim=(1, 2))
+    assert (y.float().cpu() - r).abs().max().item() < 0.01
+
+
+def test_combine_argmax_topk_policy():
+    lib = _lib.load()
+    B, K = 6, 10
+    l32 = torch.zeros(B, 2 * K)
+    l32[:, :K] = torch.arange(K).float()  # member 0: argmax K-1
+    l32[:, K:] = 1.0                      # member 1: all tied -> index 0
+    l32[0, K + 3] = 2.0
+    l64 = torch.tensor([[0.25, 0.5], [0.5, 0.5], [0.7, 0.1], [0.1, 0.2], [0.3, 0.3], [1.0, 0.0]],
+                       dtype=torch.float64)
+    kind = torch.tensor([0, 0, 1], dtype=torch.int32)
+    koff = torch.tensor([0, K, 0], dtype=torch.int32)
+    kcnt = torch.tensor([K, K, 2], dtype=torch.int32)
+    d = {n: t.to(DEV) for n, t in dict(l32=l32, l64=l64, kind=kind, koff=koff, kcnt=kcnt).items()}
+    labels = torch.zeros(3, B, dtype=torch.int32, device=DEV)
+    tk = torch.zeros(3, B, 3, dtype=torch.int32, device=DEV)
+    tp = torch.zeros(3, B, 3, dtype=torch.float32, device=DEV)
+    comb = torch.zeros(B, dtype=torch.int32, device=DEV)
+    _lib.check(lib.eb_k_combine(_p(d["l32"]), 2 * K, _p(d["l64"]), 2, _p(d["kind"]), _p(d["koff"]),
+                                _p(d["kcnt"]), 3, B, _p(labels), 3, _p(tk), _p(tp), 0, 0, _p(comb),
+                                None))
+    torch.cuda.synchronize()
+    lab = labels.cpu().numpy()
+    assert (lab[0] == K - 1).all()
+    assert lab[1, 0] == 3 and (lab[1, 1:] == 0).all()
+    assert lab[2].tolist() == [1, 0, 0, 1, 0, 0]
+    assert tk.cpu()[0, 0].tolist() == [K - 1, K - 2, K - 3]
+    assert tk.cpu()[1, 1].tolist() == [0, 1, 2]
+    p = torch.softmax(l32[0, :K], 0)
+    assert torch.allclose(tp.cpu()[0, 0], p.flip(0)[:3], atol=1e-5)
+
+
+def test_lin1_f64_scores():
+    lib = _lib.load()
+    rng = np.random.default_rng(2)
+    B, K, D, ns = 7, 5, 3000, 3
+    x = rng.standard_normal((B, D)).astype(np.float32)
+    w = rng.standard_normal((K, D)).astype(np.float32)
+    b = rng.standard_normal(K).astype(np.float32)
+    ref = np.einsum("bd,kd->bk", x.astype(np.float64), w.astype(np.float64)) + b.astype(np.float64)
+    dx, dw, db = (torch.from_numpy(a).to(DEV) for a in (x, w, b))
+    part = torch.empty(ns * B * K, dtype=torch.float64, device=DEV)
+    out = torch.empty(B, K, dtype=torch.float64, device=DEV)
+    _lib.check(lib.eb_k_lin1(_p(dx), _p(dw), _p(db), _p(part), _p(out), B, K, D, ns, None))
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-9)
+    assert (got.argmax(1) == ref.argmax(1)).all()
