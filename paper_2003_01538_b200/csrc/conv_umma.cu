@@ -14,7 +14,7 @@
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA
 // issuer (one elected lane), warps 2..5 = epilogue (TMEM -> registers ->
-// bias / residual / ReLU -> bf16 NHWC store, or fp32 logits / split-K partials).
+// bias / residual / ReLU -> bf16 NHWC store, or fp32 logits / split-K partial slices).
 // The epilogue writes into a channel slice of a wider NHWC buffer, which is how
 // DenseNet concatenation and Inception branch concatenation are realised
 // without a copy.
@@ -186,14 +186,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
       const int nvalid = (p.N - n) < 16 ? (p.N - n) : 16;
-      if (p.out_mode == kOutAtomicF32) {
-        float* o = reinterpret_cast<float*>(p.out) + static_cast<size_t>(m) * p.ldo + p.out_off + n;
-        if (nvalid == 16) {
+      const bool vec = p.vec_ok && nvalid == 16;
+      if (p.out_mode == kOutPartialF32) {
+        float* o = reinterpret_cast<float*>(p.out) +
+                   (static_cast<size_t>(blockIdx.z) * p.M + m) * p.ldo + n;
+        if (vec) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4)
-            atomicAdd(reinterpret_cast<float4*>(o + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+            *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         } else {
-          for (int j = 0; j < nvalid; ++j) atomicAdd(o + j, v[j]);
+          for (int j = 0; j < nvalid; ++j) o[j] = v[j];
         }
         continue;
       }
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (p.res) {
         const __nv_bfloat16* rp = p.res + static_cast<size_t>(m) * p.ldr + n;
-        if (nvalid == 16) {
+        if (vec) {
           uint4 q0 = *reinterpret_cast<const uint4*>(rp);
           uint4 q1 = *reinterpret_cast<const uint4*>(rp + 8);
           const __nv_bfloat16* h0 = reinterpret_cast<const __nv_bfloat16*>(&q0);
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (p.out_mode == kOutF32) {
         float* o = reinterpret_cast<float*>(p.out) + static_cast<size_t>(m) * p.ldo + p.out_off + n;
-        if (nvalid == 16) {
+        if (vec) {
 #pragma unroll
           for (int j = 0; j < 16; j += 4)
             *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         __nv_bfloat16* o =
             reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(m) * p.ldo + p.out_off + n;
-        if (nvalid == 16) {
+        if (vec) {
           uint4 q0, q1;
           q0.x = pack_bf16x2(v[0], v[1]);
           q0.y = pack_bf16x2(v[2], v[3]);

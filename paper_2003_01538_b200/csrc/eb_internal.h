@@ -18,7 +18,7 @@ enum AMode : int {
 enum OutMode : int {
   kOutBF16 = 0,       // bf16 NHWC slice, bias/residual/ReLU fused
   kOutF32 = 1,        // fp32 (logits), bias/ReLU fused
-  kOutAtomicF32 = 2,  // fp32 split-K partials, accumulated with atomics
+  kOutPartialF32 = 2,  // fp32 split-K partial of slice blockIdx.z (deterministic reduce after)
 };
 
 struct ConvParams {
@@ -33,6 +33,7 @@ struct ConvParams {
   const float* bias;
   int relu;
   int out_mode;
+  int vec_ok;  // 16-byte aligned rows/offsets: vector epilogue stores allowed
 };
 
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const ConvParams& p,

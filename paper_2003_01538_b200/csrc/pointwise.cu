@@ -272,8 +272,9 @@ cudaError_t k_gap(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int B, int 
   return cudaGetLastError();
 }
 
-// Split-K finalisation: y = act(ws + bias) -> bf16 slice or fp32.
-__global__ void splitk_finalize_kernel(const float* __restrict__ ws, int64_t M, int N,
+// Split-K finalisation: y = act(sum_z ws[z] + bias), slices added in ascending z
+// (deterministic, independent of scheduling) -> bf16 slice or fp32.
+__global__ void splitk_finalize_kernel(const float* __restrict__ ws, int splits, int64_t M, int N,
                                        const float* __restrict__ bias, int relu, void* out,
                                        int ldo, int out_off, int out_f32) {
   const int64_t total = M * N;
@@ -281,7 +282,9 @@ __global__ void splitk_finalize_kernel(const float* __restrict__ ws, int64_t M, 
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int n = static_cast<int>(i % N);
     const int64_t m = i / N;
-    float v = ws[i] + (bias ? bias[n] : 0.f);
+    float v = 0.f;
+    for (int z = 0; z < splits; ++z) v += ws[z * total + i];
+    if (bias) v += bias[n];
     if (relu) v = fmaxf(v, 0.f);
     if (out_f32)
       reinterpret_cast<float*>(out)[m * ldo + out_off + n] = v;
@@ -290,12 +293,13 @@ __global__ void splitk_finalize_kernel(const float* __restrict__ ws, int64_t M, 
   }
 }
 
-cudaError_t k_splitk_finalize(const float* ws, int64_t M, int N, const float* bias, int relu,
-                              void* out, int ldo, int out_off, int out_f32, cudaStream_t st) {
+cudaError_t k_splitk_finalize(const float* ws, int splits, int64_t M, int N, const float* bias,
+                              int relu, void* out, int ldo, int out_off, int out_f32,
+                              cudaStream_t st) {
   const int64_t total = M * N;
   if (total == 0) return cudaSuccess;
-  splitk_finalize_kernel<<<grid_for(total, 256), 256, 0, st>>>(ws, M, N, bias, relu, out, ldo,
-                                                               out_off, out_f32);
+  splitk_finalize_kernel<<<grid_for(total, 256), 256, 0, st>>>(ws, splits, M, N, bias, relu, out,
+                                                               ldo, out_off, out_f32);
   return cudaGetLastError();
 }
 

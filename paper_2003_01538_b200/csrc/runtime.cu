@@ -48,7 +48,8 @@ using namespace eb;
 namespace {
 
 constexpr int kLanes = 4;
-constexpr size_t kSplitWsFloats = static_cast<size_t>(148) * 128 * 256;
+// split-K partial slices: splits * tiles <= 2 * 148 by construction (plan_conv)
+constexpr size_t kSplitWsFloats = static_cast<size_t>(2 * 148) * 128 * 256;
 constexpr int kMaxGraphs = 256;
 
 struct Tensor {
@@ -179,9 +180,13 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.p.ldo = a.ldy;
   pl.p.out_off = a.y_off;
   pl.p.out_mode = a.out_f32 ? kOutF32 : kOutBF16;
+  {
+    const int q = a.out_f32 ? 4 : 8;  // elements per 16 bytes
+    pl.p.vec_ok = (a.ldy % q == 0) && (a.y_off % q == 0) && (!a.res || a.ldr % 8 == 0);
+  }
   pl.block_n = bn;
   pl.splits = splits;
-  pl.ws_floats = splits > 1 ? static_cast<size_t>(M) * a.cout : 0;
+  pl.ws_floats = splits > 1 ? static_cast<size_t>(splits) * M * a.cout : 0;
   pl.grid = dim3(mt, nt, splits);
   return EB_OK;
 }
@@ -194,13 +199,13 @@ int run_conv_plan(ConvPlan& pl, float* ws, size_t ws_cap, const ConvArgs& a, cud
     p.out = ws;
     p.ldo = a.cout;
     p.out_off = 0;
-    p.out_mode = kOutAtomicF32;
+    p.out_mode = kOutPartialF32;
+    p.vec_ok = (a.cout % 4 == 0);
     p.bias = nullptr;
     p.relu = 0;
-    EB_CUDA(cudaMemsetAsync(ws, 0, pl.ws_floats * sizeof(float), s));
     EB_CUDA(conv_umma_launch(pl.ma, pl.mb, p, pl.block_n, pl.grid, s));
-    EB_CUDA(k_splitk_finalize(ws, pl.p.M, a.cout, a.bias, a.relu, a.y, a.ldy, a.y_off, a.out_f32,
-                              s));
+    EB_CUDA(k_splitk_finalize(ws, pl.splits, pl.p.M, a.cout, a.bias, a.relu, a.y, a.ldy, a.y_off,
+                              a.out_f32, s));
     if (launches) *launches += 2;
   } else {
     EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.p, pl.block_n, pl.grid, s));
@@ -462,7 +467,7 @@ const char* eb_last_error(void) { return g_err.c_str(); }
 int eb_abi_version(void) { return 1; }
 
 int eb_engine_create(int device, int max_batch, int in_c, int in_h, int in_w, eb_engine** out) {
-  if (!out || max_batch < 1 || in_c < 1 || in_c > 8 || in_h < 1 || in_w < 1)
+  if (!out || max_batch < 1 || in_c < 1 || in_h < 1 || in_w < 1)
     EB_FAIL(EB_E_INVALID, "bad engine geometry");
   EB_CUDA(cudaSetDevice(device));
   eb_engine* e = new eb_engine();
@@ -522,9 +527,9 @@ int eb_set_preprocess(eb_engine* e, const float* host_mean, const float* host_st
                             std::to_string(e->C) + " channel(s)");
   cudaSetDevice(e->device);
   if (!e->d_mean) {
-    EB_CUDA(cudaMalloc(&e->d_mean, 8 * sizeof(float)));
-    EB_CUDA(cudaMalloc(&e->d_std, 8 * sizeof(float)));
-    EB_CUDA(cudaMalloc(&e->d_lut, 8 * 256 * sizeof(float)));
+    EB_CUDA(cudaMalloc(&e->d_mean, e->C * sizeof(float)));
+    EB_CUDA(cudaMalloc(&e->d_std, e->C * sizeof(float)));
+    EB_CUDA(cudaMalloc(&e->d_lut, e->C * 256 * sizeof(float)));
   }
   EB_CUDA(cudaMemcpy(e->d_mean, host_mean, n * sizeof(float), cudaMemcpyHostToDevice));
   EB_CUDA(cudaMemcpy(e->d_std, host_std, n * sizeof(float), cudaMemcpyHostToDevice));
@@ -591,8 +596,10 @@ int eb_add_op(eb_engine* e, const eb_op_desc* op) {
       EB_FAIL(EB_E_SHAPE, "conv output geometry " + std::to_string(Ho) + "x" +
                               std::to_string(Wo) + " does not match the destination tensor");
     if (op->w_off == EB_NO_OFFSET || op->w_off % 16 != 0) EB_FAIL(EB_E_INVALID, "weights offset");
-    if (op->src_c_off % 8 != 0 || op->dst_c_off % 8 != 0 || op->cout % 8 != 0)
-      EB_FAIL(EB_E_INVALID, "channel slices must be multiples of 8");
+    if (op->src_c_off % 8 != 0 || op->dst_c_off % 8 != 0)
+      EB_FAIL(EB_E_INVALID, "channel slices must start at multiples of 8");
+    if (dst.dtype == EB_BF16 && op->cout % 8 != 0)
+      EB_FAIL(EB_E_INVALID, "bf16 conv outputs need cout % 8 == 0");
     if (op->res >= 0 && (e->tensors[op->res].h != dst.h || e->tensors[op->res].w != dst.w))
       EB_FAIL(EB_E_SHAPE, "residual geometry");
   } else if (op->kind == EB_OP_LIN1) {
@@ -625,6 +632,7 @@ int eb_add_member(eb_engine* e, int kind, int logits_tensor, int k_off, int k) {
   const Tensor& t = e->tensors[logits_tensor];
   if (kind == EB_MEMBER_CNN) {
     if (t.dtype != EB_F32) EB_FAIL(EB_E_INVALID, "CNN logits must be fp32");
+    if (e->C > 8) EB_FAIL(EB_E_INVALID, "CNN members need at most 8 input channels");
     if (e->l32_tensor >= 0 && e->l32_tensor != logits_tensor)
       EB_FAIL(EB_E_INVALID, "all CNN members must share one logits tensor");
     e->l32_tensor = logits_tensor;
@@ -666,15 +674,13 @@ int eb_finalize(eb_engine* e) {
   for (const auto& op : e->ops) used[op.stream] = true;
   for (int l = 0; l < kLanes; ++l)
     if (used[l] && e->any_cnn) EB_CUDA(cudaMalloc(&e->ws[l], kSplitWsFloats * sizeof(float)));
-  // LIN1 d-slices: a function of D and the member set only (never of the batch).
+  // LIN1 d-slices: a function of D only (never of the batch); models.lin1_splits.
   int64_t lin_k = 0;
   for (const auto& op : e->ops)
     if (op.kind == EB_OP_LIN1) lin_k = std::max<int64_t>(lin_k, op.cout);
   if (lin_k > 0) {
     const int64_t D = static_cast<int64_t>(e->C) * e->H * e->W;
-    int64_t ns = std::max<int64_t>(1, std::min<int64_t>(148, D / 1024));
-    const int64_t cap = (static_cast<int64_t>(256) << 20) / (static_cast<int64_t>(mb) * lin_k * 8);
-    ns = std::max<int64_t>(1, std::min(ns, cap));
+    const int64_t ns = std::max<int64_t>(1, std::min<int64_t>(148, D / 1024));
     e->lin_nsplit = static_cast<int>(ns);
     EB_CUDA(cudaMalloc(&e->lin_part, static_cast<size_t>(ns) * mb * lin_k * sizeof(double)));
   }

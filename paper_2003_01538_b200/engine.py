@@ -1,0 +1,200 @@
+"""Python owner of one native engine (include/ensemble_b200.h).
+
+An Engine is built once per loaded ensemble: tensors and ops are declared by the
+member lowerings (zoo.py for CNN members, ensemble.py for LIN1 members), weights
+are collected into one host staging area and written into the single device
+pool at finalize(), and forward() is one native call with host buffers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_int, c_uint64, c_void_p
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import OpDesc, check
+
+_ALIGN = 256
+
+
+def _host_bytes(arr) -> np.ndarray:
+    if isinstance(arr, torch.Tensor):
+        t = arr.detach().cpu().contiguous()
+        if t.dtype == torch.bfloat16:
+            return t.view(torch.int16).numpy().view(np.uint8).reshape(-1)
+        return t.numpy().view(np.uint8).reshape(-1)
+    a = np.ascontiguousarray(arr)
+    return a.view(np.uint8).reshape(-1)
+
+
+class TRef:
+    """A channel slice of an engine tensor: (id, channel offset, channels, h, w)."""
+
+    __slots__ = ("id", "c_off", "c", "h", "w", "ctot")
+
+    def __init__(self, tid, c_off, c, h, w, ctot):
+        self.id, self.c_off, self.c, self.h, self.w, self.ctot = tid, c_off, c, h, w, ctot
+
+    def slice(self, c_off, c):
+        return TRef(self.id, self.c_off + c_off, c, self.h, self.w, self.ctot)
+
+    def __repr__(self):
+        return f"TRef(id={self.id}, c=[{self.c_off},{self.c_off + self.c}) of {self.ctot}, {self.h}x{self.w})"
+
+
+class Engine:
+    def __init__(self, in_shape, max_batch: int, device: int = 0):
+        self.lib = _lib.load()
+        c, h, w = in_shape
+        self.C, self.H, self.W = c, h, w
+        self.max_batch = max_batch
+        self.device = device
+        self._h = c_void_p()
+        check(self.lib.eb_engine_create(device, max_batch, c, h, w, byref(self._h)))
+        self._blobs: list[tuple[int, np.ndarray]] = []
+        self._pool_size = 0
+        self.members: list[tuple[int, int, int, int]] = []
+        self.n_ops = 0
+        self.finalized = False
+        self.image = TRef(_lib.EB_T_IMAGE_NHWC8, 0, 8, h, w, 8)
+        self.image_f32 = TRef(_lib.EB_T_IMAGE_F32, 0, c, h, w, c)
+
+    # ------------------------------------------------------------ declaration
+    def set_preprocess(self, mean, std, lut: np.ndarray):
+        m = np.ascontiguousarray(np.asarray(mean, dtype=np.float32))
+        s = np.ascontiguousarray(np.asarray(std, dtype=np.float32))
+        lut = np.ascontiguousarray(lut, dtype=np.float32)
+        check(self.lib.eb_set_preprocess(self._h, m.ctypes.data, s.ctypes.data, m.size,
+                                         lut.ctypes.data))
+
+    def weight(self, arr) -> int:
+        """Stage a weight blob for the pool; returns its byte offset."""
+        b = _host_bytes(arr)
+        off = self._pool_size
+        self._blobs.append((off, b))
+        self._pool_size = (off + b.size + _ALIGN - 1) // _ALIGN * _ALIGN
+        return off
+
+    def tensor(self, h, w, c, dtype=_lib.EB_BF16) -> TRef:
+        tid = c_int()
+        check(self.lib.eb_tensor(self._h, h, w, c, dtype, byref(tid)))
+        return TRef(tid.value, 0, c, h, w, c)
+
+    def op(self, kind, src: TRef, dst: TRef, *, cout=0, res: TRef | None = None, kh=1, kw=1,
+           sh=1, sw=1, ph=0, pw=0, relu=0, pool_mode=0, flatten=0, lane=0, w_off=None,
+           b_off=None, scale_off=None, shift_off=None):
+        d = OpDesc()
+        d.kind = kind
+        d.src, d.dst = src.id, dst.id
+        d.res = res.id if res is not None else -1
+        d.src_c_off, d.src_c = src.c_off, src.c
+        d.dst_c_off, d.cout = dst.c_off, cout
+        d.kh, d.kw, d.sh, d.sw, d.ph, d.pw = kh, kw, sh, sw, ph, pw
+        d.relu, d.pool_mode, d.flatten, d.stream = int(relu), pool_mode, int(flatten), lane
+        none = _lib.EB_NO_OFFSET
+        d.w_off = none if w_off is None else w_off
+        d.b_off = none if b_off is None else b_off
+        d.scale_off = none if scale_off is None else scale_off
+        d.shift_off = none if shift_off is None else shift_off
+        check(self.lib.eb_add_op(self._h, byref(d)))
+        self.n_ops += 1
+
+    def member(self, kind, logits: TRef, k_off: int, k: int):
+        check(self.lib.eb_add_member(self._h, kind, logits.id, k_off, k))
+        self.members.append((kind, logits.id, k_off, k))
+
+    def finalize(self):
+        check(self.lib.eb_pool_reserve(self._h, max(self._pool_size, _ALIGN)))
+        for off, b in self._blobs:
+            check(self.lib.eb_pool_write(self._h, off, b.ctypes.data, b.size))
+        self._blobs = []
+        check(self.lib.eb_finalize(self._h))
+        self.finalized = True
+
+    @property
+    def pool_bytes(self) -> int:
+        v = c_uint64()
+        check(self.lib.eb_pool_bytes(self._h, byref(v)))
+        return v.value
+
+    # ------------------------------------------------------------ execution
+    def forward(self, x: np.ndarray, input_kind: int, *, topk: int = 0, policy: int = 0,
+                policy_k: int = 0, want_logits: bool = False):
+        """One native eb_forward call.  x: (B, C*H*W) f32 or (B, H, W, C) u8, host."""
+        b = int(x.shape[0])
+        x = np.ascontiguousarray(x)
+        n = len(self.members)
+        labels = np.empty((n, b), dtype=np.int32)
+        kmax = max(m[3] for m in self.members)
+        logits = np.zeros((n, b, kmax), dtype=np.float32) if want_logits else None
+        tk_i = np.empty((n, b, max(topk, 1)), dtype=np.int32)
+        tk_p = np.empty((n, b, max(topk, 1)), dtype=np.float32)
+        comb = np.empty(max(b, 1), dtype=np.int32)
+        check(self.lib.eb_forward(
+            self._h, x.ctypes.data, input_kind, b, labels.ctypes.data,
+            logits.ctypes.data if logits is not None else None, topk,
+            tk_i.ctypes.data, tk_p.ctypes.data, policy, policy_k, comb.ctypes.data))
+        out = {"labels": labels}
+        if logits is not None:
+            out["logits"] = logits
+        if topk:
+            out["topk_idx"] = tk_i[:, :, :topk]
+            out["topk_prob"] = tk_p[:, :, :topk]
+        if policy:
+            out["combined"] = comb[:b]
+        return out
+
+    def forward_device(self, batch: int, input_kind: int, topk: int = 0, policy: int = 0,
+                       policy_k: int = 0):
+        check(self.lib.eb_forward_device(self._h, input_kind, batch, topk, policy, policy_k))
+
+    def input_buffer(self, input_kind: int) -> int:
+        p = c_void_p()
+        check(self.lib.eb_input_buffer(self._h, input_kind, byref(p)))
+        return p.value
+
+    def stream(self) -> int:
+        p = c_void_p()
+        check(self.lib.eb_engine_stream(self._h, byref(p)))
+        return p.value
+
+    def launch_count(self, input_kind: int, batch: int) -> int:
+        v = c_int()
+        check(self.lib.eb_launch_count(self._h, input_kind, batch, byref(v)))
+        return v.value
+
+    def tensor_view(self, t: TRef, batch: int) -> torch.Tensor:
+        """A torch view of an engine tensor (debugging / parity of intermediates)."""
+        p = c_void_p()
+        h, w, c, dt = c_int(), c_int(), c_int(), c_int()
+        check(self.lib.eb_tensor_ptr(self._h, t.id, byref(p), byref(h), byref(w), byref(c), byref(dt)))
+        dtype = {0: torch.bfloat16, 1: torch.float32, 2: torch.float64}[dt.value]
+        numel = batch * h.value * w.value * c.value
+        t_ = _wrap_device_ptr(p.value, numel, dtype, self.device)
+        return t_.view(batch, h.value, w.value, c.value)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self.lib.eb_engine_destroy(self._h)
+            self._h = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _wrap_device_ptr(ptr: int, numel: int, dtype, device: int) -> torch.Tensor:
+    """Zero-copy torch view of engine-owned device memory."""
+    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.float64: "<f8"}[dtype]
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": typestr, "data": (ptr, False),
+                                    "version": 3}
+
+    t = torch.as_tensor(_Arr(), device=f"cuda:{device}")
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t

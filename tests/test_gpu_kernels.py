@@ -33,7 +33,7 @@ def run_conv(x_nhwc, ldx, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw, *, y_
     wp = pack_conv_weight(w, mode).to(DEV)
     ld = y_ld or cout
     y = torch.zeros(B, Ho, Wo, ld, device=DEV, dtype=torch.float32 if out_f32 else torch.bfloat16)
-    ws = torch.empty(148 * 128 * 256, device=DEV, dtype=torch.float32)
+    ws = torch.empty(2 * 148 * 128 * 256, device=DEV, dtype=torch.float32)
     b = bias.to(DEV) if bias is not None else None
     _lib.check(lib.eb_k_conv(
         _p(x_nhwc), B, H, W, ldx, cin, _p(wp), _p(b), _p(res), res.shape[-1] if res is not None else 0,
