@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark of the ensemble forward path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "C2"): the 3-member ensemble ResNet-50 +
+DenseNet-121 + VGG-16 (cnn1 members, seeded random init, bf16 tcgen05 path), one
+step = one forward + combine of a batch of B = 256 synthetic 224x224 RGB u8
+images per GPU (the top of the config's 1-256 range).  Under torchrun each rank
+owns a full replica, evaluates its own 256-image shard and the logits are
+gathered to rank 0 with NCCL inside the timed step (weak scaling).
+
+Reported on one JSON line (rank 0):
+  value      device-timed images/s, inputs resident in HBM (CUDA events on the
+             engine stream, L2 flushed between steps, max over ranks)
+  e2e        the same metric through the public C-ABI call eb_forward with
+             pinned host input, H2D + forward + D2H of labels inside the timing
+  roofline   the tcgen05 conv/GEMM kernel class: algorithmic FLOPs of every conv
+             launch / its CUDA-event time (serialised per-op profile)
+  cpu_baseline  the oracle (torchvision fp32 eager on all host cores) on a
+             bounded sample of the same workload
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+MEMBERS = [("resnet50", 3), ("densenet121", 2), ("vgg16", 4)]
+GFLOP_PER_IMG = 44.787  # SURVEY.md §2.4 (conv + linear, 2*MAC, torchvision flop counter)
+MEAN = (0.485, 0.456, 0.406)
+STD = (0.229, 0.224, 0.225)
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks() -> tuple[dict, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return dict(PEAKS_FALLBACK), "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cnn_docs():
+    return [{"format": "cnn1", "id": f"{a}", "arch": a, "seed": s, "input_shape": [3, 224, 224],
+             "labels": 1000} for a, s in MEMBERS]
+
+
+def build_ensemble(batch: int, device: int):
+    from paper_2003_01538_b200 import ensemble as E
+
+    td = Path(tempfile.mkdtemp(prefix="bench_"))
+    entries = []
+    for doc in cnn_docs():
+        (td / f"{doc['id']}.json").write_text(json.dumps(doc))
+        entries.append({"id": doc["id"], "path": f"{doc['id']}.json"})
+    man = {"memory_budget_bytes": 1 << 40, "max_batch": batch,
+           "preprocess": {"mean": list(MEAN), "std": list(STD), "pixel_scale": 255.0},
+           "models": entries}
+    (td / "manifest.json").write_text(json.dumps(man))
+    return E.load_ensemble(E.load_manifest_file(td / "manifest.json"), device=device)
+
+
+def cpu_oracle_rate(n_images: int, seconds_cap: float = 30.0) -> dict:
+    """torchvision fp32 eager on all host cores, the same members and inputs."""
+    import torch
+
+    from oracle import cnn as OC
+    from paper_2003_01538_b200 import synth
+    from paper_2003_01538_b200.zoo import build_torch_model
+
+    cores = OC.set_threads()
+    models = [build_torch_model(a, s) for a, s in MEMBERS]
+    px = synth.images_fast(n_images, 224, 224, 3, seed0=4321)
+    x = OC.preprocess_u8(px, MEAN, STD, 255.0)
+    with torch.no_grad():
+        for m in models:  # warm-up on one image
+            m(x[:1])
+        t0 = time.perf_counter()
+        done = 0
+        for i in range(n_images):
+            for m in models:
+                m(x[i:i + 1])
+            done += 1
+            if time.perf_counter() - t0 > seconds_cap:
+                break
+        dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "images/s", "cores": cores, "kind": "port",
+            "sample": f"{done} image(s) x {len(MEMBERS)} members, torchvision fp32 eager, batch 1"}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    from oracle import cnn as OC
+    from paper_2003_01538_b200 import synth
+    from paper_2003_01538_b200.zoo import build_torch_model
+
+    cores = OC.set_threads()
+    per_step = args.ref_sample
+    models = [build_torch_model(a, s) for a, s in MEMBERS]
+    px = synth.images_fast(per_step, 224, 224, 3, seed0=4321)
+    times = []
+    with torch.no_grad():
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            x = OC.preprocess_u8(px, MEAN, STD, 255.0)
+            logits = np.stack([m(x).numpy() for m in models])
+            _ = np.argmax(logits, axis=-1)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+    total = sum(times)
+    value = per_step * len(times) / total
+    line = {
+        "impl": "reference", "metric": "ensemble images/s (N-model fwd+combine)", "value": value,
+        "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2 ensemble resnet50+densenet121+vgg16, 224x224 RGB u8, "
+                               f"{per_step} images per step (bounded CPU sample)",
+                   "members": [f"{a}:seed{s}" for a, s in MEMBERS]},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": f"{per_step} images per step through torchvision fp32 eager "
+                                   "(oracle port of the path; the reference has no CNN code)"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--ref-sample", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also time B in {1,8,32,64,128}")
+    ap.add_argument("--profile-json", default="", help="write the per-op profile here")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2003_01538_b200 import _lib, synth
+    from paper_2003_01538_b200.ensemble import engine_for
+    from paper_2003_01538_b200.shard import gather_rows
+
+    B = args.batch
+    ens = build_ensemble(B, local)
+    eng = engine_for(ens)
+    stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", local))
+    kind = _lib.EB_IN_U8_HWC
+
+    host = torch.from_numpy(synth.images_fast(B, 224, 224, 3, seed0=1234 + rank * B)).pin_memory()
+    dev_in = eng.input_buffer(kind)
+    torch.cuda.synchronize()
+    # resident input: one copy into the engine's staging buffer
+    from paper_2003_01538_b200.engine import _wrap_device_ptr
+
+    staging = _wrap_device_ptr(dev_in, B * 224 * 224 * 3, torch.uint8, local)
+    staging.copy_(host.view(-1).cuda())
+    logits_t = None
+    if world > 1:
+        from paper_2003_01538_b200.engine import TRef
+
+        lt = eng.members[0][1]
+        kpad = max(m[2] + m[3] for m in eng.members)
+        logits_t = eng.tensor_view(TRef(lt, 0, kpad, 1, 1, kpad), B).view(B, -1)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        eng.forward_device(B, kind)
+        if world > 1:  # logits of every shard to the serving rank, on the engine stream
+            with torch.cuda.stream(stream):
+                gather_rows(logits_t, B * world, dst=0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    n_launch = eng.launch_count(kind, B)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush (256 MiB > 126 MB L2), outside the events
+                ev[i][0].record(stream)
+            step()
+            with torch.cuda.stream(stream):
+                ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([dev_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        dist.barrier()
+    value = B * world * args.steps / (dev_ms / 1e3)
+
+    # ---- e2e: the public C-ABI call with pinned host buffers
+    host_np = host.numpy()
+    for _ in range(2):
+        eng.forward(host_np, kind)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        eng.forward(host_np, kind)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = B * world * args.steps / e2e_s
+    n_members = len(eng.members)
+
+    # ---- p50 latency at bs=1 (e2e through eb_forward) and optional batch sweep
+    one = host_np[:1].copy()
+    for _ in range(3):
+        eng.forward(one, kind)
+    lat = []
+    for _ in range(30):
+        t0 = time.perf_counter()
+        eng.forward(one, kind)
+        lat.append((time.perf_counter() - t0) * 1e3)
+    sweep = {}
+    if args.sweep:
+        for b in (1, 8, 32, 64, 128):
+            for _ in range(3):
+                eng.forward_device(b, kind)
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                s0.record(stream)
+            for _ in range(10):
+                eng.forward_device(b, kind)
+            with torch.cuda.stream(stream):
+                s1.record(stream)
+            torch.cuda.synchronize()
+            sweep[str(b)] = b * 10 / (s0.elapsed_time(s1) / 1e3)
+
+    # ---- roofline of the tcgen05 conv/GEMM kernel class (serialised per-op profile)
+    ms = eng.profile(B, kind)
+    conv_ms = conv_flops = 0.0
+    top = None
+    for m, t in zip(eng.op_meta, ms):
+        if m.get("name") == "conv":
+            conv_ms += float(t)
+            conv_flops += m["flops"] * B
+            if top is None or t > top[1]:
+                top = (m, float(t))
+    pk, pk_src = peaks()
+    achieved = conv_flops / (conv_ms / 1e3) / 1e12
+    peak = pk["bf16_tflops_sustained"]
+    if args.profile_json and rank == 0:
+        Path(args.profile_json).write_text(json.dumps(
+            [{"i": i, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in m.items()}, "ms": float(t)}
+             for i, (m, t) in enumerate(zip(eng.op_meta, ms))], indent=0))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_oracle_rate(12, seconds_cap=25.0)
+        except Exception as exc:  # the baseline is reported, never fatal
+            cpu = {"error": str(exc)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": "ensemble images/s (N-model fwd+combine)",
+            "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {
+                "workload": "C2 (BASELINE configs[1]): resnet50+densenet121+vgg16 cnn1 members, "
+                            f"{B} synthetic 224x224 RGB u8 images per GPU per step",
+                "batch_per_gpu": B, "global_batch": B * world, "members": [f"{a}:seed{s}" for a, s in MEMBERS],
+                "parallelism": f"replica x{world}, batch-sharded, NCCL logits gather to rank 0" if world > 1 else "single GPU",
+                "l2": "flushed between timed steps (256 MiB write), outside the events",
+            },
+            "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(host.numel()),
+                    "d2h_bytes_per_step": int(4 * n_members * B),
+                    "path": "eb_forward (C-ABI) with pinned host u8 input, labels read back"},
+            "latency_bs1_ms": {"p50": statistics.median(lat), "p99": sorted(lat)[int(0.99 * (len(lat) - 1))],
+                               "path": "eb_forward, B=1, host buffers"},
+            "gpu_launches": int(n_launch * args.steps),
+            "roofline": {"bound": "tensor", "kernel": "conv_umma_kernel (all conv/FC launches)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": f"{pk_src} bf16_tflops_sustained",
+                         "flops_per_step": conv_flops, "kernel_ms_per_step_serialised": conv_ms,
+                         "step_frac_of_peak": GFLOP_PER_IMG * 1e9 * B * world / (dev_ms / args.steps / 1e3) / 1e12 / peak / world,
+                         "top_launch": {"shape(ho,wo,cout,kh,kw,s,cin)": list(top[0]["shape"]), "ms": top[1]} if top else None},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        if sweep:
+            line["batch_sweep_images_per_s"] = sweep
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

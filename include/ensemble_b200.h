@@ -143,6 +143,10 @@ int eb_input_buffer(eb_engine* e, int input_kind, void** dev_ptr);
 int eb_output_labels(eb_engine* e, int32_t** dev_labels);
 int eb_tensor_ptr(eb_engine* e, int id, void** dev_ptr, int* h, int* w, int* c, int* dtype);
 int eb_engine_stream(eb_engine* e, void** stream);
+/* Per-op device time (ms) of one eager, fully serialised run of the layers
+ * (CUDA events around every op on one stream); host_ms holds one float per op
+ * in eb_add_op order.  Used for the roofline of each kernel class. */
+int eb_profile_ops(eb_engine* e, int input_kind, int batch, float* host_ms, int n_ops);
 /* Number of kernels one eb_forward_device launches for this batch size. */
 int eb_launch_count(eb_engine* e, int input_kind, int batch, int* count);
 

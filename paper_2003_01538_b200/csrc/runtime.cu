@@ -253,6 +253,8 @@ struct eb_engine {
   std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
   std::map<std::pair<int, int>, int> launch_counts;
   std::mutex mu;
+  // profiling: when set, every op runs on the main stream bracketed by events
+  std::vector<cudaEvent_t>* prof = nullptr;
 };
 
 namespace {
@@ -296,7 +298,13 @@ int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
     return off == EB_NO_OFFSET ? nullptr : static_cast<const void*>(pool + off);
   };
   for (const auto& op : e->ops) {
-    cudaStream_t ls = op.stream == 0 ? s : e->lanes[op.stream];
+    cudaStream_t ls = (op.stream == 0 || e->prof) ? s : e->lanes[op.stream];
+    if (e->prof) {
+      cudaEvent_t ev;
+      EB_CUDA(cudaEventCreate(&ev));
+      e->prof->push_back(ev);
+      EB_CUDA(cudaEventRecord(ev, s));
+    }
     Tensor& src = e->tensors[op.src];
     Tensor& dst = e->tensors[op.dst];
     const size_t es = dsize(src.dtype);
@@ -376,6 +384,12 @@ int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
       default:
         EB_FAIL(EB_E_INVALID, "unknown op kind");
     }
+  }
+  if (e->prof) {
+    cudaEvent_t ev;
+    EB_CUDA(cudaEventCreate(&ev));
+    e->prof->push_back(ev);
+    EB_CUDA(cudaEventRecord(ev, s));
   }
   for (int l = 1; l < kLanes; ++l) {
     if (!used[l]) continue;
@@ -774,6 +788,31 @@ int eb_forward(eb_engine* e, const void* host_input, int input_kind, int batch,
   }
   EB_CUDA(cudaStreamSynchronize(e->stream));
   return EB_OK;
+}
+
+int eb_profile_ops(eb_engine* e, int input_kind, int batch, float* host_ms, int n_ops) {
+  int rc = check_batch(e, batch);
+  if (rc != EB_OK) return rc;
+  if (!host_ms || n_ops != static_cast<int>(e->ops.size()))
+    EB_FAIL(EB_E_INVALID, "host_ms must hold one float per op");
+  std::lock_guard<std::mutex> lock(e->mu);
+  cudaSetDevice(e->device);
+  std::vector<cudaEvent_t> evs;
+  e->prof = &evs;
+  int launches = 0;
+  rc = enqueue_layers(e, input_kind, batch, &launches);
+  e->prof = nullptr;
+  cudaError_t ce = cudaStreamSynchronize(e->stream);
+  if (rc == EB_OK && ce != cudaSuccess) {
+    set_error(std::string("profile run: ") + cudaGetErrorString(ce));
+    rc = EB_E_CUDA;
+  }
+  if (rc == EB_OK) {
+    for (int i = 0; i < n_ops && i + 1 < static_cast<int>(evs.size()); ++i)
+      cudaEventElapsedTime(&host_ms[i], evs[i], evs[i + 1]);
+  }
+  for (auto ev : evs) cudaEventDestroy(ev);
+  return rc;
 }
 
 int eb_input_buffer(eb_engine* e, int input_kind, void** dev_ptr) {

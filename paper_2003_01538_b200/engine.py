@@ -58,6 +58,7 @@ class Engine:
         self._pool_size = 0
         self.members: list[tuple[int, int, int, int]] = []
         self.n_ops = 0
+        self.op_meta: list[dict] = []
         self.finalized = False
         self.image = TRef(_lib.EB_T_IMAGE_NHWC8, 0, 8, h, w, 8)
         self.image_f32 = TRef(_lib.EB_T_IMAGE_F32, 0, c, h, w, c)
@@ -85,7 +86,7 @@ class Engine:
 
     def op(self, kind, src: TRef, dst: TRef, *, cout=0, res: TRef | None = None, kh=1, kw=1,
            sh=1, sw=1, ph=0, pw=0, relu=0, pool_mode=0, flatten=0, lane=0, w_off=None,
-           b_off=None, scale_off=None, shift_off=None):
+           b_off=None, scale_off=None, shift_off=None, meta: dict | None = None):
         d = OpDesc()
         d.kind = kind
         d.src, d.dst = src.id, dst.id
@@ -101,6 +102,7 @@ class Engine:
         d.shift_off = none if shift_off is None else shift_off
         check(self.lib.eb_add_op(self._h, byref(d)))
         self.n_ops += 1
+        self.op_meta.append(dict(meta or {}, kind=kind, lane=lane))
 
     def member(self, kind, logits: TRef, k_off: int, k: int):
         check(self.lib.eb_add_member(self._h, kind, logits.id, k_off, k))
@@ -161,6 +163,12 @@ class Engine:
         check(self.lib.eb_engine_stream(self._h, byref(p)))
         return p.value
 
+    def profile(self, batch: int, input_kind: int) -> np.ndarray:
+        """Per-op device ms of one serialised eager run (eb_profile_ops)."""
+        ms = np.zeros(self.n_ops, dtype=np.float32)
+        check(self.lib.eb_profile_ops(self._h, input_kind, batch, ms.ctypes.data, self.n_ops))
+        return ms
+
     def launch_count(self, input_kind: int, batch: int) -> int:
         v = c_int()
         check(self.lib.eb_launch_count(self._h, input_kind, batch, byref(v)))
@@ -190,7 +198,8 @@ class Engine:
 
 def _wrap_device_ptr(ptr: int, numel: int, dtype, device: int) -> torch.Tensor:
     """Zero-copy torch view of engine-owned device memory."""
-    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.float64: "<f8"}[dtype]
+    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.float64: "<f8",
+               torch.uint8: "|u1"}[dtype]
 
     class _Arr:
         __cuda_array_interface__ = {"shape": (numel,), "typestr": typestr, "data": (ptr, False),

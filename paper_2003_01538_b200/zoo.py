@@ -119,8 +119,12 @@ class Lowering:
             out = eng.tensor(ho, wo, cout)
         w_off = eng.weight(wp)
         b_off = eng.weight(b.contiguous()) if b is not None else None
+        k_alg = w.shape[1] if w.dim() == 2 else w.shape[1] * w.shape[2] * w.shape[3]
+        meta = {"name": "conv", "flops": 2 * ho * wo * cout * k_alg,
+                "shape": (ho, wo, cout, kh, kw, sh, x.c), "weight_bytes": 2 * cout * k_alg}
         eng.op(_lib.EB_OP_CONV, x, out, cout=cout, res=res, kh=kh, kw=kw, sh=sh, sw=sw, ph=ph,
-               pw=pw, relu=relu, flatten=flatten, lane=self.lane, w_off=w_off, b_off=b_off)
+               pw=pw, relu=relu, flatten=flatten, lane=self.lane, w_off=w_off, b_off=b_off,
+               meta=meta)
         return out
 
     def pool(self, x: TRef, k, s, p, mode, out: TRef | None = None, bn=None) -> TRef:
