@@ -12,12 +12,16 @@
 // kernel) uses 16-byte im2col columns in the non-swizzled canonical layout, one
 // TMA per tap, eight taps per 64-wide K block.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA
-// issuer (one elected lane), warps 2..5 = epilogue (TMEM -> registers ->
-// bias / residual / ReLU -> bf16 NHWC store, or fp32 logits / split-K partial slices).
-// The epilogue writes into a channel slice of a wider NHWC buffer, which is how
-// DenseNet concatenation and Inception branch concatenation are realised
-// without a copy.
+// Persistent, warp-specialised (192 threads, one CTA per SM):
+//   warp 0      TMA producer: a smem ring of (A, B) stages that runs across tiles
+//   warp 1      TMEM owner + MMA issuer (one elected lane); two accumulator
+//               buffers in TMEM so tile i+1's MMAs overlap tile i's epilogue
+//   warps 2..5  epilogue: TMEM -> registers -> bias / residual / ReLU -> bf16 ->
+//               128B-swizzled smem staging -> TMA bulk store (coalesced), or
+//               direct fp32 stores for logits and split-K partial slices.
+// The output map addresses a channel slice of a wider NHWC buffer, which is how
+// DenseNet / Inception concatenation is realised without a copy; TMA clips the
+// stores at the slice's N and at M.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -40,14 +44,24 @@ struct ConvSmem {
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
-  static constexpr int kBarOffset = kStages * kStageBytes;
+  static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
+  static constexpr int kStageOutBytes = 32 * kCW * 2;         // one warp's 32-row chunk
+  static constexpr int kOutOffset = kStages * kStageBytes;
+  static constexpr int kBarOffset = kOutOffset + 4 * 2 * kStageOutBytes;
   static constexpr int kBytes = kBarOffset + 256 + 1024;  // barriers + alignment slack
 };
+
+__device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
+  // TMA SWIZZLE_128B (128 B rows): 16 B chunk ^= row % 8
+  // TMA SWIZZLE_64B  (64 B rows):  16 B chunk ^= (row / 2) % 4
+  return cw == 64 ? (chunk ^ (row & 7)) : (chunk ^ ((row >> 1) & 3));
+}
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_umma_kernel(const __grid_constant__ CUtensorMap map_a,
-                     const __grid_constant__ CUtensorMap map_b, const ConvParams p) {
+                     const __grid_constant__ CUtensorMap map_b,
+                     const __grid_constant__ CUtensorMap map_out, const ConvParams p) {
   using S = ConvSmem<BN>;
   extern __shared__ uint8_t smem_raw[];
   // 128B swizzle needs 1024-byte aligned tiles
@@ -55,28 +69,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
   uint64_t* empty = full + S::kStages;
-  uint64_t* accum_full = empty + S::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
+  uint64_t* tfull = empty + S::kStages;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id();
-  const int tile_m = blockIdx.x;
-  const int tile_n = blockIdx.y;
-  const int kb_begin = blockIdx.z * p.kb_per_split;
-  int kb_end = kb_begin + p.kb_per_split;
-  if (kb_end > p.num_kb) kb_end = p.num_kb;
-  const int nkb = kb_end - kb_begin;
+  const int mt = (p.M + kBlockM - 1) / kBlockM;
+  const int nt = (p.N + BN - 1) / BN;
+  const int splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+  const int total = mt * nt * splits;
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
+    if (p.out_mode == kOutBF16) tma_prefetch_desc(&map_out);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, BN < 32 ? 32 : BN);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -85,50 +102,57 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (elect_one()) {
-      const int m0 = tile_m * kBlockM;
-      int img = 0, oh = 0, ow = 0;
-      if (p.a_mode != kAModeTiled) {
-        const int hw = p.Ho * p.Wo;
-        img = m0 / hw;
-        const int rem = m0 - img * hw;
-        oh = rem / p.Wo;
-        ow = rem - oh * p.Wo;
-      }
-      const int base_w = ow * p.sw - p.pw;
-      const int base_h = oh * p.sh - p.ph;
-      const int n0 = tile_n * BN;
       int stage = 0;
       uint32_t phase = 0;
-      for (int i = 0; i < nkb; ++i) {
-        const int kb = kb_begin + i;
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * S::kStageBytes;
-        uint8_t* sb = sa + kABytes;
-        mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
-        if (p.a_mode == kAModeTiled) {
-          tma_load_2d(sa, &map_a, &full[stage], kb * kBlockK, m0);
-        } else if (p.a_mode == kAModeIm2col) {
-          const int tap = kb / p.cchunks;
-          const int cc = kb - tap * p.cchunks;
-          const int r = tap / p.kw;
-          const int s = tap - r * p.kw;
-          tma_load_im2col_4d(sa, &map_a, &full[stage], cc * kBlockK, base_w, base_h, img,
-                             static_cast<uint16_t>(s), static_cast<uint16_t>(r));
-        } else {  // kAModeIm2colC8: eight 8-channel taps per K block
-#pragma unroll 1
-          for (int j = 0; j < 8; ++j) {
-            int tap = kb * 8 + j;
-            if (tap >= p.taps) tap = 0;  // weights are zero there; any finite data works
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int tile_n = t % nt;
+        const int rest = t / nt;
+        const int tile_m = rest % mt;
+        const int z = rest / mt;
+        const int kb0 = z * p.kb_per_split;
+        const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
+        const int m0 = tile_m * kBlockM;
+        int img = 0, oh = 0, ow = 0;
+        if (p.a_mode != kAModeTiled) {
+          const int hw = p.Ho * p.Wo;
+          img = m0 / hw;
+          const int rem = m0 - img * hw;
+          oh = rem / p.Wo;
+          ow = rem - oh * p.Wo;
+        }
+        const int base_w = ow * p.sw - p.pw;
+        const int base_h = oh * p.sh - p.ph;
+        const int n0 = tile_n * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+          if (p.a_mode == kAModeTiled) {
+            tma_load_2d(sa, &map_a, &full[stage], kb * kBlockK, m0);
+          } else if (p.a_mode == kAModeIm2col) {
+            const int tap = kb / p.cchunks;
+            const int cc = kb - tap * p.cchunks;
             const int r = tap / p.kw;
             const int s = tap - r * p.kw;
-            tma_load_im2col_4d(sa + j * (kBlockM * 16), &map_a, &full[stage], 0, base_w, base_h,
-                               img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            tma_load_im2col_4d(sa, &map_a, &full[stage], cc * kBlockK, base_w, base_h, img,
+                               static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+          } else {  // kAModeIm2colC8: eight 8-channel taps per K block
+#pragma unroll 1
+            for (int j = 0; j < 8; ++j) {
+              int tap = kb * 8 + j;
+              if (tap >= p.taps) tap = 0;  // weights are zero there; any finite data works
+              const int r = tap / p.kw;
+              const int s = tap - r * p.kw;
+              tma_load_im2col_4d(sa + j * (kBlockM * 16), &map_a, &full[stage], 0, base_w,
+                                 base_h, img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            }
           }
-        }
-        tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
-        if (++stage == S::kStages) {
-          stage = 0;
-          phase ^= 1;
+          tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -137,132 +161,160 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc = umma_idesc_bf16(kBlockM, BN);
     int stage = 0;
     uint32_t phase = 0;
-    for (int i = 0; i < nkb; ++i) {
-      mbar_wait(&full[stage], phase);
+    int j = 0;  // local tile counter
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      const int z = t / (nt * mt);
+      const int kb0 = z * p.kb_per_split;
+      const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
+      const int acc = j & 1;
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
-        const uint32_t sb = sa + kABytes;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
+          const uint32_t sb = sa + kABytes;
 #pragma unroll
-        for (int k = 0; k < kBlockK / 16; ++k) {
-          uint64_t adesc;
-          if (p.a_mode == kAModeIm2colC8) {
-            // two 8-channel tap columns per K=16 step; core matrices 128 B apart along M,
-            // 2 KiB apart along K
-            adesc = umma_desc(sa + k * 2 * (kBlockM * 16), kBlockM * 16, 128, 0);
-          } else {
-            adesc = umma_desc_sw128(sa + k * 32);
+          for (int k = 0; k < kBlockK / 16; ++k) {
+            uint64_t adesc;
+            if (p.a_mode == kAModeIm2colC8) {
+              // two 8-channel tap columns per K=16 step; core matrices 128 B apart along M,
+              // 2 KiB apart along K
+              adesc = umma_desc(sa + k * 2 * (kBlockM * 16), kBlockM * 16, 128, 0);
+            } else {
+              adesc = umma_desc_sw128(sa + k * 32);
+            }
+            const uint64_t bdesc = umma_desc_sw128(sb + k * 32);
+            umma_bf16(tmem_d, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          const uint64_t bdesc = umma_desc_sw128(sb + k * 32);
-          umma_bf16(tmem_base, adesc, bdesc, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (kb == kb1 - 1) umma_commit(&tfull[acc]);
         }
-        umma_commit(&empty[stage]);
-        if (i == nkb - 1) umma_commit(accum_full);
-      }
-      __syncwarp();
-      if (++stage == S::kStages) {
-        stage = 0;
-        phase ^= 1;
+        __syncwarp();
+        if (++stage == S::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = static_cast<int>(quarter * 32 + lane_id());
-    const int m = tile_m * kBlockM + row;
-    const bool row_ok = m < p.M;
-    mbar_wait(accum_full, 0);
-    tc_fence_after();
-    const int n_tile0 = tile_n * BN;
+    const int lane = static_cast<int>(lane_id());
+    const int row = static_cast<int>(quarter * 32) + lane;
+    uint8_t* stage_out = smem + S::kOutOffset + (warp - 2) * 2 * S::kStageOutBytes;
+    int obuf = 0;
+    int j = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
+      const int tile_n = t % nt;
+      const int rest = t / nt;
+      const int tile_m = rest % mt;
+      const int z = rest / mt;
+      const int acc = j & 1;
+      const int m = tile_m * kBlockM + row;
+      const bool row_ok = m < p.M;
+      const int n_tile0 = tile_n * BN;
+      mbar_wait(&tfull[acc], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * BN + ((quarter * 32) << 16);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      const int n = n_tile0 + c;
-      if (n >= p.N) break;  // warp-uniform
-      uint32_t r[16];
-      tmem_ld16(tmem_base + ((quarter * 32) << 16) + c, r);
-      tmem_ld_wait();
-      if (!row_ok) continue;
-      float v[16];
+      for (int c = 0; c < BN; c += S::kCW) {
+        const int n = n_tile0 + c;
+        if (n >= p.N) break;  // warp-uniform
+        uint32_t r[S::kCW];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-      const int nvalid = (p.N - n) < 16 ? (p.N - n) : 16;
-      const bool vec = p.vec_ok && nvalid == 16;
-      if (p.out_mode == kOutPartialF32) {
-        float* o = reinterpret_cast<float*>(p.out) +
-                   (static_cast<size_t>(blockIdx.z) * p.M + m) * p.ldo + n;
-        if (vec) {
+        for (int q = 0; q < S::kCW; q += 32) tmem_ld32(tbase + c + q, r + q);
+        tmem_ld_wait();
+        float v[S::kCW];
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        } else {
-          for (int j = 0; j < nvalid; ++j) o[j] = v[j];
-        }
-        continue;
-      }
-      if (p.bias) {
+        for (int i = 0; i < S::kCW; ++i) v[i] = __uint_as_float(r[i]);
+        const int nvalid = (p.N - n) < S::kCW ? (p.N - n) : S::kCW;
+        if (p.out_mode != kOutBF16) {
+          // fp32 logits or a split-K partial slice: direct stores (small outputs)
+          if (row_ok) {
+            float* o;
+            if (p.out_mode == kOutPartialF32) {
+              o = reinterpret_cast<float*>(p.out) + (static_cast<size_t>(z) * p.M + m) * p.ldo + n;
+            } else {
+              o = reinterpret_cast<float*>(p.out) + static_cast<size_t>(m) * p.ldo + p.out_off + n;
+              if (p.bias)
+                for (int i = 0; i < nvalid; ++i) v[i] += __ldg(p.bias + n + i);
+              if (p.relu)
+                for (int i = 0; i < nvalid; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
+            if (p.vec_ok && nvalid == S::kCW) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] += (j < nvalid) ? __ldg(p.bias + n + j) : 0.f;
-      }
-      if (p.res) {
-        const __nv_bfloat16* rp = p.res + static_cast<size_t>(m) * p.ldr + n;
-        if (vec) {
-          uint4 q0 = *reinterpret_cast<const uint4*>(rp);
-          uint4 q1 = *reinterpret_cast<const uint4*>(rp + 8);
-          const __nv_bfloat16* h0 = reinterpret_cast<const __nv_bfloat16*>(&q0);
-          const __nv_bfloat16* h1 = reinterpret_cast<const __nv_bfloat16*>(&q1);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            v[j] += __bfloat162float(h0[j]);
-            v[j + 8] += __bfloat162float(h1[j]);
+              for (int i = 0; i < S::kCW; i += 4)
+                *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            } else {
+              for (int i = 0; i < nvalid; ++i) o[i] = v[i];
+            }
           }
-        } else {
-          for (int j = 0; j < nvalid; ++j) v[j] += __bfloat162float(rp[j]);
+          continue;
         }
-      }
-      if (p.relu) {
+        if (p.bias) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
-      }
-      if (p.out_mode == kOutF32) {
-        float* o = reinterpret_cast<float*>(p.out) + static_cast<size_t>(m) * p.ldo + p.out_off + n;
-        if (vec) {
+          for (int i = 0; i < S::kCW; ++i) v[i] += (i < nvalid) ? __ldg(p.bias + n + i) : 0.f;
+        }
+        if (p.res && row_ok) {
+          const __nv_bfloat16* rp = p.res + static_cast<size_t>(m) * p.ldr + n;
+          if (nvalid == S::kCW && (p.ldr & 7) == 0) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        } else {
-          for (int j = 0; j < nvalid; ++j) o[j] = v[j];
+            for (int i = 0; i < S::kCW; i += 8) {
+              uint4 q = *reinterpret_cast<const uint4*>(rp + i);
+              const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[i + e] += __bfloat162float(h[e]);
+            }
+          } else {
+            for (int i = 0; i < nvalid; ++i) v[i] += __bfloat162float(rp[i]);
+          }
         }
-      } else {
-        __nv_bfloat16* o =
-            reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<size_t>(m) * p.ldo + p.out_off + n;
-        if (vec) {
-          uint4 q0, q1;
-          q0.x = pack_bf16x2(v[0], v[1]);
-          q0.y = pack_bf16x2(v[2], v[3]);
-          q0.z = pack_bf16x2(v[4], v[5]);
-          q0.w = pack_bf16x2(v[6], v[7]);
-          q1.x = pack_bf16x2(v[8], v[9]);
-          q1.y = pack_bf16x2(v[10], v[11]);
-          q1.z = pack_bf16x2(v[12], v[13]);
-          q1.w = pack_bf16x2(v[14], v[15]);
-          *reinterpret_cast<uint4*>(o) = q0;
-          *reinterpret_cast<uint4*>(o + 8) = q1;
-        } else {
-          for (int j = 0; j < nvalid; ++j) o[j] = __float2bfloat16_rn(v[j]);
+        if (p.relu) {
+#pragma unroll
+          for (int i = 0; i < S::kCW; ++i) v[i] = fmaxf(v[i], 0.f);
         }
+        // stage the warp's 32 x kCW chunk in swizzled smem, then one TMA store
+        uint8_t* buf = stage_out + obuf * S::kStageOutBytes;
+        if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
+        __syncwarp();
+        uint8_t* rowp = buf + lane * (S::kCW * 2);
+#pragma unroll
+        for (int ch = 0; ch < S::kCW / 8; ++ch) {
+          uint4 q;
+          q.x = pack_bf16x2(v[ch * 8 + 0], v[ch * 8 + 1]);
+          q.y = pack_bf16x2(v[ch * 8 + 2], v[ch * 8 + 3]);
+          q.z = pack_bf16x2(v[ch * 8 + 4], v[ch * 8 + 5]);
+          q.w = pack_bf16x2(v[ch * 8 + 6], v[ch * 8 + 7]);
+          *reinterpret_cast<uint4*>(rowp + swz_chunk(ch, lane, S::kCW) * 16) = q;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_out, buf, n, tile_m * kBlockM + static_cast<int>(quarter) * 32);
+          bulk_commit();
+        }
+        obuf ^= 1;
       }
+      // accumulator drained (all tcgen05.ld of this tile completed above)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, BN < 32 ? 32 : BN);
+  if (warp == 1) tmem_dealloc(tmem_base, 2 * BN < 32 ? 32 : 2 * BN);
 }
 
 // ---------------------------------------------------------------- host side
 
 template <int BN>
-static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const ConvParams& p,
-                             dim3 grid, cudaStream_t stream) {
+static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                             const ConvParams& p, int grid, cudaStream_t stream) {
   using S = ConvSmem<BN>;
   static bool configured = false;  // attribute is per-function; idempotent
   if (!configured) {
@@ -271,17 +323,19 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  conv_umma_kernel<BN><<<grid, kThreads, S::kBytes, stream>>>(ma, mb, p);
+  conv_umma_kernel<BN><<<grid, kThreads, S::kBytes, stream>>>(ma, mb, mo, p);
   return cudaGetLastError();
 }
 
-cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const ConvParams& p,
-                             int block_n, dim3 grid, cudaStream_t stream) {
+int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
+
+cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                             const ConvParams& p, int block_n, int grid, cudaStream_t stream) {
   switch (block_n) {
-    case 32: return launch_bn<32>(ma, mb, p, grid, stream);
-    case 64: return launch_bn<64>(ma, mb, p, grid, stream);
-    case 128: return launch_bn<128>(ma, mb, p, grid, stream);
-    case 256: return launch_bn<256>(ma, mb, p, grid, stream);
+    case 32: return launch_bn<32>(ma, mb, mo, p, grid, stream);
+    case 64: return launch_bn<64>(ma, mb, mo, p, grid, stream);
+    case 128: return launch_bn<128>(ma, mb, mo, p, grid, stream);
+    case 256: return launch_bn<256>(ma, mb, mo, p, grid, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -36,14 +36,15 @@ struct ConvParams {
   int vec_ok;  // 16-byte aligned rows/offsets: vector epilogue stores allowed
 };
 
-cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const ConvParams& p,
-                             int block_n, dim3 grid, cudaStream_t stream);
+cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                             const ConvParams& p, int block_n, int grid, cudaStream_t stream);
+int conv_umma_chunk(int block_n);
 
 // Driver entry point for tensor-map encoding (resolved through the runtime so the
 // library does not link libcuda directly).
 bool encode_tiled_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                           uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer,
-                          std::string* err);
+                          std::string* err, int swizzle_bytes = 128);
 bool encode_im2col_bf16(CUtensorMap* map, const void* base, int n, int h, int w, int c, int ldc,
                         int kh, int kw, int sh, int sw, int ph, int pw, int chans_per_pixel,
                         int pixels, bool swizzle128, std::string* err);

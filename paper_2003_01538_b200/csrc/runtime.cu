@@ -96,10 +96,21 @@ int64_t packed_k(int cin, int kh, int kw, bool c8, bool flatten, int H, int W) {
   return static_cast<int64_t>(kh) * kw * ((cin + 63) / 64) * 64;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
 struct ConvPlan {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mo;
   ConvParams p;
-  dim3 grid;
+  int grid;
   int block_n;
   int splits;
   size_t ws_floats;
@@ -187,7 +198,16 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.block_n = bn;
   pl.splits = splits;
   pl.ws_floats = splits > 1 ? static_cast<size_t>(splits) * M * a.cout : 0;
-  pl.grid = dim3(mt, nt, splits);
+  const int64_t total = static_cast<int64_t>(mt) * nt * splits;
+  pl.grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
+  if (!a.out_f32 && splits == 1) {
+    const int cw = conv_umma_chunk(bn);
+    if (!encode_tiled_2d_bf16(&pl.mo, static_cast<const __nv_bfloat16*>(a.y) + a.y_off, a.cout, M64,
+                              a.ldy, cw, 32, &err, cw * 2))
+      EB_FAIL(EB_E_INVALID, err);
+  } else {
+    pl.mo = pl.mb;  // unused: fp32 outputs are stored directly
+  }
   return EB_OK;
 }
 
@@ -203,12 +223,12 @@ int run_conv_plan(ConvPlan& pl, float* ws, size_t ws_cap, const ConvArgs& a, cud
     p.vec_ok = (a.cout % 4 == 0);
     p.bias = nullptr;
     p.relu = 0;
-    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, p, pl.block_n, pl.grid, s));
+    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.mo, p, pl.block_n, pl.grid, s));
     EB_CUDA(k_splitk_finalize(ws, pl.splits, pl.p.M, a.cout, a.bias, a.relu, a.y, a.ldy, a.y_off,
                               a.out_f32, s));
     if (launches) *launches += 2;
   } else {
-    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.p, pl.block_n, pl.grid, s));
+    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.mo, pl.p, pl.block_n, pl.grid, s));
     if (launches) *launches += 1;
   }
   return EB_OK;

@@ -49,15 +49,19 @@ static bool resolve(std::string* err) {
 
 bool encode_tiled_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                           uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer,
-                          std::string* err) {
+                          std::string* err, int swizzle_bytes) {
   if (!resolve(err)) return false;
+  const CUtensorMapSwizzle swz = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                 : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {ld_elems * 2};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_tiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     if (err)
@@ -93,8 +97,8 @@ bool encode_im2col_bf16(CUtensorMap* map, const void* base, int n, int h, int w,
     return false;
   }
   // Drivers up to 13.1 mis-handle an im2col descriptor flag for tensors under
-  // 128 KiB; clearing bit 21 of the second descriptor word is the documented
-  // workaround applied by CUTLASS's im2col TMA path as well.
+  // 128 KiB; clearing bit 21 of the second descriptor word is the same
+  // workaround CUTLASS's im2col TMA path applies.
   const uint64_t bytes = px * static_cast<uint64_t>(w) * h * n;
   if (g_driver_version <= 13010 && bytes < 131072) {
     reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
