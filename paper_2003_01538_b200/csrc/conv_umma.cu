@@ -41,14 +41,19 @@ constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KiB
 
 template <int BN>
 struct ConvSmem {
+  static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "tile width");
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kStages = (BN >= 256) ? 3 : (BN >= 128 ? 4 : (BN >= 64 ? 6 : 7));
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
   static constexpr int kStageOutBytes = 32 * kCW * 2;         // one warp's 32-row chunk
   static constexpr int kOutOffset = kStages * kStageBytes;
-  static constexpr int kBarOffset = kOutOffset + 4 * 2 * kStageOutBytes;
-  static constexpr int kBytes = kBarOffset + 256 + 1024;  // barriers + alignment slack
+  // per epilogue warp: 2 output staging buffers + 2 residual buffers
+  static constexpr int kResOffset = kOutOffset + 4 * 2 * kStageOutBytes;
+  static constexpr int kBiasOffset = kResOffset + 4 * 2 * kStageOutBytes;  // 4 x BN floats
+  static constexpr int kBarOffset = kBiasOffset + 4 * BN * 4;
+  static constexpr int kBytes = kBarOffset + 512 + 1024;  // barriers + alignment slack
+  static_assert(kBytes <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
 __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
@@ -61,7 +66,8 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_umma_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
-                     const __grid_constant__ CUtensorMap map_out, const ConvParams p) {
+                     const __grid_constant__ CUtensorMap map_out,
+                     const __grid_constant__ CUtensorMap map_res, const ConvParams p) {
   using S = ConvSmem<BN>;
   extern __shared__ uint8_t smem_raw[];
   // 128B swizzle needs 1024-byte aligned tiles
@@ -71,7 +77,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;          // [4 warps][2] residual chunk landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 8);
 
   const uint32_t warp = warp_id();
   const int mt = (p.M + kBlockM - 1) / kBlockM;
@@ -83,6 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
     if (p.out_mode == kOutBF16) tma_prefetch_desc(&map_out);
+    if (p.res) tma_prefetch_desc(&map_res);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -91,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
+    for (int a = 0; a < 8; ++a) mbar_init(&rfull[a], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
@@ -201,11 +210,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // All per-element loops are fully unrolled with predicates so the chunk stays
+    // in registers.  The bias of the current N tile is cached in smem per warp;
+    // the residual arrives by TMA (same 32 x CW swizzled box as the output),
+    // double-buffered one chunk ahead.
+    const int ew = static_cast<int>(warp) - 2;
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int lane = static_cast<int>(lane_id());
     const int row = static_cast<int>(quarter * 32) + lane;
-    uint8_t* stage_out = smem + S::kOutOffset + (warp - 2) * 2 * S::kStageOutBytes;
+    constexpr int CW = S::kCW;
+    constexpr int NCH = BN / CW;
+    uint8_t* stage_out = smem + S::kOutOffset + ew * 2 * S::kStageOutBytes;
+    uint8_t* stage_res = smem + S::kResOffset + ew * 2 * S::kStageOutBytes;
+    float* bias_s = reinterpret_cast<float*>(smem + S::kBiasOffset) + ew * BN;
+    uint64_t* rbar = rfull + ew * 2;
+    uint32_t rphase = 0;  // bit b: parity of residual buffer b
+    const bool has_res = p.res != nullptr && p.out_mode == kOutBF16;
     int obuf = 0;
+    int cached_n = -1;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
       const int tile_n = t % nt;
@@ -216,84 +238,115 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m = tile_m * kBlockM + row;
       const bool row_ok = m < p.M;
       const int n_tile0 = tile_n * BN;
+      const int m_slab = tile_m * kBlockM + static_cast<int>(quarter) * 32;
+      if (p.bias && tile_n != cached_n) {
+        __syncwarp();
+        for (int i = lane; i < BN; i += 32) bias_s[i] = (n_tile0 + i < p.N) ? __ldg(p.bias + n_tile0 + i) : 0.f;
+        __syncwarp();
+        cached_n = tile_n;
+      }
+      if (has_res && lane == 0) {  // residual chunk 0, before waiting for the accumulator
+        mbar_arrive_expect_tx(&rbar[0], S::kStageOutBytes);
+        tma_load_2d(stage_res, &map_res, &rbar[0], n_tile0, m_slab);
+      }
       mbar_wait(&tfull[acc], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + ((quarter * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += S::kCW) {
+      for (int ci = 0; ci < NCH; ++ci) {
+        const int c = ci * CW;
         const int n = n_tile0 + c;
         if (n >= p.N) break;  // warp-uniform
-        uint32_t r[S::kCW];
+        const bool full_chunk = n + CW <= p.N;
+        float v[CW];
+        {
+          uint32_t r[CW];
 #pragma unroll
-        for (int q = 0; q < S::kCW; q += 32) tmem_ld32(tbase + c + q, r + q);
-        tmem_ld_wait();
-        float v[S::kCW];
+          for (int q = 0; q < CW; q += 32) tmem_ld32(tbase + c + q, r + q);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < S::kCW; ++i) v[i] = __uint_as_float(r[i]);
-        const int nvalid = (p.N - n) < S::kCW ? (p.N - n) : S::kCW;
+          for (int i = 0; i < CW; ++i) v[i] = __uint_as_float(r[i]);
+        }
         if (p.out_mode != kOutBF16) {
           // fp32 logits or a split-K partial slice: direct stores (small outputs)
           if (row_ok) {
             float* o;
-            if (p.out_mode == kOutPartialF32) {
+            const bool logits = p.out_mode == kOutF32;
+            if (!logits)
               o = reinterpret_cast<float*>(p.out) + (static_cast<size_t>(z) * p.M + m) * p.ldo + n;
-            } else {
+            else
               o = reinterpret_cast<float*>(p.out) + static_cast<size_t>(m) * p.ldo + p.out_off + n;
-              if (p.bias)
-                for (int i = 0; i < nvalid; ++i) v[i] += __ldg(p.bias + n + i);
-              if (p.relu)
-                for (int i = 0; i < nvalid; ++i) v[i] = fmaxf(v[i], 0.f);
-            }
-            if (p.vec_ok && nvalid == S::kCW) {
 #pragma unroll
-              for (int i = 0; i < S::kCW; i += 4)
+            for (int i = 0; i < CW; ++i) {
+              float x = v[i];
+              if (logits && p.bias) x += bias_s[c + i];
+              if (logits && p.relu) x = fmaxf(x, 0.f);
+              v[i] = x;
+            }
+            if (p.vec_ok && full_chunk) {
+#pragma unroll
+              for (int i = 0; i < CW; i += 4)
                 *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
             } else {
-              for (int i = 0; i < nvalid; ++i) o[i] = v[i];
+#pragma unroll
+              for (int i = 0; i < CW; ++i)
+                if (n + i < p.N) o[i] = v[i];
             }
           }
           continue;
         }
         if (p.bias) {
 #pragma unroll
-          for (int i = 0; i < S::kCW; ++i) v[i] += (i < nvalid) ? __ldg(p.bias + n + i) : 0.f;
-        }
-        if (p.res && row_ok) {
-          const __nv_bfloat16* rp = p.res + static_cast<size_t>(m) * p.ldr + n;
-          if (nvalid == S::kCW && (p.ldr & 7) == 0) {
-#pragma unroll
-            for (int i = 0; i < S::kCW; i += 8) {
-              uint4 q = *reinterpret_cast<const uint4*>(rp + i);
-              const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) v[i + e] += __bfloat162float(h[e]);
-            }
-          } else {
-            for (int i = 0; i < nvalid; ++i) v[i] += __bfloat162float(rp[i]);
+          for (int i = 0; i < CW; i += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c + i);
+            v[i] += b4.x;
+            v[i + 1] += b4.y;
+            v[i + 2] += b4.z;
+            v[i + 3] += b4.w;
           }
+        }
+        if (has_res) {
+          const int rb = ci & 1;
+          // prefetch the next chunk's residual into the other buffer
+          if (lane == 0 && ci + 1 < NCH && n + CW < p.N) {
+            mbar_arrive_expect_tx(&rbar[rb ^ 1], S::kStageOutBytes);
+            tma_load_2d(stage_res + (rb ^ 1) * S::kStageOutBytes, &map_res, &rbar[rb ^ 1], n + CW,
+                        m_slab);
+          }
+          mbar_wait(&rbar[rb], (rphase >> rb) & 1u);
+          rphase ^= 1u << rb;
+          const uint8_t* rrow = stage_res + rb * S::kStageOutBytes + lane * (CW * 2);
+#pragma unroll
+          for (int ch = 0; ch < CW / 8; ++ch) {
+            const uint4 q = *reinterpret_cast<const uint4*>(rrow + swz_chunk(ch, lane, CW) * 16);
+            const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[ch * 8 + e] += __bfloat162float(h[e]);
+          }
+          __syncwarp();  // every lane has read the buffer before it is refilled
         }
         if (p.relu) {
 #pragma unroll
-          for (int i = 0; i < S::kCW; ++i) v[i] = fmaxf(v[i], 0.f);
+          for (int i = 0; i < CW; ++i) v[i] = fmaxf(v[i], 0.f);
         }
-        // stage the warp's 32 x kCW chunk in swizzled smem, then one TMA store
+        // stage the warp's 32 x CW chunk in swizzled smem, then one TMA store
         uint8_t* buf = stage_out + obuf * S::kStageOutBytes;
         if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
         __syncwarp();
-        uint8_t* rowp = buf + lane * (S::kCW * 2);
+        uint8_t* rowp = buf + lane * (CW * 2);
 #pragma unroll
-        for (int ch = 0; ch < S::kCW / 8; ++ch) {
+        for (int ch = 0; ch < CW / 8; ++ch) {
           uint4 q;
           q.x = pack_bf16x2(v[ch * 8 + 0], v[ch * 8 + 1]);
           q.y = pack_bf16x2(v[ch * 8 + 2], v[ch * 8 + 3]);
           q.z = pack_bf16x2(v[ch * 8 + 4], v[ch * 8 + 5]);
           q.w = pack_bf16x2(v[ch * 8 + 6], v[ch * 8 + 7]);
-          *reinterpret_cast<uint4*>(rowp + swz_chunk(ch, lane, S::kCW) * 16) = q;
+          *reinterpret_cast<uint4*>(rowp + swz_chunk(ch, lane, CW) * 16) = q;
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&map_out, buf, n, tile_m * kBlockM + static_cast<int>(quarter) * 32);
+          tma_store_2d(&map_out, buf, n, m_slab);
           bulk_commit();
         }
         obuf ^= 1;
@@ -314,7 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN>
 static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
-                             const ConvParams& p, int grid, cudaStream_t stream) {
+                             const CUtensorMap& mr, const ConvParams& p, int grid,
+                             cudaStream_t stream) {
   using S = ConvSmem<BN>;
   static bool configured = false;  // attribute is per-function; idempotent
   if (!configured) {
@@ -323,19 +377,20 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  conv_umma_kernel<BN><<<grid, kThreads, S::kBytes, stream>>>(ma, mb, mo, p);
+  conv_umma_kernel<BN><<<grid, kThreads, S::kBytes, stream>>>(ma, mb, mo, mr, p);
   return cudaGetLastError();
 }
 
 int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
 
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
-                             const ConvParams& p, int block_n, int grid, cudaStream_t stream) {
+                             const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
+                             cudaStream_t stream) {
   switch (block_n) {
-    case 32: return launch_bn<32>(ma, mb, mo, p, grid, stream);
-    case 64: return launch_bn<64>(ma, mb, mo, p, grid, stream);
-    case 128: return launch_bn<128>(ma, mb, mo, p, grid, stream);
-    case 256: return launch_bn<256>(ma, mb, mo, p, grid, stream);
+    case 32: return launch_bn<32>(ma, mb, mo, mr, p, grid, stream);
+    case 64: return launch_bn<64>(ma, mb, mo, mr, p, grid, stream);
+    case 128: return launch_bn<128>(ma, mb, mo, mr, p, grid, stream);
+    case 256: return launch_bn<256>(ma, mb, mo, mr, p, grid, stream);
     default: return cudaErrorInvalidValue;
   }
 }

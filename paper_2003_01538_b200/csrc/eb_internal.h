@@ -37,7 +37,8 @@ struct ConvParams {
 };
 
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
-                             const ConvParams& p, int block_n, int grid, cudaStream_t stream);
+                             const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
+                             cudaStream_t stream);
 int conv_umma_chunk(int block_n);
 
 // Driver entry point for tensor-map encoding (resolved through the runtime so the

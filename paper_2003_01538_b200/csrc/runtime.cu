@@ -108,7 +108,7 @@ int num_sms() {
 }
 
 struct ConvPlan {
-  CUtensorMap ma, mb, mo;
+  CUtensorMap ma, mb, mo, mr;
   ConvParams p;
   int grid;
   int block_n;
@@ -208,6 +208,13 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   } else {
     pl.mo = pl.mb;  // unused: fp32 outputs are stored directly
   }
+  pl.mr = pl.mb;
+  if (a.res) {
+    const int cw = conv_umma_chunk(bn);
+    if (a.out_f32 || a.ldr % 8 != 0) EB_FAIL(EB_E_INVALID, "residual needs a bf16 output, ldr % 8 == 0");
+    if (!encode_tiled_2d_bf16(&pl.mr, a.res, a.cout, M64, a.ldr, cw, 32, &err, cw * 2))
+      EB_FAIL(EB_E_INVALID, err);
+  }
   return EB_OK;
 }
 
@@ -223,12 +230,12 @@ int run_conv_plan(ConvPlan& pl, float* ws, size_t ws_cap, const ConvArgs& a, cud
     p.vec_ok = (a.cout % 4 == 0);
     p.bias = nullptr;
     p.relu = 0;
-    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.mo, p, pl.block_n, pl.grid, s));
+    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.mo, pl.mr, p, pl.block_n, pl.grid, s));
     EB_CUDA(k_splitk_finalize(ws, pl.splits, pl.p.M, a.cout, a.bias, a.relu, a.y, a.ldy, a.y_off,
                               a.out_f32, s));
     if (launches) *launches += 2;
   } else {
-    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.mo, pl.p, pl.block_n, pl.grid, s));
+    EB_CUDA(conv_umma_launch(pl.ma, pl.mb, pl.mo, pl.mr, pl.p, pl.block_n, pl.grid, s));
     if (launches) *launches += 1;
   }
   return EB_OK;

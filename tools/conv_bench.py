@@ -1,0 +1,54 @@
+"""Time one conv layer through the kernel-level ABI (eb_k_conv) with CUDA events.
+
+    python tools/conv_bench.py B H W CIN COUT KH KW S P [--res] [--iters N]
+"""
+import argparse
+import ctypes
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2003_01538_b200 import _lib  # noqa: E402
+from paper_2003_01538_b200.packing import conv_mode, pack_conv_weight  # noqa: E402
+
+ap = argparse.ArgumentParser()
+for n in ("B", "H", "W", "CIN", "COUT", "KH", "KW", "S", "P"):
+    ap.add_argument(n, type=int)
+ap.add_argument("--res", action="store_true")
+ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--block-n", type=int, default=0)
+a = ap.parse_args()
+lib = _lib.load()
+P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+x = torch.randn(a.B, a.H, a.W, a.CIN, device="cuda").to(torch.bfloat16)
+w = torch.randn(a.COUT, a.CIN, a.KH, a.KW) * 0.05
+wp = pack_conv_weight(w, conv_mode(a.KH, a.KW, a.S, a.S, a.P, a.P, a.CIN, False)).cuda()
+Ho = (a.H + 2 * a.P - a.KH) // a.S + 1
+Wo = (a.W + 2 * a.P - a.KW) // a.S + 1
+y = torch.empty(a.B, Ho, Wo, a.COUT, device="cuda", dtype=torch.bfloat16)
+res = torch.randn_like(y) if a.res else None
+bias = torch.randn(a.COUT, device="cuda")
+ws = torch.empty(2 * 148 * 128 * 256, device="cuda")
+
+
+def run():
+    _lib.check(lib.eb_k_conv(P(x), a.B, a.H, a.W, a.CIN, a.CIN, P(wp), P(bias), P(res),
+                             a.COUT if res is not None else 0, P(y), a.COUT, 0, a.COUT, a.KH, a.KW,
+                             a.S, a.S, a.P, a.P, 1, 0, 0, 0, a.block_n, P(ws), None))
+
+
+for _ in range(3):
+    run()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(a.iters):
+    run()
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.iters
+flops = 2 * a.B * Ho * Wo * a.COUT * a.CIN * a.KH * a.KW
+bytes_ = 2 * (x.numel() + y.numel() + (res.numel() if res is not None else 0) + wp.numel())
+print(f"{ms*1e3:.1f} us  {flops/ms/1e9:.0f} TFLOP/s  {bytes_/ms/1e6:.0f} GB/s")
