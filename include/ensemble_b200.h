@@ -94,6 +94,9 @@ typedef struct {
   int32_t pool_mode;
   int32_t flatten; /* CONV: treat src (H, W, C) as one row of H*W*C features */
   int32_t stream;  /* concurrency lane (0..3); ops on different lanes may overlap */
+  /* CONV: scale/shift = optional per-input-channel BN-ReLU applied to A inside
+   * the kernel (1x1 only; arrays zero-padded to a multiple of 64).
+   * POOL/GAP/BNRELU: the same BN-ReLU applied to the input elements. */
   uint64_t w_off, b_off, scale_off, shift_off;
 } eb_op_desc;
 
@@ -160,7 +163,7 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
               const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
               int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
               int out_f32, int c8_stem, int split_k, int block_n, void* dev_workspace,
-              void* stream);
+              const float* dev_pre_scale, const float* dev_pre_shift, void* stream);
 int eb_k_pool(const void* dev_x, int ldx, void* dev_y, int ldy, int y_off, int batch, int h,
               int w, int c, int k, int s, int pad, int mode, const float* dev_scale,
               const float* dev_shift, void* stream);

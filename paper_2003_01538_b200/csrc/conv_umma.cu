@@ -36,7 +36,7 @@ namespace eb {
 
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // one 128-byte swizzle atom of bf16
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // 2 control warps + 4 epilogue warps + 4 A-transform warps
 constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KiB
 
 template <int BN>
@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + S::kStages;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
   uint64_t* rfull = tempty + 2;          // [4 warps][2] residual chunk landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 8);
+  uint64_t* xfull = rfull + 8;           // [stages] A tile transformed (pre-activation)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + S::kStages);
 
   const uint32_t warp = warp_id();
   const int mt = (p.M + kBlockM - 1) / kBlockM;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[a], 4);
     }
     for (int a = 0; a < 8; ++a) mbar_init(&rfull[a], 1);
+    for (int s = 0; s < S::kStages; ++s) mbar_init(&xfull[s], 128);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait(p.pre_scale ? &xfull[stage] : &full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue
     // All per-element loops are fully unrolled with predicates so the chunk stays
     // in registers.  The bias of the current N tile is cached in smem per warp;
@@ -357,6 +359,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) bulk_wait<0>();
+  } else if (p.pre_scale) {
+    // ------------------------------------------------------------ A transform
+    // One thread per A row: relu(a * scale[k] + shift[k]) in place on the
+    // swizzled tile, then a proxy fence so the tensor core sees the result.
+    const int r = static_cast<int>(threadIdx.x) - 192;  // 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int z = t / (nt * mt);
+      const int kb0 = z * p.kb_per_split;
+      const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        uint8_t* rowp = smem + stage * S::kStageBytes + r * 128;
+        const float* sc = p.pre_scale + kb * kBlockK;
+        const float* sh = p.pre_shift + kb * kBlockK;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint4* q = reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) * 16));
+          uint4 x = *q;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
+          const float4 s0 = __ldg(reinterpret_cast<const float4*>(sc + ch * 8));
+          const float4 s1 = __ldg(reinterpret_cast<const float4*>(sc + ch * 8 + 4));
+          const float4 t0 = __ldg(reinterpret_cast<const float4*>(sh + ch * 8));
+          const float4 t1 = __ldg(reinterpret_cast<const float4*>(sh + ch * 8 + 4));
+          const float scv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          const float shv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            h[e] = __floats2bfloat162_rn(fmaxf(fmaf(f.x, scv[2 * e], shv[2 * e]), 0.f),
+                                         fmaxf(fmaf(f.y, scv[2 * e + 1], shv[2 * e + 1]), 0.f));
+          }
+          *q = x;
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&xfull[stage]);
+        if (++stage == S::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();

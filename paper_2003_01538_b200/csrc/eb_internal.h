@@ -34,6 +34,10 @@ struct ConvParams {
   int relu;
   int out_mode;
   int vec_ok;  // 16-byte aligned rows/offsets: vector epilogue stores allowed
+  // optional pre-activation on A (DenseNet BN-ReLU on the concatenated input):
+  // a = relu(a * pre_scale[k] + pre_shift[k]); arrays padded with zeros to 64
+  const float* pre_scale;
+  const float* pre_shift;
 };
 
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,

@@ -78,6 +78,8 @@ struct ConvArgs {
   int relu, out_f32, c8_stem, flatten;
   int split_k;  // 0 = auto
   int block_n;  // 0 = auto
+  const float* pre_scale = nullptr;  // pre-activation on A (tiled mode only)
+  const float* pre_shift = nullptr;
 };
 
 int conv_out(int in, int k, int s, int p) { return (in + 2 * p - k) / s + 1; }
@@ -191,6 +193,10 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.p.ldo = a.ldy;
   pl.p.out_off = a.y_off;
   pl.p.out_mode = a.out_f32 ? kOutF32 : kOutBF16;
+  pl.p.pre_scale = a.pre_scale;
+  pl.p.pre_shift = a.pre_shift;
+  if (a.pre_scale && (pl.p.a_mode != kAModeTiled || !a.pre_shift))
+    EB_FAIL(EB_E_INVALID, "pre-activation is only supported on 1x1 (tiled) convolutions");
   {
     const int q = a.out_f32 ? 4 : 8;  // elements per 16 bytes
     pl.p.vec_ok = (a.ldy % q == 0) && (a.y_off % q == 0) && (!a.res || a.ldr % 8 == 0);
@@ -365,6 +371,8 @@ int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
         a.out_f32 = dst.dtype == EB_F32;
         a.c8_stem = op.src == EB_T_IMAGE_NHWC8;
         a.flatten = op.flatten;
+        a.pre_scale = static_cast<const float*>(P(op.scale_off));
+        a.pre_shift = static_cast<const float*>(P(op.shift_off));
         ConvPlan pl;
         int rc = plan_conv(a, &pl);
         if (rc != EB_OK) return rc;
@@ -902,8 +910,10 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
               const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
               int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
               int out_f32, int c8_stem, int split_k, int block_n, void* dev_workspace,
-              void* stream) {
+              const float* dev_pre_scale, const float* dev_pre_shift, void* stream) {
   ConvArgs a{};
+  a.pre_scale = dev_pre_scale;
+  a.pre_shift = dev_pre_shift;
   a.x = dev_x;
   a.B = batch;
   a.H = h;

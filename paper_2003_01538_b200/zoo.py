@@ -85,7 +85,7 @@ class Lowering:
 
     # -- primitives --------------------------------------------------------
     def conv(self, x: TRef, conv: nn.Conv2d | nn.Linear, bn=None, relu=False, res=None,
-             out: TRef | None = None, flatten=False) -> TRef:
+             out: TRef | None = None, flatten=False, pre_bn=None) -> TRef:
         eng = self.eng
         if isinstance(conv, nn.Linear):
             w = conv.weight.detach().float()
@@ -119,12 +119,18 @@ class Lowering:
             out = eng.tensor(ho, wo, cout)
         w_off = eng.weight(wp)
         b_off = eng.weight(b.contiguous()) if b is not None else None
+        so = sho = None
+        if pre_bn is not None:  # BN-ReLU of the input, applied to A inside the kernel
+            sc, sf = bn_affine(pre_bn)
+            kpad = (x.c + 63) // 64 * 64
+            so = eng.weight(torch.cat([sc, torch.zeros(kpad - x.c)]))
+            sho = eng.weight(torch.cat([sf, torch.zeros(kpad - x.c)]))
         k_alg = w.shape[1] if w.dim() == 2 else w.shape[1] * w.shape[2] * w.shape[3]
         meta = {"name": "conv", "flops": 2 * ho * wo * cout * k_alg,
                 "shape": (ho, wo, cout, kh, kw, sh, x.c), "weight_bytes": 2 * cout * k_alg}
         eng.op(_lib.EB_OP_CONV, x, out, cout=cout, res=res, kh=kh, kw=kw, sh=sh, sw=sw, ph=ph,
                pw=pw, relu=relu, flatten=flatten, lane=self.lane, w_off=w_off, b_off=b_off,
-               meta=meta)
+               scale_off=so, shift_off=sho, meta=meta)
         return out
 
     def pool(self, x: TRef, k, s, p, mode, out: TRef | None = None, bn=None) -> TRef:
@@ -195,12 +201,13 @@ class Lowering:
                 self.pool(x, 3, 2, 1, _lib.EB_POOL_MAX, out=buf.slice(0, c_in))
             else:
                 self.conv(pending[0], pending[1], out=buf.slice(0, c_in))
-            act = self.eng.tensor(h, h, c_tot - growth)
             bott = self.eng.tensor(h, h, width)
             for li, layer in enumerate(layers):
                 c_cur = c_in + li * growth
-                a = self.bnrelu(buf.slice(0, c_cur), layer.norm1, act.slice(0, c_cur))
-                y = self.conv(a, layer.conv1, layer.norm2, relu=True, out=bott)
+                # norm1-ReLU on the concatenated input is applied to A inside the 1x1
+                # kernel; norm2 folds into conv1 (bias + ReLU in the epilogue)
+                y = self.conv(buf.slice(0, c_cur), layer.conv1, layer.norm2, relu=True, out=bott,
+                              pre_bn=layer.norm1)
                 self.conv(y, layer.conv2, out=buf.slice(c_cur, growth))
             if trans[bi] is not None:
                 t = trans[bi]

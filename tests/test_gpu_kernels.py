@@ -23,7 +23,7 @@ def _p(t: torch.Tensor | None):
 
 
 def run_conv(x_nhwc, ldx, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw, *, y_ld=None,
-             y_off=0, out_f32=False, stem=False, split_k=0, block_n=0):
+             y_off=0, out_f32=False, stem=False, split_k=0, block_n=0, pre=None):
     lib = _lib.load()
     B, H, W, _ = x_nhwc.shape
     cout = w.shape[0]
@@ -35,10 +35,17 @@ def run_conv(x_nhwc, ldx, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw, *, y_
     y = torch.zeros(B, Ho, Wo, ld, device=DEV, dtype=torch.float32 if out_f32 else torch.bfloat16)
     ws = torch.empty(2 * 148 * 128 * 256, device=DEV, dtype=torch.float32)
     b = bias.to(DEV) if bias is not None else None
+    pre_s = pre_t = None
+    if pre is not None:
+        kpad = (cin + 63) // 64 * 64
+        pre_s = torch.zeros(kpad, device=DEV)
+        pre_t = torch.zeros(kpad, device=DEV)
+        pre_s[:cin] = pre[0].to(DEV)
+        pre_t[:cin] = pre[1].to(DEV)
     _lib.check(lib.eb_k_conv(
         _p(x_nhwc), B, H, W, ldx, cin, _p(wp), _p(b), _p(res), res.shape[-1] if res is not None else 0,
         _p(y), ld, y_off, cout, kh, kw, sh, sw, ph, pw, int(relu), int(out_f32), int(stem),
-        split_k, block_n, _p(ws), None))
+        split_k, block_n, _p(ws), _p(pre_s), _p(pre_t), None))
     torch.cuda.synchronize()
     return y
 
@@ -245,3 +252,19 @@ def test_lin1_f64_scores():
     got = out.cpu().numpy()
     assert np.allclose(got, ref, rtol=1e-12, atol=1e-9)
     assert (got.argmax(1) == ref.argmax(1)).all()
+
+
+def test_conv_pre_activation_bnrelu():
+    """DenseNet: relu(x * s + t) on the (sliced) input, fused into the A path."""
+    g = torch.Generator().manual_seed(13)
+    B, H, W, ld, cin, cout = 3, 28, 28, 256, 160, 128
+    x = torch.randn(B, H, W, ld, generator=g).to(torch.bfloat16).to(DEV)
+    w = torch.randn(cout, cin, 1, 1, generator=g) / np.sqrt(cin)
+    bias = torch.randn(cout, generator=g) * 0.1
+    s = torch.rand(cin, generator=g) + 0.5
+    t = torch.randn(cin, generator=g) * 0.3
+    y = run_conv(x, ld, cin, w, bias, None, True, 1, 1, 1, 1, 0, 0, pre=(s, t))
+    xa = torch.relu(x[..., :cin].float().cpu() * s + t).to(torch.bfloat16)
+    r = ref_conv(xa, cin, w, bias, None, True, 1, 1, 1, 1, 0, 0)
+    err = (y.float().cpu() - r).abs().max().item()
+    assert err <= 0.02 * r.abs().max().item() + 1e-2, err

@@ -36,7 +36,7 @@ ws = torch.empty(2 * 148 * 128 * 256, device="cuda")
 def run():
     _lib.check(lib.eb_k_conv(P(x), a.B, a.H, a.W, a.CIN, a.CIN, P(wp), P(bias), P(res),
                              a.COUT if res is not None else 0, P(y), a.COUT, 0, a.COUT, a.KH, a.KW,
-                             a.S, a.S, a.P, a.P, 1, 0, 0, 0, a.block_n, P(ws), None))
+                             a.S, a.S, a.P, a.P, 1, 0, 0, 0, a.block_n, P(ws), None, None, None))
 
 
 for _ in range(3):
