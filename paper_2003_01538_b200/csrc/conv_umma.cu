@@ -9,8 +9,8 @@
 // 128B-swizzled shared memory (zero-filled at the padded borders and past the
 // last image).  1x1/stride-1 convolutions and FC layers use a plain 2-D TMA
 // tile instead.  The stem (Cin=3, padded to 8 channels by the preprocess
-// kernel) uses 16-byte im2col columns in the non-swizzled canonical layout, one
-// TMA per tap, eight taps per 64-wide K block.
+// kernel) is gathered with cp.async by four extra warps: per filter row, the 8
+// consecutive input pixels of a receptive-field row are one 128-byte A row.
 //
 // Persistent, warp-specialised (192 threads, one CTA per SM):
 //   warp 0      TMA producer: a smem ring of (A, B) stages that runs across tiles
@@ -71,8 +71,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   using S = ConvSmem<BN>;
   extern __shared__ uint8_t smem_raw[];
   // 128B swizzle needs 1024-byte aligned tiles
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // (offset arithmetic on the __shared__ array keeps the address space visible to the
+  // compiler, so staging accesses compile to STS/LDS rather than generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;  // [2] accumulator ready
@@ -101,7 +102,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[a], 4);
     }
     for (int a = 0; a < 8; ++a) mbar_init(&rfull[a], 1);
-    for (int s = 0; s < S::kStages; ++s) mbar_init(&xfull[s], 128);
+    // A-gather mode: 128 per-thread cp.async arrivals; A-transform mode: one arrive per warp
+    const uint32_t xcount = p.a_mode == kAModeGatherC8 ? 128u : 4u;
+    for (int s = 0; s < S::kStages; ++s) mbar_init(&xfull[s], xcount);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + kABytes;
-          mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+          mbar_arrive_expect_tx(&full[stage], p.a_mode == kAModeGatherC8 ? S::kBBytes : S::kStageBytes);
           if (p.a_mode == kAModeTiled) {
             tma_load_2d(sa, &map_a, &full[stage], kb * kBlockK, m0);
           } else if (p.a_mode == kAModeIm2col) {
@@ -148,17 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = tap - r * p.kw;
             tma_load_im2col_4d(sa, &map_a, &full[stage], cc * kBlockK, base_w, base_h, img,
                                static_cast<uint16_t>(s), static_cast<uint16_t>(r));
-          } else {  // kAModeIm2colC8: eight 8-channel taps per K block
-#pragma unroll 1
-            for (int j = 0; j < 8; ++j) {
-              int tap = kb * 8 + j;
-              if (tap >= p.taps) tap = 0;  // weights are zero there; any finite data works
-              const int r = tap / p.kw;
-              const int s = tap - r * p.kw;
-              tma_load_im2col_4d(sa + j * (kBlockM * 16), &map_a, &full[stage], 0, base_w,
-                                 base_h, img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
-            }
-          }
+          }  // kAModeGatherC8: A is gathered by warps 6..9
           tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
           if (++stage == S::kStages) {
             stage = 0;
@@ -183,20 +176,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(p.pre_scale ? &xfull[stage] : &full[stage], phase);
+        if (p.a_mode == kAModeGatherC8) mbar_wait(&xfull[stage], phase);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
           const uint32_t sb = sa + kABytes;
 #pragma unroll
           for (int k = 0; k < kBlockK / 16; ++k) {
-            uint64_t adesc;
-            if (p.a_mode == kAModeIm2colC8) {
-              // two 8-channel tap columns per K=16 step; core matrices 128 B apart along M,
-              // 2 KiB apart along K
-              adesc = umma_desc(sa + k * 2 * (kBlockM * 16), kBlockM * 16, 128, 0);
-            } else {
-              adesc = umma_desc_sw128(sa + k * 32);
-            }
+            const uint64_t adesc = umma_desc_sw128(sa + k * 32);
             const uint64_t bdesc = umma_desc_sw128(sb + k * 32);
             umma_bf16(tmem_d, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
@@ -359,6 +346,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) bulk_wait<0>();
+  } else if (p.a_mode == kAModeGatherC8) {
+    // ------------------------------------------------------------ A gather (stem)
+    // Thread r builds A row r: for filter row kb, the 8 consecutive input pixels
+    // starting at the receptive field's left edge are 8 x 16 B = one 128-byte
+    // swizzled smem row (pixels beyond kw meet zero weights; outside the image
+    // they are zero-filled).  Completion is signalled asynchronously with
+    // cp.async.mbarrier.arrive, so each thread streams as many stages as the ring
+    // has free slots.
+    const int r = static_cast<int>(threadIdx.x) - 192;  // 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int rest = t / nt;
+      const int tile_m = rest % mt;
+      const int z = rest / mt;
+      const int kb0 = z * p.kb_per_split;
+      const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
+      const int m = tile_m * kBlockM + r;
+      const bool row_ok = m < p.M;
+      const int hw = p.Ho * p.Wo;
+      const int img = row_ok ? m / hw : 0;
+      const int rem = m - img * hw;
+      const int oh = rem / p.Wo;
+      const int ow = rem - oh * p.Wo;
+      const int iw0 = ow * p.sw - p.pw;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* rowp = smem + stage * S::kStageBytes + r * 128;
+        const int ih = oh * p.sh - p.ph + kb;
+        const bool hok = row_ok && ih >= 0 && ih < p.H;
+        const __nv_bfloat16* src = p.x + ((static_cast<int64_t>(img) * p.H + (hok ? ih : 0)) * p.W) * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int iw = iw0 + j;
+          const bool ok = hok && iw >= 0 && iw < p.W;
+          cp_async_16(rowp + ((j ^ (r & 7)) * 16), src + (ok ? iw : 0) * 8, ok ? 16u : 0u);
+        }
+        cp_async_arrive_noinc(&xfull[stage]);
+        if (++stage == S::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    cp_async_wait<0>();
   } else if (p.pre_scale) {
     // ------------------------------------------------------------ A transform
     // One thread per A row: relu(a * scale[k] + shift[k]) in place on the
@@ -395,7 +427,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           *q = x;
         }
         fence_proxy_async_smem();
-        mbar_arrive(&xfull[stage]);
+        __syncwarp();
+        if ((r & 31) == 0) mbar_arrive(&xfull[stage]);
         if (++stage == S::kStages) {
           stage = 0;
           phase ^= 1;

@@ -12,7 +12,7 @@ namespace eb {
 enum AMode : int {
   kAModeTiled = 0,     // A is a plain [M, K] matrix (1x1 stride-1 conv, FC)
   kAModeIm2col = 1,    // TMA im2col, 64-channel chunks, 128B swizzle
-  kAModeIm2colC8 = 2,  // TMA im2col, 8-channel taps (stem), no swizzle
+  kAModeGatherC8 = 2,  // stem (Cin <= 8): cp.async gather, one K block per filter row
 };
 
 enum OutMode : int {
@@ -26,6 +26,8 @@ struct ConvParams {
   int num_kb, kb_per_split;
   int a_mode;
   int Ho, Wo, sh, sw, ph, pw, kw, taps, cchunks;
+  int H, W;                  // input geometry (gather mode)
+  const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
   void* out;
   int ldo, out_off;
   const __nv_bfloat16* res;

@@ -94,7 +94,7 @@ int pick_block_n(int cout) {
 // K extent (elements) of the packed weight rows for a conv of this geometry.
 int64_t packed_k(int cin, int kh, int kw, bool c8, bool flatten, int H, int W) {
   if (flatten) return ((static_cast<int64_t>(H) * W * cin + 63) / 64) * 64;
-  if (c8) return ((static_cast<int64_t>(kh) * kw + 7) / 8) * 64;
+  if (c8) return static_cast<int64_t>(kh) * 64;  // one K block (8 px x 8 ch) per filter row
   return static_cast<int64_t>(kh) * kw * ((cin + 63) / 64) * 64;
 }
 
@@ -143,10 +143,12 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     pl.p.a_mode = kAModeTiled;
   } else if (a.c8_stem) {
     if (a.cin != 8 || a.ldx != 8) EB_FAIL(EB_E_INVALID, "stem mode expects an 8-channel image");
-    if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, 8, 8, a.kh, a.kw, a.sh, a.sw, a.ph, a.pw,
-                            8, 128, false, &err))
-      EB_FAIL(EB_E_INVALID, err);
-    pl.p.a_mode = kAModeIm2colC8;
+    if (a.kw > 8) EB_FAIL(EB_E_INVALID, "stem mode needs kw <= 8");
+    pl.ma = {};
+    pl.p.a_mode = kAModeGatherC8;
+    pl.p.x = static_cast<const __nv_bfloat16*>(a.x);
+    pl.p.H = a.H;
+    pl.p.W = a.W;
   } else {
     if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, a.cin, a.ldx, a.kh, a.kw, a.sh, a.sw, a.ph,
                             a.pw, 64, 128, true, &err))

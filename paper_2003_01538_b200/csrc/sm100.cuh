@@ -142,6 +142,26 @@ EB_DEVICE void tmem_ld32(uint32_t taddr, uint32_t* r) {
 }
 EB_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ---------------------------------------------------------------- cp.async (LDGSTS)
+// 16-byte global->shared copy through L1 (.ca: overlapping windows of
+// neighbouring rows hit the same lines); src_bytes = 0 zero-fills the destination.
+EB_DEVICE void cp_async_16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+EB_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// Arrive on the mbarrier when all of this thread's prior cp.async complete
+// (non-blocking; the barrier's expected count includes this arrival).
+EB_DEVICE void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+template <int N>
+EB_DEVICE void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------- TMA store
 EB_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

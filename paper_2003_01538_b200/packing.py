@@ -8,8 +8,8 @@ match the order in which the A operand (activations) is gathered:
   axis padded to a multiple of 64 per tap -- one TMA im2col load per (tap,
   64-channel chunk);
 * ``tiled`` (1x1, stride 1): K = channel padded to 64;
-* ``c8`` (the stem, Cin <= 8): K = (tap, 8 channels), taps padded to a multiple
-  of 8 -- eight 16-byte im2col columns per K block;
+* ``c8`` (the stem, Cin <= 8): K = (filter row, 8 pixel slots, 8 channels) --
+  one 64-wide K block per filter row, slots >= kw and channels >= Cin are zero;
 * ``flatten`` (FC on an H x W x C feature map): K = NHWC order of the feature
   map (torchvision flattens NCHW, so the columns are permuted here), padded to 64.
 
@@ -49,10 +49,10 @@ def pack_conv_weight(w: torch.Tensor, mode: str, hw: tuple[int, int] | None = No
     taps = kh * kw
     wt = w.permute(0, 2, 3, 1).reshape(cout, taps, cin)  # (Cout, tap, Cin)
     if mode == "c8":
-        if cin > 8:
-            raise ValueError("c8 packing needs Cin <= 8")
-        out = torch.zeros(cout, _round_up(taps, 8), 8, dtype=torch.float32)
-        out[:, :taps, :cin] = wt
+        if cin > 8 or kw > 8:
+            raise ValueError("c8 packing needs Cin <= 8 and kw <= 8")
+        out = torch.zeros(cout, kh, 8, 8, dtype=torch.float32)
+        out[:, :, :kw, :cin] = wt.reshape(cout, kh, kw, cin)
     else:
         cpad = _round_up(cin, 64)
         out = torch.zeros(cout, taps, cpad, dtype=torch.float32)

@@ -19,12 +19,14 @@ for n in ("B", "H", "W", "CIN", "COUT", "KH", "KW", "S", "P"):
 ap.add_argument("--res", action="store_true")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--block-n", type=int, default=0)
+ap.add_argument("--stem", action="store_true", help="CIN<=8 image in NHWC8 (gather mode)")
 a = ap.parse_args()
 lib = _lib.load()
 P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
-x = torch.randn(a.B, a.H, a.W, a.CIN, device="cuda").to(torch.bfloat16)
+LD = 8 if a.stem else a.CIN
+x = torch.randn(a.B, a.H, a.W, LD, device="cuda").to(torch.bfloat16)
 w = torch.randn(a.COUT, a.CIN, a.KH, a.KW) * 0.05
-wp = pack_conv_weight(w, conv_mode(a.KH, a.KW, a.S, a.S, a.P, a.P, a.CIN, False)).cuda()
+wp = pack_conv_weight(w, conv_mode(a.KH, a.KW, a.S, a.S, a.P, a.P, a.CIN, a.stem)).cuda()
 Ho = (a.H + 2 * a.P - a.KH) // a.S + 1
 Wo = (a.W + 2 * a.P - a.KW) // a.S + 1
 y = torch.empty(a.B, Ho, Wo, a.COUT, device="cuda", dtype=torch.bfloat16)
@@ -34,9 +36,9 @@ ws = torch.empty(2 * 148 * 128 * 256, device="cuda")
 
 
 def run():
-    _lib.check(lib.eb_k_conv(P(x), a.B, a.H, a.W, a.CIN, a.CIN, P(wp), P(bias), P(res),
+    _lib.check(lib.eb_k_conv(P(x), a.B, a.H, a.W, LD, LD, P(wp), P(bias), P(res),
                              a.COUT if res is not None else 0, P(y), a.COUT, 0, a.COUT, a.KH, a.KW,
-                             a.S, a.S, a.P, a.P, 1, 0, 0, 0, a.block_n, P(ws), None, None, None))
+                             a.S, a.S, a.P, a.P, 1, 0, int(a.stem), 0, a.block_n, P(ws), None, None, None))
 
 
 for _ in range(3):
