@@ -37,16 +37,23 @@ namespace eb {
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kThreads = 320;  // 2 control warps + 4 epilogue warps + 4 A-transform warps
-constexpr int kABytes = kBlockM * kBlockK * 2;  // 16 KiB
 
-template <int BN>
+// TS = filter taps consumed per pipeline stage: 1 (one TMA im2col load per tap)
+// or 3 (tap-shift mode: one 136-row load per filter row serves its 3 horizontal taps).
+template <int BN, int TS>
 struct ConvSmem {
   static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "tile width");
-  static constexpr int kBBytes = BN * kBlockK * 2;
+  static constexpr int kARows = TS == 1 ? kBlockM : kBlockM + 8;    // +8: row shifts 0..2
+  static constexpr int kALoadBytes = kARows * 128;                  // bytes TMA delivers
+  static constexpr int kABytes = (kALoadBytes + 1023) / 1024 * 1024;
+  static constexpr int kBBytes = TS * BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (BN >= 256) ? 3 : (BN >= 128 ? 4 : (BN >= 64 ? 6 : 7));
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
   static constexpr int kStageOutBytes = 32 * kCW * 2;         // one warp's 32-row chunk
+  static constexpr int kEpiBytes = 4 * 2 * kStageOutBytes * 2 + 4 * BN * 4;
+  static constexpr int kFit = (232448 - 1536 - kEpiBytes) / kStageBytes;
+  static constexpr int kStages = kFit > 8 ? 8 : kFit;
+  static_assert(kStages >= 2, "pipeline needs two stages");
   static constexpr int kOutOffset = kStages * kStageBytes;
   // per epilogue warp: 2 output staging buffers + 2 residual buffers
   static constexpr int kResOffset = kOutOffset + 4 * 2 * kStageOutBytes;
@@ -62,13 +69,13 @@ __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
   return cw == 64 ? (chunk ^ (row & 7)) : (chunk ^ ((row >> 1) & 3));
 }
 
-template <int BN>
+template <int BN, int TS>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_umma_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ CUtensorMap map_out,
                      const __grid_constant__ CUtensorMap map_res, const ConvParams p) {
-  using S = ConvSmem<BN>;
+  using S = ConvSmem<BN, TS>;
   extern __shared__ uint8_t smem_raw[];
   // 128B swizzle needs 1024-byte aligned tiles
   // (offset arithmetic on the __shared__ array keeps the address space visible to the
@@ -128,11 +135,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = tile_m * kBlockM;
         int img = 0, oh = 0, ow = 0;
         if (p.a_mode != kAModeTiled) {
-          const int hw = p.Ho * p.Wo;
+          const int gw = TS > 1 ? p.Wp : p.Wo;  // tap-shift tiles walk the padded grid
+          const int hw = p.Ho * gw;
           img = m0 / hw;
           const int rem = m0 - img * hw;
-          oh = rem / p.Wo;
-          ow = rem - oh * p.Wo;
+          oh = rem / gw;
+          ow = rem - oh * gw;
         }
         const int base_w = ow * p.sw - p.pw;
         const int base_h = oh * p.sh - p.ph;
@@ -140,9 +148,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
-          uint8_t* sb = sa + kABytes;
-          mbar_arrive_expect_tx(&full[stage], p.a_mode == kAModeGatherC8 ? S::kBBytes : S::kStageBytes);
-          if (p.a_mode == kAModeTiled) {
+          uint8_t* sb = sa + S::kABytes;
+          mbar_arrive_expect_tx(&full[stage], p.a_mode == kAModeGatherC8
+                                                  ? S::kBBytes
+                                                  : S::kALoadBytes + S::kBBytes);
+          if (TS > 1) {
+            // filter row r, channel chunk cc: 136 consecutive padded-grid pixels at tap (r, 0);
+            // tap (r, s) is the same buffer shifted down by s rows
+            const int r = kb / p.cchunks;
+            const int cc = kb - r * p.cchunks;
+            tma_load_im2col_4d(sa, &map_a, &full[stage], cc * kBlockK, base_w, base_h, img, 0,
+                               static_cast<uint16_t>(r));
+#pragma unroll
+            for (int s2 = 0; s2 < TS; ++s2)
+              tma_load_2d(sb + s2 * (BN * 128), &map_b, &full[stage],
+                          ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, n0);
+          } else if (p.a_mode == kAModeTiled) {
             tma_load_2d(sa, &map_a, &full[stage], kb * kBlockK, m0);
           } else if (p.a_mode == kAModeIm2col) {
             const int tap = kb / p.cchunks;
@@ -152,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_im2col_4d(sa, &map_a, &full[stage], cc * kBlockK, base_w, base_h, img,
                                static_cast<uint16_t>(s), static_cast<uint16_t>(r));
           }  // kAModeGatherC8: A is gathered by warps 6..9
-          tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
+          if (TS == 1) tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
           if (++stage == S::kStages) {
             stage = 0;
             phase ^= 1;
@@ -180,12 +201,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
-          const uint32_t sb = sa + kABytes;
+          const uint32_t sb = sa + S::kABytes;
 #pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k) {
-            const uint64_t adesc = umma_desc_sw128(sa + k * 32);
-            const uint64_t bdesc = umma_desc_sw128(sb + k * 32);
-            umma_bf16(tmem_d, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          for (int s2 = 0; s2 < TS; ++s2) {
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k) {
+              // a shift of s2 rows is a start address 128 B further: the 128B swizzle is
+              // applied on absolute smem address bits (base offset field stays 0), which
+              // is also what the TMA used when it wrote the tile (verified on B200)
+              const uint64_t adesc = umma_desc_sw128(sa + s2 * 128 + k * 32);
+              const uint64_t bdesc = umma_desc_sw128(sb + s2 * (BN * 128) + k * 32);
+              umma_bf16(tmem_d, adesc, bdesc, idesc, (kb > kb0 || s2 > 0 || k > 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty[stage]);
           if (kb == kb1 - 1) umma_commit(&tfull[acc]);
@@ -225,7 +252,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int z = rest / mt;
       const int acc = j & 1;
       const int m = tile_m * kBlockM + row;
-      const bool row_ok = m < p.M;
+      bool row_ok = m < p.M;
+      size_t orow = static_cast<size_t>(m);
+      if (TS > 1) {  // padded-grid row -> output pixel; the kw-1 junk columns are dropped
+        const int hw = p.Ho * p.Wp;
+        const int img = m / hw;
+        const int rem = m - img * hw;
+        const int oh = rem / p.Wp;
+        const int owp = rem - oh * p.Wp;
+        row_ok = row_ok && owp < p.Wo;
+        orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + owp;
+      }
       const int n_tile0 = tile_n * BN;
       const int m_slab = tile_m * kBlockM + static_cast<int>(quarter) * 32;
       if (p.bias && tile_n != cached_n) {
@@ -317,6 +354,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.relu) {
 #pragma unroll
           for (int i = 0; i < CW; ++i) v[i] = fmaxf(v[i], 0.f);
+        }
+        if (TS > 1) {
+          // tap-shift tiles are not contiguous in the output: direct 16-byte stores
+          if (row_ok) {
+            __nv_bfloat16* o =
+                reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
+            if (full_chunk && p.vec_ok) {
+#pragma unroll
+              for (int ch = 0; ch < CW / 8; ++ch) {
+                uint4 q;
+                q.x = pack_bf16x2(v[ch * 8 + 0], v[ch * 8 + 1]);
+                q.y = pack_bf16x2(v[ch * 8 + 2], v[ch * 8 + 3]);
+                q.z = pack_bf16x2(v[ch * 8 + 4], v[ch * 8 + 5]);
+                q.w = pack_bf16x2(v[ch * 8 + 6], v[ch * 8 + 7]);
+                *reinterpret_cast<uint4*>(o + ch * 8) = q;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < CW; ++i)
+                if (n + i < p.N) o[i] = __float2bfloat16_rn(v[i]);
+            }
+          }
+          continue;
         }
         // stage the warp's 32 x CW chunk in swizzled smem, then one TMA store
         uint8_t* buf = stage_out + obuf * S::kStageOutBytes;
@@ -443,19 +503,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------- host side
 
-template <int BN>
+template <int BN, int TS>
 static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int grid,
                              cudaStream_t stream) {
-  using S = ConvSmem<BN>;
+  using S = ConvSmem<BN, TS>;
   static bool configured = false;  // attribute is per-function; idempotent
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<BN>,
+    cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<BN, TS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  conv_umma_kernel<BN><<<grid, kThreads, S::kBytes, stream>>>(ma, mb, mo, mr, p);
+  conv_umma_kernel<BN, TS><<<grid, kThreads, S::kBytes, stream>>>(ma, mb, mo, mr, p);
   return cudaGetLastError();
 }
 
@@ -464,11 +524,19 @@ int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
                              cudaStream_t stream) {
+  if (p.a_mode == kAModeTapShift) {
+    switch (block_n) {
+      case 32: return launch_bn<32, 3>(ma, mb, mo, mr, p, grid, stream);
+      case 64: return launch_bn<64, 3>(ma, mb, mo, mr, p, grid, stream);
+      case 128: return launch_bn<128, 3>(ma, mb, mo, mr, p, grid, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (block_n) {
-    case 32: return launch_bn<32>(ma, mb, mo, mr, p, grid, stream);
-    case 64: return launch_bn<64>(ma, mb, mo, mr, p, grid, stream);
-    case 128: return launch_bn<128>(ma, mb, mo, mr, p, grid, stream);
-    case 256: return launch_bn<256>(ma, mb, mo, mr, p, grid, stream);
+    case 32: return launch_bn<32, 1>(ma, mb, mo, mr, p, grid, stream);
+    case 64: return launch_bn<64, 1>(ma, mb, mo, mr, p, grid, stream);
+    case 128: return launch_bn<128, 1>(ma, mb, mo, mr, p, grid, stream);
+    case 256: return launch_bn<256, 1>(ma, mb, mo, mr, p, grid, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -13,6 +13,7 @@ enum AMode : int {
   kAModeTiled = 0,     // A is a plain [M, K] matrix (1x1 stride-1 conv, FC)
   kAModeIm2col = 1,    // TMA im2col, 64-channel chunks, 128B swizzle
   kAModeGatherC8 = 2,  // stem (Cin <= 8): cp.async gather, one K block per filter row
+  kAModeTapShift = 3,  // 3-wide stride-1 filters: one load per filter row, taps by row shift
 };
 
 enum OutMode : int {
@@ -27,6 +28,7 @@ struct ConvParams {
   int a_mode;
   int Ho, Wo, sh, sw, ph, pw, kw, taps, cchunks;
   int H, W;                  // input geometry (gather mode)
+  int Wp;                    // padded-grid width (tap-shift mode): Wo + kw - 1
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
   void* out;
   int ldo, out_off;
@@ -54,7 +56,7 @@ bool encode_tiled_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, ui
                           std::string* err, int swizzle_bytes = 128);
 bool encode_im2col_bf16(CUtensorMap* map, const void* base, int n, int h, int w, int c, int ldc,
                         int kh, int kw, int sh, int sw, int ph, int pw, int chans_per_pixel,
-                        int pixels, bool swizzle128, std::string* err);
+                        int pixels, bool swizzle128, std::string* err, int upper_w_extra = 0);
 
 void set_error(const std::string& msg);
 

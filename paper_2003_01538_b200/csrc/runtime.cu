@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -98,6 +99,16 @@ int64_t packed_k(int cin, int kh, int kw, bool c8, bool flatten, int H, int W) {
   return static_cast<int64_t>(kh) * kw * ((cin + 63) / 64) * 64;
 }
 
+bool env_flag(const char* name, bool dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return !(v[0] == '0' || v[0] == 'n' || v[0] == 'N' || v[0] == 'f' || v[0] == 'F');
+}
+bool tap_shift_enabled() {
+  static const bool on = env_flag("EB_TAPSHIFT", true);
+  return on;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -124,7 +135,11 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   const int Ho = a.flatten ? 1 : conv_out(a.H, a.kh, a.sh, a.ph);
   const int Wo = a.flatten ? 1 : conv_out(a.W, a.kw, a.sw, a.pw);
   if (Ho <= 0 || Wo <= 0) EB_FAIL(EB_E_SHAPE, "conv output would be empty");
-  const int64_t M64 = static_cast<int64_t>(a.B) * Ho * Wo;
+  const int bn_guess = a.block_n ? a.block_n : pick_block_n(a.cout);
+  const bool tap_shift = !tiled && !a.c8_stem && !a.flatten && a.kw == 3 && a.pw == 1 &&
+                         a.sh == 1 && a.sw == 1 && !a.res && !a.out_f32 && bn_guess <= 128 &&
+                         tap_shift_enabled();
+  const int64_t M64 = static_cast<int64_t>(a.B) * Ho * (tap_shift ? Wo + a.kw - 1 : Wo);
   if (M64 > (1ll << 31) - 1) EB_FAIL(EB_E_INVALID, "conv M too large");
   const int M = static_cast<int>(M64);
   const int64_t kpad = packed_k(a.cin, a.kh, a.kw, a.c8_stem, a.flatten, a.H, a.W);
@@ -149,6 +164,14 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     pl.p.x = static_cast<const __nv_bfloat16*>(a.x);
     pl.p.H = a.H;
     pl.p.W = a.W;
+  } else if (tap_shift) {
+    // one 136-pixel load per (filter row, channel chunk) serves taps s = 0..2 by row shift;
+    // tiles walk the padded grid (Wo + 2 columns per row, the 2 extra are dropped)
+    if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, a.cin, a.ldx, a.kh, a.kw, a.sh, a.sw, a.ph,
+                            a.pw, 64, 136, true, &err, a.kw - 1))
+      EB_FAIL(EB_E_INVALID, err);
+    pl.p.a_mode = kAModeTapShift;
+    pl.p.Wp = Wo + a.kw - 1;
   } else {
     if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, a.cin, a.ldx, a.kh, a.kw, a.sh, a.sw, a.ph,
                             a.pw, 64, 128, true, &err))
@@ -158,14 +181,15 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   const int bn = a.block_n ? a.block_n : pick_block_n(a.cout);
   if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn, &err))
     EB_FAIL(EB_E_INVALID, err);
-  const int num_kb = static_cast<int>(kpad / 64);
+  // tap-shift stages cover all kw taps of one filter row
+  const int num_kb = tap_shift ? a.kh * ((a.cin + 63) / 64) : static_cast<int>(kpad / 64);
   const int mt = (M + 127) / 128;
   const int nt = (a.cout + bn - 1) / bn;
   int splits = a.split_k;
   if (splits <= 0) {
     splits = 1;
     const int64_t tiles = static_cast<int64_t>(mt) * nt;
-    if (!a.res && tiles < 148 && num_kb >= 8) {
+    if (!a.res && !tap_shift && tiles < 148 && num_kb >= 8) {
       splits = static_cast<int>(std::min<int64_t>((148 + tiles - 1) / tiles, num_kb / 4));
       splits = std::max(1, std::min(splits, 32));
     }
@@ -208,7 +232,8 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.ws_floats = splits > 1 ? static_cast<size_t>(splits) * M * a.cout : 0;
   const int64_t total = static_cast<int64_t>(mt) * nt * splits;
   pl.grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
-  if (!a.out_f32 && splits == 1) {
+  if (tap_shift && splits != 1) EB_FAIL(EB_E_INVALID, "tap-shift mode does not split K");
+  if (!a.out_f32 && splits == 1 && !tap_shift) {
     const int cw = conv_umma_chunk(bn);
     if (!encode_tiled_2d_bf16(&pl.mo, static_cast<const __nv_bfloat16*>(a.y) + a.y_off, a.cout, M64,
                               a.ldy, cw, 32, &err, cw * 2))
