@@ -50,7 +50,8 @@ struct ConvSmem {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
   static constexpr int kStageOutBytes = 32 * kCW * 2;         // one warp's 32-row chunk
-  static constexpr int kEpiBytes = 4 * 2 * kStageOutBytes * 2 + 4 * BN * 4;
+  static constexpr int kEpiBytes =
+      4 * 2 * kStageOutBytes * 2 + 4 * BN * 4 + ((BN == 128 && TS == 1) ? 2 * 2048 * 4 : 0);
   static constexpr int kFit = (232448 - 1536 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kFit > 8 ? 8 : kFit;
   static_assert(kStages >= 2, "pipeline needs two stages");
@@ -58,7 +59,10 @@ struct ConvSmem {
   // per epilogue warp: 2 output staging buffers + 2 residual buffers
   static constexpr int kResOffset = kOutOffset + 4 * 2 * kStageOutBytes;
   static constexpr int kBiasOffset = kResOffset + 4 * 2 * kStageOutBytes;  // 4 x BN floats
-  static constexpr int kBarOffset = kBiasOffset + 4 * BN * 4;
+  // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
+  static constexpr int kPreMax = (BN == 128 && TS == 1) ? 2048 : 0;
+  static constexpr int kPreOffset = kBiasOffset + 4 * BN * 4;
+  static constexpr int kBarOffset = kPreOffset + 2 * kPreMax * 4;
   static constexpr int kBytes = kBarOffset + 512 + 1024;  // barriers + alignment slack
   static_assert(kBytes <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
@@ -453,45 +457,60 @@ __global__ void __launch_bounds__(kThreads, 1)
     cp_async_wait<0>();
   } else if (p.pre_scale) {
     // ------------------------------------------------------------ A transform
-    // One thread per A row: relu(a * scale[k] + shift[k]) in place on the
-    // swizzled tile, then a proxy fence so the tensor core sees the result.
-    const int r = static_cast<int>(threadIdx.x) - 192;  // 0..127
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const int z = t / (nt * mt);
-      const int kb0 = z * p.kb_per_split;
-      const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
-        uint8_t* rowp = smem + stage * S::kStageBytes + r * 128;
-        const float* sc = p.pre_scale + kb * kBlockK;
-        const float* sh = p.pre_shift + kb * kBlockK;
+    // relu(a * scale[k] + shift[k]) in place on the swizzled A tile, then a proxy
+    // fence so the tensor core sees the result.  Thread t owns logical 16-byte chunk
+    // j = t % 8 (8 channels) of rows 8*(t/8) .. +7: its scale/shift are read once
+    // per stage (from an smem copy of the whole vector), and each warp's accesses
+    // cover whole 128-byte rows (conflict-free).
+    if constexpr (S::kPreMax > 0) {
+      const int t = static_cast<int>(threadIdx.x) - 192;  // 0..127
+      const int j = t & 7;
+      const int r0 = (t >> 3) * 8;
+      float* sc_s = reinterpret_cast<float*>(smem + S::kPreOffset);
+      float* sh_s = sc_s + S::kPreMax;
+      const int kpad = p.num_kb * kBlockK;
+      for (int i = t; i < kpad; i += 128) {
+        sc_s[i] = __ldg(p.pre_scale + i);
+        sh_s[i] = __ldg(p.pre_shift + i);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the four transform warps only
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tt = blockIdx.x; tt < total; tt += gridDim.x) {
+        const int z = tt / (nt * mt);
+        const int kb0 = z * p.kb_per_split;
+        const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int c0 = kb * kBlockK + j * 8;
+          const float4 s0 = *reinterpret_cast<const float4*>(sc_s + c0);
+          const float4 s1 = *reinterpret_cast<const float4*>(sc_s + c0 + 4);
+          const float4 t0 = *reinterpret_cast<const float4*>(sh_s + c0);
+          const float4 t1 = *reinterpret_cast<const float4*>(sh_s + c0 + 4);
+          // packed bf16x2 math: one HFMA2 + one HMNMX2 per channel pair
+          const __nv_bfloat162 sc2[4] = {__floats2bfloat162_rn(s0.x, s0.y), __floats2bfloat162_rn(s0.z, s0.w),
+                                         __floats2bfloat162_rn(s1.x, s1.y), __floats2bfloat162_rn(s1.z, s1.w)};
+          const __nv_bfloat162 sh2[4] = {__floats2bfloat162_rn(t0.x, t0.y), __floats2bfloat162_rn(t0.z, t0.w),
+                                         __floats2bfloat162_rn(t1.x, t1.y), __floats2bfloat162_rn(t1.z, t1.w)};
+          const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
+          mbar_wait(&full[stage], phase);
+          uint8_t* tile = smem + stage * S::kStageBytes;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          uint4* q = reinterpret_cast<uint4*>(rowp + ((ch ^ (r & 7)) * 16));
-          uint4 x = *q;
-          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
-          const float4 s0 = __ldg(reinterpret_cast<const float4*>(sc + ch * 8));
-          const float4 s1 = __ldg(reinterpret_cast<const float4*>(sc + ch * 8 + 4));
-          const float4 t0 = __ldg(reinterpret_cast<const float4*>(sh + ch * 8));
-          const float4 t1 = __ldg(reinterpret_cast<const float4*>(sh + ch * 8 + 4));
-          const float scv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-          const float shv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+          for (int i = 0; i < 8; ++i) {
+            const int r = r0 + i;  // r & 7 == i
+            uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + ((j ^ i) * 16));
+            uint4 x = *q;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(h[e]);
-            h[e] = __floats2bfloat162_rn(fmaxf(fmaf(f.x, scv[2 * e], shv[2 * e]), 0.f),
-                                         fmaxf(fmaf(f.y, scv[2 * e + 1], shv[2 * e + 1]), 0.f));
+            for (int e = 0; e < 4; ++e) h[e] = __hmax2(__hfma2(h[e], sc2[e], sh2[e]), zero2);
+            *q = x;
           }
-          *q = x;
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if ((r & 31) == 0) mbar_arrive(&xfull[stage]);
-        if (++stage == S::kStages) {
-          stage = 0;
-          phase ^= 1;
+          fence_proxy_async_smem();
+          __syncwarp();
+          if ((t & 31) == 0) mbar_arrive(&xfull[stage]);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }

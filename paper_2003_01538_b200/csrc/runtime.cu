@@ -189,8 +189,11 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   if (splits <= 0) {
     splits = 1;
     const int64_t tiles = static_cast<int64_t>(mt) * nt;
-    if (!a.res && !tap_shift && tiles < 148 && num_kb >= 8) {
-      splits = static_cast<int>(std::min<int64_t>((148 + tiles - 1) / tiles, num_kb / 4));
+    // Split K only when the tile grid leaves most SMs idle AND each split keeps a long
+    // K loop: the partial slices cost an extra pass and a second launch (measured on
+    // B200: a 98-tile 7x7 layer is 3x slower split in two than unsplit).
+    if (!a.res && !tap_shift && tiles * 4 <= 148 && num_kb >= 32) {
+      splits = static_cast<int>(std::min<int64_t>(148 / tiles, num_kb / 16));
       splits = std::max(1, std::min(splits, 32));
     }
   }
@@ -223,6 +226,8 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.p.pre_shift = a.pre_shift;
   if (a.pre_scale && (pl.p.a_mode != kAModeTiled || !a.pre_shift))
     EB_FAIL(EB_E_INVALID, "pre-activation is only supported on 1x1 (tiled) convolutions");
+  if (a.pre_scale && (bn != 128 || num_kb * 64 > 2048))
+    EB_FAIL(EB_E_INVALID, "pre-activation needs cout in (64, 128] and Cin <= 2048");
   {
     const int q = a.out_f32 ? 4 : 8;  // elements per 16 bytes
     pl.p.vec_ok = (a.ldy % q == 0) && (a.y_off % q == 0) && (!a.res || a.ldr % 8 == 0);

@@ -20,6 +20,8 @@ ap.add_argument("--res", action="store_true")
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--block-n", type=int, default=0)
 ap.add_argument("--stem", action="store_true", help="CIN<=8 image in NHWC8 (gather mode)")
+ap.add_argument("--pre", action="store_true", help="fused BN-ReLU pre-activation on A")
+ap.add_argument("--split", type=int, default=0)
 a = ap.parse_args()
 lib = _lib.load()
 P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
@@ -33,12 +35,15 @@ y = torch.empty(a.B, Ho, Wo, a.COUT, device="cuda", dtype=torch.bfloat16)
 res = torch.randn_like(y) if a.res else None
 bias = torch.randn(a.COUT, device="cuda")
 ws = torch.empty(2 * 148 * 128 * 256, device="cuda")
+kp = (a.CIN + 63) // 64 * 64
+pre_s = torch.rand(kp, device="cuda") if a.pre else None
+pre_t = torch.rand(kp, device="cuda") if a.pre else None
 
 
 def run():
     _lib.check(lib.eb_k_conv(P(x), a.B, a.H, a.W, LD, LD, P(wp), P(bias), P(res),
                              a.COUT if res is not None else 0, P(y), a.COUT, 0, a.COUT, a.KH, a.KW,
-                             a.S, a.S, a.P, a.P, 1, 0, int(a.stem), 0, a.block_n, P(ws), None, None, None))
+                             a.S, a.S, a.P, a.P, 1, 0, int(a.stem), a.split, a.block_n, P(ws), P(pre_s), P(pre_t), None))
 
 
 for _ in range(3):
