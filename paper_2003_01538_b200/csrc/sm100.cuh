@@ -150,6 +150,9 @@ EB_DEVICE void cp_async_16(void* dst, const void* src, uint32_t src_bytes) {
                "r"(src_bytes)
                : "memory");
 }
+EB_DEVICE void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 EB_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // Arrive on the mbarrier when all of this thread's prior cp.async complete
 // (non-blocking; the barrier's expected count includes this arrival).
