@@ -69,7 +69,8 @@ enum {
   EB_OP_POOL = 1,   /* max / avg pooling, optional per-channel BN-ReLU on the input */
   EB_OP_BNRELU = 2, /* y = relu(x * scale + shift) per channel */
   EB_OP_GAP = 3,    /* global average pool (optional BN-ReLU first) -> (1, 1, C) */
-  EB_OP_LIN1 = 4    /* fp64 linear scores of all LIN1 members: (C*H*W) -> (sum K) */
+  EB_OP_LIN1 = 4,   /* fp64 linear scores of all LIN1 members: (C*H*W) -> (sum K) */
+  EB_OP_RESIZE = 5  /* bilinear resize (align_corners=False) of an NHWC image to dst's H x W */
 };
 
 enum { EB_POOL_MAX = 0, EB_POOL_AVG = 1, EB_POOL_AVG_EXCL_PAD = 2 };
@@ -94,6 +95,7 @@ typedef struct {
   int32_t pool_mode;
   int32_t flatten; /* CONV: treat src (H, W, C) as one row of H*W*C features */
   int32_t stream;  /* concurrency lane (0..3); ops on different lanes may overlap */
+  int32_t groups;  /* CONV: grouped convolution (Cin == Cout, block-diagonal per N tile) */
   /* CONV: scale/shift = optional per-input-channel BN-ReLU applied to A inside
    * the kernel (1x1 only; arrays zero-padded to a multiple of 64).
    * POOL/GAP/BNRELU: the same BN-ReLU applied to the input elements. */
@@ -162,8 +164,11 @@ int eb_k_preprocess_u8_nhwc8(const uint8_t* dev_x, void* dev_y_bf16, int batch, 
 int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, const void* dev_w,
               const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
               int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
-              int out_f32, int c8_stem, int split_k, int block_n, void* dev_workspace,
-              const float* dev_pre_scale, const float* dev_pre_shift, void* stream);
+              int out_f32, int c8_stem, int split_k, int block_n, int groups,
+              void* dev_workspace, const float* dev_pre_scale, const float* dev_pre_shift,
+              void* stream);
+int eb_k_resize(const void* dev_x, int ldx, void* dev_y, int ldy, int batch, int h, int w, int c,
+                int ho, int wo, void* stream);
 int eb_k_pool(const void* dev_x, int ldx, void* dev_y, int ldy, int y_off, int batch, int h,
               int w, int c, int k, int s, int pad, int mode, const float* dev_scale,
               const float* dev_shift, void* stream);

@@ -28,6 +28,12 @@ def preprocess_u8(pixels_hwc: np.ndarray, mean, std, pixel_scale: float = 255.0)
     return torch.from_numpy(x.reshape(b, c, h, w))
 
 
+def resize(x_nchw: torch.Tensor, size: int) -> torch.Tensor:
+    """Bilinear, align_corners=False, no antialias (torch.nn.functional.interpolate)."""
+    return torch.nn.functional.interpolate(x_nchw, size=(size, size), mode="bilinear",
+                                           align_corners=False)
+
+
 def set_threads() -> int:
     n = len(os.sched_getaffinity(0))
     torch.set_num_threads(n)

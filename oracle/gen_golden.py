@@ -123,6 +123,10 @@ CNN_SETS = {
     "c1": ([("resnet18", 1), ("densenet121", 2)], 8, 224),
     "c2": ([("resnet50", 3), ("densenet121", 2), ("vgg16", 4)], 4, 224),
     "inception": ([("inception_v3", 5)], 2, 299),
+    # config 5: requests at 299 (the largest member); 224 members see a bilinear resize
+    "c5": ([("resnet152", 6), ("densenet201", 7), ("vgg19", 8), ("inception_v3", 5),
+            ("resnext50_32x4d", 9)], 2, 299),
+    "resnext": ([("resnext50_32x4d", 9)], 4, 224),
 }
 
 
@@ -131,7 +135,7 @@ def gen_cnn(names) -> None:
 
     from oracle import cnn
     from paper_2003_01538_b200 import synth
-    from paper_2003_01538_b200.zoo import build_torch_model
+    from paper_2003_01538_b200.zoo import NATIVE_SIZE, build_torch_model
 
     cnn.set_threads()
     for name in names:
@@ -141,7 +145,9 @@ def gen_cnn(names) -> None:
         logits = []
         for arch, seed in members:
             model = build_torch_model(arch, seed)
-            logits.append(cnn.logits(model, x))
+            native = NATIVE_SIZE.get(arch, 224)
+            xm = x if native == size else cnn.resize(x, native)
+            logits.append(cnn.logits(model, xm))
             del model
         arr = np.stack(logits).astype(np.float32)
         np.savez_compressed(GOLDEN / f"cnn_{name}.npz", logits=arr,

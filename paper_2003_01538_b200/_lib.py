@@ -33,7 +33,7 @@ EB_BF16, EB_F32, EB_F64 = 0, 1, 2
 EB_T_IMAGE_NHWC8 = 0
 EB_T_IMAGE_F32 = 1
 
-EB_OP_CONV, EB_OP_POOL, EB_OP_BNRELU, EB_OP_GAP, EB_OP_LIN1 = 0, 1, 2, 3, 4
+EB_OP_CONV, EB_OP_POOL, EB_OP_BNRELU, EB_OP_GAP, EB_OP_LIN1, EB_OP_RESIZE = 0, 1, 2, 3, 4, 5
 EB_POOL_MAX, EB_POOL_AVG, EB_POOL_AVG_EXCL_PAD = 0, 1, 2
 EB_POLICY_NONE, EB_POLICY_ANY, EB_POLICY_ALL, EB_POLICY_AT_LEAST = 0, 1, 2, 3
 EB_MEMBER_CNN, EB_MEMBER_LIN1 = 0, 1
@@ -52,6 +52,7 @@ class OpDesc(ctypes.Structure):
         ("pool_mode", c_int32),
         ("flatten", c_int32),
         ("stream", c_int32),
+        ("groups", c_int32),
         ("w_off", c_uint64), ("b_off", c_uint64), ("scale_off", c_uint64), ("shift_off", c_uint64),
     ]
 
@@ -93,8 +94,10 @@ _SIGS = {
                                          c_void_p]),
     "eb_k_conv": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
                           c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
-                          c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p,
-                          c_void_p, c_void_p, c_void_p]),
+                          c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                          c_void_p, c_void_p, c_void_p, c_void_p]),
+    "eb_k_resize": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
+                            c_int, c_void_p]),
     "eb_k_pool": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
                           c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "eb_k_gap": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,

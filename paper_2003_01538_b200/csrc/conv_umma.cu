@@ -149,6 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int base_w = ow * p.sw - p.pw;
         const int base_h = oh * p.sh - p.ph;
         const int n0 = tile_n * BN;
+        // grouped conv (block-diagonal weights): this N tile's input channel window
+        const int c_base = p.grouped ? n0 : 0;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
@@ -161,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // tap (r, s) is the same buffer shifted down by s rows
             const int r = kb / p.cchunks;
             const int cc = kb - r * p.cchunks;
-            tma_load_im2col_4d(sa, &map_a, &full[stage], cc * kBlockK, base_w, base_h, img, 0,
-                               static_cast<uint16_t>(r));
+            tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
+                               img, 0, static_cast<uint16_t>(r));
 #pragma unroll
             for (int s2 = 0; s2 < TS; ++s2)
               tma_load_2d(sb + s2 * (BN * 128), &map_b, &full[stage],
@@ -174,8 +176,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int cc = kb - tap * p.cchunks;
             const int r = tap / p.kw;
             const int s = tap - r * p.kw;
-            tma_load_im2col_4d(sa, &map_a, &full[stage], cc * kBlockK, base_w, base_h, img,
-                               static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+            tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
+                               img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
           }  // kAModeGatherC8: A is gathered by warps 6..9
           if (TS == 1) tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
           if (++stage == S::kStages) {

@@ -29,6 +29,7 @@ struct ConvParams {
   int Ho, Wo, sh, sw, ph, pw, kw, taps, cchunks;
   int H, W;                  // input geometry (gather mode)
   int Wp;                    // padded-grid width (tap-shift mode): Wo + kw - 1
+  int grouped;               // grouped conv: N tile t reads input channels [t*BN, t*BN + BN)
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
   void* out;
   int ldo, out_off;

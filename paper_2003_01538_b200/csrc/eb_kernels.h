@@ -24,6 +24,8 @@ cudaError_t k_bnrelu(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy,
                      const float* scale, const float* shift, cudaStream_t st);
 cudaError_t k_gap(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int B, int HW, int C,
                   const float* scale, const float* shift, cudaStream_t st);
+cudaError_t k_resize_bilinear(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, int B,
+                              int H, int W, int C, int Ho, int Wo, cudaStream_t st);
 cudaError_t k_splitk_finalize(const float* ws, int splits, int64_t M, int N, const float* bias,
                               int relu, void* out, int ldo, int out_off, int out_f32,
                               cudaStream_t st);

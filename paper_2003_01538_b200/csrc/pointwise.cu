@@ -288,6 +288,50 @@ cudaError_t k_gap(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int B, int 
   return cudaGetLastError();
 }
 
+// Bilinear resize of an NHWC bf16 image (align_corners=False, no antialias: the
+// semantics of torch.nn.functional.interpolate(mode="bilinear")), 8 channels per thread.
+// K1's second output for members whose native resolution differs from the request's.
+__global__ void resize_bilinear_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
+                                       __nv_bfloat16* __restrict__ y, int ldy, int B, int H, int W,
+                                       int C, int Ho, int Wo) {
+  const int cg = C / 8;
+  const int64_t total = static_cast<int64_t>(B) * Ho * Wo * cg;
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= total) return;
+  const int c = static_cast<int>(i % cg) * 8;
+  int64_t t = i / cg;
+  const int ox = static_cast<int>(t % Wo);
+  t /= Wo;
+  const int oy = static_cast<int>(t % Ho);
+  const int b = static_cast<int>(t / Ho);
+  const float sy = fmaxf((oy + 0.5f) * (static_cast<float>(H) / Ho) - 0.5f, 0.f);
+  const float sx = fmaxf((ox + 0.5f) * (static_cast<float>(W) / Wo) - 0.5f, 0.f);
+  const int y0 = min(static_cast<int>(sy), H - 1), x0 = min(static_cast<int>(sx), W - 1);
+  const int y1 = min(y0 + 1, H - 1), x1 = min(x0 + 1, W - 1);
+  const float ly = sy - y0, lx = sx - x0;
+  const __nv_bfloat16* xb = x + static_cast<int64_t>(b) * H * W * ldx + c;
+  const Vec8 a = load8(xb + (static_cast<int64_t>(y0) * W + x0) * ldx);
+  const Vec8 bq = load8(xb + (static_cast<int64_t>(y0) * W + x1) * ldx);
+  const Vec8 cq = load8(xb + (static_cast<int64_t>(y1) * W + x0) * ldx);
+  const Vec8 d = load8(xb + (static_cast<int64_t>(y1) * W + x1) * ldx);
+  Vec8 o;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float top = a.v[j] + lx * (bq.v[j] - a.v[j]);
+    const float bot = cq.v[j] + lx * (d.v[j] - cq.v[j]);
+    o.v[j] = top + ly * (bot - top);
+  }
+  store8(y + (static_cast<int64_t>(b) * Ho * Wo + static_cast<int64_t>(oy) * Wo + ox) * ldy + c, o);
+}
+
+cudaError_t k_resize_bilinear(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, int B,
+                              int H, int W, int C, int Ho, int Wo, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(B) * Ho * Wo * (C / 8);
+  if (total == 0) return cudaSuccess;
+  resize_bilinear_kernel<<<(total + 255) / 256, 256, 0, st>>>(x, ldx, y, ldy, B, H, W, C, Ho, Wo);
+  return cudaGetLastError();
+}
+
 // Split-K finalisation: y = act(sum_z ws[z] + bias), slices added in ascending z
 // (deterministic, independent of scheduling) -> bf16 slice or fp32.
 __global__ void splitk_finalize_kernel(const float* __restrict__ ws, int splits, int64_t M, int N,

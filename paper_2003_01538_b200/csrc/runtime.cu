@@ -79,6 +79,7 @@ struct ConvArgs {
   int relu, out_f32, c8_stem, flatten;
   int split_k;  // 0 = auto
   int block_n;  // 0 = auto
+  int groups = 1;                    // grouped conv (block-diagonal weights per N tile)
   const float* pre_scale = nullptr;  // pre-activation on A (tiled mode only)
   const float* pre_shift = nullptr;
 };
@@ -130,19 +131,32 @@ struct ConvPlan {
 };
 
 int plan_conv(const ConvArgs& a, ConvPlan* out) {
-  const bool tiled = a.flatten || (a.kh == 1 && a.kw == 1 && a.sh == 1 && a.sw == 1 &&
-                                   a.ph == 0 && a.pw == 0 && !a.c8_stem);
+  const bool tiled = a.groups == 1 &&
+                     (a.flatten || (a.kh == 1 && a.kw == 1 && a.sh == 1 && a.sw == 1 &&
+                                    a.ph == 0 && a.pw == 0 && !a.c8_stem));
   const int Ho = a.flatten ? 1 : conv_out(a.H, a.kh, a.sh, a.ph);
   const int Wo = a.flatten ? 1 : conv_out(a.W, a.kw, a.sw, a.pw);
   if (Ho <= 0 || Wo <= 0) EB_FAIL(EB_E_SHAPE, "conv output would be empty");
-  const int bn_guess = a.block_n ? a.block_n : pick_block_n(a.cout);
+  const int bn_guess = a.block_n ? a.block_n
+                                 : (a.groups > 1 ? std::min(128, pick_block_n(a.cout))
+                                                 : pick_block_n(a.cout));
+  if (a.groups > 1) {
+    // block-diagonal grouped conv: an N tile of BN outputs reads the BN input channels of
+    // its own groups, so groups must not straddle tiles and Cin == Cout
+    const int cpg = a.cout / a.groups;
+    if (a.cin != a.cout || a.cout % a.groups != 0 || bn_guess % cpg != 0 || bn_guess > 128 ||
+        a.c8_stem || a.flatten || a.res)
+      EB_FAIL(EB_E_INVALID, "unsupported grouped convolution geometry");
+  }
   const bool tap_shift = !tiled && !a.c8_stem && !a.flatten && a.kw == 3 && a.pw == 1 &&
                          a.sh == 1 && a.sw == 1 && !a.res && !a.out_f32 && bn_guess <= 128 &&
                          tap_shift_enabled();
   const int64_t M64 = static_cast<int64_t>(a.B) * Ho * (tap_shift ? Wo + a.kw - 1 : Wo);
   if (M64 > (1ll << 31) - 1) EB_FAIL(EB_E_INVALID, "conv M too large");
   const int M = static_cast<int>(M64);
-  const int64_t kpad = packed_k(a.cin, a.kh, a.kw, a.c8_stem, a.flatten, a.H, a.W);
+  const int64_t kpad =
+      a.groups > 1 ? static_cast<int64_t>(a.kh) * a.kw * ((bn_guess + 63) / 64 * 64)
+                   : packed_k(a.cin, a.kh, a.kw, a.c8_stem, a.flatten, a.H, a.W);
   std::string err;
   ConvPlan& pl = *out;
   memset(&pl.p, 0, sizeof(pl.p));
@@ -178,11 +192,12 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
       EB_FAIL(EB_E_INVALID, err);
     pl.p.a_mode = kAModeIm2col;
   }
-  const int bn = a.block_n ? a.block_n : pick_block_n(a.cout);
+  const int bn = bn_guess;
   if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn, &err))
     EB_FAIL(EB_E_INVALID, err);
-  // tap-shift stages cover all kw taps of one filter row
-  const int num_kb = tap_shift ? a.kh * ((a.cin + 63) / 64) : static_cast<int>(kpad / 64);
+  // tap-shift stages cover all kw taps of one filter row; a grouped tile sees BN channels
+  const int cin_tile = a.groups > 1 ? bn : a.cin;
+  const int num_kb = tap_shift ? a.kh * ((cin_tile + 63) / 64) : static_cast<int>(kpad / 64);
   const int mt = (M + 127) / 128;
   const int nt = (a.cout + bn - 1) / bn;
   int splits = a.split_k;
@@ -213,7 +228,8 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.p.pw = a.pw;
   pl.p.kw = a.kw;
   pl.p.taps = a.kh * a.kw;
-  pl.p.cchunks = (a.cin + 63) / 64;
+  pl.p.cchunks = (cin_tile + 63) / 64;
+  pl.p.grouped = a.groups > 1 ? 1 : 0;
   pl.p.res = static_cast<const __nv_bfloat16*>(a.res);
   pl.p.ldr = a.ldr;
   pl.p.bias = a.bias;
@@ -353,6 +369,17 @@ int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
       ++*launches;
     }
   }
+  // K1's resized copies are inputs shared by members on every lane: produce them on the
+  // main stream before the fork.
+  for (const auto& op : e->ops) {
+    if (op.kind != EB_OP_RESIZE) continue;
+    const Tensor& src = e->tensors[op.src];
+    const Tensor& dst = e->tensors[op.dst];
+    EB_CUDA(k_resize_bilinear(static_cast<const __nv_bfloat16*>(src.dev) + op.src_c_off, src.c,
+                              static_cast<__nv_bfloat16*>(dst.dev), dst.c, B, src.h, src.w,
+                              op.src_c, dst.h, dst.w, s));
+    ++*launches;
+  }
   bool used[kLanes] = {};
   for (const auto& op : e->ops) used[op.stream] = true;
   EB_CUDA(cudaEventRecord(e->ev_fork, s));
@@ -401,13 +428,20 @@ int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
         a.pw = op.pw;
         a.relu = op.relu;
         a.out_f32 = dst.dtype == EB_F32;
-        a.c8_stem = op.src == EB_T_IMAGE_NHWC8;
+        // an 8-channel source is a (possibly resized) K1 image: gathered stem mode
+        a.c8_stem = src.c == 8 && op.src_c == 8 && op.src_c_off == 0;
         a.flatten = op.flatten;
+        a.groups = op.groups > 1 ? op.groups : 1;
         a.pre_scale = static_cast<const float*>(P(op.scale_off));
         a.pre_shift = static_cast<const float*>(P(op.shift_off));
         ConvPlan pl;
         int rc = plan_conv(a, &pl);
         if (rc != EB_OK) return rc;
+        static const bool dbg = env_flag("EB_DEBUG_PLAN", false);
+        if (dbg)
+          fprintf(stderr, "[eb] conv src=%d dst=%d mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d x=%p\n",
+                  op.src, op.dst, pl.p.a_mode, pl.block_n, pl.grid, pl.splits, pl.p.M, pl.p.N,
+                  pl.p.num_kb, a.x);
         rc = run_conv_plan(pl, e->ws[op.stream], kSplitWsFloats, a, ls, launches);
         if (rc != EB_OK) return rc;
         break;
@@ -440,6 +474,8 @@ int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
         ++*launches;
         break;
       }
+      case EB_OP_RESIZE:
+        break;  // done before the fork (above)
       case EB_OP_LIN1: {
         const int64_t D = static_cast<int64_t>(src.c) * src.h * src.w;
         EB_CUDA(k_lin1(static_cast<const float*>(src.dev), static_cast<const float*>(P(op.w_off)),
@@ -474,8 +510,9 @@ int run_layers(eb_engine* e, int input_kind, int B) {
     return EB_OK;
   }
   int launches = 0;
-  if (static_cast<int>(e->graphs.size()) >= kMaxGraphs) {
-    return enqueue_layers(e, input_kind, B, &launches);  // cache full: plain launches
+  static const bool no_graph = env_flag("EB_NO_GRAPH", false);
+  if (no_graph || static_cast<int>(e->graphs.size()) >= kMaxGraphs) {
+    return enqueue_layers(e, input_kind, B, &launches);  // plain launches
   }
   EB_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
   int rc = enqueue_layers(e, input_kind, B, &launches);
@@ -686,6 +723,9 @@ int eb_add_op(eb_engine* e, const eb_op_desc* op) {
   } else if (op->kind == EB_OP_LIN1) {
     if (op->src != EB_T_IMAGE_F32 || dst.dtype != EB_F64 || dst.c != op->cout)
       EB_FAIL(EB_E_INVALID, "LIN1 op must read the f32 image and write fp64 scores");
+  } else if (op->kind == EB_OP_RESIZE) {
+    if (src.dtype != EB_BF16 || dst.dtype != EB_BF16 || op->src_c % 8 != 0 || op->dst_c_off != 0)
+      EB_FAIL(EB_E_INVALID, "resize works on bf16 NHWC with 8-channel groups");
   } else if (op->kind == EB_OP_POOL || op->kind == EB_OP_BNRELU || op->kind == EB_OP_GAP) {
     if (src.dtype != EB_BF16 || dst.dtype != EB_BF16) EB_FAIL(EB_E_INVALID, "pool dtypes");
     if (op->src_c % 8 != 0 || op->src_c_off % 8 != 0 || op->dst_c_off % 8 != 0)
@@ -782,6 +822,9 @@ int eb_finalize(eb_engine* e) {
   EB_CUDA(cudaMalloc(&e->d_topk_idx, static_cast<size_t>(n) * mb * e->max_topk * sizeof(int32_t)));
   EB_CUDA(cudaMalloc(&e->d_topk_prob, static_cast<size_t>(n) * mb * e->max_topk * sizeof(float)));
   EB_CUDA(cudaMalloc(&e->d_combined, static_cast<size_t>(mb) * sizeof(int32_t)));
+  // The arena memsets above run on the legacy default stream, which does not order
+  // against the engine's non-blocking streams: drain them before any forward.
+  EB_CUDA(cudaDeviceSynchronize());
   e->finalized = true;
   return EB_OK;
 }
@@ -941,9 +984,11 @@ int eb_k_preprocess_u8_nhwc8(const uint8_t* dev_x, void* dev_y_bf16, int batch, 
 int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, const void* dev_w,
               const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
               int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
-              int out_f32, int c8_stem, int split_k, int block_n, void* dev_workspace,
-              const float* dev_pre_scale, const float* dev_pre_shift, void* stream) {
+              int out_f32, int c8_stem, int split_k, int block_n, int groups,
+              void* dev_workspace, const float* dev_pre_scale, const float* dev_pre_shift,
+              void* stream) {
   ConvArgs a{};
+  a.groups = groups > 1 ? groups : 1;
   a.pre_scale = dev_pre_scale;
   a.pre_shift = dev_pre_shift;
   a.x = dev_x;
@@ -977,6 +1022,14 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
   if (rc != EB_OK) return rc;
   return run_conv_plan(pl, static_cast<float*>(dev_workspace), kSplitWsFloats, a,
                        static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int eb_k_resize(const void* dev_x, int ldx, void* dev_y, int ldy, int batch, int h, int w, int c,
+                int ho, int wo, void* stream) {
+  EB_CUDA(k_resize_bilinear(static_cast<const __nv_bfloat16*>(dev_x), ldx,
+                            static_cast<__nv_bfloat16*>(dev_y), ldy, batch, h, w, c, ho, wo,
+                            static_cast<cudaStream_t>(stream)));
+  return EB_OK;
 }
 
 int eb_k_pool(const void* dev_x, int ldx, void* dev_y, int ldy, int y_off, int batch, int h,

@@ -86,7 +86,7 @@ class Engine:
 
     def op(self, kind, src: TRef, dst: TRef, *, cout=0, res: TRef | None = None, kh=1, kw=1,
            sh=1, sw=1, ph=0, pw=0, relu=0, pool_mode=0, flatten=0, lane=0, w_off=None,
-           b_off=None, scale_off=None, shift_off=None, meta: dict | None = None):
+           b_off=None, scale_off=None, shift_off=None, meta: dict | None = None, groups=1):
         d = OpDesc()
         d.kind = kind
         d.src, d.dst = src.id, dst.id
@@ -95,6 +95,7 @@ class Engine:
         d.dst_c_off, d.cout = dst.c_off, cout
         d.kh, d.kw, d.sh, d.sw, d.ph, d.pw = kh, kw, sh, sw, ph, pw
         d.relu, d.pool_mode, d.flatten, d.stream = int(relu), pool_mode, int(flatten), lane
+        d.groups = int(groups)
         none = _lib.EB_NO_OFFSET
         d.w_off = none if w_off is None else w_off
         d.b_off = none if b_off is None else b_off
@@ -102,7 +103,7 @@ class Engine:
         d.shift_off = none if shift_off is None else shift_off
         check(self.lib.eb_add_op(self._h, byref(d)))
         self.n_ops += 1
-        self.op_meta.append(dict(meta or {}, kind=kind, lane=lane))
+        self.op_meta.append(dict(meta or {}, kind=kind, lane=lane, src=src.id, dst=dst.id))
 
     def member(self, kind, logits: TRef, k_off: int, k: int):
         check(self.lib.eb_add_member(self._h, kind, logits.id, k_off, k))

@@ -222,8 +222,17 @@ def load_ensemble(manifest: ModelManifest, device: int = 0) -> Ensemble:
             raise MalformedModel(f"model file {path} has id {model.id!r} but the manifest says {entry.id!r}")
         loaded.append(model)
     shape = loaded[0].input_shape
+    if all(getattr(m, "kind", "lin1") == "cnn1" for m in loaded) and len(
+            {m.input_shape for m in loaded}) > 1:
+        # Mixed native resolutions (config 5: Inception-v3 at 299 beside 224 members) are
+        # allowed for CNN members only: requests arrive at the largest resolution and K1
+        # emits a bilinear-resized copy for the others.  LIN1 ensembles keep the
+        # reference's uniform-shape rule (eg/ensemble.py:202-208).
+        if len({m.input_shape.dims[0] for m in loaded}) > 1:
+            raise ShapeMismatch("CNN members must agree on the channel count")
+        shape = max((m.input_shape for m in loaded), key=lambda s: s.dims[1] * s.dims[2])
     for m in loaded[1:]:
-        if m.input_shape != shape:
+        if m.input_shape != shape and getattr(m, "kind", "lin1") != "cnn1":
             raise ShapeMismatch(f"model {m.id!r} has input shape {list(m.input_shape.dims)}, "
                                 f"expected {list(shape.dims)} shared by the ensemble")
     for name, vals in (("mean", manifest.preprocess.mean), ("std", manifest.preprocess.std)):
@@ -279,10 +288,13 @@ def build_engine(models, shape, spec, max_batch: int, device: int = 0):
         eng.op(_lib.EB_OP_LIN1, eng.image_f32, scores64, cout=off, lane=0,
                w_off=eng.weight(wcat), b_off=eng.weight(bcat))
     lane = 0
+    images: dict = {}
     for m in models:
         k = len(m.labels)
         if _kind(m) == "cnn1":
-            zoo.lower(eng, m.arch, m.torch_model(), logits32.slice(koffs[m.id], k), lane % 4)
+            img = zoo.resized_image(eng, tuple(m.input_shape.dims[1:]), images)
+            zoo.lower(eng, m.arch, m.torch_model(), logits32.slice(koffs[m.id], k), lane % 4,
+                      image=img)
             lane += 1
             eng.member(_lib.EB_MEMBER_CNN, logits32, koffs[m.id], k)
         else:

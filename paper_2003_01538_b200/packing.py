@@ -91,3 +91,31 @@ def u8_lut(mean, std, pixel_scale: float, channels: int) -> np.ndarray:
         s = std[0] if std.size == 1 else std[c]
         lut[c] = (v - m) / s
     return lut
+
+
+def pick_block_n(cout: int, groups: int = 1) -> int:
+    """The N-tile width the native planner uses (runtime.cu pick_block_n)."""
+    bn = 32 if cout <= 32 else 64 if cout <= 64 else 128 if cout <= 128 else (256 if cout % 256 == 0 else 128)
+    return min(bn, 128) if groups > 1 else bn
+
+
+def pack_grouped_conv_weight(w: torch.Tensor, groups: int, block_n: int) -> torch.Tensor:
+    """Grouped conv (Cin == Cout) as block-diagonal N tiles.
+
+    fp32 [Cout, Cout/groups, kh, kw] -> bf16 [Cout, taps * ceil(BN/64)*64]: output row o
+    (tile t = o // BN) holds its group's weights at input positions relative to the
+    tile's channel window [t*BN, t*BN + BN); everything else is zero.
+    """
+    w = w.detach().to(torch.float32).cpu()
+    cout, cpg, kh, kw = w.shape
+    if block_n % cpg != 0:
+        raise ValueError("a group must not straddle N tiles")
+    taps = kh * kw
+    bpad = _round_up(block_n, 64)
+    out = torch.zeros(cout, taps, bpad, dtype=torch.float32)
+    wt = w.permute(0, 2, 3, 1).reshape(cout, taps, cpg)
+    for o in range(cout):
+        g = o // cpg
+        rel = g * cpg - (o // block_n) * block_n
+        out[o, :, rel:rel + cpg] = wt[o]
+    return out.reshape(cout, -1).to(torch.bfloat16).contiguous()

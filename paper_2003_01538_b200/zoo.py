@@ -27,10 +27,12 @@ import torch.nn as nn
 
 from . import _lib
 from .engine import Engine, TRef
-from .packing import bn_affine, conv_mode, fold_bn, pack_conv_weight
+from .packing import (bn_affine, conv_mode, fold_bn, pack_conv_weight, pack_grouped_conv_weight,
+                      pick_block_n)
 
 ARCHS = (
     "resnet18", "resnet34", "resnet50", "resnet101", "resnet152",
+    "resnext50_32x4d", "resnext101_32x8d",
     "densenet121", "densenet169", "densenet201",
     "vgg11", "vgg13", "vgg16", "vgg19",
     "inception_v3",
@@ -101,8 +103,8 @@ class Lowering:
             ph = pw = 0
             ho = wo = 1
         else:
-            if conv.groups != 1 or conv.dilation != (1, 1):
-                raise NotImplementedError("grouped / dilated convolution")
+            if conv.dilation != (1, 1):
+                raise NotImplementedError("dilated convolution")
             w = conv.weight.detach().float()
             b = conv.bias.detach().float() if conv.bias is not None else None
             if bn is not None:
@@ -111,8 +113,11 @@ class Lowering:
             sh, sw = conv.stride
             ph, pw = conv.padding
             cout = conv.out_channels
-            stem = x.id == _lib.EB_T_IMAGE_NHWC8
-            wp = pack_conv_weight(w, conv_mode(kh, kw, sh, sw, ph, pw, x.c, stem))
+            stem = x.ctot == 8 and x.c == 8  # a K1 image (native or resized)
+            if conv.groups > 1:  # ResNeXt: block-diagonal N tiles
+                wp = pack_grouped_conv_weight(w, conv.groups, pick_block_n(cout, conv.groups))
+            else:
+                wp = pack_conv_weight(w, conv_mode(kh, kw, sh, sw, ph, pw, x.c, stem))
             ho = (x.h + 2 * ph - kh) // sh + 1
             wo = (x.w + 2 * pw - kw) // sw + 1
         if out is None:
@@ -130,7 +135,8 @@ class Lowering:
                 "shape": (ho, wo, cout, kh, kw, sh, x.c), "weight_bytes": 2 * cout * k_alg}
         eng.op(_lib.EB_OP_CONV, x, out, cout=cout, res=res, kh=kh, kw=kw, sh=sh, sw=sw, ph=ph,
                pw=pw, relu=relu, flatten=flatten, lane=self.lane, w_off=w_off, b_off=b_off,
-               scale_off=so, shift_off=sho, meta=meta)
+               scale_off=so, shift_off=sho, meta=meta,
+               groups=getattr(conv, "groups", 1))
         return out
 
     def pool(self, x: TRef, k, s, p, mode, out: TRef | None = None, bn=None) -> TRef:
@@ -333,11 +339,16 @@ class Lowering:
         return out
 
 
-def lower(eng: Engine, arch: str, model: nn.Module, logits: TRef, lane: int) -> None:
-    """Declare the ops of one member; its logits land in ``logits`` (fp32 slice)."""
+def lower(eng: Engine, arch: str, model: nn.Module, logits: TRef, lane: int,
+          image: TRef | None = None) -> None:
+    """Declare the ops of one member; its logits land in ``logits`` (fp32 slice).
+
+    ``image`` is the member's K1 input (the engine image, or a resized copy when the
+    member's native resolution differs from the request's).
+    """
     lw = Lowering(eng, lane)
-    x = eng.image
-    if arch.startswith("resnet"):
+    x = image if image is not None else eng.image
+    if arch.startswith("resnet") or arch.startswith("resnext"):
         lw.resnet(model, x, logits)
     elif arch.startswith("densenet"):
         lw.densenet(model, x, logits)
@@ -358,3 +369,15 @@ def packed_parameter_bytes(model: nn.Module) -> int:
         elif isinstance(mod, nn.BatchNorm2d):
             total += 8 * mod.num_features
     return total
+
+
+def resized_image(eng: Engine, size: tuple[int, int], cache: dict) -> TRef:
+    """The K1 image at another resolution (bilinear, align_corners=False), shared by
+    every member of that native size."""
+    if (eng.H, eng.W) == tuple(size):
+        return eng.image
+    if size not in cache:
+        t = eng.tensor(size[0], size[1], 8)
+        eng.op(_lib.EB_OP_RESIZE, eng.image, t, lane=0, meta={"name": "resize"})
+        cache[size] = t
+    return cache[size]

@@ -45,11 +45,16 @@ def _check(logits_gpu, logits_ref, name):
     return report
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "inception"])
+@pytest.mark.parametrize("name", ["c1", "c2", "inception", "resnext", "c5"])
 def test_members_match_golden_logits(tmp_path, name):
+    """Config 5 mixes native resolutions: requests arrive at 299, K1 also emits a
+    bilinear 224 copy for the 224 members (oracle: F.interpolate on the fp32 image)."""
+    from paper_2003_01538_b200.zoo import NATIVE_SIZE
+
     g = np.load(GOLDEN / f"cnn_{name}.npz")
     size, b = int(g["size"]), int(g["batch"])
-    docs = [cnn1_doc(f"{a}_{s}", str(a), int(s), size) for a, s in zip(g["archs"], g["seeds"])]
+    docs = [cnn1_doc(f"{a}_{s}", str(a), int(s), NATIVE_SIZE.get(str(a), 224))
+            for a, s in zip(g["archs"], g["seeds"])]
     ens = build(tmp_path, docs, max_batch=16, mean=IMAGENET_MEAN, std=IMAGENET_STD)
     px = synth.images(b, size, size, 3, seed0=int(g["seed0"]), kind="structured")
     out, _, res = E.predict_u8(ens, px, topk=TOPK, want_logits=True)

@@ -11,7 +11,8 @@ import torch
 import torch.nn.functional as F
 
 from paper_2003_01538_b200 import _lib
-from paper_2003_01538_b200.packing import conv_mode, pack_conv_weight, u8_lut
+from paper_2003_01538_b200.packing import (conv_mode, pack_conv_weight, pack_grouped_conv_weight,
+                                          pick_block_n, u8_lut)
 
 pytestmark = pytest.mark.gpu
 
@@ -23,14 +24,16 @@ def _p(t: torch.Tensor | None):
 
 
 def run_conv(x_nhwc, ldx, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw, *, y_ld=None,
-             y_off=0, out_f32=False, stem=False, split_k=0, block_n=0, pre=None):
+             y_off=0, out_f32=False, stem=False, split_k=0, block_n=0, pre=None, groups=1):
     lib = _lib.load()
     B, H, W, _ = x_nhwc.shape
     cout = w.shape[0]
     Ho = (H + 2 * ph - kh) // sh + 1
     Wo = (W + 2 * pw - kw) // sw + 1
-    mode = conv_mode(kh, kw, sh, sw, ph, pw, cin, stem)
-    wp = pack_conv_weight(w, mode).to(DEV)
+    if groups > 1:
+        wp = pack_grouped_conv_weight(w, groups, block_n or pick_block_n(cout, groups)).to(DEV)
+    else:
+        wp = pack_conv_weight(w, conv_mode(kh, kw, sh, sw, ph, pw, cin, stem)).to(DEV)
     ld = y_ld or cout
     y = torch.zeros(B, Ho, Wo, ld, device=DEV, dtype=torch.float32 if out_f32 else torch.bfloat16)
     ws = torch.empty(2 * 148 * 128 * 256, device=DEV, dtype=torch.float32)
@@ -45,15 +48,16 @@ def run_conv(x_nhwc, ldx, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw, *, y_
     _lib.check(lib.eb_k_conv(
         _p(x_nhwc), B, H, W, ldx, cin, _p(wp), _p(b), _p(res), res.shape[-1] if res is not None else 0,
         _p(y), ld, y_off, cout, kh, kw, sh, sw, ph, pw, int(relu), int(out_f32), int(stem),
-        split_k, block_n, _p(ws), _p(pre_s), _p(pre_t), None))
+        split_k, block_n, groups, _p(ws), _p(pre_s), _p(pre_t), None))
     torch.cuda.synchronize()
     return y
 
 
-def ref_conv(x_nhwc, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw):
+def ref_conv(x_nhwc, cin, w, bias, res, relu, kh, kw, sh, sw, ph, pw, groups=1):
     x = x_nhwc[..., :cin].float().cpu().permute(0, 3, 1, 2)
     wr = w.to(torch.bfloat16).float()
-    y = F.conv2d(x, wr, None if bias is None else bias.float(), stride=(sh, sw), padding=(ph, pw))
+    y = F.conv2d(x, wr, None if bias is None else bias.float(), stride=(sh, sw), padding=(ph, pw),
+                 groups=groups)
     y = y.permute(0, 2, 3, 1)
     if res is not None:
         y = y + res.float().cpu()
@@ -268,3 +272,31 @@ def test_conv_pre_activation_bnrelu():
     r = ref_conv(xa, cin, w, bias, None, True, 1, 1, 1, 1, 0, 0)
     err = (y.float().cpu() - r).abs().max().item()
     assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+
+
+@pytest.mark.parametrize("width,stride", [(128, 1), (256, 2), (512, 1), (1024, 1)])
+def test_grouped_conv_resnext(width, stride):
+    """ResNeXt 3x3 grouped conv (32 groups) as block-diagonal N tiles."""
+    g = torch.Generator().manual_seed(width + stride)
+    B, H = 2, 14
+    x = torch.randn(B, H, H, width, generator=g).to(torch.bfloat16).to(DEV)
+    w = torch.randn(width, width // 32, 3, 3, generator=g) / np.sqrt(9 * width // 32)
+    bias = torch.randn(width, generator=g) * 0.1
+    y = run_conv(x, width, width, w, bias, None, True, 3, 3, stride, stride, 1, 1, groups=32)
+    r = ref_conv(x, width, w, bias, None, True, 3, 3, stride, stride, 1, 1, groups=32)
+    err = (y.float().cpu() - r).abs().max().item()
+    assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+
+
+@pytest.mark.parametrize("hw,out", [((299, 299), (224, 224)), ((224, 224), (299, 299)), ((17, 9), (8, 12))])
+def test_resize_bilinear_matches_interpolate(hw, out):
+    lib = _lib.load()
+    g = torch.Generator().manual_seed(17)
+    B, C = 3, 8
+    x = torch.randn(B, hw[0], hw[1], C, generator=g).to(torch.bfloat16).to(DEV)
+    y = torch.zeros(B, out[0], out[1], C, dtype=torch.bfloat16, device=DEV)
+    _lib.check(lib.eb_k_resize(_p(x), C, _p(y), C, B, hw[0], hw[1], C, out[0], out[1], None))
+    torch.cuda.synchronize()
+    r = F.interpolate(x.float().cpu().permute(0, 3, 1, 2), size=out, mode="bilinear",
+                      align_corners=False).permute(0, 2, 3, 1)
+    assert (y.float().cpu() - r).abs().max().item() < 0.03

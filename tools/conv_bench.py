@@ -22,6 +22,7 @@ ap.add_argument("--block-n", type=int, default=0)
 ap.add_argument("--stem", action="store_true", help="CIN<=8 image in NHWC8 (gather mode)")
 ap.add_argument("--pre", action="store_true", help="fused BN-ReLU pre-activation on A")
 ap.add_argument("--split", type=int, default=0)
+ap.add_argument("--groups", type=int, default=1)
 a = ap.parse_args()
 lib = _lib.load()
 P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
@@ -43,7 +44,7 @@ pre_t = torch.rand(kp, device="cuda") if a.pre else None
 def run():
     _lib.check(lib.eb_k_conv(P(x), a.B, a.H, a.W, LD, LD, P(wp), P(bias), P(res),
                              a.COUT if res is not None else 0, P(y), a.COUT, 0, a.COUT, a.KH, a.KW,
-                             a.S, a.S, a.P, a.P, 1, 0, int(a.stem), a.split, a.block_n, P(ws), P(pre_s), P(pre_t), None))
+                             a.S, a.S, a.P, a.P, 1, 0, int(a.stem), a.split, a.block_n, a.groups, P(ws), P(pre_s), P(pre_t), None))
 
 
 for _ in range(3):
