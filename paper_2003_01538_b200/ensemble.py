@@ -25,17 +25,7 @@ from pathlib import Path
 import numpy as np
 
 from . import _lib
-from .errors import (
-    BadK,
-    BadPolicy,
-    BatchTooLarge,
-    BudgetExceeded,
-    EmptyBatch,
-    MalformedManifest,
-    MalformedModel,
-    PolicyUnavailable,
-    ShapeMismatch,
-)
+from . import errors
 from .models import (
     BINARY_LABELS,
     MODEL_ID_RE,
@@ -70,19 +60,19 @@ class ModelManifest:
 
     def __post_init__(self):
         if self.memory_budget_bytes < 1:
-            raise MalformedManifest(f"memory_budget_bytes must be >= 1, got {self.memory_budget_bytes}")
+            raise errors.MalformedManifest(f"memory_budget_bytes must be >= 1, got {self.memory_budget_bytes}")
         if self.max_batch < 1:
-            raise MalformedManifest(f"max_batch must be >= 1, got {self.max_batch}")
+            raise errors.MalformedManifest(f"max_batch must be >= 1, got {self.max_batch}")
         entries = tuple(self.models)
         if not entries:
-            raise MalformedManifest("manifest needs at least one model entry")
+            raise errors.MalformedManifest("manifest needs at least one model entry")
         ids = [e.id for e in entries]
         dup = sorted({i for i in ids if ids.count(i) > 1})
         if dup:
-            raise MalformedManifest(f"duplicate model ids: {dup}")
+            raise errors.MalformedManifest(f"duplicate model ids: {dup}")
         for e in entries:
             if not isinstance(e.id, str) or not MODEL_ID_RE.fullmatch(e.id):
-                raise MalformedManifest(f"bad model id {e.id!r}")
+                raise errors.MalformedManifest(f"bad model id {e.id!r}")
         object.__setattr__(self, "models", entries)
         object.__setattr__(self, "base_dir", Path(self.base_dir))
 
@@ -93,59 +83,59 @@ class ModelManifest:
 
 def _count(v, name):
     if isinstance(v, bool) or not isinstance(v, int):
-        raise MalformedManifest(f"{name} must be an integer, got {v!r}")
+        raise errors.MalformedManifest(f"{name} must be an integer, got {v!r}")
     return v
 
 
 def _preprocess_spec(raw) -> PreprocessSpec:
     if not isinstance(raw, dict):
-        raise MalformedManifest("preprocess must be an object")
+        raise errors.MalformedManifest("preprocess must be an object")
     unknown = sorted(set(raw) - _PRE_FIELDS)
     if unknown:
-        raise MalformedManifest(f"unknown preprocess fields: {unknown}")
+        raise errors.MalformedManifest(f"unknown preprocess fields: {unknown}")
     for key in ("mean", "std"):
         if key not in raw:
-            raise MalformedManifest(f"preprocess.{key} is required")
+            raise errors.MalformedManifest(f"preprocess.{key} is required")
         vals = raw[key]
         if not isinstance(vals, list) or not vals:
-            raise MalformedManifest(f"preprocess.{key} must be a non-empty array")
+            raise errors.MalformedManifest(f"preprocess.{key} must be a non-empty array")
         for v in vals:
             if isinstance(v, bool) or not isinstance(v, (int, float)):
-                raise MalformedManifest(f"preprocess.{key}: {v!r} is not a number")
+                raise errors.MalformedManifest(f"preprocess.{key}: {v!r} is not a number")
     scale = raw.get("pixel_scale", 255.0)
     if isinstance(scale, bool) or not isinstance(scale, (int, float)):
-        raise MalformedManifest(f"preprocess.pixel_scale must be a number, got {scale!r}")
+        raise errors.MalformedManifest(f"preprocess.pixel_scale must be a number, got {scale!r}")
     try:
         return PreprocessSpec(tuple(raw["mean"]), tuple(raw["std"]), float(scale))
     except ValueError as exc:
-        raise MalformedManifest(f"bad preprocess: {exc}") from exc
+        raise errors.MalformedManifest(f"bad preprocess: {exc}") from exc
 
 
 def load_manifest(data: bytes, base_dir=".") -> ModelManifest:
     try:
         doc = loads_strict(data)
     except ValueError as exc:
-        raise MalformedManifest(f"unreadable manifest: {exc}") from exc
+        raise errors.MalformedManifest(f"unreadable manifest: {exc}") from exc
     if not isinstance(doc, dict):
-        raise MalformedManifest("manifest must be a JSON object")
+        raise errors.MalformedManifest("manifest must be a JSON object")
     unknown = sorted(set(doc) - _MANIFEST_FIELDS)
     if unknown:
-        raise MalformedManifest(f"unknown manifest fields: {unknown}")
+        raise errors.MalformedManifest(f"unknown manifest fields: {unknown}")
     missing = sorted(_MANIFEST_FIELDS - set(doc))
     if missing:
-        raise MalformedManifest(f"missing manifest fields: {missing}")
+        raise errors.MalformedManifest(f"missing manifest fields: {missing}")
     budget = _count(doc["memory_budget_bytes"], "memory_budget_bytes")
     max_batch = _count(doc["max_batch"], "max_batch")
     spec = _preprocess_spec(doc["preprocess"])
     raw_models = doc["models"]
     if not isinstance(raw_models, list):
-        raise MalformedManifest("models must be an array")
+        raise errors.MalformedManifest("models must be an array")
     entries = []
     for i, e in enumerate(raw_models):
         if not isinstance(e, dict) or set(e) != _ENTRY_FIELDS:
-            raise MalformedManifest(f"models[{i}] must be an object with exactly 'id' and 'path'")
+            raise errors.MalformedManifest(f"models[{i}] must be an object with exactly 'id' and 'path'")
         if not isinstance(e["id"], str) or not isinstance(e["path"], str):
-            raise MalformedManifest(f"models[{i}]: id and path must be strings")
+            raise errors.MalformedManifest(f"models[{i}]: id and path must be strings")
         entries.append(ManifestEntry(e["id"], e["path"]))
     return ModelManifest(budget, max_batch, spec, tuple(entries), Path(base_dir))
 
@@ -216,10 +206,10 @@ def load_ensemble(manifest: ModelManifest, device: int = 0) -> Ensemble:
         try:
             data = path.read_bytes()
         except OSError as exc:
-            raise MalformedModel(f"cannot read model file {path}: {exc}") from exc
+            raise errors.MalformedModel(f"cannot read model file {path}: {exc}") from exc
         model = parse_model_file(data)
         if model.id != entry.id:
-            raise MalformedModel(f"model file {path} has id {model.id!r} but the manifest says {entry.id!r}")
+            raise errors.MalformedModel(f"model file {path} has id {model.id!r} but the manifest says {entry.id!r}")
         loaded.append(model)
     shape = loaded[0].input_shape
     if all(getattr(m, "kind", "lin1") == "cnn1" for m in loaded) and len(
@@ -229,19 +219,19 @@ def load_ensemble(manifest: ModelManifest, device: int = 0) -> Ensemble:
         # emits a bilinear-resized copy for the others.  LIN1 ensembles keep the
         # reference's uniform-shape rule (eg/ensemble.py:202-208).
         if len({m.input_shape.dims[0] for m in loaded}) > 1:
-            raise ShapeMismatch("CNN members must agree on the channel count")
+            raise errors.ShapeMismatch("CNN members must agree on the channel count")
         shape = max((m.input_shape for m in loaded), key=lambda s: s.dims[1] * s.dims[2])
     for m in loaded[1:]:
         if m.input_shape != shape and getattr(m, "kind", "lin1") != "cnn1":
-            raise ShapeMismatch(f"model {m.id!r} has input shape {list(m.input_shape.dims)}, "
+            raise errors.ShapeMismatch(f"model {m.id!r} has input shape {list(m.input_shape.dims)}, "
                                 f"expected {list(shape.dims)} shared by the ensemble")
     for name, vals in (("mean", manifest.preprocess.mean), ("std", manifest.preprocess.std)):
         if len(vals) not in (1, shape.channels):
-            raise ShapeMismatch(f"preprocess {name} has {len(vals)} entries; input shape "
+            raise errors.ShapeMismatch(f"preprocess {name} has {len(vals)} entries; input shape "
                                 f"{list(shape.dims)} has {shape.channels} channel(s)")
     used = sum(m.parameter_bytes for m in loaded)
     if used > manifest.memory_budget_bytes:
-        raise BudgetExceeded(f"memory budget exceeded: ensemble needs {used} bytes, "
+        raise errors.BudgetExceeded(f"memory budget exceeded: ensemble needs {used} bytes, "
                              f"budget is {manifest.memory_budget_bytes} bytes")
     return Ensemble(tuple(loaded), shape, manifest.preprocess, used, manifest.memory_budget_bytes,
                     manifest.max_batch, all(m.labels == BINARY_LABELS for m in loaded), device)
@@ -330,11 +320,11 @@ def engine_for(ensemble):
 
 def _validate(ensemble, b: int, dims) -> None:
     if b == 0:
-        raise EmptyBatch("batch has no samples")
+        raise errors.EmptyBatch("batch has no samples")
     if b > ensemble.max_batch:
-        raise BatchTooLarge(f"batch size {b} exceeds max_batch {ensemble.max_batch}")
+        raise errors.BatchTooLarge(f"batch size {b} exceeds max_batch {ensemble.max_batch}")
     if tuple(dims) != tuple(ensemble.shared_shape.dims):
-        raise ShapeMismatch(f"batch shape {list(dims)} does not match ensemble "
+        raise errors.ShapeMismatch(f"batch shape {list(dims)} does not match ensemble "
                             f"input shape {list(ensemble.shared_shape.dims)}")
 
 
@@ -344,7 +334,7 @@ def _count_and_check_spec(ensemble) -> None:
     ch = shape.dims[0] if len(shape.dims) == 3 else 1
     for name, vals in (("mean", spec.mean), ("std", spec.std)):
         if len(vals) not in (1, ch):
-            raise ShapeMismatch(f"{name} has {len(vals)} entries; shape {list(shape.dims)} "
+            raise errors.ShapeMismatch(f"{name} has {len(vals)} entries; shape {list(shape.dims)} "
                                 f"has {ch} channel(s)")
 
 
@@ -352,17 +342,17 @@ def _policy_args(ensemble, policy):
     if policy is None:
         return _lib.EB_POLICY_NONE, 0
     if not ensemble.binary_compatible:
-        raise PolicyUnavailable("policy unavailable: every model must use the labels ['absent', 'present']")
+        raise errors.PolicyUnavailable("policy unavailable: every model must use the labels ['absent', 'present']")
     kind = getattr(policy, "kind", None)
     if kind not in POLICY_CODES:
-        raise BadPolicy(f"unknown policy kind {kind!r}")
+        raise errors.BadPolicy(f"unknown policy kind {kind!r}")
     k = getattr(policy, "k", None)
     if kind == "at_least":
         n = len(ensemble.models)
         if isinstance(k, bool) or not isinstance(k, int):
-            raise BadK(f"k must be an integer, got {k!r}")
+            raise errors.BadK(f"k must be an integer, got {k!r}")
         if not 1 <= k <= n:
-            raise BadK(f"k must be between 1 and {n} for this ensemble, got {k}")
+            raise errors.BadK(f"k must be between 1 and {n} for this ensemble, got {k}")
         return POLICY_CODES[kind], k
     return POLICY_CODES[kind], 0
 
@@ -384,8 +374,8 @@ def predict(ensemble, raw, policy=None, topk: int = 0, want_logits: bool = False
     """
     b = int(raw.data.shape[0])
     _validate(ensemble, b, raw.shape.dims)
+    _count_and_check_spec(ensemble)  # forward's preprocess runs before the policy checks
     pk, kk = _policy_args(ensemble, policy)
-    _count_and_check_spec(ensemble)
     eng = engine_for(ensemble)
     res = eng.forward(np.ascontiguousarray(raw.data, dtype=np.float32), _lib.EB_IN_F32_CHW,
                       topk=topk, policy=pk, policy_k=kk, want_logits=want_logits)
@@ -409,11 +399,11 @@ def forward(ensemble, raw):
 def predict_u8(ensemble, pixels: np.ndarray, policy=None, topk: int = 0, want_logits=False):
     """Raw uint8 (B, H, W, C) images: /pixel_scale and normalisation fused into K1."""
     if pixels.dtype != np.uint8 or pixels.ndim != 4:
-        raise ShapeMismatch("pixels must be a (B, H, W, C) uint8 array")
+        raise errors.ShapeMismatch("pixels must be a (B, H, W, C) uint8 array")
     b, h, w, c = pixels.shape
     _validate(ensemble, b, (c, h, w))
-    pk, kk = _policy_args(ensemble, policy)
     _count_and_check_spec(ensemble)
+    pk, kk = _policy_args(ensemble, policy)
     eng = engine_for(ensemble)
     res = eng.forward(np.ascontiguousarray(pixels), _lib.EB_IN_U8_HWC, topk=topk, policy=pk,
                       policy_k=kk, want_logits=want_logits)

@@ -1,0 +1,144 @@
+"""GPU: the reference's unchanged REST gateway, with the seam installed, answers
+byte-for-byte like the reference itself (config 3's endpoint path)."""
+
+from __future__ import annotations
+
+import concurrent.futures as cf
+import json
+import threading
+import urllib.request
+
+import numpy as np
+import pytest
+
+from helpers import IMAGENET_MEAN, IMAGENET_STD, cnn1_doc, lin1_doc, write_manifest
+from oracle import lin1 as O
+from reference_import import import_reference
+
+eg = import_reference()
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(eg is None, reason="reference not installed")]
+
+
+def _requests(d, rng):
+    from ensemblegate.wire import encode_request, f32le_sample
+
+    reqs = []
+    for b in (1, 2, 5, 16):
+        x = rng.standard_normal((b, d)).astype(np.float32)
+        reqs.append(encode_request([f32le_sample(r, (d,)) for r in x]))
+        reqs.append(encode_request([f32le_sample(r, (d,)) for r in x], {"kind": "any"}))
+        reqs.append(encode_request([f32le_sample(r, (d,)) for r in x], {"kind": "at_least", "k": 2}))
+        reqs.append(encode_request([f32le_sample(r, (d,)) for r in x], {"kind": "at_least", "k": 9}))
+    reqs.append(encode_request([f32le_sample(np.zeros(d + 1), (d + 1,))]))  # shape mismatch
+    reqs.append(b'{"samples": []}')
+    reqs.append(encode_request([f32le_sample(np.zeros(d), (d,))] * 17))  # > max_batch
+    return reqs
+
+
+def _ensemble_docs(d, binary=True):
+    docs = []
+    for s in (31, 32, 33):
+        w, b = O.gen_model_arrays(s, 2 if binary else 4, d)
+        labels = ("absent", "present") if binary else ("a", "b", "c", "d")
+        docs.append(lin1_doc(f"m{s}", (d,), labels, w, b))
+    return docs
+
+
+@pytest.mark.parametrize("binary", [True, False])
+def test_gateway_bytes_match_reference(tmp_path, binary):
+    from ensemblegate.gateway import GatewayApp
+
+    from paper_2003_01538_b200 import seam
+
+    d = 96
+    mp = write_manifest(tmp_path, _ensemble_docs(d, binary), max_batch=16)
+    reqs = _requests(d, np.random.default_rng(4))
+    ref_app = GatewayApp(eg.load_ensemble(eg.load_manifest_file(mp)))
+    expected = [ref_app.handle("POST", "/v1/predict", r) for r in reqs]
+    seam.install()
+    try:
+        app = GatewayApp(eg.gateway.load_ensemble(eg.load_manifest_file(mp)))
+        got = [app.handle("POST", "/v1/predict", r) for r in reqs]
+        assert got == expected
+        assert app.handle("GET", "/v1/models") == ref_app.handle("GET", "/v1/models")
+    finally:
+        seam.uninstall()
+
+
+def test_known_answer_body(tmp_path):
+    from ensemblegate.gateway import GatewayApp
+    from ensemblegate.wire import encode_request, f32le_sample
+
+    from paper_2003_01538_b200 import seam
+
+    mp = write_manifest(tmp_path, [lin1_doc()])
+    seam.install()
+    try:
+        app = GatewayApp(eg.gateway.load_ensemble(eg.load_manifest_file(mp)))
+        body = encode_request([f32le_sample([0.2, 0.9], (2,)), f32le_sample([0.9, 0.2], (2,))])
+        assert app.handle("POST", "/v1/predict", body) == (
+            200, b'{"_batch_size":2,"m1":["present","absent"]}')
+    finally:
+        seam.uninstall()
+
+
+def test_live_server_concurrent_equals_sequential(tmp_path):
+    from ensemblegate.gateway import GatewayApp, GatewayServer
+
+    from paper_2003_01538_b200 import seam
+
+    d = 64
+    mp = write_manifest(tmp_path, _ensemble_docs(d), max_batch=16)
+    reqs = _requests(d, np.random.default_rng(9))[:16]
+    seam.install()
+    try:
+        app = GatewayApp(eg.gateway.load_ensemble(eg.load_manifest_file(mp)))
+        seq = [app.handle("POST", "/v1/predict", r) for r in reqs]
+        server = GatewayServer(("127.0.0.1", 0), app, 8)
+        t = threading.Thread(target=server.serve_forever, kwargs={"poll_interval": 0.05}, daemon=True)
+        t.start()
+        url = f"http://127.0.0.1:{server.port}/v1/predict"
+
+        def post(body):
+            req = urllib.request.Request(url, data=body, method="POST",
+                                         headers={"Content-Type": "application/json"})
+            try:
+                with urllib.request.urlopen(req, timeout=30) as r:
+                    return r.status, r.read()
+            except urllib.error.HTTPError as e:
+                return e.code, e.read()
+
+        with cf.ThreadPoolExecutor(8) as ex:
+            got = list(ex.map(post, reqs * 2))
+        server.shutdown()
+        t.join(5)
+        server.server_close()
+        assert got == seq * 2
+    finally:
+        seam.uninstall()
+
+
+def test_cnn_ensemble_through_endpoint(tmp_path):
+    """A cnn1 ensemble served by the reference gateway (f32le RGB samples)."""
+    from ensemblegate.gateway import GatewayApp
+    from ensemblegate.wire import encode_request, f32le_sample
+
+    from paper_2003_01538_b200 import ensemble as E
+    from paper_2003_01538_b200 import seam, synth
+
+    mp = write_manifest(tmp_path, [cnn1_doc("r18", "resnet18", 1)], max_batch=8,
+                        mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    px = synth.images(3, 224, 224, 3, seed0=77)
+    f32 = px.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0)
+    seam.install()
+    try:
+        ens = eg.gateway.load_ensemble(eg.load_manifest_file(mp))
+        app = GatewayApp(ens)
+        body = encode_request([f32le_sample(x.reshape(-1), (3, 224, 224)) for x in f32])
+        status, out = app.handle("POST", "/v1/predict", body)
+        assert status == 200
+        labels = json.loads(out)["r18"]
+        res, _, _ = E.predict_u8(ens, px)
+        assert labels == [ens.models[0].labels[i] for i in res.per_model[0]]
+    finally:
+        seam.uninstall()
