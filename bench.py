@@ -198,6 +198,8 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time B in {1,8,32,64,128}")
     ap.add_argument("--profile-json", default="", help="write the per-op profile here")
+    ap.add_argument("--minimal", action="store_true",
+                    help="timed steps only (for ncu launch lists): no e2e / latency / profile / cpu")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -276,6 +278,11 @@ def main() -> None:
         dist.barrier()
     value = B * world * args.steps / (dev_ms / 1e3)
 
+    if args.minimal:
+        if rank == 0:
+            print(json.dumps({"minimal": True, "value": value, "ms_per_step": dev_ms / args.steps,
+                              "launches_per_step": n_launch}), flush=True)
+        return
     # ---- e2e: the public C-ABI call with pinned host buffers
     host_np = host.numpy()
     for _ in range(2):
