@@ -28,11 +28,14 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "eb_internal.h"
 #include "sm100.cuh"
 
 namespace eb {
+
+bool pdl_enabled();
 
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // one 128-byte swizzle atom of bf16
@@ -123,6 +126,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: everything above overlapped the previous layer's tail; from here on we read
+  // its output.  Let the next layer's CTAs start their own prologue as SMs free up.
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -536,11 +543,28 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  conv_umma_kernel<BN, TS><<<grid, kThreads, S::kBytes, stream>>>(ma, mb, mo, mr, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = S::kBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, conv_umma_kernel<BN, TS>, ma, mb, mo, mr, p);
 }
 
 int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("EB_PDL");
+    return !(v && (v[0] == '0' || v[0] == 'n' || v[0] == 'N'));
+  }();
+  return on;
+}
 
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,

@@ -142,6 +142,15 @@ EB_DEVICE void tmem_ld32(uint32_t taddr, uint32_t* r) {
 }
 EB_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Wait until the preceding grid in the stream has completed and its memory is visible
+// (no-op when the kernel was not launched with programmatic stream serialization).
+EB_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the next PDL-launched grid to start its prologue now.
+EB_DEVICE void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- cp.async (LDGSTS)
 // 16-byte global->shared copy through L1 (.ca: overlapping windows of
 // neighbouring rows hit the same lines); src_bytes = 0 zero-fills the destination.
