@@ -155,6 +155,15 @@ int eb_profile_ops(eb_engine* e, int input_kind, int batch, float* host_ms, int 
 /* Number of kernels one eb_forward_device launches for this batch size. */
 int eb_launch_count(eb_engine* e, int input_kind, int batch, int* count);
 
+/* F1 wire fast path (host): decode a well-formed f32le /v1/predict body
+ * (eg/wire.py:76-109) straight into host_out (n x prod(dims) floats, e.g. pinned),
+ * base64 decoded in parallel, finiteness checked.  Returns EB_E_INVALID for anything
+ * it does not accept (the caller then uses the reference decoder for its exact error).
+ * The optional "policy" member is returned as a byte range of body. */
+int eb_decode_request(const char* body, uint64_t len, const int32_t* dims, int ndims,
+                      float* host_out, int max_samples, int* n_samples, uint64_t* policy_off,
+                      uint64_t* policy_len);
+
 /* Kernel-level entry points on caller-owned device memory (used by the parity
  * tests; `stream` is a cudaStream_t, NULL = legacy default stream). */
 int eb_k_preprocess_f32(const float* dev_x, float* dev_y, int batch, int c, int64_t plane,

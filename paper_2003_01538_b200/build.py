@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include"), "-I", str(CSRC)]
 
-SOURCES = ["conv_umma.cu", "pointwise.cu", "combine.cu", "runtime.cu", "tmap.cpp"]
+SOURCES = ["conv_umma.cu", "pointwise.cu", "combine.cu", "runtime.cu", "tmap.cpp", "wire_decode.cpp"]
 
 
 def _needs(obj: Path, deps) -> bool:

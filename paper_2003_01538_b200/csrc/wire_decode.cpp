@@ -1,0 +1,255 @@
+// wire_decode.cpp -- F1: native fast path for the /v1/predict request body.
+//
+// The reference decodes requests with json.loads + base64.b64decode + np.frombuffer +
+// np.stack (eg/wire.py:76-109), ~8 ms per 224x224 RGB f32le sample.  This scanner
+// accepts exactly the well-formed f32le case of that protocol:
+//
+//   {"samples": [{"encoding": "f32le", "shape": [...], "data": "<base64>"}, ...],
+//    "policy": {...}}                               (keys in any order, any whitespace)
+//
+// and base64-decodes every sample straight into one caller-provided (pinned) buffer,
+// in parallel across samples, checking finiteness.  Anything else -- another
+// encoding, an unexpected key, a duplicate key, an escape sequence, a shape or length
+// mismatch, invalid base64, a non-finite value -- returns EB_E_INVALID and the caller
+// falls back to the reference decoder, which produces the reference's exact error.
+// The optional "policy" value is returned as a byte range for the caller to parse.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/ensemble_b200.h"
+#include "eb_internal.h"
+
+namespace {
+
+struct Scanner {
+  const char* p;
+  const char* end;
+  bool ok = true;
+
+  void ws() {
+    while (p < end && (*p == ' ' || *p == '\t' || *p == '\n' || *p == '\r')) ++p;
+  }
+  bool lit(char c) {
+    ws();
+    if (p < end && *p == c) {
+      ++p;
+      return true;
+    }
+    return false;
+  }
+  // a JSON string without escapes; returns [b, e)
+  bool str(const char** b, const char** e) {
+    ws();
+    if (p >= end || *p != '"') return false;
+    const char* s = ++p;
+    const char* q = static_cast<const char*>(memchr(p, '"', end - p));
+    if (!q) return false;
+    if (memchr(s, '\\', q - s)) return false;  // escapes: leave to the reference
+    *b = s;
+    *e = q;
+    p = q + 1;
+    return true;
+  }
+  bool integer(long long* v) {
+    ws();
+    const char* s = p;
+    if (p < end && *p == '-') ++p;
+    if (p >= end || *p < '0' || *p > '9') return false;
+    long long x = 0;
+    while (p < end && *p >= '0' && *p <= '9') {
+      x = x * 10 + (*p - '0');
+      if (x > (1ll << 40)) return false;
+      ++p;
+    }
+    if (p < end && (*p == '.' || *p == 'e' || *p == 'E')) return false;
+    *v = (*s == '-') ? -x : x;
+    return true;
+  }
+  // skip any JSON value (used for "policy"); strings may not contain escapes
+  bool skip_value() {
+    ws();
+    if (p >= end) return false;
+    if (*p == '"') {
+      const char *b, *e;
+      return str(&b, &e);
+    }
+    if (*p == '{' || *p == '[') {
+      const char open = *p, close = (*p == '{') ? '}' : ']';
+      ++p;
+      if (lit(close)) return true;
+      for (;;) {
+        if (open == '{') {
+          const char *b, *e;
+          if (!str(&b, &e) || !lit(':')) return false;
+        }
+        if (!skip_value()) return false;
+        if (lit(',')) continue;
+        return lit(close);
+      }
+    }
+    while (p < end && *p != ',' && *p != '}' && *p != ']' && *p != ' ' && *p != '\n' &&
+           *p != '\r' && *p != '\t')
+      ++p;
+    return true;
+  }
+};
+
+bool key_is(const char* b, const char* e, const char* k) {
+  const size_t n = strlen(k);
+  return static_cast<size_t>(e - b) == n && memcmp(b, k, n) == 0;
+}
+
+int8_t kB64[256];
+bool b64_init() {
+  memset(kB64, -1, sizeof(kB64));
+  const char* a = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz0123456789+/";
+  for (int i = 0; i < 64; ++i) kB64[static_cast<unsigned char>(a[i])] = static_cast<int8_t>(i);
+  return true;
+}
+const bool kB64Ready = b64_init();
+
+// strict base64 (as base64.b64decode(validate=True)) into exactly n_out bytes
+bool b64_decode(const char* s, size_t len, uint8_t* out, size_t n_out) {
+  if (len % 4 != 0) return false;
+  size_t pad = 0;
+  if (len >= 1 && s[len - 1] == '=') ++pad;
+  if (len >= 2 && s[len - 2] == '=') ++pad;
+  if (len / 4 * 3 - pad != n_out) return false;
+  size_t o = 0;
+  for (size_t i = 0; i < len; i += 4) {
+    const int a = kB64[static_cast<unsigned char>(s[i])];
+    const int b = kB64[static_cast<unsigned char>(s[i + 1])];
+    const bool last = (i + 4 == len);
+    const int c = (last && pad >= 2) ? 0 : kB64[static_cast<unsigned char>(s[i + 2])];
+    const int d = (last && pad >= 1) ? 0 : kB64[static_cast<unsigned char>(s[i + 3])];
+    if ((a | b | c | d) < 0) return false;
+    const uint32_t v = (a << 18) | (b << 12) | (c << 6) | d;
+    out[o++] = static_cast<uint8_t>(v >> 16);
+    if (o < n_out) out[o++] = static_cast<uint8_t>(v >> 8);
+    if (o < n_out) out[o++] = static_cast<uint8_t>(v);
+  }
+  return true;
+}
+
+struct Sample {
+  const char* data_b;
+  const char* data_e;
+};
+
+}  // namespace
+
+extern "C" int eb_decode_request(const char* body, uint64_t len, const int32_t* dims, int ndims,
+                                 float* out, int max_samples, int* n_samples,
+                                 uint64_t* policy_off, uint64_t* policy_len) {
+  if (!body || !dims || !out || !n_samples || ndims < 1 || ndims > 3) return EB_E_INVALID;
+  int64_t D = 1;
+  for (int i = 0; i < ndims; ++i) D *= dims[i];
+  Scanner sc{body, body + len};
+  std::vector<Sample> samples;
+  bool have_samples = false, have_policy = false;
+  *policy_off = 0;
+  *policy_len = 0;
+  if (!sc.lit('{')) return EB_E_INVALID;
+  if (!sc.lit('}')) {
+    for (;;) {
+      const char *kb, *ke;
+      if (!sc.str(&kb, &ke) || !sc.lit(':')) return EB_E_INVALID;
+      if (key_is(kb, ke, "samples")) {
+        if (have_samples) return EB_E_INVALID;
+        have_samples = true;
+        if (!sc.lit('[')) return EB_E_INVALID;
+        if (sc.lit(']')) return EB_E_INVALID;  // empty: reference error path
+        for (;;) {
+          if (!sc.lit('{')) return EB_E_INVALID;
+          bool h_enc = false, h_shape = false, h_data = false;
+          Sample smp{};
+          for (;;) {
+            const char *fb, *fe;
+            if (!sc.str(&fb, &fe) || !sc.lit(':')) return EB_E_INVALID;
+            if (key_is(fb, fe, "encoding")) {
+              const char *vb, *ve;
+              if (h_enc || !sc.str(&vb, &ve) || !key_is(vb, ve, "f32le")) return EB_E_INVALID;
+              h_enc = true;
+            } else if (key_is(fb, fe, "shape")) {
+              if (h_shape || !sc.lit('[')) return EB_E_INVALID;
+              for (int i = 0; i < ndims; ++i) {
+                long long v;
+                if (!sc.integer(&v) || v != dims[i]) return EB_E_INVALID;
+                if (i + 1 < ndims && !sc.lit(',')) return EB_E_INVALID;
+              }
+              if (!sc.lit(']')) return EB_E_INVALID;
+              h_shape = true;
+            } else if (key_is(fb, fe, "data")) {
+              if (h_data || !sc.str(&smp.data_b, &smp.data_e)) return EB_E_INVALID;
+              h_data = true;
+            } else {
+              return EB_E_INVALID;
+            }
+            if (sc.lit(',')) continue;
+            if (!sc.lit('}')) return EB_E_INVALID;
+            break;
+          }
+          if (!(h_enc && h_shape && h_data)) return EB_E_INVALID;
+          samples.push_back(smp);
+          if (static_cast<int>(samples.size()) > max_samples) return EB_E_TOO_LARGE;
+          if (sc.lit(',')) continue;
+          if (!sc.lit(']')) return EB_E_INVALID;
+          break;
+        }
+      } else if (key_is(kb, ke, "policy")) {
+        if (have_policy) return EB_E_INVALID;
+        have_policy = true;
+        sc.ws();
+        const char* vb = sc.p;
+        if (!sc.skip_value()) return EB_E_INVALID;
+        *policy_off = static_cast<uint64_t>(vb - body);
+        *policy_len = static_cast<uint64_t>(sc.p - vb);
+      } else {
+        return EB_E_INVALID;
+      }
+      if (sc.lit(',')) continue;
+      if (!sc.lit('}')) return EB_E_INVALID;
+      break;
+    }
+  }
+  sc.ws();
+  if (sc.p != sc.end || !have_samples) return EB_E_INVALID;
+
+  const int n = static_cast<int>(samples.size());
+  const size_t nbytes = static_cast<size_t>(D) * 4;
+  std::vector<char> bad(n, 0);
+  auto work = [&](int lo, int hi) {
+    for (int i = lo; i < hi; ++i) {
+      float* dst = out + static_cast<size_t>(i) * D;
+      if (!b64_decode(samples[i].data_b, samples[i].data_e - samples[i].data_b,
+                      reinterpret_cast<uint8_t*>(dst), nbytes)) {
+        bad[i] = 1;
+        continue;
+      }
+      for (int64_t k = 0; k < D; ++k)
+        if (!std::isfinite(dst[k])) {
+          bad[i] = 1;
+          break;
+        }
+    }
+  };
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const int nt = std::min({n, hw, 32});
+  if (nt <= 1 || static_cast<int64_t>(n) * D < (1 << 20)) {
+    work(0, n);
+  } else {
+    std::vector<std::thread> th;
+    const int per = (n + nt - 1) / nt;
+    for (int t = 0; t < nt; ++t) th.emplace_back(work, t * per, std::min(n, (t + 1) * per));
+    for (auto& t : th) t.join();
+  }
+  for (int i = 0; i < n; ++i)
+    if (bad[i]) return EB_E_INVALID;
+  *n_samples = n;
+  return EB_OK;
+}

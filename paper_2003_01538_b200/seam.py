@@ -42,6 +42,7 @@ def install() -> None:
     import ensemblegate.errors as eg_err
     import ensemblegate.gateway as eg_gw
     import ensemblegate.models as eg_models
+    import ensemblegate.wire as eg_wire
 
     from . import ensemble as ours
     from . import errors as our_err
@@ -72,9 +73,32 @@ def install() -> None:
             ensemble = self._require_ensemble()
             if ensemble is None:
                 return 503, eg_gw._error_body("loading", "ensemble is still loading")
-            batch, policy = eg_gw.decode_request(body, pixel_scale=ensemble.preprocess.pixel_scale)
+            decoded = _fast_path(ensemble, body)
+            if decoded is None:  # anything unusual: the reference decoder and its errors
+                batch, policy = eg_gw.decode_request(body, pixel_scale=ensemble.preprocess.pixel_scale)
+            else:
+                batch, policy = decoded
             output, combined, _ = ours.predict(ensemble, batch, policy)
             return 200, eg_gw.dumps_canonical(eg_gw.render_prediction(ensemble, output, combined))
+
+        def _fast_path(ensemble, body):
+            from types import SimpleNamespace
+
+            from .wire import fast_decode
+
+            got = fast_decode(body, ensemble.shared_shape.dims, ensemble.max_batch)
+            if got is None:
+                return None
+            data, policy_raw = got
+            policy = None
+            if policy_raw is not None:
+                try:
+                    policy_obj = eg_wire.loads_strict(policy_raw)
+                except ValueError:
+                    return None
+                policy = eg_wire.parse_policy(policy_obj)
+            # already validated (shape, finiteness) by the native decoder: a view, no copy
+            return SimpleNamespace(data=data, shape=ensemble.shared_shape), policy
 
         _set(eg_gw.GatewayApp, "_predict", _predict)
 

@@ -1,0 +1,82 @@
+"""CPU: the native f32le request decoder (F1) returns exactly what the reference's
+decode_request returns, and declines everything else (so errors stay the reference's)."""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from reference_import import import_reference
+
+eg = import_reference()
+pytestmark = pytest.mark.skipif(eg is None, reason="reference package not importable")
+
+
+def _check_same(body, dims, max_batch=64):
+    from ensemblegate.wire import decode_request
+
+    from paper_2003_01538_b200.wire import fast_decode
+
+    got = fast_decode(body, dims, max_batch, pinned=False)
+    assert got is not None
+    ref_batch, ref_policy = decode_request(body)
+    assert np.array_equal(got[0].view(np.uint32), ref_batch.data.view(np.uint32))
+    if ref_policy is None:
+        assert got[1] is None
+    else:
+        assert eg.parse_policy(json.loads(got[1])) == ref_policy
+
+
+@pytest.mark.parametrize("dims,b", [((2,), 1), ((6,), 5), ((3, 8, 8), 7), ((3, 224, 224), 3)])
+def test_matches_reference_decode(dims, b):
+    from ensemblegate.wire import encode_request, f32le_sample
+
+    rng = np.random.default_rng(b)
+    x = rng.standard_normal((b, int(np.prod(dims)))).astype(np.float32)
+    _check_same(encode_request([f32le_sample(r, dims) for r in x]), dims)
+    _check_same(encode_request([f32le_sample(r, dims) for r in x], {"kind": "at_least", "k": 2}), dims)
+
+
+def test_whitespace_and_key_order():
+    from ensemblegate.wire import f32le_sample
+
+    s = f32le_sample([1.5, -2.0], (2,))
+    body = ('{ "policy" : {"kind":"any"} ,\n "samples": [ {"shape": [ 2 ], "data": "%s",'
+            ' "encoding":"f32le"} ] }' % s["data"]).encode()
+    _check_same(body, (2,))
+
+
+@pytest.mark.parametrize("body", [
+    b'{"samples": []}',
+    b'{"samples": [{"encoding": "pgm", "data": "UDUKMSAxCjI1NQoA"}]}',
+    b'{"samples": [{"encoding": "f32le", "shape": [2], "data": "AAAA"}]}',
+    b'{"samples": [{"encoding": "f32le", "shape": [3], "data": "AACAPwAAAEA="}]}',
+    b'{"samples": [{"encoding": "f32le", "shape": [2], "data": "AACAPwAAAEA=", "x": 1}]}',
+    b'{"samples": [{"encoding": "f32le", "shape": [2], "data": "AACAPwAAgH8="}]}',  # inf
+    b'{"samples": [{"encoding": "f32le", "shape": [2], "data": "AACAPwAA\\nAEA="}]}',
+    b'{"samples": [], "samples": []}',
+    b'{"extra": 1, "samples": [{"encoding": "f32le", "shape": [2], "data": "AACAPwAAAEA="}]}',
+    b'not json',
+])
+def test_declines_everything_else(body):
+    from paper_2003_01538_b200.wire import fast_decode
+
+    assert fast_decode(body, (2,), 8, pinned=False) is None
+
+
+def test_decode_speed_64_rgb():
+    import time
+
+    from ensemblegate.wire import encode_request, f32le_sample
+
+    from paper_2003_01538_b200.wire import fast_decode
+
+    x = np.random.default_rng(0).random((64, 3 * 224 * 224), dtype=np.float32)
+    body = encode_request([f32le_sample(r, (3, 224, 224)) for r in x])
+    t = time.perf_counter()
+    got = fast_decode(body, (3, 224, 224), 64, pinned=False)
+    dt = time.perf_counter() - t
+    assert got is not None and np.array_equal(got[0], x)
+    assert dt < 0.5, dt  # the reference takes ~0.4 s on 8 cores for this body
