@@ -96,6 +96,8 @@ typedef struct {
   int32_t flatten; /* CONV: treat src (H, W, C) as one row of H*W*C features */
   int32_t stream;  /* concurrency lane (0..3); ops on different lanes may overlap */
   int32_t groups;  /* CONV: grouped convolution (Cin == Cout, block-diagonal per N tile) */
+  int32_t prefork; /* run on the main stream before the lanes fork (shared inputs) */
+  int32_t dst2, dst2_c_off, n_split; /* CONV grouped launch: columns >= n_split -> dst2 */
   /* CONV: scale/shift = optional per-input-channel BN-ReLU applied to A inside
    * the kernel (1x1 only; arrays zero-padded to a multiple of 64).
    * POOL/GAP/BNRELU: the same BN-ReLU applied to the input elements. */

@@ -53,6 +53,8 @@ class OpDesc(ctypes.Structure):
         ("flatten", c_int32),
         ("stream", c_int32),
         ("groups", c_int32),
+        ("prefork", c_int32),
+        ("dst2", c_int32), ("dst2_c_off", c_int32), ("n_split", c_int32),
         ("w_off", c_uint64), ("b_off", c_uint64), ("scale_off", c_uint64), ("shift_off", c_uint64),
     ]
 

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
     if (p.out_mode == kOutBF16) tma_prefetch_desc(&map_out);
-    if (p.res) tma_prefetch_desc(&map_res);
+    if (p.res || p.n_split) tma_prefetch_desc(&map_res);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -408,7 +408,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&map_out, buf, n, m_slab);
+          // a grouped launch (members sharing a stem) writes its second column range
+          // to another tensor through the residual map slot
+          if (p.n_split > 0 && n >= p.n_split)
+            tma_store_2d(&map_res, buf, n - p.n_split, m_slab);
+          else
+            tma_store_2d(&map_out, buf, n, m_slab);
           bulk_commit();
         }
         obuf ^= 1;

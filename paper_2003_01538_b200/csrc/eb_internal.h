@@ -30,6 +30,7 @@ struct ConvParams {
   int H, W;                  // input geometry (gather mode)
   int Wp;                    // padded-grid width (tap-shift mode): Wo + kw - 1
   int grouped;               // grouped conv: N tile t reads input channels [t*BN, t*BN + BN)
+  int n_split;               // grouped launch: columns >= n_split are stored through map_res
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
   void* out;
   int ldo, out_off;

@@ -77,6 +77,8 @@ struct ConvArgs {
   int ldy, y_off, cout;
   int kh, kw, sh, sw, ph, pw;
   int relu, out_f32, c8_stem, flatten;
+  void* y2 = nullptr;  // grouped launch: columns >= n_split are written here
+  int ldy2 = 0, y2_off = 0, n_split = 0;
   int split_k;  // 0 = auto
   int block_n;  // 0 = auto
   int groups = 1;                    // grouped conv (block-diagonal weights per N tile)
@@ -254,15 +256,26 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   const int64_t total = static_cast<int64_t>(mt) * nt * splits;
   pl.grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
   if (tap_shift && splits != 1) EB_FAIL(EB_E_INVALID, "tap-shift mode does not split K");
+  if (a.n_split > 0 && (a.res || a.out_f32 || splits != 1 || tap_shift ||
+                        a.n_split % conv_umma_chunk(bn) != 0 || a.n_split >= a.cout))
+    EB_FAIL(EB_E_INVALID, "unsupported grouped-launch split");
+  pl.p.n_split = a.n_split;
   if (!a.out_f32 && splits == 1 && !tap_shift) {
     const int cw = conv_umma_chunk(bn);
-    if (!encode_tiled_2d_bf16(&pl.mo, static_cast<const __nv_bfloat16*>(a.y) + a.y_off, a.cout, M64,
+    const int n1 = a.n_split > 0 ? a.n_split : a.cout;
+    if (!encode_tiled_2d_bf16(&pl.mo, static_cast<const __nv_bfloat16*>(a.y) + a.y_off, n1, M64,
                               a.ldy, cw, 32, &err, cw * 2))
       EB_FAIL(EB_E_INVALID, err);
   } else {
     pl.mo = pl.mb;  // unused: fp32 outputs are stored directly
   }
   pl.mr = pl.mb;
+  if (a.n_split > 0) {
+    const int cw = conv_umma_chunk(bn);
+    if (!encode_tiled_2d_bf16(&pl.mr, static_cast<const __nv_bfloat16*>(a.y2) + a.y2_off,
+                              a.cout - a.n_split, M64, a.ldy2, cw, 32, &err, cw * 2))
+      EB_FAIL(EB_E_INVALID, err);
+  }
   if (a.res) {
     const int cw = conv_umma_chunk(bn);
     if (a.out_f32 || a.ldr % 8 != 0) EB_FAIL(EB_E_INVALID, "residual needs a bf16 output, ldr % 8 == 0");
@@ -340,8 +353,119 @@ struct eb_engine {
 
 namespace {
 
+bool is_prefork(const eb_op_desc& op) { return op.kind == EB_OP_RESIZE || op.prefork; }
+
+// One op on stream ls.
+int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* launches) {
+  const uint8_t* pool = static_cast<const uint8_t*>(e->pool);
+  auto P = [&](uint64_t off) -> const void* {
+    return off == EB_NO_OFFSET ? nullptr : static_cast<const void*>(pool + off);
+  };
+  Tensor& src = e->tensors[op.src];
+  Tensor& dst = e->tensors[op.dst];
+  const size_t es = dsize(src.dtype);
+  const void* x = static_cast<const uint8_t*>(src.dev) + static_cast<size_t>(op.src_c_off) * es;
+  switch (op.kind) {
+    case EB_OP_CONV: {
+      ConvArgs a{};
+      a.x = x;
+      a.B = B;
+      a.H = src.h;
+      a.W = src.w;
+      a.ldx = src.c;
+      a.cin = op.src_c;
+      a.w = P(op.w_off);
+      a.bias = static_cast<const float*>(P(op.b_off));
+      if (op.res >= 0) {
+        a.res = e->tensors[op.res].dev;
+        a.ldr = e->tensors[op.res].c;
+      }
+      a.y = dst.dev;
+      a.ldy = dst.c;
+      a.y_off = op.dst_c_off;
+      a.cout = op.cout;
+      if (op.n_split > 0) {  // grouped launch: columns >= n_split go to dst2
+        const Tensor& d2 = e->tensors[op.dst2];
+        a.y2 = d2.dev;
+        a.ldy2 = d2.c;
+        a.y2_off = op.dst2_c_off;
+        a.n_split = op.n_split;
+      }
+      a.kh = op.kh;
+      a.kw = op.kw;
+      a.sh = op.sh;
+      a.sw = op.sw;
+      a.ph = op.ph;
+      a.pw = op.pw;
+      a.relu = op.relu;
+      a.out_f32 = dst.dtype == EB_F32;
+      // an 8-channel source is a (possibly resized) K1 image: gathered stem mode
+      a.c8_stem = src.c == 8 && op.src_c == 8 && op.src_c_off == 0;
+      a.flatten = op.flatten;
+      a.groups = op.groups > 1 ? op.groups : 1;
+      a.pre_scale = static_cast<const float*>(P(op.scale_off));
+      a.pre_shift = static_cast<const float*>(P(op.shift_off));
+      ConvPlan pl;
+      int rc = plan_conv(a, &pl);
+      if (rc != EB_OK) return rc;
+      static const bool dbg = env_flag("EB_DEBUG_PLAN", false);
+      if (dbg)
+        fprintf(stderr, "[eb] conv src=%d dst=%d mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d\n",
+                op.src, op.dst, pl.p.a_mode, pl.block_n, pl.grid, pl.splits, pl.p.M, pl.p.N,
+                pl.p.num_kb);
+      return run_conv_plan(pl, e->ws[op.stream], kSplitWsFloats, a, ls, launches);
+    }
+    case EB_OP_POOL: {
+      const int Ho = conv_out(src.h, op.kh, op.sh, op.ph);
+      const int Wo = conv_out(src.w, op.kw, op.sw, op.pw);
+      EB_CUDA(k_pool(static_cast<const __nv_bfloat16*>(x), src.c,
+                     static_cast<__nv_bfloat16*>(dst.dev), dst.c, op.dst_c_off, B, src.h, src.w,
+                     op.src_c, Ho, Wo, op.kh, op.sh, op.ph, op.pool_mode,
+                     static_cast<const float*>(P(op.scale_off)),
+                     static_cast<const float*>(P(op.shift_off)), ls));
+      ++*launches;
+      return EB_OK;
+    }
+    case EB_OP_BNRELU: {
+      EB_CUDA(k_bnrelu(static_cast<const __nv_bfloat16*>(x), src.c,
+                       static_cast<__nv_bfloat16*>(dst.dev) + op.dst_c_off, dst.c,
+                       static_cast<int64_t>(B) * src.h * src.w, op.src_c,
+                       static_cast<const float*>(P(op.scale_off)),
+                       static_cast<const float*>(P(op.shift_off)), ls));
+      ++*launches;
+      return EB_OK;
+    }
+    case EB_OP_GAP: {
+      EB_CUDA(k_gap(static_cast<const __nv_bfloat16*>(x), src.c,
+                    static_cast<__nv_bfloat16*>(dst.dev), B, src.h * src.w, op.src_c,
+                    static_cast<const float*>(P(op.scale_off)),
+                    static_cast<const float*>(P(op.shift_off)), ls));
+      ++*launches;
+      return EB_OK;
+    }
+    case EB_OP_RESIZE: {
+      EB_CUDA(k_resize_bilinear(static_cast<const __nv_bfloat16*>(x), src.c,
+                                static_cast<__nv_bfloat16*>(dst.dev), dst.c, B, src.h, src.w,
+                                op.src_c, dst.h, dst.w, ls));
+      ++*launches;
+      return EB_OK;
+    }
+    case EB_OP_LIN1: {
+      const int64_t D = static_cast<int64_t>(src.c) * src.h * src.w;
+      EB_CUDA(k_lin1(static_cast<const float*>(src.dev), static_cast<const float*>(P(op.w_off)),
+                     static_cast<const float*>(P(op.b_off)), e->lin_part,
+                     static_cast<double*>(dst.dev), B, op.cout, D, e->lin_nsplit, ls));
+      *launches += 2;
+      return EB_OK;
+    }
+    default:
+      EB_FAIL(EB_E_INVALID, "unknown op kind");
+  }
+}
+
 // Enqueue preprocess + every op for batch B on e->stream (fork/join over lanes).
-int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
+int enqueue_layers(
+eb_engine* e, int input_kind, int B, int* launches) {
   cudaStream_t s = e->stream;
   const int64_t plane = static_cast<int64_t>(e->H) * e->W;
   Tensor& img8 = e->tensors[EB_T_IMAGE_NHWC8];
@@ -369,130 +493,40 @@ int enqueue_layers(eb_engine* e, int input_kind, int B, int* launches) {
       ++*launches;
     }
   }
-  // K1's resized copies are inputs shared by members on every lane: produce them on the
-  // main stream before the fork.
-  for (const auto& op : e->ops) {
-    if (op.kind != EB_OP_RESIZE) continue;
-    const Tensor& src = e->tensors[op.src];
-    const Tensor& dst = e->tensors[op.dst];
-    EB_CUDA(k_resize_bilinear(static_cast<const __nv_bfloat16*>(src.dev) + op.src_c_off, src.c,
-                              static_cast<__nv_bfloat16*>(dst.dev), dst.c, B, src.h, src.w,
-                              op.src_c, dst.h, dst.w, s));
-    ++*launches;
-  }
-  bool used[kLanes] = {};
-  for (const auto& op : e->ops) used[op.stream] = true;
-  EB_CUDA(cudaEventRecord(e->ev_fork, s));
-  for (int l = 0; l < kLanes; ++l)
-    if (used[l] && l != 0) EB_CUDA(cudaStreamWaitEvent(e->lanes[l], e->ev_fork, 0));
-  const uint8_t* pool = static_cast<const uint8_t*>(e->pool);
-  auto P = [&](uint64_t off) -> const void* {
-    return off == EB_NO_OFFSET ? nullptr : static_cast<const void*>(pool + off);
-  };
-  for (const auto& op : e->ops) {
-    cudaStream_t ls = (op.stream == 0 || e->prof) ? s : e->lanes[op.stream];
-    if (e->prof) {
+  if (e->prof) {
+    // profiling: every op serialised on the main stream in declaration order,
+    // bracketed by events (one elapsed time per op)
+    for (const auto& op : e->ops) {
       cudaEvent_t ev;
       EB_CUDA(cudaEventCreate(&ev));
       e->prof->push_back(ev);
       EB_CUDA(cudaEventRecord(ev, s));
+      const int rc = enqueue_op(e, op, B, s, launches);
+      if (rc != EB_OK) return rc;
     }
-    Tensor& src = e->tensors[op.src];
-    Tensor& dst = e->tensors[op.dst];
-    const size_t es = dsize(src.dtype);
-    const void* x = static_cast<const uint8_t*>(src.dev) + static_cast<size_t>(op.src_c_off) * es;
-    switch (op.kind) {
-      case EB_OP_CONV: {
-        ConvArgs a{};
-        a.x = x;
-        a.B = B;
-        a.H = src.h;
-        a.W = src.w;
-        a.ldx = src.c;
-        a.cin = op.src_c;
-        a.w = P(op.w_off);
-        a.bias = static_cast<const float*>(P(op.b_off));
-        if (op.res >= 0) {
-          a.res = e->tensors[op.res].dev;
-          a.ldr = e->tensors[op.res].c;
-        }
-        a.y = dst.dev;
-        a.ldy = dst.c;
-        a.y_off = op.dst_c_off;
-        a.cout = op.cout;
-        a.kh = op.kh;
-        a.kw = op.kw;
-        a.sh = op.sh;
-        a.sw = op.sw;
-        a.ph = op.ph;
-        a.pw = op.pw;
-        a.relu = op.relu;
-        a.out_f32 = dst.dtype == EB_F32;
-        // an 8-channel source is a (possibly resized) K1 image: gathered stem mode
-        a.c8_stem = src.c == 8 && op.src_c == 8 && op.src_c_off == 0;
-        a.flatten = op.flatten;
-        a.groups = op.groups > 1 ? op.groups : 1;
-        a.pre_scale = static_cast<const float*>(P(op.scale_off));
-        a.pre_shift = static_cast<const float*>(P(op.shift_off));
-        ConvPlan pl;
-        int rc = plan_conv(a, &pl);
-        if (rc != EB_OK) return rc;
-        static const bool dbg = env_flag("EB_DEBUG_PLAN", false);
-        if (dbg)
-          fprintf(stderr, "[eb] conv src=%d dst=%d mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d x=%p\n",
-                  op.src, op.dst, pl.p.a_mode, pl.block_n, pl.grid, pl.splits, pl.p.M, pl.p.N,
-                  pl.p.num_kb, a.x);
-        rc = run_conv_plan(pl, e->ws[op.stream], kSplitWsFloats, a, ls, launches);
-        if (rc != EB_OK) return rc;
-        break;
-      }
-      case EB_OP_POOL: {
-        const int Ho = conv_out(src.h, op.kh, op.sh, op.ph);
-        const int Wo = conv_out(src.w, op.kw, op.sw, op.pw);
-        EB_CUDA(k_pool(static_cast<const __nv_bfloat16*>(x), src.c,
-                       static_cast<__nv_bfloat16*>(dst.dev), dst.c, op.dst_c_off, B, src.h, src.w,
-                       op.src_c, Ho, Wo, op.kh, op.sh, op.ph, op.pool_mode,
-                       static_cast<const float*>(P(op.scale_off)),
-                       static_cast<const float*>(P(op.shift_off)), ls));
-        ++*launches;
-        break;
-      }
-      case EB_OP_BNRELU: {
-        EB_CUDA(k_bnrelu(static_cast<const __nv_bfloat16*>(x), src.c,
-                         static_cast<__nv_bfloat16*>(dst.dev) + op.dst_c_off, dst.c,
-                         static_cast<int64_t>(B) * src.h * src.w, op.src_c,
-                         static_cast<const float*>(P(op.scale_off)),
-                         static_cast<const float*>(P(op.shift_off)), ls));
-        ++*launches;
-        break;
-      }
-      case EB_OP_GAP: {
-        EB_CUDA(k_gap(static_cast<const __nv_bfloat16*>(x), src.c,
-                      static_cast<__nv_bfloat16*>(dst.dev), B, src.h * src.w, op.src_c,
-                      static_cast<const float*>(P(op.scale_off)),
-                      static_cast<const float*>(P(op.shift_off)), ls));
-        ++*launches;
-        break;
-      }
-      case EB_OP_RESIZE:
-        break;  // done before the fork (above)
-      case EB_OP_LIN1: {
-        const int64_t D = static_cast<int64_t>(src.c) * src.h * src.w;
-        EB_CUDA(k_lin1(static_cast<const float*>(src.dev), static_cast<const float*>(P(op.w_off)),
-                       static_cast<const float*>(P(op.b_off)), e->lin_part,
-                       static_cast<double*>(dst.dev), B, op.cout, D, e->lin_nsplit, ls));
-        *launches += 2;
-        break;
-      }
-      default:
-        EB_FAIL(EB_E_INVALID, "unknown op kind");
-    }
-  }
-  if (e->prof) {
     cudaEvent_t ev;
     EB_CUDA(cudaEventCreate(&ev));
     e->prof->push_back(ev);
     EB_CUDA(cudaEventRecord(ev, s));
+    return EB_OK;
+  }
+  // Inputs shared by members on several lanes (K1's resized copies, grouped stems) are
+  // produced on the main stream before the fork.
+  for (const auto& op : e->ops) {
+    if (!is_prefork(op)) continue;
+    const int rc = enqueue_op(e, op, B, s, launches);
+    if (rc != EB_OK) return rc;
+  }
+  bool used[kLanes] = {};
+  for (const auto& op : e->ops)
+    if (!is_prefork(op)) used[op.stream] = true;
+  EB_CUDA(cudaEventRecord(e->ev_fork, s));
+  for (int l = 1; l < kLanes; ++l)
+    if (used[l]) EB_CUDA(cudaStreamWaitEvent(e->lanes[l], e->ev_fork, 0));
+  for (const auto& op : e->ops) {
+    if (is_prefork(op)) continue;
+    const int rc = enqueue_op(e, op, B, op.stream == 0 ? s : e->lanes[op.stream], launches);
+    if (rc != EB_OK) return rc;
   }
   for (int l = 1; l < kLanes; ++l) {
     if (!used[l]) continue;
@@ -720,6 +754,14 @@ int eb_add_op(eb_engine* e, const eb_op_desc* op) {
       EB_FAIL(EB_E_INVALID, "bf16 conv outputs need cout % 8 == 0");
     if (op->res >= 0 && (e->tensors[op->res].h != dst.h || e->tensors[op->res].w != dst.w))
       EB_FAIL(EB_E_SHAPE, "residual geometry");
+    if (op->n_split > 0) {
+      if (op->dst2 < 0 || op->dst2 >= nt || op->res >= 0 || op->n_split >= op->cout)
+        EB_FAIL(EB_E_INVALID, "grouped launch needs dst2 and no residual");
+      const Tensor& d2 = e->tensors[op->dst2];
+      if (d2.h != dst.h || d2.w != dst.w || d2.dtype != EB_BF16 ||
+          op->dst2_c_off + (op->cout - op->n_split) > d2.c || op->dst2_c_off % 8 != 0)
+        EB_FAIL(EB_E_SHAPE, "grouped launch: second destination geometry");
+    }
   } else if (op->kind == EB_OP_LIN1) {
     if (op->src != EB_T_IMAGE_F32 || dst.dtype != EB_F64 || dst.c != op->cout)
       EB_FAIL(EB_E_INVALID, "LIN1 op must read the f32 image and write fp64 scores");

@@ -86,7 +86,8 @@ class Engine:
 
     def op(self, kind, src: TRef, dst: TRef, *, cout=0, res: TRef | None = None, kh=1, kw=1,
            sh=1, sw=1, ph=0, pw=0, relu=0, pool_mode=0, flatten=0, lane=0, w_off=None,
-           b_off=None, scale_off=None, shift_off=None, meta: dict | None = None, groups=1):
+           b_off=None, scale_off=None, shift_off=None, meta: dict | None = None, groups=1,
+           prefork=False, dst2: TRef | None = None, n_split=0):
         d = OpDesc()
         d.kind = kind
         d.src, d.dst = src.id, dst.id
@@ -96,6 +97,10 @@ class Engine:
         d.kh, d.kw, d.sh, d.sw, d.ph, d.pw = kh, kw, sh, sw, ph, pw
         d.relu, d.pool_mode, d.flatten, d.stream = int(relu), pool_mode, int(flatten), lane
         d.groups = int(groups)
+        d.prefork = int(prefork)
+        d.dst2 = dst2.id if dst2 is not None else -1
+        d.dst2_c_off = dst2.c_off if dst2 is not None else 0
+        d.n_split = int(n_split)
         none = _lib.EB_NO_OFFSET
         d.w_off = none if w_off is None else w_off
         d.b_off = none if b_off is None else b_off

@@ -279,18 +279,43 @@ def build_engine(models, shape, spec, max_batch: int, device: int = 0):
                w_off=eng.weight(wcat), b_off=eng.weight(bcat))
     lane = 0
     images: dict = {}
+    torch_models = {m.id: m.torch_model() for m in cnn}
+    # members with an identical first layer on the same image share one grouped launch
+    stem_groups: dict = {}
+    for m in cnn:
+        st = zoo.stem_of(m.arch, torch_models[m.id])
+        if st is None:
+            continue
+        c = st[0]
+        key = (tuple(m.input_shape.dims), c.kernel_size, c.stride, c.padding, c.in_channels)
+        stem_groups.setdefault(key, []).append(m)
+    stem_out: dict = {}
+    if grouped_stems_enabled():
+        for key, group in stem_groups.items():
+            if len(group) < 2:
+                continue
+            img = zoo.resized_image(eng, key[0][1:], images)
+            outs = zoo.grouped_stem(eng, img, [zoo.stem_of(g.arch, torch_models[g.id]) for g in group])
+            for g, o in zip(group, outs):
+                stem_out[g.id] = o
     for m in models:
         k = len(m.labels)
         if _kind(m) == "cnn1":
             img = zoo.resized_image(eng, tuple(m.input_shape.dims[1:]), images)
-            zoo.lower(eng, m.arch, m.torch_model(), logits32.slice(koffs[m.id], k), lane % 4,
-                      image=img)
+            zoo.lower(eng, m.arch, torch_models[m.id], logits32.slice(koffs[m.id], k), lane % 4,
+                      image=img, stem_out=stem_out.get(m.id))
             lane += 1
             eng.member(_lib.EB_MEMBER_CNN, logits32, koffs[m.id], k)
         else:
             eng.member(_lib.EB_MEMBER_LIN1, scores64, koffs[m.id], k)
     eng.finalize()
     return eng
+
+
+def grouped_stems_enabled() -> bool:
+    import os
+
+    return os.environ.get("EB_GROUPED_STEM", "1") not in ("0", "no", "false")
 
 
 def engine_for(ensemble):

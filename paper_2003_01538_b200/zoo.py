@@ -168,8 +168,8 @@ class Lowering:
         return out
 
     # -- architectures -----------------------------------------------------
-    def resnet(self, m, x: TRef, logits: TRef) -> None:
-        x = self.conv(x, m.conv1, m.bn1, relu=True)
+    def resnet(self, m, x: TRef, logits: TRef, stem_out: TRef | None = None) -> None:
+        x = stem_out if stem_out is not None else self.conv(x, m.conv1, m.bn1, relu=True)
         x = self.pool(x, 3, 2, 1, _lib.EB_POOL_MAX)
         for layer in (m.layer1, m.layer2, m.layer3, m.layer4):
             for blk in layer:
@@ -188,9 +188,9 @@ class Lowering:
         x = self.gap(x)
         self.conv(x, m.fc, out=logits)
 
-    def densenet(self, m, x: TRef, logits: TRef) -> None:
+    def densenet(self, m, x: TRef, logits: TRef, stem_out: TRef | None = None) -> None:
         f = m.features
-        x = self.conv(x, f.conv0, f.norm0, relu=True)
+        x = stem_out if stem_out is not None else self.conv(x, f.conv0, f.norm0, relu=True)
         blocks = [getattr(f, f"denseblock{i}") for i in range(1, 5)]
         trans = [getattr(f, f"transition{i}", None) for i in range(1, 5)]
         h = (x.h + 2 - 3) // 2 + 1
@@ -339,8 +339,51 @@ class Lowering:
         return out
 
 
+def stem_of(arch: str, model: nn.Module):
+    """(conv, bn) of the architecture's first layer when it is the shared
+    conv7x7/s2 + BN + ReLU stem of the ResNet / ResNeXt / DenseNet families."""
+    if arch.startswith("resnet") or arch.startswith("resnext"):
+        return model.conv1, model.bn1
+    if arch.startswith("densenet"):
+        return model.features.conv0, model.features.norm0
+    return None
+
+
+def grouped_stem(eng: Engine, image: TRef, stems) -> list[TRef]:
+    """One launch for the identical stems of several members (north star: "where members
+    share an input layout, their first layers run as a grouped launch"): their folded
+    weights are concatenated along Cout, the output is one NHWC tensor, and member i
+    reads its channel slice.  Runs before the lanes fork."""
+    ws, bs, couts = [], [], []
+    c0 = stems[0][0]
+    for conv, bn in stems:
+        w, b = fold_bn(conv.weight.detach().float(), None, bn)
+        ws.append(w)
+        bs.append(b)
+        couts.append(conv.out_channels)
+    w = torch.cat(ws, 0)
+    b = torch.cat(bs, 0)
+    kh, kw = c0.kernel_size
+    sh, sw = c0.stride
+    ph, pw = c0.padding
+    ho = (image.h + 2 * ph - kh) // sh + 1
+    wo = (image.w + 2 * pw - kw) // sw + 1
+    out = eng.tensor(ho, wo, sum(couts))
+    meta = {"name": "conv", "flops": 2 * ho * wo * sum(couts) * w.shape[1] * kh * kw,
+            "shape": (ho, wo, sum(couts), kh, kw, sh, image.c), "weight_bytes": 2 * w[0].numel() * len(w),
+            "grouped_members": len(stems)}
+    eng.op(_lib.EB_OP_CONV, image, out, cout=sum(couts), kh=kh, kw=kw, sh=sh, sw=sw, ph=ph, pw=pw,
+           relu=True, lane=0, w_off=eng.weight(pack_conv_weight(w, "c8")),
+           b_off=eng.weight(b.contiguous()), meta=meta, prefork=True)
+    slices, off = [], 0
+    for c in couts:
+        slices.append(out.slice(off, c))
+        off += c
+    return slices
+
+
 def lower(eng: Engine, arch: str, model: nn.Module, logits: TRef, lane: int,
-          image: TRef | None = None) -> None:
+          image: TRef | None = None, stem_out: TRef | None = None) -> None:
     """Declare the ops of one member; its logits land in ``logits`` (fp32 slice).
 
     ``image`` is the member's K1 input (the engine image, or a resized copy when the
@@ -349,9 +392,9 @@ def lower(eng: Engine, arch: str, model: nn.Module, logits: TRef, lane: int,
     lw = Lowering(eng, lane)
     x = image if image is not None else eng.image
     if arch.startswith("resnet") or arch.startswith("resnext"):
-        lw.resnet(model, x, logits)
+        lw.resnet(model, x, logits, stem_out)
     elif arch.startswith("densenet"):
-        lw.densenet(model, x, logits)
+        lw.densenet(model, x, logits, stem_out)
     elif arch.startswith("vgg"):
         lw.vgg(model, x, logits)
     elif arch == "inception_v3":
