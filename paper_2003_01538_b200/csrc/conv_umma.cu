@@ -52,16 +52,17 @@ struct ConvSmem {
   static constexpr int kBBytes = TS * BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
-  static constexpr int kStageOutBytes = 32 * kCW * 2;         // one warp's 32-row chunk
+  // one warp's 32-row chunk; tap-shift tiles store directly (no staging, no residual)
+  static constexpr int kStageOutBytes = TS == 1 ? 32 * kCW * 2 : 0;
   static constexpr int kEpiBytes =
       4 * 2 * kStageOutBytes * 2 + 4 * BN * 4 + ((BN == 128 && TS == 1) ? 2 * 2048 * 4 : 0);
   static constexpr int kFit = (232448 - 1536 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kFit > 8 ? 8 : kFit;
   static_assert(kStages >= 2, "pipeline needs two stages");
   static constexpr int kOutOffset = kStages * kStageBytes;
-  // per epilogue warp: 2 output staging buffers + 2 residual buffers
-  static constexpr int kResOffset = kOutOffset + 4 * 2 * kStageOutBytes;
-  static constexpr int kBiasOffset = kResOffset + 4 * 2 * kStageOutBytes;  // 4 x BN floats
+  // per epilogue warp: a ring of 4 chunk buffers shared by residual loads and stores
+  static constexpr int kRingBufs = 4;
+  static constexpr int kBiasOffset = kOutOffset + 4 * kRingBufs * kStageOutBytes;  // 4 x BN floats
   // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
   static constexpr int kPreMax = (BN == 128 && TS == 1) ? 2048 : 0;
   static constexpr int kPreOffset = kBiasOffset + 4 * BN * 4;
@@ -92,8 +93,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
-  uint64_t* rfull = tempty + 2;          // [4 warps][2] residual chunk landed
-  uint64_t* xfull = rfull + 8;           // [stages] A tile transformed (pre-activation)
+  uint64_t* rfull = tempty + 2;          // [4 warps][4] residual chunk landed in ring buffer
+  uint64_t* xfull = rfull + 16;          // [stages] A tile transformed (pre-activation)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + S::kStages);
 
   const uint32_t warp = warp_id();
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
     }
-    for (int a = 0; a < 8; ++a) mbar_init(&rfull[a], 1);
+    for (int a = 0; a < 16; ++a) mbar_init(&rfull[a], 1);
     // A-gather mode: 128 per-thread cp.async arrivals; A-transform mode: one arrive per warp
     const uint32_t xcount = p.a_mode == kAModeGatherC8 ? 128u : 4u;
     for (int s = 0; s < S::kStages; ++s) mbar_init(&xfull[s], xcount);
@@ -240,22 +241,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < 6) {
     // ------------------------------------------------------------ epilogue
     // All per-element loops are fully unrolled with predicates so the chunk stays
-    // in registers.  The bias of the current N tile is cached in smem per warp;
-    // the residual arrives by TMA (same 32 x CW swizzled box as the output),
-    // double-buffered one chunk ahead.
+    // in registers.  The bias of the current N tile is cached in smem per warp.  Each
+    // warp owns a ring of 4 swizzled 32 x CW chunk buffers: the residual of every chunk
+    // of a tile is TMA-loaded into the ring as soon as the tile starts (overlapping its
+    // MMAs), the result is written back in place and TMA-stored from there.
     const int ew = static_cast<int>(warp) - 2;
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int lane = static_cast<int>(lane_id());
     const int row = static_cast<int>(quarter * 32) + lane;
     constexpr int CW = S::kCW;
     constexpr int NCH = BN / CW;
-    uint8_t* stage_out = smem + S::kOutOffset + ew * 2 * S::kStageOutBytes;
-    uint8_t* stage_res = smem + S::kResOffset + ew * 2 * S::kStageOutBytes;
+    constexpr int NB = S::kRingBufs;
+    uint8_t* ring = smem + S::kOutOffset + ew * NB * S::kStageOutBytes;
     float* bias_s = reinterpret_cast<float*>(smem + S::kBiasOffset) + ew * BN;
-    uint64_t* rbar = rfull + ew * 2;
-    uint32_t rphase = 0;  // bit b: parity of residual buffer b
+    uint64_t* rbar = rfull + ew * NB;
+    uint32_t rphase = 0;  // bit b: parity of ring buffer b's residual barrier
+    uint32_t seq = 0;     // chunks this warp has staged so far (ring position)
     const bool has_res = p.res != nullptr && p.out_mode == kOutBF16;
-    int obuf = 0;
     int cached_n = -1;
     int j = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
@@ -284,9 +286,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         cached_n = tile_n;
       }
-      if (has_res && lane == 0) {  // residual chunk 0, before waiting for the accumulator
-        mbar_arrive_expect_tx(&rbar[0], S::kStageOutBytes);
-        tma_load_2d(stage_res, &map_res, &rbar[0], n_tile0, m_slab);
+      if (has_res && lane == 0) {
+        // every earlier store has finished reading the ring -> prefetch the whole tile's
+        // residual now, while its MMAs run
+        bulk_wait_read<0>();
+        for (int ci = 0; ci < NCH && n_tile0 + ci * CW < p.N; ++ci) {
+          const uint32_t b = (seq + ci) & (NB - 1);
+          mbar_arrive_expect_tx(&rbar[b], S::kStageOutBytes);
+          tma_load_2d(ring + b * S::kStageOutBytes, &map_res, &rbar[b], n_tile0 + ci * CW, m_slab);
+        }
       }
       mbar_wait(&tfull[acc], (j >> 1) & 1);
       tc_fence_after();
@@ -344,25 +352,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             v[i + 3] += b4.w;
           }
         }
+        const uint32_t b = seq & (NB - 1);
+        uint8_t* buf = ring + b * S::kStageOutBytes;
+        uint8_t* rowp = buf + lane * (CW * 2);
         if (has_res) {
-          const int rb = ci & 1;
-          // prefetch the next chunk's residual into the other buffer
-          if (lane == 0 && ci + 1 < NCH && n + CW < p.N) {
-            mbar_arrive_expect_tx(&rbar[rb ^ 1], S::kStageOutBytes);
-            tma_load_2d(stage_res + (rb ^ 1) * S::kStageOutBytes, &map_res, &rbar[rb ^ 1], n + CW,
-                        m_slab);
-          }
-          mbar_wait(&rbar[rb], (rphase >> rb) & 1u);
-          rphase ^= 1u << rb;
-          const uint8_t* rrow = stage_res + rb * S::kStageOutBytes + lane * (CW * 2);
+          mbar_wait(&rbar[b], (rphase >> b) & 1u);
+          rphase ^= 1u << b;
 #pragma unroll
           for (int ch = 0; ch < CW / 8; ++ch) {
-            const uint4 q = *reinterpret_cast<const uint4*>(rrow + swz_chunk(ch, lane, CW) * 16);
+            const uint4 q = *reinterpret_cast<const uint4*>(rowp + swz_chunk(ch, lane, CW) * 16);
             const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[ch * 8 + e] += __bfloat162float(h[e]);
           }
-          __syncwarp();  // every lane has read the buffer before it is refilled
         }
         if (p.relu) {
 #pragma unroll
@@ -391,11 +393,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
-        // stage the warp's 32 x CW chunk in swizzled smem, then one TMA store
-        uint8_t* buf = stage_out + obuf * S::kStageOutBytes;
-        if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 chunks ago
-        __syncwarp();
-        uint8_t* rowp = buf + lane * (CW * 2);
+        if (!has_res) {
+          // the store that last used this ring buffer (NB chunks ago) has read it
+          if (lane == 0) bulk_wait_read<NB - 1>();
+          __syncwarp();
+        }
+        // (with a residual each lane rewrites the row it just read, in place)
 #pragma unroll
         for (int ch = 0; ch < CW / 8; ++ch) {
           uint4 q;
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_store_2d(&map_out, buf, n, m_slab);
           bulk_commit();
         }
-        obuf ^= 1;
+        ++seq;
       }
       // accumulator drained (all tcgen05.ld of this tile completed above)
       tc_fence_before();
