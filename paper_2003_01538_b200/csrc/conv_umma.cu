@@ -101,7 +101,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int mt = (p.M + kBlockM - 1) / kBlockM;
   const int nt = (p.N + BN - 1) / BN;
   const int splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
-  const int total = mt * nt * splits;
+  // Tile walk.  In multicast mode the two CTAs of a cluster take the two M tiles of a
+  // pair (same N tile, same K range) and each loads half of the shared B tile for both.
+  const uint32_t crank = p.mcast ? cluster_ctarank() : 0;
+  const int mtp = p.mcast ? (mt + 1) / 2 : mt;
+  const int total = mtp * nt * splits;
+  const int t_first = p.mcast ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int t_step = p.mcast ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+  auto decode = [&](int t, int& tm, int& tn, int& z) {
+    tn = t % nt;
+    const int rest = t / nt;
+    const int pm = rest % mtp;
+    z = rest / mtp;
+    tm = p.mcast ? 2 * pm + static_cast<int>(crank) : pm;
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&map_a);
@@ -110,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.res || p.n_split) tma_prefetch_desc(&map_res);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], p.mcast ? 2 : 1);  // multicast: both CTAs' MMAs free a slot
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -125,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
   tc_fence_before();
   __syncthreads();
+  if (p.mcast) cluster_sync();  // the peer's barriers exist before we multicast into it
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // PDL: everything above overlapped the previous layer's tail; from here on we read
@@ -137,11 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int tile_n = t % nt;
-        const int rest = t / nt;
-        const int tile_m = rest % mt;
-        const int z = rest / mt;
+      for (int t = t_first; t < total; t += t_step) {
+        int tile_m, tile_n, z;
+        decode(t, tile_m, tile_n, z);
         const int kb0 = z * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
         const int m0 = tile_m * kBlockM;
@@ -187,7 +199,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
                                img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
           }  // kAModeGatherC8: A is gathered by warps 6..9
-          if (TS == 1) tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
+          if (TS == 1) {
+            if (p.mcast)  // our half of B, written into both CTAs
+              tma_load_2d_mcast(sb + crank * (BN / 2) * 128, &map_b, &full[stage], kb * kBlockK,
+                                n0 + static_cast<int>(crank) * (BN / 2), 0x3);
+            else
+              tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
+          }
           if (++stage == S::kStages) {
             stage = 0;
             phase ^= 1;
@@ -201,8 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int j = 0;  // local tile counter
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
-      const int z = t / (nt * mt);
+    for (int t = t_first; t < total; t += t_step, ++j) {
+      const int z = t / (nt * mtp);
       const int kb0 = z * p.kb_per_split;
       const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
       const int acc = j & 1;
@@ -228,7 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               umma_bf16(tmem_d, adesc, bdesc, idesc, (kb > kb0 || s2 > 0 || k > 0) ? 1u : 0u);
             }
           }
-          umma_commit(&empty[stage]);
+          if (p.mcast)
+            umma_commit_mcast(&empty[stage], 0x3);  // the slot is free in both CTAs
+          else
+            umma_commit(&empty[stage]);
           if (kb == kb1 - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
@@ -260,11 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool has_res = p.res != nullptr && p.out_mode == kOutBF16;
     int cached_n = -1;
     int j = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++j) {
-      const int tile_n = t % nt;
-      const int rest = t / nt;
-      const int tile_m = rest % mt;
-      const int z = rest / mt;
+    for (int t = t_first; t < total; t += t_step, ++j) {
+      int tile_m, tile_n, z;
+      decode(t, tile_m, tile_n, z);
       const int acc = j & 1;
       const int m = tile_m * kBlockM + row;
       bool row_ok = m < p.M;
@@ -438,10 +457,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = static_cast<int>(threadIdx.x) - 192;  // 0..127
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const int rest = t / nt;
-      const int tile_m = rest % mt;
-      const int z = rest / mt;
+    for (int t = t_first; t < total; t += t_step) {
+      int tile_m, tile_n, z;
+      decode(t, tile_m, tile_n, z);
       const int kb0 = z * p.kb_per_split;
       const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
       const int m = tile_m * kBlockM + r;
@@ -493,8 +511,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");  // the four transform warps only
       int stage = 0;
       uint32_t phase = 0;
-      for (int tt = blockIdx.x; tt < total; tt += gridDim.x) {
-        const int z = tt / (nt * mt);
+      for (int tt = t_first; tt < total; tt += t_step) {
+        const int z = tt / (nt * mtp);
         const int kb0 = z * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -534,6 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.mcast) cluster_sync();  // no CTA leaves while its peer may still write into it
   if (warp == 1) tmem_dealloc(tmem_base, 2 * BN < 32 ? 32 : 2 * BN);
 }
 
@@ -556,11 +575,15 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = S::kBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = p.mcast ? 2 : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, conv_umma_kernel<BN, TS>, ma, mb, mo, mr, p);
 }
 

@@ -31,6 +31,7 @@ struct ConvParams {
   int Wp;                    // padded-grid width (tap-shift mode): Wo + kw - 1
   int grouped;               // grouped conv: N tile t reads input channels [t*BN, t*BN + BN)
   int n_split;               // grouped launch: columns >= n_split are stored through map_res
+  int mcast;                 // 2-CTA cluster: M-tile pairs share the B tile via TMA multicast
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
   void* out;
   int ldo, out_off;

@@ -107,6 +107,10 @@ bool env_flag(const char* name, bool dflt) {
   if (!v || !*v) return dflt;
   return !(v[0] == '0' || v[0] == 'n' || v[0] == 'N' || v[0] == 'f' || v[0] == 'F');
 }
+bool mcast_enabled() {
+  static const bool on = env_flag("EB_MCAST", true);
+  return on;
+}
 bool tap_shift_enabled() {
   static const bool on = env_flag("EB_TAPSHIFT", true);
   return on;
@@ -253,8 +257,20 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.block_n = bn;
   pl.splits = splits;
   pl.ws_floats = splits > 1 ? static_cast<size_t>(splits) * M * a.cout : 0;
-  const int64_t total = static_cast<int64_t>(mt) * nt * splits;
-  pl.grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
+  // 2-CTA clusters sharing the B tile (TMA multicast) for MMA-heavy tiles: halves the
+  // per-SM operand traffic of wide-N layers; only for plain TMA A modes.
+  const bool mcast = mcast_enabled() && splits == 1 && bn >= 128 && mt >= 2 && num_kb >= 8 &&
+                     !a.pre_scale && (pl.p.a_mode == kAModeTiled || pl.p.a_mode == kAModeIm2col);
+  pl.p.mcast = mcast ? 1 : 0;
+  if (mcast) {
+    if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn / 2, &err))
+      EB_FAIL(EB_E_INVALID, err);
+    const int64_t pairs = static_cast<int64_t>((mt + 1) / 2) * nt;
+    pl.grid = 2 * static_cast<int>(std::min<int64_t>(pairs, num_sms() / 2));
+  } else {
+    const int64_t total = static_cast<int64_t>(mt) * nt * splits;
+    pl.grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
+  }
   if (tap_shift && splits != 1) EB_FAIL(EB_E_INVALID, "tap-shift mode does not split K");
   if (a.n_split > 0 && (a.res || a.out_f32 || splits != 1 || tap_shift ||
                         a.n_split % conv_umma_chunk(bn) != 0 || a.n_split >= a.cout))

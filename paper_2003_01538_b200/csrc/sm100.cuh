@@ -70,6 +70,25 @@ EB_DEVICE void tma_load_2d(void* dst, const void* map, uint64_t* bar, int c0, in
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// Multicast tile load: the box lands at the same smem offset in every CTA of the
+// cluster named in cta_mask and completes tx bytes on each CTA's mbarrier there.
+EB_DEVICE void tma_load_2d_mcast(void* dst, const void* map, uint64_t* bar, int c0, int c1,
+                                 uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(cta_mask)
+      : "memory");
+}
+EB_DEVICE uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+EB_DEVICE void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 // im2col: coordinates are (c, w, h, n) of the receptive-field origin of the
 // first output pixel of the column; (off_w, off_h) select the filter tap.
 EB_DEVICE void tma_load_im2col_4d(void* dst, const void* map, uint64_t* bar, int c, int w, int h,
@@ -113,6 +132,15 @@ EB_DEVICE void umma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
+      : "memory");
+}
+
+// Arrive on the same mbarrier in every CTA of cta_mask once prior tcgen05 ops complete.
+EB_DEVICE void umma_commit_mcast(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(cta_mask)
       : "memory");
 }
 
