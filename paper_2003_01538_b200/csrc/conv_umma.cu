@@ -43,19 +43,24 @@ constexpr int kThreads = 320;  // 2 control warps + 4 epilogue warps + 4 A-trans
 
 // TS = filter taps consumed per pipeline stage: 1 (one TMA im2col load per tap)
 // or 3 (tap-shift mode: one 136-row load per filter row serves its 3 horizontal taps).
-template <int BN, int TS>
+// PAIR: 2-SM mode (cta_group::2) -- the CTA pair of a cluster runs one M=256 x BN MMA
+// per K step; each CTA stages its own 128 A rows and half of the B tile.
+template <int BN, int TS, bool PAIR>
 struct ConvSmem {
   static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "tile width");
   static constexpr int kARows = TS == 1 ? kBlockM : kBlockM + 8;    // +8: row shifts 0..2
   static constexpr int kALoadBytes = kARows * 128;                  // bytes TMA delivers
   static constexpr int kABytes = (kALoadBytes + 1023) / 1024 * 1024;
-  static constexpr int kBBytes = TS * BN * kBlockK * 2;
+  static constexpr int kBRows = PAIR ? BN / 2 : BN;                 // B rows held per tap
+  static constexpr int kBTapBytes = kBRows * kBlockK * 2;
+  static constexpr int kBBytes = TS * kBTapBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
   // one warp's 32-row chunk; tap-shift tiles store directly (no staging, no residual)
   static constexpr int kStageOutBytes = TS == 1 ? 32 * kCW * 2 : 0;
-  static constexpr int kEpiBytes =
-      4 * 2 * kStageOutBytes * 2 + 4 * BN * 4 + ((BN == 128 && TS == 1) ? 2 * 2048 * 4 : 0);
+  // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
+  static constexpr int kPreMax = (BN == 128 && TS == 1 && !PAIR) ? 2048 : 0;
+  static constexpr int kEpiBytes = 4 * 2 * kStageOutBytes * 2 + 4 * BN * 4 + 2 * kPreMax * 4;
   static constexpr int kFit = (232448 - 1536 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kFit > 8 ? 8 : kFit;
   static_assert(kStages >= 2, "pipeline needs two stages");
@@ -63,8 +68,6 @@ struct ConvSmem {
   // per epilogue warp: a ring of 4 chunk buffers shared by residual loads and stores
   static constexpr int kRingBufs = 4;
   static constexpr int kBiasOffset = kOutOffset + 4 * kRingBufs * kStageOutBytes;  // 4 x BN floats
-  // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
-  static constexpr int kPreMax = (BN == 128 && TS == 1) ? 2048 : 0;
   static constexpr int kPreOffset = kBiasOffset + 4 * BN * 4;
   static constexpr int kBarOffset = kPreOffset + 2 * kPreMax * 4;
   static constexpr int kBytes = kBarOffset + 512 + 1024;  // barriers + alignment slack
@@ -77,13 +80,13 @@ __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
   return cw == 64 ? (chunk ^ (row & 7)) : (chunk ^ ((row >> 1) & 3));
 }
 
-template <int BN, int TS>
+template <int BN, int TS, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_umma_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ CUtensorMap map_out,
                      const __grid_constant__ CUtensorMap map_res, const ConvParams p) {
-  using S = ConvSmem<BN, TS>;
+  using S = ConvSmem<BN, TS, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   // 128B swizzle needs 1024-byte aligned tiles
   // (offset arithmetic on the __shared__ array keeps the address space visible to the
@@ -101,8 +104,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int mt = (p.M + kBlockM - 1) / kBlockM;
   const int nt = (p.N + BN - 1) / BN;
   const int splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
-  // Tile walk.  In multicast mode the two CTAs of a cluster take the two M tiles of a
-  // pair (same N tile, same K range) and each loads half of the shared B tile for both.
+  // Tile walk.  In cluster modes the two CTAs of a cluster take the two M tiles of a
+  // pair (same N tile, same K range).  Multicast mode: each CTA loads half of the shared
+  // B tile into both CTAs and runs its own M=128 MMAs.  PAIR mode: each CTA loads half
+  // of B into its own smem and the leader (rank 0) issues M=256 2-SM MMAs for both.
   const uint32_t crank = p.mcast ? cluster_ctarank() : 0;
   const int mtp = p.mcast ? (mt + 1) / 2 : mt;
   const int total = mtp * nt * splits;
@@ -123,11 +128,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.res || p.n_split) tma_prefetch_desc(&map_res);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], p.mcast ? 2 : 1);  // multicast: both CTAs' MMAs free a slot
+      // multicast: both CTAs' MMAs free a slot; PAIR: the leader's MMAs free it in both
+      mbar_init(&empty[s], (p.mcast && !PAIR) ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], PAIR ? 8 : 4);  // PAIR: the leader waits for both epilogues
     }
     for (int a = 0; a < 16; ++a) mbar_init(&rfull[a], 1);
     // A-gather mode: 128 per-thread cp.async arrivals; A-transform mode: one arrive per warp
@@ -135,7 +141,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < S::kStages; ++s) mbar_init(&xfull[s], xcount);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_alloc_pair(tmem_slot, 2 * BN);
+    else
+      tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
+  }
   tc_fence_before();
   __syncthreads();
   if (p.mcast) cluster_sync();  // the peer's barriers exist before we multicast into it
@@ -175,6 +186,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
+          if constexpr (PAIR) {
+            // both CTAs' loads complete on the leader's barrier, which expects them all
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (S::kALoadBytes + S::kBBytes));
+            const int nb = n0 + static_cast<int>(crank) * S::kBRows;
+            if (TS > 1) {
+              const int r = kb / p.cchunks;
+              const int cc = kb - r * p.cchunks;
+              tma_load_im2col_4d_pair(sa, &map_a, fb, c_base + cc * kBlockK, base_w, base_h, img, 0,
+                                      static_cast<uint16_t>(r));
+#pragma unroll
+              for (int s2 = 0; s2 < TS; ++s2)
+                tma_load_2d_pair(sb + s2 * S::kBTapBytes, &map_b, fb,
+                                 ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, nb);
+            } else {
+              if (p.a_mode == kAModeTiled) {
+                tma_load_2d_pair(sa, &map_a, fb, kb * kBlockK, m0);
+              } else {
+                const int tap = kb / p.cchunks;
+                const int cc = kb - tap * p.cchunks;
+                const int r = tap / p.kw;
+                const int s = tap - r * p.kw;
+                tma_load_im2col_4d_pair(sa, &map_a, fb, c_base + cc * kBlockK, base_w, base_h, img,
+                                        static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+              }
+              tma_load_2d_pair(sb, &map_b, fb, kb * kBlockK, nb);
+            }
+            if (++stage == S::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           mbar_arrive_expect_tx(&full[stage], p.a_mode == kAModeGatherC8
                                                   ? S::kBBytes
                                                   : S::kALoadBytes + S::kBBytes);
@@ -187,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                img, 0, static_cast<uint16_t>(r));
 #pragma unroll
             for (int s2 = 0; s2 < TS; ++s2)
-              tma_load_2d(sb + s2 * (BN * 128), &map_b, &full[stage],
+              tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, &full[stage],
                           ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, n0);
           } else if (p.a_mode == kAModeTiled) {
             tma_load_2d(sa, &map_a, &full[stage], kb * kBlockK, m0);
@@ -212,14 +256,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (p.mcast) {
+        // producer tail: every MMA commit aimed at this CTA's empty barriers (some come
+        // from the peer) has landed before the cluster may tear down
+        for (int i = 0; i < S::kStages; ++i) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(kBlockM, BN);
+    constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * kBlockM : kBlockM, BN);
     int stage = 0;
     uint32_t phase = 0;
     int j = 0;  // local tile counter
-    for (int t = t_first; t < total; t += t_step, ++j) {
+    // PAIR: the peer's MMA warp idles; the leader issues for both CTAs
+    const int t_mma_end = (PAIR && crank != 0) ? 0 : total;
+    for (int t = t_first; t < t_mma_end; t += t_step, ++j) {
       const int z = t / (nt * mtp);
       const int kb0 = z * p.kb_per_split;
       const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
@@ -242,15 +299,24 @@ __global__ void __launch_bounds__(kThreads, 1)
               // applied on absolute smem address bits (base offset field stays 0), which
               // is also what the TMA used when it wrote the tile (verified on B200)
               const uint64_t adesc = umma_desc_sw128(sa + s2 * 128 + k * 32);
-              const uint64_t bdesc = umma_desc_sw128(sb + s2 * (BN * 128) + k * 32);
-              umma_bf16(tmem_d, adesc, bdesc, idesc, (kb > kb0 || s2 > 0 || k > 0) ? 1u : 0u);
+              const uint64_t bdesc = umma_desc_sw128(sb + s2 * S::kBTapBytes + k * 32);
+              const uint32_t accum = (kb > kb0 || s2 > 0 || k > 0) ? 1u : 0u;
+              if constexpr (PAIR)
+                umma_bf16_pair(tmem_d, adesc, bdesc, idesc, accum);
+              else
+                umma_bf16(tmem_d, adesc, bdesc, idesc, accum);
             }
           }
-          if (p.mcast)
-            umma_commit_mcast(&empty[stage], 0x3);  // the slot is free in both CTAs
-          else
-            umma_commit(&empty[stage]);
-          if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+          if constexpr (PAIR) {
+            umma_commit_pair_mcast(&empty[stage], 0x3);
+            if (kb == kb1 - 1) umma_commit_pair_mcast(&tfull[acc], 0x3);
+          } else {
+            if (p.mcast)
+              umma_commit_mcast(&empty[stage], 0x3);  // the slot is free in both CTAs
+            else
+              umma_commit(&empty[stage]);
+            if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+          }
         }
         __syncwarp();
         if (++stage == S::kStages) {
@@ -443,7 +509,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // accumulator drained (all tcgen05.ld of this tile completed above)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR && crank != 0)  // the leader's MMAs write our TMEM: release it there
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        else
+          mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) bulk_wait<0>();
   } else if (p.a_mode == kAModeGatherC8) {
@@ -553,19 +624,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (p.mcast) cluster_sync();  // no CTA leaves while its peer may still write into it
-  if (warp == 1) tmem_dealloc(tmem_base, 2 * BN < 32 ? 32 : 2 * BN);
+  if (warp == 1) {
+    if constexpr (PAIR)
+      tmem_dealloc_pair(tmem_base, 2 * BN);
+    else
+      tmem_dealloc(tmem_base, 2 * BN < 32 ? 32 : 2 * BN);
+  }
 }
 
 // ---------------------------------------------------------------- host side
 
-template <int BN, int TS>
+template <int BN, int TS, bool PAIR>
 static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int grid,
                              cudaStream_t stream) {
-  using S = ConvSmem<BN, TS>;
+  using S = ConvSmem<BN, TS, PAIR>;
   static bool configured = false;  // attribute is per-function; idempotent
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<BN, TS>,
+    cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<BN, TS, PAIR>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -584,7 +660,7 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, conv_umma_kernel<BN, TS>, ma, mb, mo, mr, p);
+  return cudaLaunchKernelEx(&cfg, conv_umma_kernel<BN, TS, PAIR>, ma, mb, mo, mr, p);
 }
 
 int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
@@ -600,19 +676,35 @@ bool pdl_enabled() {
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
                              cudaStream_t stream) {
+  if (p.pair) {
+    if (!p.mcast) return cudaErrorInvalidValue;
+    if (p.a_mode == kAModeTapShift) {
+      switch (block_n) {
+        case 64: return launch_bn<64, 3, true>(ma, mb, mo, mr, p, grid, stream);
+        case 128: return launch_bn<128, 3, true>(ma, mb, mo, mr, p, grid, stream);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+    switch (block_n) {
+      case 64: return launch_bn<64, 1, true>(ma, mb, mo, mr, p, grid, stream);
+      case 128: return launch_bn<128, 1, true>(ma, mb, mo, mr, p, grid, stream);
+      case 256: return launch_bn<256, 1, true>(ma, mb, mo, mr, p, grid, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (p.a_mode == kAModeTapShift) {
     switch (block_n) {
-      case 32: return launch_bn<32, 3>(ma, mb, mo, mr, p, grid, stream);
-      case 64: return launch_bn<64, 3>(ma, mb, mo, mr, p, grid, stream);
-      case 128: return launch_bn<128, 3>(ma, mb, mo, mr, p, grid, stream);
+      case 32: return launch_bn<32, 3, false>(ma, mb, mo, mr, p, grid, stream);
+      case 64: return launch_bn<64, 3, false>(ma, mb, mo, mr, p, grid, stream);
+      case 128: return launch_bn<128, 3, false>(ma, mb, mo, mr, p, grid, stream);
       default: return cudaErrorInvalidValue;
     }
   }
   switch (block_n) {
-    case 32: return launch_bn<32, 1>(ma, mb, mo, mr, p, grid, stream);
-    case 64: return launch_bn<64, 1>(ma, mb, mo, mr, p, grid, stream);
-    case 128: return launch_bn<128, 1>(ma, mb, mo, mr, p, grid, stream);
-    case 256: return launch_bn<256, 1>(ma, mb, mo, mr, p, grid, stream);
+    case 32: return launch_bn<32, 1, false>(ma, mb, mo, mr, p, grid, stream);
+    case 64: return launch_bn<64, 1, false>(ma, mb, mo, mr, p, grid, stream);
+    case 128: return launch_bn<128, 1, false>(ma, mb, mo, mr, p, grid, stream);
+    case 256: return launch_bn<256, 1, false>(ma, mb, mo, mr, p, grid, stream);
     default: return cudaErrorInvalidValue;
   }
 }

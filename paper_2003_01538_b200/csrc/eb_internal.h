@@ -32,6 +32,7 @@ struct ConvParams {
   int grouped;               // grouped conv: N tile t reads input channels [t*BN, t*BN + BN)
   int n_split;               // grouped launch: columns >= n_split are stored through map_res
   int mcast;                 // 2-CTA cluster: M-tile pairs share the B tile via TMA multicast
+  int pair;                  // with mcast: 2-SM MMA (cta_group::2), M = 256 per CTA pair
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
   void* out;
   int ldo, out_off;

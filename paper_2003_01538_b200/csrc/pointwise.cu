@@ -160,73 +160,93 @@ __device__ __forceinline__ void bnrelu8(Vec8& r, const float* scale, const float
 
 // mode 0 = max (padding ignored), 1 = avg count_include_pad, 2 = avg exclude pad.
 // Optional per-channel BN-ReLU applied to every input element before pooling.
-// One thread per (output pixel, 8-channel group); the window loop is unrolled for
-// the common K = 2 / 3 so all window loads are in flight together.
+// One CTA per output row (image b, row oh); the CTA size is a multiple of the number
+// of 8-channel groups, so each thread keeps one channel group (and its BN-ReLU
+// constants, in registers) for the whole row and walks output columns -- 32-bit
+// index math only.  The window loop is unrolled for the common K = 2 / 3 so all
+// window loads are in flight together.
 template <int KT>
-__global__ void pool_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
-                            __nv_bfloat16* __restrict__ y, int ldy, int y_off, int B, int H,
-                            int W, int C, int Ho, int Wo, int kdyn, int s, int pad, int mode,
-                            const float* __restrict__ scale, const float* __restrict__ shift) {
+__global__ void __launch_bounds__(256)
+    pool_kernel(const __nv_bfloat16* __restrict__ x, int ldx, __nv_bfloat16* __restrict__ y,
+                int ldy, int y_off, int H, int W, int C, int Ho, int Wo, int kdyn, int s, int pad,
+                int mode, const float* __restrict__ scale, const float* __restrict__ shift) {
   const int k = KT > 0 ? KT : kdyn;
-  const int cg = C / 8;
-  const int64_t total = static_cast<int64_t>(B) * Ho * Wo * cg;
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= total) return;
-  const int c = static_cast<int>(i % cg) * 8;
-  int64_t t = i / cg;
-  const int ow = static_cast<int>(t % Wo);
-  t /= Wo;
-  const int oh = static_cast<int>(t % Ho);
-  const int b = static_cast<int>(t / Ho);
-  Vec8 acc;
+  const int cg = C >> 3;
+  const int b = blockIdx.x / Ho;
+  const int oh = blockIdx.x - b * Ho;
+  const int per = blockDim.x / cg;  // output columns per pass (blockDim is a multiple of cg)
+  const int c = static_cast<int>(threadIdx.x % cg) * 8;
+  const int ow0 = static_cast<int>(threadIdx.x / cg);
+  if (ow0 >= per) return;
+  float sc[8], sf[8];
+  if (scale) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc.v[j] = (mode == 0) ? -INFINITY : 0.f;
-  int cnt = 0;
-  const __nv_bfloat16* xb = x + static_cast<int64_t>(b) * H * W * ldx + c;
-#pragma unroll
-  for (int dh = 0; dh < (KT > 0 ? KT : 8); ++dh) {
-    if (KT == 0 && dh >= k) break;
-    const int ih = oh * s - pad + dh;
-#pragma unroll
-    for (int dw = 0; dw < (KT > 0 ? KT : 8); ++dw) {
-      if (KT == 0 && dw >= k) break;
-      const int iw = ow * s - pad + dw;
-      if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
-      Vec8 v = load8(xb + (static_cast<int64_t>(ih) * W + iw) * ldx);
-      if (scale) bnrelu8(v, scale, shift, c);
-      ++cnt;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc.v[j] = (mode == 0) ? fmaxf(acc.v[j], v.v[j]) : acc.v[j] + v.v[j];
+    for (int j = 0; j < 8; ++j) {
+      sc[j] = __ldg(scale + c + j);
+      sf[j] = __ldg(shift + c + j);
     }
   }
-  if (mode == 1) {
-    const float inv = 1.f / static_cast<float>(k * k);
+  const __nv_bfloat16* xb = x + static_cast<int64_t>(b) * H * W * ldx + c;
+  __nv_bfloat16* yb = y + (static_cast<int64_t>(b) * Ho + oh) * Wo * ldy + y_off + c;
+  const int ih0 = oh * s - pad;
+  for (int ow = ow0; ow < Wo; ow += per) {
+    Vec8 acc;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc.v[j] *= inv;
-  } else if (mode == 2) {
-    const float inv = 1.f / static_cast<float>(cnt > 0 ? cnt : 1);
+    for (int j = 0; j < 8; ++j) acc.v[j] = (mode == 0) ? -INFINITY : 0.f;
+    int cnt = 0;
+    const int iw0 = ow * s - pad;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc.v[j] *= inv;
+    for (int dh = 0; dh < (KT > 0 ? KT : 8); ++dh) {
+      if (KT == 0 && dh >= k) break;
+      const int ih = ih0 + dh;
+#pragma unroll
+      for (int dw = 0; dw < (KT > 0 ? KT : 8); ++dw) {
+        if (KT == 0 && dw >= k) break;
+        const int iw = iw0 + dw;
+        if (ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
+        Vec8 v = load8(xb + (ih * W + iw) * ldx);
+        if (scale) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v.v[j] = fmaxf(fmaf(v.v[j], sc[j], sf[j]), 0.f);
+        }
+        ++cnt;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          acc.v[j] = (mode == 0) ? fmaxf(acc.v[j], v.v[j]) : acc.v[j] + v.v[j];
+      }
+    }
+    if (mode == 1) {
+      const float inv = 1.f / static_cast<float>(k * k);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc.v[j] *= inv;
+    } else if (mode == 2) {
+      const float inv = 1.f / static_cast<float>(cnt > 0 ? cnt : 1);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc.v[j] *= inv;
+    }
+    store8(yb + ow * ldy, acc);
   }
-  store8(y + (static_cast<int64_t>(b) * Ho * Wo + static_cast<int64_t>(oh) * Wo + ow) * ldy + y_off + c, acc);
 }
 
 cudaError_t k_pool(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, int y_off, int B,
                    int H, int W, int C, int Ho, int Wo, int k, int s, int pad, int mode,
                    const float* scale, const float* shift, cudaStream_t st) {
-  const int64_t total = static_cast<int64_t>(B) * Ho * Wo * (C / 8);
-  if (total == 0) return cudaSuccess;
-  if (k > 8) return cudaErrorInvalidValue;
-  const int64_t blocks = (total + 255) / 256;
+  if (static_cast<int64_t>(B) * Ho * Wo * (C / 8) == 0) return cudaSuccess;
+  if (k > 8 || C % 8 != 0 || C / 8 > 256) return cudaErrorInvalidValue;
+  // in-image offsets are 32-bit
+  if (static_cast<int64_t>(H) * W * ldx >= (1ll << 31)) return cudaErrorInvalidValue;
+  const int cg = C / 8;
+  const int threads = (256 / cg) * cg;
+  const int rows = B * Ho;
   if (k == 2)
-    pool_kernel<2><<<blocks, 256, 0, st>>>(x, ldx, y, ldy, y_off, B, H, W, C, Ho, Wo, k, s, pad,
-                                           mode, scale, shift);
+    pool_kernel<2><<<rows, threads, 0, st>>>(x, ldx, y, ldy, y_off, H, W, C, Ho, Wo, k, s, pad,
+                                             mode, scale, shift);
   else if (k == 3)
-    pool_kernel<3><<<blocks, 256, 0, st>>>(x, ldx, y, ldy, y_off, B, H, W, C, Ho, Wo, k, s, pad,
-                                           mode, scale, shift);
+    pool_kernel<3><<<rows, threads, 0, st>>>(x, ldx, y, ldy, y_off, H, W, C, Ho, Wo, k, s, pad,
+                                             mode, scale, shift);
   else
-    pool_kernel<0><<<blocks, 256, 0, st>>>(x, ldx, y, ldy, y_off, B, H, W, C, Ho, Wo, k, s, pad,
-                                           mode, scale, shift);
+    pool_kernel<0><<<rows, threads, 0, st>>>(x, ldx, y, ldy, y_off, H, W, C, Ho, Wo, k, s, pad,
+                                             mode, scale, shift);
   return cudaGetLastError();
 }
 

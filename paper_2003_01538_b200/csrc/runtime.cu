@@ -111,6 +111,10 @@ bool mcast_enabled() {
   static const bool on = env_flag("EB_MCAST", true);
   return on;
 }
+bool pair_enabled() {
+  static const bool on = env_flag("EB_PAIR", true);
+  return on;
+}
 bool tap_shift_enabled() {
   static const bool on = env_flag("EB_TAPSHIFT", true);
   return on;
@@ -257,11 +261,20 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.block_n = bn;
   pl.splits = splits;
   pl.ws_floats = splits > 1 ? static_cast<size_t>(splits) * M * a.cout : 0;
-  // 2-CTA clusters sharing the B tile (TMA multicast) for MMA-heavy tiles: halves the
-  // per-SM operand traffic of wide-N layers; only for plain TMA A modes.
-  const bool mcast = mcast_enabled() && splits == 1 && bn >= 128 && mt >= 2 && num_kb >= 8 &&
-                     !a.pre_scale && (pl.p.a_mode == kAModeTiled || pl.p.a_mode == kAModeIm2col);
+  // 2-CTA clusters for MMA-heavy tiles.  Preferred: 2-SM MMAs (cta_group::2), where each
+  // SM stages its 128 A rows and half of B and the pair runs M=256 MMAs -- per-SM smem
+  // operand traffic per MMA drops from (A + B) to (A + B/2), which is what limits
+  // SS-mode MMAs at N >= 128.  Otherwise M-tile pairs share B by TMA multicast.
+  const bool plain_a = pl.p.a_mode == kAModeTiled || pl.p.a_mode == kAModeIm2col;
+  // (short K loops stay unpaired: the pair's lock-step costs more than it saves when the
+  // layer is memory-bound -- measured on B200, 1x1 256->64 at 56x56: 79 us single vs 107 us)
+  const bool pair = pair_enabled() && splits == 1 && mt >= 2 && !a.pre_scale &&
+                    (tap_shift ? ((bn == 64 || bn == 128) && num_kb >= 4)
+                               : (plain_a && bn >= 64 && num_kb >= 8));
+  const bool mcast = pair || (mcast_enabled() && splits == 1 && bn >= 128 && mt >= 2 &&
+                              num_kb >= 8 && !a.pre_scale && plain_a);
   pl.p.mcast = mcast ? 1 : 0;
+  pl.p.pair = pair ? 1 : 0;
   if (mcast) {
     if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn / 2, &err))
       EB_FAIL(EB_E_INVALID, err);
@@ -426,9 +439,9 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
       if (rc != EB_OK) return rc;
       static const bool dbg = env_flag("EB_DEBUG_PLAN", false);
       if (dbg)
-        fprintf(stderr, "[eb] conv src=%d dst=%d mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d\n",
+        fprintf(stderr, "[eb] conv src=%d dst=%d mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d cl=%d pair=%d\n",
                 op.src, op.dst, pl.p.a_mode, pl.block_n, pl.grid, pl.splits, pl.p.M, pl.p.N,
-                pl.p.num_kb);
+                pl.p.num_kb, pl.p.mcast, pl.p.pair);
       return run_conv_plan(pl, e->ws[op.stream], kSplitWsFloats, a, ls, launches);
     }
     case EB_OP_POOL: {

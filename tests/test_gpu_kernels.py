@@ -209,6 +209,36 @@ def test_pool_and_gap():
     assert (y.float().cpu() - r).abs().max().item() < 0.01
 
 
+@pytest.mark.parametrize("C,ldx,k,s,p,mode", [
+    (288, 320, 2, 2, 0, 1),    # DenseNet transition: 36 channel groups, strided source
+    (40, 40, 3, 2, 1, 0),      # 5 groups (CTA of 255 threads)
+    (512, 512, 2, 2, 0, 0),    # VGG: 64 groups
+    (24, 48, 3, 1, 1, 2),      # exclude-pad average
+])
+def test_pool_geometries_bnrelu(C, ldx, k, s, p, mode):
+    lib = _lib.load()
+    g = torch.Generator().manual_seed(C + k)
+    B, H, W = 3, 15, 13
+    x = torch.randn(B, H, W, ldx, generator=g).to(torch.bfloat16).to(DEV)
+    scale = (torch.rand(C, generator=g) + 0.5).to(DEV)
+    shift = (torch.randn(C, generator=g) * 0.1).to(DEV)
+    Ho, Wo = (H + 2 * p - k) // s + 1, (W + 2 * p - k) // s + 1
+    ldy, y_off = C + 16, 8
+    y = torch.zeros(B, Ho, Wo, ldy, dtype=torch.bfloat16, device=DEV)
+    _lib.check(lib.eb_k_pool(_p(x), ldx, _p(y), ldy, y_off, B, H, W, C, k, s, p, mode,
+                             _p(scale), _p(shift), None))
+    torch.cuda.synchronize()
+    xa = torch.relu(x[..., :C].float().cpu() * scale.cpu() + shift.cpu()).permute(0, 3, 1, 2)
+    if mode == 0:
+        r = F.max_pool2d(xa, k, s, p)
+    else:
+        r = F.avg_pool2d(xa, k, s, p, count_include_pad=(mode == 1))
+    r = r.permute(0, 2, 3, 1)
+    yy = y.float().cpu()
+    assert (yy[..., :y_off] == 0).all() and (yy[..., y_off + C:] == 0).all()
+    assert (yy[..., y_off:y_off + C] - r).abs().max().item() < 0.03
+
+
 def test_combine_argmax_topk_policy():
     lib = _lib.load()
     B, K = 6, 10
