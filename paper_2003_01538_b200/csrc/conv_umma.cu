@@ -40,12 +40,17 @@ bool pdl_enabled();
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // one 128-byte swizzle atom of bf16
 constexpr int kThreads = 320;  // 2 control warps + 4 epilogue warps + 4 A-transform warps
+constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels x 8 bf16
 
 // TS = filter taps consumed per pipeline stage: 1 (one TMA im2col load per tap)
 // or 3 (tap-shift mode: one 136-row load per filter row serves its 3 horizontal taps).
 // PAIR: 2-SM mode (cta_group::2) -- the CTA pair of a cluster runs one M=256 x BN MMA
 // per K step; each CTA stages its own 128 A rows and half of the B tile.
-template <int BN, int TS, bool PAIR>
+// TAPN: taps-in-N mode for 3-wide stride-1 filters with small Cout -- one MMA per K block
+// with the 3 horizontal taps' weights stacked along N (N = 3 x BN); the epilogue adds the
+// tap planes shifted by 0/1/2 rows.  The A tile is 4 x 32 rows overlapping by 2, so each
+// lane quarter can form its 30 outputs with warp shuffles; tiles advance 120 rows.
+template <int BN, int TS, bool PAIR, bool TAPN = false>
 struct ConvSmem {
   static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "tile width");
   static constexpr int kARows = TS == 1 ? kBlockM : kBlockM + 8;    // +8: row shifts 0..2
@@ -53,25 +58,57 @@ struct ConvSmem {
   static constexpr int kABytes = (kALoadBytes + 1023) / 1024 * 1024;
   static constexpr int kBRows = PAIR ? BN / 2 : BN;                 // B rows held per tap
   static constexpr int kBTapBytes = kBRows * kBlockK * 2;
-  static constexpr int kBBytes = TS * kBTapBytes;
+  static constexpr int kBBytes = (TAPN ? 3 : TS) * kBTapBytes;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
   // one warp's 32-row chunk; tap-shift tiles store directly (no staging, no residual)
-  static constexpr int kStageOutBytes = TS == 1 ? 32 * kCW * 2 : 0;
+  static constexpr int kStageOutBytes = (TS == 1 && !TAPN) ? 32 * kCW * 2 : 0;
   // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
-  static constexpr int kPreMax = (BN == 128 && TS == 1 && !PAIR) ? 2048 : 0;
-  static constexpr int kEpiBytes = 4 * 2 * kStageOutBytes * 2 + 4 * BN * 4 + 2 * kPreMax * 4;
+  static constexpr int kPreMax = (BN == 128 && TS == 1 && !PAIR && !TAPN) ? 2048 : 0;
+  // ring: 16 chunk buffers (4 warps x 4 or 8 warps x 2); bias cache: 8 warps x BN floats
+  static constexpr int kEpiBytes = 16 * kStageOutBytes + 8 * BN * 4 + 2 * kPreMax * 4;
   static constexpr int kFit = (232448 - 1536 - kEpiBytes) / kStageBytes;
   static constexpr int kStages = kFit > 8 ? 8 : kFit;
   static_assert(kStages >= 2, "pipeline needs two stages");
   static constexpr int kOutOffset = kStages * kStageBytes;
-  // per epilogue warp: a ring of 4 chunk buffers shared by residual loads and stores
-  static constexpr int kRingBufs = 4;
-  static constexpr int kBiasOffset = kOutOffset + 4 * kRingBufs * kStageOutBytes;  // 4 x BN floats
-  static constexpr int kPreOffset = kBiasOffset + 4 * BN * 4;
+  // epilogue warps: rings of chunk buffers shared by residual loads and stores
+  static constexpr int kBiasOffset = kOutOffset + 16 * kStageOutBytes;  // 8 x BN floats
+  static constexpr int kPreOffset = kBiasOffset + 8 * BN * 4;
   static constexpr int kBarOffset = kPreOffset + 2 * kPreMax * 4;
   static constexpr int kBytes = kBarOffset + 512 + 1024;  // barriers + alignment slack
   static_assert(kBytes <= 232448, "exceeds the 227 KB dynamic shared memory limit");
+};
+
+// Persistent tile walk t = t_first, t_first + t_step, ...; t = (z * mtp + pm) * nt + tn.
+// Advanced incrementally (the step is decomposed once) so no warp divides per tile.
+struct TileWalk {
+  int tn, pm, z;
+  int dn, dm, dz, nt, mtp;
+  __device__ __forceinline__ void init(int t, int step, int nt_, int mtp_) {
+    nt = nt_;
+    mtp = mtp_;
+    tn = t % nt;
+    pm = (t / nt) % mtp;
+    z = t / nt / mtp;
+    dn = step % nt;
+    dm = (step / nt) % mtp;
+    dz = step / nt / mtp;
+  }
+  __device__ __forceinline__ void next() {
+    tn += dn;
+    int c = 0;
+    if (tn >= nt) {
+      tn -= nt;
+      c = 1;
+    }
+    pm += dm + c;
+    c = 0;
+    if (pm >= mtp) {
+      pm -= mtp;
+      c = 1;
+    }
+    z += dz + c;
+  }
 };
 
 __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
@@ -80,13 +117,13 @@ __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
   return cw == 64 ? (chunk ^ (row & 7)) : (chunk ^ ((row >> 1) & 3));
 }
 
-template <int BN, int TS, bool PAIR>
+template <int BN, int TS, bool PAIR, bool TAPN>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_umma_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ CUtensorMap map_out,
                      const __grid_constant__ CUtensorMap map_res, const ConvParams p) {
-  using S = ConvSmem<BN, TS, PAIR>;
+  using S = ConvSmem<BN, TS, PAIR, TAPN>;
   extern __shared__ uint8_t smem_raw[];
   // 128B swizzle needs 1024-byte aligned tiles
   // (offset arithmetic on the __shared__ array keeps the address space visible to the
@@ -101,7 +138,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + S::kStages);
 
   const uint32_t warp = warp_id();
-  const int mt = (p.M + kBlockM - 1) / kBlockM;
+  constexpr int kTileRows = TAPN ? 120 : kBlockM;  // output rows a tile advances
+  constexpr int kAccCols = TAPN ? 3 * BN : BN;      // TMEM columns per accumulator
+  constexpr int kTmemCols = 2 * kAccCols <= 32 ? 32 : 2 * kAccCols <= 64 ? 64 : 2 * kAccCols <= 128 ? 128
+                          : 2 * kAccCols <= 256 ? 256 : 512;
+  const int mt = (p.M + kTileRows - 1) / kTileRows;
   const int nt = (p.N + BN - 1) / BN;
   const int splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
   // Tile walk.  In cluster modes the two CTAs of a cluster take the two M tiles of a
@@ -113,14 +154,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total = mtp * nt * splits;
   const int t_first = p.mcast ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
   const int t_step = p.mcast ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
-  auto decode = [&](int t, int& tm, int& tn, int& z) {
-    tn = t % nt;
-    const int rest = t / nt;
-    const int pm = rest % mtp;
-    z = rest / mtp;
-    tm = p.mcast ? 2 * pm + static_cast<int>(crank) : pm;
-  };
+  // warps 6..9 help with A (stem gather / pre-activation) or, otherwise, double the epilogue
+  const bool a_helper = p.a_mode == kAModeGatherC8 || p.pre_scale != nullptr;
+  const int n_epi = a_helper ? 4 : 8;
 
+  if (p.a_mode == kAModeTapC8) {
+    // K groups >= kw are never loaded: make them finite (zero) once
+    for (int i = threadIdx.x; i < S::kStages * (S::kABytes / 16); i += kThreads) {
+      const int st = i / (S::kABytes / 16);
+      const int off = i - st * (S::kABytes / 16);
+      *reinterpret_cast<uint4*>(smem + st * S::kStageBytes + off * 16) = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
+  }
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
@@ -133,7 +179,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], PAIR ? 8 : 4);  // PAIR: the leader waits for both epilogues
+      // arrivals that drain one accumulator: the epilogue warps that read it (8 when the
+      // two epilogue groups split each tile's chunks), doubled in PAIR mode where the
+      // leader waits for both CTAs' epilogues
+      const uint32_t drain = (n_epi == 8 && BN / S::kCW > 1) ? 8u : 4u;
+      mbar_init(&tempty[a], PAIR ? 2 * drain : drain);
     }
     for (int a = 0; a < 16; ++a) mbar_init(&rfull[a], 1);
     // A-gather mode: 128 per-thread cp.async arrivals; A-transform mode: one arrive per warp
@@ -143,9 +193,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) {
     if constexpr (PAIR)
-      tmem_alloc_pair(tmem_slot, 2 * BN);
+      tmem_alloc_pair(tmem_slot, kTmemCols);
     else
-      tmem_alloc(tmem_slot, 2 * BN < 32 ? 32 : 2 * BN);
+      tmem_alloc(tmem_slot, kTmemCols);
   }
   tc_fence_before();
   __syncthreads();
@@ -162,9 +212,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = t_first; t < total; t += t_step) {
-        int tile_m, tile_n, z;
-        decode(t, tile_m, tile_n, z);
+      TileWalk tw;
+      tw.init(t_first, t_step, nt, mtp);
+      for (int t = t_first; t < total; t += t_step, tw.next()) {
+        const int tile_n = tw.tn;
+        const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
+        const int z = tw.z;
         const int kb0 = z * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
         const int m0 = tile_m * kBlockM;
@@ -186,6 +239,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
+          if constexpr (TAPN) {
+            // filter row r, channel chunk cc: lane quarter q's 32 rows are the padded-grid
+            // pixels m0 + 30q ..; B = the row's 3 taps stacked along N
+            const int r = kb / p.cchunks;
+            const int cc = kb - r * p.cchunks;
+            mbar_arrive_expect_tx(&full[stage], 4 * 32 * 128 + S::kBBytes);
+            const int hw = p.Ho * p.Wp;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int mq = tile_m * kTileRows + 30 * q;
+              const int qi = mq / hw;
+              const int qrem = mq - qi * hw;
+              const int qh = qrem / p.Wp;
+              const int qw = qrem - qh * p.Wp;
+              tma_load_im2col_4d(sa + q * 4096, &map_a, &full[stage], cc * kBlockK, qw - p.pw,
+                                 qh - p.ph, qi, 0, static_cast<uint16_t>(r));
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < 3; ++s2)
+              tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, &full[stage],
+                          ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, n0);
+            if (++stage == S::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if constexpr (PAIR) {
             // both CTAs' loads complete on the leader's barrier, which expects them all
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
@@ -219,8 +299,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             continue;
           }
-          mbar_arrive_expect_tx(&full[stage], p.a_mode == kAModeGatherC8
-                                                  ? S::kBBytes
+          const bool skip_b = p.dbg == 1 && t != t_first;  // timing probe: B stays resident
+          if (skip_b) {
+            mbar_arrive_expect_tx(&full[stage], S::kALoadBytes);
+            const int r = kb / p.cchunks;
+            const int cc = kb - r * p.cchunks;
+            if (TS > 1)
+              tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
+                                 img, 0, static_cast<uint16_t>(r));
+            else
+              tma_load_2d(sa, &map_a, &full[stage], kb * kBlockK, m0);
+            if (++stage == S::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          mbar_arrive_expect_tx(&full[stage], p.a_mode == kAModeGatherC8 ? S::kBBytes
+                                              : p.a_mode == kAModeTapC8
+                                                  ? p.kw * kTapC8Bytes + S::kBBytes
                                                   : S::kALoadBytes + S::kBBytes);
           if (TS > 1) {
             // filter row r, channel chunk cc: 136 consecutive padded-grid pixels at tap (r, 0);
@@ -242,6 +339,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = tap - r * p.kw;
             tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
                                img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+          } else if (p.a_mode == kAModeTapC8) {
+            // filter row kb: tap s brings 128 pixels x 8 channels (16 B) = the K group s
+            // column of core matrices (2 KiB, no swizzle); groups s >= kw keep stale
+            // finite data that meets zero weights
+            for (int s = 0; s < p.kw; ++s)
+              tma_load_im2col_4d(sa + s * kTapC8Bytes, &map_a, &full[stage], 0, base_w, base_h, img,
+                                 static_cast<uint16_t>(s), static_cast<uint16_t>(kb));
           }  // kAModeGatherC8: A is gathered by warps 6..9
           if (TS == 1) {
             if (p.mcast)  // our half of B, written into both CTAs
@@ -270,18 +374,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * kBlockM : kBlockM, BN);
+    constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * kBlockM : kBlockM, TAPN ? 3 * BN : BN);
     int stage = 0;
     uint32_t phase = 0;
     int j = 0;  // local tile counter
     // PAIR: the peer's MMA warp idles; the leader issues for both CTAs
     const int t_mma_end = (PAIR && crank != 0) ? 0 : total;
-    for (int t = t_first; t < t_mma_end; t += t_step, ++j) {
-      const int z = t / (nt * mtp);
+    TileWalk tw;
+    tw.init(t_first, t_step, nt, mtp);
+    for (int t = t_first; t < t_mma_end; t += t_step, ++j, tw.next()) {
+      const int z = tw.z;
       const int kb0 = z * p.kb_per_split;
       const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
       const int acc = j & 1;
-      const uint32_t tmem_d = tmem_base + acc * BN;
+      const uint32_t tmem_d = tmem_base + acc * kAccCols;
       mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -298,7 +404,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               // a shift of s2 rows is a start address 128 B further: the 128B swizzle is
               // applied on absolute smem address bits (base offset field stays 0), which
               // is also what the TMA used when it wrote the tile (verified on B200)
-              const uint64_t adesc = umma_desc_sw128(sa + s2 * 128 + k * 32);
+              // tap-C8 tiles: K-major, no swizzle, core matrices 8 rows x 16 B; K groups
+              // (taps) 2 KiB apart (LBO), 8-row groups 128 B apart (SBO)
+              const uint64_t adesc = p.a_mode == kAModeTapC8
+                                         ? umma_desc(sa + k * 2 * kTapC8Bytes, kTapC8Bytes, 128, 0)
+                                         : umma_desc_sw128(sa + s2 * 128 + k * 32);
               const uint64_t bdesc = umma_desc_sw128(sb + s2 * S::kBTapBytes + k * 32);
               const uint32_t accum = (kb > kb0 || s2 > 0 || k > 0) ? 1u : 0u;
               if constexpr (PAIR)
@@ -325,31 +435,135 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp < 6) {
-    // ------------------------------------------------------------ epilogue
-    // All per-element loops are fully unrolled with predicates so the chunk stays
-    // in registers.  The bias of the current N tile is cached in smem per warp.  Each
-    // warp owns a ring of 4 swizzled 32 x CW chunk buffers: the residual of every chunk
-    // of a tile is TMA-loaded into the ring as soon as the tile starts (overlapping its
-    // MMAs), the result is written back in place and TMA-stored from there.
+  } else if (TAPN && warp < 2 + n_epi) {
+    // ------------------------------------------------------------ epilogue, taps-in-N
+    // Lane l of quarter q owns padded-grid row m = tile*120 + 30q + l; its output is
+    //   out[m] = D0[m] + D1[m+1] + D2[m+2]   (D_s = the tap-s column block)
+    // and rows m+1, m+2 live in lanes l+1, l+2 of the same warp (quarters overlap by 2
+    // rows, lanes 30/31 only feed their neighbours).  Two epilogue groups take
+    // alternate tiles.  Direct 16-byte stores (rows are not contiguous in the output).
     const int ew = static_cast<int>(warp) - 2;
+    const int half = ew >> 2;
+    const uint32_t quarter = warp & 3;
+    const int lane = static_cast<int>(lane_id());
+    const bool alt = n_epi == 8;
+    const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
+    const int hw = p.Ho * p.Wp;
+    float* bias_s = reinterpret_cast<float*>(smem + S::kBiasOffset) + ew * BN;
+    int cached_n = -1;
+    int j = 0;
+    TileWalk tw;
+    tw.init(t_first, t_step, nt, mtp);
+    for (int t = t_first; t < total; t += t_step, ++j, tw.next()) {
+      if (alt && (j & 1) != half) continue;
+      if (tw.tn != cached_n) {
+        __syncwarp();
+        for (int i = lane; i < BN; i += 32)
+          bias_s[i] = (p.bias && tw.tn * BN + i < p.N) ? __ldg(p.bias + tw.tn * BN + i) : 0.f;
+        __syncwarp();
+        cached_n = tw.tn;
+      }
+      const int acc = j & 1;
+      const int m = tw.pm * kTileRows + static_cast<int>(quarter) * 30 + lane;
+      const int img = m / hw;
+      const int rem = m - img * hw;
+      const int oh = rem / p.Wp;
+      const int owp = rem - oh * p.Wp;
+      const bool ok = lane < 30 && m < p.M && owp < p.Wo;
+      const size_t orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + owp;
+      const int n_tile0 = tw.tn * BN;
+      mbar_wait(&tfull[acc], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + acc * kAccCols + ((quarter * 32) << 16);
+#pragma unroll
+      for (int c = 0; c < BN; c += 32) {
+        const int n = n_tile0 + c;
+        uint32_t r0[32], r1[32], r2[32];
+        tmem_ld32(tb + c, r0);
+        tmem_ld32(tb + BN + c, r1);
+        tmem_ld32(tb + 2 * BN + c, r2);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float d1 = __shfl_down_sync(0xffffffffu, __uint_as_float(r1[i]), 1);
+          const float d2 = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[i]), 2);
+          v[i] = (__uint_as_float(r0[i]) + d1) + d2;
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c + i);
+          v[i] += b4.x;
+          v[i + 1] += b4.y;
+          v[i + 2] += b4.z;
+          v[i + 3] += b4.w;
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+          if (p.relu) h2 = __hmax2(h2, zero2);
+          pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        if (ok && n < p.N) {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
+          if (p.vec_ok && n + 32 <= p.N) {
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+              *reinterpret_cast<uint4*>(o + ch * 8) =
+                  make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+          } else {
+            const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(pk);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (n + i < p.N) o[i] = hv[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  } else if (warp < 2 + n_epi) {
+    // ------------------------------------------------------------ epilogue
+    // All per-element loops are fully unrolled with predicates so the chunk stays in
+    // registers; the math runs on fp32 pairs (FADD2) and packed bf16 pairs (ReLU after
+    // rounding is exact: rounding preserves sign).  The bias of the current N tile is
+    // cached in smem per warp.  Each warp owns a ring of swizzled 32 x CW chunk
+    // buffers: the residual of every chunk it will handle in a tile is TMA-loaded into
+    // the ring as soon as the tile starts (overlapping its MMAs), the result is written
+    // back in place and TMA-stored from there.
+    // With 8 epilogue warps (no A helper in this mode) two warps share each TMEM lane
+    // quarter: they split every tile's chunks, or -- one chunk per tile -- take
+    // alternate tiles (and so alternate accumulator buffers).
+    const int ew = static_cast<int>(warp) - 2;
+    const int half = ew >> 2;
     const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int lane = static_cast<int>(lane_id());
     const int row = static_cast<int>(quarter * 32) + lane;
     constexpr int CW = S::kCW;
     constexpr int NCH = BN / CW;
-    constexpr int NB = S::kRingBufs;
-    uint8_t* ring = smem + S::kOutOffset + ew * NB * S::kStageOutBytes;
+    const bool wide = n_epi == 8;
+    const bool alt_tiles = wide && NCH == 1;
+    const int c_first = (wide && NCH > 1) ? half : 0;
+    const int c_step = (wide && NCH > 1) ? 2 : 1;
+    const int nb = wide ? 2 : 4;  // ring buffers per warp (>= chunks this warp owns per tile)
+    uint8_t* ring = smem + S::kOutOffset + ew * nb * S::kStageOutBytes;
     float* bias_s = reinterpret_cast<float*>(smem + S::kBiasOffset) + ew * BN;
-    uint64_t* rbar = rfull + ew * NB;
+    uint64_t* rbar = rfull + ew * nb;
     uint32_t rphase = 0;  // bit b: parity of ring buffer b's residual barrier
     uint32_t seq = 0;     // chunks this warp has staged so far (ring position)
     const bool has_res = p.res != nullptr && p.out_mode == kOutBF16;
+    const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
     int cached_n = -1;
     int j = 0;
-    for (int t = t_first; t < total; t += t_step, ++j) {
-      int tile_m, tile_n, z;
-      decode(t, tile_m, tile_n, z);
+    TileWalk tw;
+    tw.init(t_first, t_step, nt, mtp);
+    for (int t = t_first; t < total; t += t_step, ++j, tw.next()) {
+      if (alt_tiles && (j & 1) != half) continue;
+      const int tile_n = tw.tn;
+      const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
+      const int z = tw.z;
       const int acc = j & 1;
       const int m = tile_m * kBlockM + row;
       bool row_ok = m < p.M;
@@ -372,11 +586,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         cached_n = tile_n;
       }
       if (has_res && lane == 0) {
-        // every earlier store has finished reading the ring -> prefetch the whole tile's
-        // residual now, while its MMAs run
+        // every earlier store has finished reading the ring -> prefetch this tile's
+        // residual chunks now, while its MMAs run
         bulk_wait_read<0>();
-        for (int ci = 0; ci < NCH && n_tile0 + ci * CW < p.N; ++ci) {
-          const uint32_t b = (seq + ci) & (NB - 1);
+        uint32_t k = 0;
+        for (int ci = c_first; ci < NCH && n_tile0 + ci * CW < p.N; ci += c_step, ++k) {
+          const uint32_t b = (seq + k) & (nb - 1);
           mbar_arrive_expect_tx(&rbar[b], S::kStageOutBytes);
           tma_load_2d(ring + b * S::kStageOutBytes, &map_res, &rbar[b], n_tile0 + ci * CW, m_slab);
         }
@@ -385,20 +600,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + ((quarter * 32) << 16);
 #pragma unroll 1
-      for (int ci = 0; ci < NCH; ++ci) {
+      for (int ci = c_first; ci < NCH; ci += c_step) {
         const int c = ci * CW;
         const int n = n_tile0 + c;
         if (n >= p.N) break;  // warp-uniform
         const bool full_chunk = n + CW <= p.N;
-        float v[CW];
-        {
-          uint32_t r[CW];
+        uint32_t r[CW];
 #pragma unroll
-          for (int q = 0; q < CW; q += 32) tmem_ld32(tbase + c + q, r + q);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < CW; ++i) v[i] = __uint_as_float(r[i]);
-        }
+        for (int q = 0; q < CW; q += 32) tmem_ld32(tbase + c + q, r + q);
+        tmem_ld_wait();
         if (p.out_mode != kOutBF16) {
           // fp32 logits or a split-K partial slice: direct stores (small outputs)
           if (row_ok) {
@@ -408,9 +618,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               o = reinterpret_cast<float*>(p.out) + (static_cast<size_t>(z) * p.M + m) * p.ldo + n;
             else
               o = reinterpret_cast<float*>(p.out) + static_cast<size_t>(m) * p.ldo + p.out_off + n;
+            float v[CW];
 #pragma unroll
             for (int i = 0; i < CW; ++i) {
-              float x = v[i];
+              float x = __uint_as_float(r[i]);
               if (logits && p.bias) x += bias_s[c + i];
               if (logits && p.relu) x = fmaxf(x, 0.f);
               v[i] = x;
@@ -427,17 +638,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
+        float2 v2[CW / 2];
+#pragma unroll
+        for (int i = 0; i < CW / 2; ++i) v2[i] = make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
         if (p.bias) {
 #pragma unroll
           for (int i = 0; i < CW; i += 4) {
             const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c + i);
-            v[i] += b4.x;
-            v[i + 1] += b4.y;
-            v[i + 2] += b4.z;
-            v[i + 3] += b4.w;
+            v2[i / 2] = __fadd2_rn(v2[i / 2], make_float2(b4.x, b4.y));
+            v2[i / 2 + 1] = __fadd2_rn(v2[i / 2 + 1], make_float2(b4.z, b4.w));
           }
         }
-        const uint32_t b = seq & (NB - 1);
+        const uint32_t b = seq & (nb - 1);
         uint8_t* buf = ring + b * S::kStageOutBytes;
         uint8_t* rowp = buf + lane * (CW * 2);
         if (has_res) {
@@ -446,14 +658,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int ch = 0; ch < CW / 8; ++ch) {
             const uint4 q = *reinterpret_cast<const uint4*>(rowp + swz_chunk(ch, lane, CW) * 16);
-            const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q);
+            const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[ch * 8 + e] += __bfloat162float(h[e]);
+            for (int e = 0; e < 4; ++e)  // bf16 -> fp32 is a 16-bit shift
+              v2[ch * 4 + e] = __fadd2_rn(v2[ch * 4 + e], make_float2(__uint_as_float(qq[e] << 16),
+                                                                      __uint_as_float(qq[e] & 0xffff0000u)));
           }
         }
-        if (p.relu) {
+        uint32_t pk[CW / 2];
 #pragma unroll
-          for (int i = 0; i < CW; ++i) v[i] = fmaxf(v[i], 0.f);
+        for (int i = 0; i < CW / 2; ++i) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(v2[i].x, v2[i].y);
+          if (p.relu) h2 = __hmax2(h2, zero2);
+          pk[i] = *reinterpret_cast<uint32_t*>(&h2);
         }
         if (TS > 1) {
           // tap-shift tiles are not contiguous in the output: direct 16-byte stores
@@ -462,37 +679,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                 reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
             if (full_chunk && p.vec_ok) {
 #pragma unroll
-              for (int ch = 0; ch < CW / 8; ++ch) {
-                uint4 q;
-                q.x = pack_bf16x2(v[ch * 8 + 0], v[ch * 8 + 1]);
-                q.y = pack_bf16x2(v[ch * 8 + 2], v[ch * 8 + 3]);
-                q.z = pack_bf16x2(v[ch * 8 + 4], v[ch * 8 + 5]);
-                q.w = pack_bf16x2(v[ch * 8 + 6], v[ch * 8 + 7]);
-                *reinterpret_cast<uint4*>(o + ch * 8) = q;
-              }
+              for (int ch = 0; ch < CW / 8; ++ch)
+                *reinterpret_cast<uint4*>(o + ch * 8) =
+                    make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
             } else {
+              const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(pk);
 #pragma unroll
               for (int i = 0; i < CW; ++i)
-                if (n + i < p.N) o[i] = __float2bfloat16_rn(v[i]);
+                if (n + i < p.N) o[i] = hv[i];
             }
           }
           continue;
         }
         if (!has_res) {
-          // the store that last used this ring buffer (NB chunks ago) has read it
-          if (lane == 0) bulk_wait_read<NB - 1>();
+          // the store that last used this ring buffer (nb chunks ago) has read it
+          if (lane == 0) {
+            if (wide)
+              bulk_wait_read<1>();
+            else
+              bulk_wait_read<3>();
+          }
           __syncwarp();
         }
         // (with a residual each lane rewrites the row it just read, in place)
 #pragma unroll
-        for (int ch = 0; ch < CW / 8; ++ch) {
-          uint4 q;
-          q.x = pack_bf16x2(v[ch * 8 + 0], v[ch * 8 + 1]);
-          q.y = pack_bf16x2(v[ch * 8 + 2], v[ch * 8 + 3]);
-          q.z = pack_bf16x2(v[ch * 8 + 4], v[ch * 8 + 5]);
-          q.w = pack_bf16x2(v[ch * 8 + 6], v[ch * 8 + 7]);
-          *reinterpret_cast<uint4*>(rowp + swz_chunk(ch, lane, CW) * 16) = q;
-        }
+        for (int ch = 0; ch < CW / 8; ++ch)
+          *reinterpret_cast<uint4*>(rowp + swz_chunk(ch, lane, CW) * 16) =
+              make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -528,9 +741,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = static_cast<int>(threadIdx.x) - 192;  // 0..127
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = t_first; t < total; t += t_step) {
-      int tile_m, tile_n, z;
-      decode(t, tile_m, tile_n, z);
+    TileWalk tw;
+    tw.init(t_first, t_step, nt, mtp);
+    for (int t = t_first; t < total; t += t_step, tw.next()) {
+      const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
+      const int z = tw.z;
       const int kb0 = z * p.kb_per_split;
       const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
       const int m = tile_m * kBlockM + r;
@@ -582,8 +797,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");  // the four transform warps only
       int stage = 0;
       uint32_t phase = 0;
-      for (int tt = t_first; tt < total; tt += t_step) {
-        const int z = tt / (nt * mtp);
+      TileWalk tw;
+      tw.init(t_first, t_step, nt, mtp);
+      for (int tt = t_first; tt < total; tt += t_step, tw.next()) {
+        const int z = tw.z;
         const int kb0 = z * p.kb_per_split;
         const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -626,22 +843,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.mcast) cluster_sync();  // no CTA leaves while its peer may still write into it
   if (warp == 1) {
     if constexpr (PAIR)
-      tmem_dealloc_pair(tmem_base, 2 * BN);
+      tmem_dealloc_pair(tmem_base, kTmemCols);
     else
-      tmem_dealloc(tmem_base, 2 * BN < 32 ? 32 : 2 * BN);
+      tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 
 // ---------------------------------------------------------------- host side
 
-template <int BN, int TS, bool PAIR>
+template <int BN, int TS, bool PAIR, bool TAPN = false>
 static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int grid,
                              cudaStream_t stream) {
-  using S = ConvSmem<BN, TS, PAIR>;
+  using S = ConvSmem<BN, TS, PAIR, TAPN>;
   static bool configured = false;  // attribute is per-function; idempotent
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<BN, TS, PAIR>,
+    cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<BN, TS, PAIR, TAPN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -660,7 +877,7 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, conv_umma_kernel<BN, TS, PAIR>, ma, mb, mo, mr, p);
+  return cudaLaunchKernelEx(&cfg, conv_umma_kernel<BN, TS, PAIR, TAPN>, ma, mb, mo, mr, p);
 }
 
 int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
@@ -676,6 +893,14 @@ bool pdl_enabled() {
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
                              cudaStream_t stream) {
+  if (p.a_mode == kAModeTapN) {
+    if (p.mcast || p.pair) return cudaErrorInvalidValue;
+    switch (block_n) {
+      case 32: return launch_bn<32, 1, false, true>(ma, mb, mo, mr, p, grid, stream);
+      case 64: return launch_bn<64, 1, false, true>(ma, mb, mo, mr, p, grid, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (p.pair) {
     if (!p.mcast) return cudaErrorInvalidValue;
     if (p.a_mode == kAModeTapShift) {

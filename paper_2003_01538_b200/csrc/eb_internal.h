@@ -14,6 +14,9 @@ enum AMode : int {
   kAModeIm2col = 1,    // TMA im2col, 64-channel chunks, 128B swizzle
   kAModeGatherC8 = 2,  // stem (Cin <= 8): cp.async gather, one K block per filter row
   kAModeTapShift = 3,  // 3-wide stride-1 filters: one load per filter row, taps by row shift
+  kAModeTapC8 = 4,     // stem (Cin <= 8): per filter row, one TMA im2col load of 8-channel
+                       // pixels per horizontal tap into a no-swizzle K-major tile
+  kAModeTapN = 5,      // 3-wide stride-1 filters, Cout <= 64: the 3 taps stacked along N
 };
 
 enum OutMode : int {
@@ -33,6 +36,7 @@ struct ConvParams {
   int n_split;               // grouped launch: columns >= n_split are stored through map_res
   int mcast;                 // 2-CTA cluster: M-tile pairs share the B tile via TMA multicast
   int pair;                  // with mcast: 2-SM MMA (cta_group::2), M = 256 per CTA pair
+  int dbg;                   // experiments only (timing probes); 0 in production
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
   void* out;
   int ldo, out_off;

@@ -115,6 +115,30 @@ bool pair_enabled() {
   static const bool on = env_flag("EB_PAIR", true);
   return on;
 }
+int pair_min_kb_ts() {
+  static const int v = [] {
+    const char* e = getenv("EB_PAIR_TS_KB");
+    return (e && *e) ? atoi(e) : 4;
+  }();
+  return v;
+}
+int tapn_max_cout() {
+  static const int v = [] {
+    const char* e = getenv("EB_TAPN_MAX_COUT");
+    return (e && *e) ? atoi(e) : 64;
+  }();
+  return v;
+}
+bool tapn_enabled() {
+  static const bool on = env_flag("EB_TAPN", true);
+  return on;
+}
+bool stem_tma_enabled() {
+  // measured on B200: the cp.async gather is as fast for the 3x3/s1 stem and 1.6x faster
+  // for the 7x7/s2 one (16-byte im2col elements are TMA-request bound)
+  static const bool on = env_flag("EB_STEM_TMA", false);
+  return on;
+}
 bool tap_shift_enabled() {
   static const bool on = env_flag("EB_TAPSHIFT", true);
   return on;
@@ -161,6 +185,11 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   const bool tap_shift = !tiled && !a.c8_stem && !a.flatten && a.kw == 3 && a.pw == 1 &&
                          a.sh == 1 && a.sw == 1 && !a.res && !a.out_f32 && bn_guess <= 128 &&
                          tap_shift_enabled();
+  // taps-in-N: small Cout (the MMA would otherwise re-read A from smem per 32 columns).
+  // Measured on B200 (B=256): 3x3 128->32 at 56x56 152 -> 105 us, at 28x28 45 -> 32 us;
+  // 3x3 64->64 at 56x56 92 -> 83 us.
+  const bool tapn = tap_shift && a.cout <= tapn_max_cout() && a.groups == 1 && !a.pre_scale && a.n_split == 0 &&
+                    tapn_enabled();
   const int64_t M64 = static_cast<int64_t>(a.B) * Ho * (tap_shift ? Wo + a.kw - 1 : Wo);
   if (M64 > (1ll << 31) - 1) EB_FAIL(EB_E_INVALID, "conv M too large");
   const int M = static_cast<int>(M64);
@@ -183,18 +212,27 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   } else if (a.c8_stem) {
     if (a.cin != 8 || a.ldx != 8) EB_FAIL(EB_E_INVALID, "stem mode expects an 8-channel image");
     if (a.kw > 8) EB_FAIL(EB_E_INVALID, "stem mode needs kw <= 8");
-    pl.ma = {};
-    pl.p.a_mode = kAModeGatherC8;
     pl.p.x = static_cast<const __nv_bfloat16*>(a.x);
     pl.p.H = a.H;
     pl.p.W = a.W;
+    if (stem_tma_enabled()) {
+      // per filter row: one TMA im2col load per horizontal tap, 128 pixels x 8 channels
+      if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, 8, 8, a.kh, a.kw, a.sh, a.sw, a.ph,
+                              a.pw, 8, 128, false, &err))
+        EB_FAIL(EB_E_INVALID, err);
+      pl.p.a_mode = kAModeTapC8;
+    } else {
+      pl.ma = {};
+      pl.p.a_mode = kAModeGatherC8;
+    }
   } else if (tap_shift) {
-    // one 136-pixel load per (filter row, channel chunk) serves taps s = 0..2 by row shift;
-    // tiles walk the padded grid (Wo + 2 columns per row, the 2 extra are dropped)
+    // one 136-pixel load per (filter row, channel chunk) serves taps s = 0..2 by row shift
+    // (taps-in-N: four 32-pixel loads); tiles walk the padded grid (Wo + 2 columns per
+    // row, the 2 extra are dropped)
     if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, a.cin, a.ldx, a.kh, a.kw, a.sh, a.sw, a.ph,
-                            a.pw, 64, 136, true, &err, a.kw - 1))
+                            a.pw, 64, tapn ? 32 : 136, true, &err, a.kw - 1))
       EB_FAIL(EB_E_INVALID, err);
-    pl.p.a_mode = kAModeTapShift;
+    pl.p.a_mode = tapn ? kAModeTapN : kAModeTapShift;
     pl.p.Wp = Wo + a.kw - 1;
   } else {
     if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, a.cin, a.ldx, a.kh, a.kw, a.sh, a.sw, a.ph,
@@ -208,7 +246,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // tap-shift stages cover all kw taps of one filter row; a grouped tile sees BN channels
   const int cin_tile = a.groups > 1 ? bn : a.cin;
   const int num_kb = tap_shift ? a.kh * ((cin_tile + 63) / 64) : static_cast<int>(kpad / 64);
-  const int mt = (M + 127) / 128;
+  const int mt = tapn ? (M + 119) / 120 : (M + 127) / 128;
   const int nt = (a.cout + bn - 1) / bn;
   int splits = a.split_k;
   if (splits <= 0) {
@@ -268,13 +306,14 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   const bool plain_a = pl.p.a_mode == kAModeTiled || pl.p.a_mode == kAModeIm2col;
   // (short K loops stay unpaired: the pair's lock-step costs more than it saves when the
   // layer is memory-bound -- measured on B200, 1x1 256->64 at 56x56: 79 us single vs 107 us)
-  const bool pair = pair_enabled() && splits == 1 && mt >= 2 && !a.pre_scale &&
-                    (tap_shift ? ((bn == 64 || bn == 128) && num_kb >= 4)
+  const bool pair = pair_enabled() && splits == 1 && mt >= 2 && !a.pre_scale && !tapn &&
+                    (tap_shift ? ((bn == 64 || bn == 128) && num_kb >= pair_min_kb_ts())
                                : (plain_a && bn >= 64 && num_kb >= 8));
   const bool mcast = pair || (mcast_enabled() && splits == 1 && bn >= 128 && mt >= 2 &&
                               num_kb >= 8 && !a.pre_scale && plain_a);
   pl.p.mcast = mcast ? 1 : 0;
   pl.p.pair = pair ? 1 : 0;
+  pl.p.dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
   if (mcast) {
     if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn / 2, &err))
       EB_FAIL(EB_E_INVALID, err);

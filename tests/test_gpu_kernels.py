@@ -78,6 +78,11 @@ CASES = [
     ("5x5", 2, 35, 35, 48, 64, 5, 5, 1, 1, 2, 2),
     ("3x3s2valid", 2, 35, 35, 96, 96, 3, 3, 2, 2, 0, 0),
     ("growth32", 2, 56, 56, 128, 32, 3, 3, 1, 1, 1, 1),
+    # taps-in-N mode edges: partial N tiles, ragged Cin, odd image sizes, 1x3 filters
+    ("3x3c48", 3, 15, 13, 64, 48, 3, 3, 1, 1, 1, 1),
+    ("3x3c24ragged", 2, 9, 11, 40, 24, 3, 3, 1, 1, 1, 1),
+    ("1x3c64", 2, 8, 8, 96, 64, 1, 3, 1, 1, 0, 1),
+    ("3x3c64big", 4, 30, 30, 64, 64, 3, 3, 1, 1, 1, 1),
 ]
 
 
