@@ -53,32 +53,52 @@ constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels 
 template <int BN, int TS, bool PAIR, bool TAPN = false>
 struct ConvSmem {
   static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "tile width");
+  static constexpr int kBN = BN;
   static constexpr int kARows = TS == 1 ? kBlockM : kBlockM + 8;    // +8: row shifts 0..2
   static constexpr int kALoadBytes = kARows * 128;                  // bytes TMA delivers
   static constexpr int kABytes = (kALoadBytes + 1023) / 1024 * 1024;
   static constexpr int kBRows = PAIR ? BN / 2 : BN;                 // B rows held per tap
   static constexpr int kBTapBytes = kBRows * kBlockK * 2;
   static constexpr int kBBytes = (TAPN ? 3 : TS) * kBTapBytes;
-  static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
   // one warp's 32-row chunk; tap-shift tiles store directly (no staging, no residual)
   static constexpr int kStageOutBytes = (TS == 1 && !TAPN) ? 32 * kCW * 2 : 0;
   // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
   static constexpr int kPreMax = (BN == 128 && TS == 1 && !PAIR && !TAPN) ? 2048 : 0;
-  // ring: 16 chunk buffers (4 warps x 4 or 8 warps x 2); bias cache: 8 warps x BN floats
-  static constexpr int kEpiBytes = 16 * kStageOutBytes + 8 * BN * 4 + 2 * kPreMax * 4;
-  static constexpr int kFit = (232448 - 1536 - kEpiBytes) / kStageBytes;
-  static constexpr int kStages = kFit > 8 ? 8 : kFit;
-  static_assert(kStages >= 2, "pipeline needs two stages");
-  static constexpr int kOutOffset = kStages * kStageBytes;
-  // epilogue warps: rings of chunk buffers shared by residual loads and stores
-  static constexpr int kBiasOffset = kOutOffset + 16 * kStageOutBytes;  // 8 x BN floats
-  static constexpr int kPreOffset = kBiasOffset + 8 * BN * 4;
-  static constexpr int kBarOffset = kPreOffset + 2 * kPreMax * 4;
-  static constexpr int kBytes = kBarOffset + 512 + 1024;  // barriers + alignment slack
-  static_assert(kBytes <= 232448, "exceeds the 227 KB dynamic shared memory limit");
+  // ring: 16 chunk buffers (4 warps x 4 or 8 warps x 2); tap-shift / taps-in-N tiles
+  // instead stage 32 rows x 32 columns per warp for coalesced row stores
+  static constexpr int kRowStageBytes = 32 * 32 * 2;
+  static constexpr int kRingArea = (TS == 1 && !TAPN) ? 16 * kStageOutBytes : 8 * kRowStageBytes;
+  // bias cache: 8 warps x BN floats
+  static constexpr int kEpiBytes = kRingArea + 8 * BN * 4 + 2 * kPreMax * 4;
+  // dynamic smem: everything (one CTA per SM); 1 KiB alignment slack + barrier block
+  static constexpr int kBytes = 232448;
+  static constexpr int kBarBytes = 512;
+  static constexpr int kBudget = kBytes - 1024 - kBarBytes;
+  static constexpr int kMaxStages = 12;  // barrier block: 3 x 12 + 20 mbarriers + slot
+  static_assert((kBudget - kEpiBytes) / (kABytes + kBBytes) >= 2, "pipeline needs two stages");
 };
 
+// Shared-memory layout, chosen per launch: [resident B (optional)] [stage ring of A (+B)]
+// [epilogue rings] [bias caches] [pre-activation cache] [barriers].  With resident B
+// (single N tile, short K) the weights are loaded once per CTA and the ring holds A only,
+// so the same space buys a deeper A pipeline.
+struct SmemLayout {
+  int resb_bytes, stage_bytes, stages, out_off, bias_off, pre_off, bar_off;
+};
+template <class S>
+__host__ __device__ inline SmemLayout make_layout(int resb, int num_kb) {
+  SmemLayout L;
+  L.resb_bytes = resb ? num_kb * S::kBBytes : 0;
+  L.stage_bytes = S::kABytes + (resb ? 0 : S::kBBytes);
+  int st = (S::kBudget - S::kEpiBytes - L.resb_bytes) / L.stage_bytes;
+  L.stages = st > S::kMaxStages ? S::kMaxStages : st;
+  L.out_off = L.resb_bytes + L.stages * L.stage_bytes;
+  L.bias_off = L.out_off + S::kRingArea;
+  L.pre_off = L.bias_off + 8 * S::kBN * 4;
+  L.bar_off = L.pre_off + 2 * S::kPreMax * 4;
+  return L;
+}
 // Persistent tile walk t = t_first, t_first + t_step, ...; t = (z * mtp + pm) * nt + tn.
 // Advanced incrementally (the step is decomposed once) so no warp divides per tile.
 struct TileWalk {
@@ -111,6 +131,31 @@ struct TileWalk {
   }
 };
 
+// Coalesced store of a warp's 32 rows x 32 bf16 columns whose output rows are not
+// contiguous (tap-shift / taps-in-N tiles walk a padded pixel grid).  Each lane stages
+// its row (4 x 16 B, XOR-swizzled against bank conflicts), then the warp writes 8 rows
+// x 64 B per instruction using the row addresses of the lanes that own them (null =
+// row not stored).
+__device__ __forceinline__ void stage_store_rows32(uint8_t* buf, const uint32_t* pk, int lane,
+                                                   __nv_bfloat16* dst) {
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    *reinterpret_cast<uint4*>(buf + lane * 64 + ((u ^ sw) * 16)) =
+        make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+  __syncwarp();
+  const unsigned long long d = reinterpret_cast<unsigned long long>(dst);
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int row = it * 8 + (lane >> 2);
+    const int u = lane & 3;
+    const unsigned long long rd = __shfl_sync(0xffffffffu, d, row);
+    const uint4 q = *reinterpret_cast<const uint4*>(buf + row * 64 + ((u ^ ((row >> 1) & 3)) * 16));
+    if (rd) *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(rd) + u * 8) = q;
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
   // TMA SWIZZLE_128B (128 B rows): 16 B chunk ^= row % 8
   // TMA SWIZZLE_64B  (64 B rows):  16 B chunk ^= (row / 2) % 4
@@ -129,13 +174,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (offset arithmetic on the __shared__ array keeps the address space visible to the
   // compiler, so staging accesses compile to STS/LDS rather than generic ST/LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
-  uint64_t* empty = full + S::kStages;
-  uint64_t* tfull = empty + S::kStages;  // [2] accumulator ready
+  const SmemLayout L = make_layout<S>(p.resb, p.num_kb);
+  uint8_t* const ring_base = smem + L.resb_bytes;  // stage s at ring_base + s * stage_bytes
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* empty = full + L.stages;
+  uint64_t* tfull = empty + L.stages;  // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained
   uint64_t* rfull = tempty + 2;          // [4 warps][4] residual chunk landed in ring buffer
   uint64_t* xfull = rfull + 16;          // [stages] A tile transformed (pre-activation)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + S::kStages);
+  uint64_t* bres = xfull + L.stages;     // resident B landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const uint32_t warp = warp_id();
   constexpr int kTileRows = TAPN ? 120 : kBlockM;  // output rows a tile advances
@@ -160,10 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (p.a_mode == kAModeTapC8) {
     // K groups >= kw are never loaded: make them finite (zero) once
-    for (int i = threadIdx.x; i < S::kStages * (S::kABytes / 16); i += kThreads) {
+    for (int i = threadIdx.x; i < L.stages * (S::kABytes / 16); i += kThreads) {
       const int st = i / (S::kABytes / 16);
       const int off = i - st * (S::kABytes / 16);
-      *reinterpret_cast<uint4*>(smem + st * S::kStageBytes + off * 16) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(ring_base + st * L.stage_bytes + off * 16) = make_uint4(0, 0, 0, 0);
     }
     fence_proxy_async_smem();
   }
@@ -172,7 +220,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&map_b);
     if (p.out_mode == kOutBF16) tma_prefetch_desc(&map_out);
     if (p.res || p.n_split) tma_prefetch_desc(&map_res);
-    for (int s = 0; s < S::kStages; ++s) {
+    mbar_init(bres, 1);
+    for (int s = 0; s < L.stages; ++s) {
       mbar_init(&full[s], 1);
       // multicast: both CTAs' MMAs free a slot; PAIR: the leader's MMAs free it in both
       mbar_init(&empty[s], (p.mcast && !PAIR) ? 2 : 1);
@@ -188,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 16; ++a) mbar_init(&rfull[a], 1);
     // A-gather mode: 128 per-thread cp.async arrivals; A-transform mode: one arrive per warp
     const uint32_t xcount = p.a_mode == kAModeGatherC8 ? 128u : 4u;
-    for (int s = 0; s < S::kStages; ++s) mbar_init(&xfull[s], xcount);
+    for (int s = 0; s < L.stages; ++s) mbar_init(&xfull[s], xcount);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -212,6 +261,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
+      if (p.resb) {
+        // resident B (single N tile): every K block's weights, once per CTA
+        mbar_arrive_expect_tx(bres, L.resb_bytes);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          uint8_t* sb = smem + kb * S::kBBytes;
+          if (TAPN || TS > 1) {
+            const int r = kb / p.cchunks;
+            const int cc = kb - r * p.cchunks;
+            for (int s2 = 0; s2 < (TAPN ? 3 : TS); ++s2)
+              tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, bres,
+                          ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, 0);
+          } else {
+            tma_load_2d(sb, &map_b, bres, kb * kBlockK, 0);
+          }
+        }
+      }
       TileWalk tw;
       tw.init(t_first, t_step, nt, mtp);
       for (int t = t_first; t < total; t += t_step, tw.next()) {
@@ -235,32 +300,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n0 = tile_n * BN;
         // grouped conv (block-diagonal weights): this N tile's input channel window
         const int c_base = p.grouped ? n0 : 0;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        // taps-in-N: receptive-field origins of the four 32-row quarter loads (per tile)
+        int qw[4] = {0, 0, 0, 0}, qh[4] = {0, 0, 0, 0}, qi[4] = {0, 0, 0, 0};
+        if constexpr (TAPN) {
+          const int hw = p.Ho * p.Wp;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int mq = tile_m * kTileRows + 30 * q;
+            qi[q] = mq / hw;
+            const int qrem = mq - qi[q] * hw;
+            qh[q] = qrem / p.Wp;
+            qw[q] = qrem - qh[q] * p.Wp - p.pw;
+            qh[q] -= p.ph;
+          }
+        }
+        // K-block coordinates, advanced incrementally: kb = (row_or_tap * cchunks + cc), and
+        // for im2col tap = r * kw + s
+        int cc = kb0 % p.cchunks;
+        int outer = kb0 / p.cchunks;
+        int rr = outer / p.kw;
+        int ss = outer - rr * p.kw;
+        auto next_k = [&] {
+          if (++cc == p.cchunks) {
+            cc = 0;
+            ++outer;
+            if (++ss == p.kw) {
+              ss = 0;
+              ++rr;
+            }
+          }
+        };
+        for (int kb = kb0; kb < kb1; ++kb, next_k()) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * S::kStageBytes;
-          uint8_t* sb = sa + S::kABytes;
+          uint8_t* sa = ring_base + stage * L.stage_bytes;
+          uint8_t* sb = p.resb ? smem + kb * S::kBBytes : sa + S::kABytes;
           if constexpr (TAPN) {
             // filter row r, channel chunk cc: lane quarter q's 32 rows are the padded-grid
             // pixels m0 + 30q ..; B = the row's 3 taps stacked along N
-            const int r = kb / p.cchunks;
-            const int cc = kb - r * p.cchunks;
-            mbar_arrive_expect_tx(&full[stage], 4 * 32 * 128 + S::kBBytes);
-            const int hw = p.Ho * p.Wp;
+            const int r = outer;
+            mbar_arrive_expect_tx(&full[stage], 4 * 32 * 128 + (p.resb ? 0 : S::kBBytes));
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int mq = tile_m * kTileRows + 30 * q;
-              const int qi = mq / hw;
-              const int qrem = mq - qi * hw;
-              const int qh = qrem / p.Wp;
-              const int qw = qrem - qh * p.Wp;
-              tma_load_im2col_4d(sa + q * 4096, &map_a, &full[stage], cc * kBlockK, qw - p.pw,
-                                 qh - p.ph, qi, 0, static_cast<uint16_t>(r));
+            for (int q = 0; q < 4; ++q)
+              tma_load_im2col_4d(sa + q * 4096, &map_a, &full[stage], cc * kBlockK, qw[q], qh[q], qi[q],
+                                 0, static_cast<uint16_t>(r));
+            if (!p.resb) {
+#pragma unroll
+              for (int s2 = 0; s2 < 3; ++s2)
+                tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, &full[stage],
+                            ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, n0);
             }
-#pragma unroll
-            for (int s2 = 0; s2 < 3; ++s2)
-              tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, &full[stage],
-                          ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, n0);
-            if (++stage == S::kStages) {
+            if (++stage == L.stages) {
               stage = 0;
               phase ^= 1;
             }
@@ -272,8 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2u * (S::kALoadBytes + S::kBBytes));
             const int nb = n0 + static_cast<int>(crank) * S::kBRows;
             if (TS > 1) {
-              const int r = kb / p.cchunks;
-              const int cc = kb - r * p.cchunks;
+              const int r = outer;
               tma_load_im2col_4d_pair(sa, &map_a, fb, c_base + cc * kBlockK, base_w, base_h, img, 0,
                                       static_cast<uint16_t>(r));
 #pragma unroll
@@ -284,61 +372,43 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (p.a_mode == kAModeTiled) {
                 tma_load_2d_pair(sa, &map_a, fb, kb * kBlockK, m0);
               } else {
-                const int tap = kb / p.cchunks;
-                const int cc = kb - tap * p.cchunks;
-                const int r = tap / p.kw;
-                const int s = tap - r * p.kw;
                 tma_load_im2col_4d_pair(sa, &map_a, fb, c_base + cc * kBlockK, base_w, base_h, img,
-                                        static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+                                        static_cast<uint16_t>(ss), static_cast<uint16_t>(rr));
               }
               tma_load_2d_pair(sb, &map_b, fb, kb * kBlockK, nb);
             }
-            if (++stage == S::kStages) {
+            if (++stage == L.stages) {
               stage = 0;
               phase ^= 1;
             }
             continue;
           }
-          const bool skip_b = p.dbg == 1 && t != t_first;  // timing probe: B stays resident
-          if (skip_b) {
-            mbar_arrive_expect_tx(&full[stage], S::kALoadBytes);
-            const int r = kb / p.cchunks;
-            const int cc = kb - r * p.cchunks;
-            if (TS > 1)
-              tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
-                                 img, 0, static_cast<uint16_t>(r));
-            else
-              tma_load_2d(sa, &map_a, &full[stage], kb * kBlockK, m0);
-            if (++stage == S::kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
-            continue;
+          {
+            const uint32_t bbytes = p.resb ? 0u : static_cast<uint32_t>(S::kBBytes);
+            const uint32_t abytes = p.a_mode == kAModeGatherC8 ? 0u
+                                    : p.a_mode == kAModeTapC8
+                                        ? static_cast<uint32_t>(p.kw * kTapC8Bytes)
+                                        : static_cast<uint32_t>(S::kALoadBytes);
+            // (gather mode with resident B: this stage only waits for the cp.async arrivals)
+            mbar_arrive_expect_tx(&full[stage], abytes + bbytes);
           }
-          mbar_arrive_expect_tx(&full[stage], p.a_mode == kAModeGatherC8 ? S::kBBytes
-                                              : p.a_mode == kAModeTapC8
-                                                  ? p.kw * kTapC8Bytes + S::kBBytes
-                                                  : S::kALoadBytes + S::kBBytes);
           if (TS > 1) {
             // filter row r, channel chunk cc: 136 consecutive padded-grid pixels at tap (r, 0);
             // tap (r, s) is the same buffer shifted down by s rows
-            const int r = kb / p.cchunks;
-            const int cc = kb - r * p.cchunks;
+            const int r = outer;
             tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
                                img, 0, static_cast<uint16_t>(r));
+            if (!p.resb) {
 #pragma unroll
-            for (int s2 = 0; s2 < TS; ++s2)
-              tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, &full[stage],
-                          ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, n0);
+              for (int s2 = 0; s2 < TS; ++s2)
+                tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, &full[stage],
+                            ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, n0);
+            }
           } else if (p.a_mode == kAModeTiled) {
             tma_load_2d(sa, &map_a, &full[stage], kb * kBlockK, m0);
           } else if (p.a_mode == kAModeIm2col) {
-            const int tap = kb / p.cchunks;
-            const int cc = kb - tap * p.cchunks;
-            const int r = tap / p.kw;
-            const int s = tap - r * p.kw;
             tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
-                               img, static_cast<uint16_t>(s), static_cast<uint16_t>(r));
+                               img, static_cast<uint16_t>(ss), static_cast<uint16_t>(rr));
           } else if (p.a_mode == kAModeTapC8) {
             // filter row kb: tap s brings 128 pixels x 8 channels (16 B) = the K group s
             // column of core matrices (2 KiB, no swizzle); groups s >= kw keep stale
@@ -347,14 +417,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_im2col_4d(sa + s * kTapC8Bytes, &map_a, &full[stage], 0, base_w, base_h, img,
                                  static_cast<uint16_t>(s), static_cast<uint16_t>(kb));
           }  // kAModeGatherC8: A is gathered by warps 6..9
-          if (TS == 1) {
+          if (TS == 1 && !p.resb) {
             if (p.mcast)  // our half of B, written into both CTAs
               tma_load_2d_mcast(sb + crank * (BN / 2) * 128, &map_b, &full[stage], kb * kBlockK,
                                 n0 + static_cast<int>(crank) * (BN / 2), 0x3);
             else
               tma_load_2d(sb, &map_b, &full[stage], kb * kBlockK, n0);
           }
-          if (++stage == S::kStages) {
+          if (++stage == L.stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -363,9 +433,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.mcast) {
         // producer tail: every MMA commit aimed at this CTA's empty barriers (some come
         // from the peer) has landed before the cluster may tear down
-        for (int i = 0; i < S::kStages; ++i) {
+        for (int i = 0; i < L.stages; ++i) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (++stage == S::kStages) {
+          if (++stage == L.stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -380,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int j = 0;  // local tile counter
     // PAIR: the peer's MMA warp idles; the leader issues for both CTAs
     const int t_mma_end = (PAIR && crank != 0) ? 0 : total;
+    if (p.resb && t_first < t_mma_end) mbar_wait(bres, 0);
     TileWalk tw;
     tw.init(t_first, t_step, nt, mtp);
     for (int t = t_first; t < t_mma_end; t += t_step, ++j, tw.next()) {
@@ -395,8 +466,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.a_mode == kAModeGatherC8) mbar_wait(&xfull[stage], phase);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
-          const uint32_t sb = sa + S::kABytes;
+          const uint32_t sa = smem_u32(ring_base + stage * L.stage_bytes);
+          const uint32_t sb = p.resb ? smem_u32(smem + kb * S::kBBytes) : sa + S::kABytes;
 #pragma unroll
           for (int s2 = 0; s2 < TS; ++s2) {
 #pragma unroll
@@ -429,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();
-        if (++stage == S::kStages) {
+        if (++stage == L.stages) {
           stage = 0;
           phase ^= 1;
         }
@@ -449,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool alt = n_epi == 8;
     const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
     const int hw = p.Ho * p.Wp;
-    float* bias_s = reinterpret_cast<float*>(smem + S::kBiasOffset) + ew * BN;
+    float* bias_s = reinterpret_cast<float*>(smem + L.bias_off) + ew * BN;
     int cached_n = -1;
     int j = 0;
     TileWalk tw;
@@ -505,14 +576,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.relu) h2 = __hmax2(h2, zero2);
           pk[i] = *reinterpret_cast<uint32_t*>(&h2);
         }
-        if (ok && n < p.N) {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
-          if (p.vec_ok && n + 32 <= p.N) {
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch)
-              *reinterpret_cast<uint4*>(o + ch * 8) =
-                  make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
-          } else {
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
+        if (p.vec_ok && n + 32 <= p.N) {
+          stage_store_rows32(smem + L.out_off + ew * S::kRowStageBytes, pk, lane, ok ? o : nullptr);
+        } else if (ok && n < p.N) {
+          {
             const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(pk);
 #pragma unroll
             for (int i = 0; i < 32; ++i)
@@ -548,8 +616,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int c_first = (wide && NCH > 1) ? half : 0;
     const int c_step = (wide && NCH > 1) ? 2 : 1;
     const int nb = wide ? 2 : 4;  // ring buffers per warp (>= chunks this warp owns per tile)
-    uint8_t* ring = smem + S::kOutOffset + ew * nb * S::kStageOutBytes;
-    float* bias_s = reinterpret_cast<float*>(smem + S::kBiasOffset) + ew * BN;
+    uint8_t* ring = smem + L.out_off + ew * nb * S::kStageOutBytes;
+    float* bias_s = reinterpret_cast<float*>(smem + L.bias_off) + ew * BN;
     uint64_t* rbar = rfull + ew * nb;
     uint32_t rphase = 0;  // bit b: parity of ring buffer b's residual barrier
     uint32_t seq = 0;     // chunks this warp has staged so far (ring position)
@@ -673,16 +741,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[i] = *reinterpret_cast<uint32_t*>(&h2);
         }
         if (TS > 1) {
-          // tap-shift tiles are not contiguous in the output: direct 16-byte stores
-          if (row_ok) {
-            __nv_bfloat16* o =
-                reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
-            if (full_chunk && p.vec_ok) {
+          // tap-shift tiles are not contiguous in the output (padded grid): row stores
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
+          if (full_chunk && p.vec_ok && CW % 32 == 0) {
+            uint8_t* stg = smem + L.out_off + ew * S::kRowStageBytes;
 #pragma unroll
-              for (int ch = 0; ch < CW / 8; ++ch)
-                *reinterpret_cast<uint4*>(o + ch * 8) =
-                    make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
-            } else {
+            for (int h = 0; h < CW / 32; ++h)
+              stage_store_rows32(stg, pk + 16 * h, lane, row_ok ? o + 32 * h : nullptr);
+          } else if (row_ok) {
+            {
               const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(pk);
 #pragma unroll
               for (int i = 0; i < CW; ++i)
@@ -758,7 +825,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int iw0 = ow * p.sw - p.pw;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* rowp = smem + stage * S::kStageBytes + r * 128;
+        uint8_t* rowp = ring_base + stage * L.stage_bytes + r * 128;
         const int ih = oh * p.sh - p.ph + kb;
         const bool hok = row_ok && ih >= 0 && ih < p.H;
         const __nv_bfloat16* src = p.x + ((static_cast<int64_t>(img) * p.H + (hok ? ih : 0)) * p.W) * 8;
@@ -769,7 +836,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           cp_async_16(rowp + ((j ^ (r & 7)) * 16), src + (ok ? iw : 0) * 8, ok ? 16u : 0u);
         }
         cp_async_arrive_noinc(&xfull[stage]);
-        if (++stage == S::kStages) {
+        if (++stage == L.stages) {
           stage = 0;
           phase ^= 1;
         }
@@ -787,7 +854,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t = static_cast<int>(threadIdx.x) - 192;  // 0..127
       const int j = t & 7;
       const int r0 = (t >> 3) * 8;
-      float* sc_s = reinterpret_cast<float*>(smem + S::kPreOffset);
+      float* sc_s = reinterpret_cast<float*>(smem + L.pre_off);
       float* sh_s = sc_s + S::kPreMax;
       const int kpad = p.num_kb * kBlockK;
       for (int i = t; i < kpad; i += 128) {
@@ -816,7 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                          __floats2bfloat162_rn(t1.x, t1.y), __floats2bfloat162_rn(t1.z, t1.w)};
           const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
           mbar_wait(&full[stage], phase);
-          uint8_t* tile = smem + stage * S::kStageBytes;
+          uint8_t* tile = ring_base + stage * L.stage_bytes;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = r0 + i;  // r & 7 == i
@@ -830,7 +897,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if ((t & 31) == 0) mbar_arrive(&xfull[stage]);
-          if (++stage == S::kStages) {
+          if (++stage == L.stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -881,6 +948,26 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
 }
 
 int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
+
+template <int BN, int TS, bool PAIR, bool TAPN = false>
+static int stages_of(const ConvParams& p) {
+  return make_layout<ConvSmem<BN, TS, PAIR, TAPN>>(p.resb, p.num_kb).stages;
+}
+int conv_umma_stages(const ConvParams& p, int block_n) {
+  const bool ts = p.a_mode == kAModeTapShift;
+  if (p.a_mode == kAModeTapN) return block_n == 32 ? stages_of<32, 1, false, true>(p) : stages_of<64, 1, false, true>(p);
+  if (p.pair) {
+    if (ts) return block_n == 64 ? stages_of<64, 3, true>(p) : stages_of<128, 3, true>(p);
+    return block_n == 64 ? stages_of<64, 1, true>(p) : block_n == 128 ? stages_of<128, 1, true>(p) : stages_of<256, 1, true>(p);
+  }
+  if (ts) return block_n == 32 ? stages_of<32, 3, false>(p) : block_n == 64 ? stages_of<64, 3, false>(p) : stages_of<128, 3, false>(p);
+  switch (block_n) {
+    case 32: return stages_of<32, 1, false>(p);
+    case 64: return stages_of<64, 1, false>(p);
+    case 128: return stages_of<128, 1, false>(p);
+    default: return stages_of<256, 1, false>(p);
+  }
+}
 
 bool pdl_enabled() {
   static const bool on = [] {

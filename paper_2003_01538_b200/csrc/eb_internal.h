@@ -36,7 +36,7 @@ struct ConvParams {
   int n_split;               // grouped launch: columns >= n_split are stored through map_res
   int mcast;                 // 2-CTA cluster: M-tile pairs share the B tile via TMA multicast
   int pair;                  // with mcast: 2-SM MMA (cta_group::2), M = 256 per CTA pair
-  int dbg;                   // experiments only (timing probes); 0 in production
+  int resb;                  // single N tile: all K blocks of B resident in smem (loaded once)
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
   void* out;
   int ldo, out_off;
@@ -56,6 +56,8 @@ cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
                              cudaStream_t stream);
 int conv_umma_chunk(int block_n);
+// pipeline stages the kernel instance for this plan would get (host-side layout query)
+int conv_umma_stages(const ConvParams& p, int block_n);
 
 // Driver entry point for tensor-map encoding (resolved through the runtime so the
 // library does not link libcuda directly).

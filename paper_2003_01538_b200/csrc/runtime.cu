@@ -129,6 +129,10 @@ int tapn_max_cout() {
   }();
   return v;
 }
+bool resb_enabled() {
+  static const bool on = env_flag("EB_RESB", true);
+  return on;
+}
 bool tapn_enabled() {
   static const bool on = env_flag("EB_TAPN", true);
   return on;
@@ -313,7 +317,15 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
                               num_kb >= 8 && !a.pre_scale && plain_a);
   pl.p.mcast = mcast ? 1 : 0;
   pl.p.pair = pair ? 1 : 0;
-  pl.p.dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
+  // Resident B: with a single N tile every CTA re-streams the same weights per tile; keep
+  // them in smem instead when they fit and the A ring stays deep (it gets all the space).
+  if (resb_enabled() && nt == 1 && splits == 1 && !mcast) {
+    const int s_stream = conv_umma_stages(pl.p, bn);
+    pl.p.resb = 1;
+    const int s_res = conv_umma_stages(pl.p, bn);
+    const int64_t rb = static_cast<int64_t>(num_kb) * (tap_shift ? 3 : 1) * bn * 128;
+    if (rb > 112 * 1024 || s_res < 4 || s_res < s_stream) pl.p.resb = 0;
+  }
   if (mcast) {
     if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn / 2, &err))
       EB_FAIL(EB_E_INVALID, err);
@@ -478,9 +490,9 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
       if (rc != EB_OK) return rc;
       static const bool dbg = env_flag("EB_DEBUG_PLAN", false);
       if (dbg)
-        fprintf(stderr, "[eb] conv src=%d dst=%d mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d cl=%d pair=%d\n",
+        fprintf(stderr, "[eb] conv src=%d dst=%d mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d cl=%d pair=%d resb=%d\n",
                 op.src, op.dst, pl.p.a_mode, pl.block_n, pl.grid, pl.splits, pl.p.M, pl.p.N,
-                pl.p.num_kb, pl.p.mcast, pl.p.pair);
+                pl.p.num_kb, pl.p.mcast, pl.p.pair, pl.p.resb);
       return run_conv_plan(pl, e->ws[op.stream], kSplitWsFloats, a, ls, launches);
     }
     case EB_OP_POOL: {
