@@ -228,6 +228,103 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// K x K windows with the mode and the BN-ReLU fixed at compile time: every window load
+// of a thread is issued (predicated, clamped address) before any is used, so a thread
+// keeps K*K 16-byte loads in flight.  Same CTA/row mapping as pool_kernel.
+__device__ __forceinline__ void unpack8(const uint4& q, float* f) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    f[2 * e] = __uint_as_float(w[e] << 16);
+    f[2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
+  }
+}
+template <int K, int MODE, bool PRE>
+__global__ void __launch_bounds__(256)
+    pool_fixed_kernel(const __nv_bfloat16* __restrict__ x, int ldx, __nv_bfloat16* __restrict__ y,
+                      int ldy, int y_off, int H, int W, int C, int Ho, int Wo, int s, int pad,
+                      const float* __restrict__ scale, const float* __restrict__ shift) {
+  const int cg = C >> 3;
+  const int b = blockIdx.x / Ho;
+  const int oh = blockIdx.x - b * Ho;
+  const int per = blockDim.x / cg;
+  const int c = static_cast<int>(threadIdx.x % cg) * 8;
+  const int ow0 = static_cast<int>(threadIdx.x / cg);
+  if (ow0 >= per) return;
+  float sc[8], sf[8];
+  if (PRE) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sc[j] = __ldg(scale + c + j);
+      sf[j] = __ldg(shift + c + j);
+    }
+  }
+  const __nv_bfloat16* xb = x + static_cast<int64_t>(b) * H * W * ldx + c;
+  __nv_bfloat16* yb = y + (static_cast<int64_t>(b) * Ho + oh) * Wo * ldy + y_off + c;
+  const int ih0 = oh * s - pad;
+  for (int ow = ow0; ow < Wo; ow += per) {
+    const int iw0 = ow * s - pad;
+    uint4 raw[K * K];
+    bool ok[K * K];
+#pragma unroll
+    for (int dh = 0; dh < K; ++dh) {
+#pragma unroll
+      for (int dw = 0; dw < K; ++dw) {
+        const int ih = ih0 + dh, iw = iw0 + dw;
+        const bool v = ih >= 0 && ih < H && iw >= 0 && iw < W;
+        ok[dh * K + dw] = v;
+        const int off = v ? (ih * W + iw) * ldx : 0;
+        raw[dh * K + dw] = *reinterpret_cast<const uint4*>(xb + off);
+      }
+    }
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = MODE == 0 ? -INFINITY : 0.f;
+    int cnt = 0;
+#pragma unroll
+    for (int t = 0; t < K * K; ++t) {
+      float f[8];
+      unpack8(raw[t], f);
+      if (PRE) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = fmaxf(fmaf(f[j], sc[j], sf[j]), 0.f);
+      }
+      if (ok[t]) {
+        ++cnt;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = MODE == 0 ? fmaxf(acc[j], f[j]) : acc[j] + f[j];
+      }
+    }
+    if (MODE != 0) {
+      const float inv = MODE == 1 ? 1.f / static_cast<float>(K * K) : 1.f / static_cast<float>(cnt > 0 ? cnt : 1);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] *= inv;
+    }
+    Vec8 r;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r.v[j] = acc[j];
+    store8(yb + ow * ldy, r);
+  }
+}
+
+template <int K>
+static void launch_pool_fixed(int mode, bool pre, int rows, int threads, cudaStream_t st,
+                              const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, int y_off,
+                              int H, int W, int C, int Ho, int Wo, int s, int pad, const float* scale,
+                              const float* shift) {
+#define EB_POOL_LAUNCH(M, P)                                                                    \
+  pool_fixed_kernel<K, M, P><<<rows, threads, 0, st>>>(x, ldx, y, ldy, y_off, H, W, C, Ho, Wo, s, \
+                                                       pad, scale, shift)
+  if (mode == 0) {
+    if (pre) EB_POOL_LAUNCH(0, true); else EB_POOL_LAUNCH(0, false);
+  } else if (mode == 1) {
+    if (pre) EB_POOL_LAUNCH(1, true); else EB_POOL_LAUNCH(1, false);
+  } else {
+    if (pre) EB_POOL_LAUNCH(2, true); else EB_POOL_LAUNCH(2, false);
+  }
+#undef EB_POOL_LAUNCH
+}
+
 cudaError_t k_pool(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, int y_off, int B,
                    int H, int W, int C, int Ho, int Wo, int k, int s, int pad, int mode,
                    const float* scale, const float* shift, cudaStream_t st) {
@@ -238,12 +335,12 @@ cudaError_t k_pool(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, i
   const int cg = C / 8;
   const int threads = (256 / cg) * cg;
   const int rows = B * Ho;
-  if (k == 2)
-    pool_kernel<2><<<rows, threads, 0, st>>>(x, ldx, y, ldy, y_off, H, W, C, Ho, Wo, k, s, pad,
-                                             mode, scale, shift);
-  else if (k == 3)
-    pool_kernel<3><<<rows, threads, 0, st>>>(x, ldx, y, ldy, y_off, H, W, C, Ho, Wo, k, s, pad,
-                                             mode, scale, shift);
+  if (k == 2 && mode >= 0 && mode <= 2)
+    launch_pool_fixed<2>(mode, scale != nullptr, rows, threads, st, x, ldx, y, ldy, y_off, H, W, C,
+                         Ho, Wo, s, pad, scale, shift);
+  else if (k == 3 && mode >= 0 && mode <= 2)
+    launch_pool_fixed<3>(mode, scale != nullptr, rows, threads, st, x, ldx, y, ldy, y_off, H, W, C,
+                         Ho, Wo, s, pad, scale, shift);
   else
     pool_kernel<0><<<rows, threads, 0, st>>>(x, ldx, y, ldy, y_off, H, W, C, Ho, Wo, k, s, pad,
                                              mode, scale, shift);
