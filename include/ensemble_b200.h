@@ -178,8 +178,18 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
               int out_f32, int c8_stem, int split_k, int block_n, int groups,
               void* dev_workspace, const float* dev_pre_scale, const float* dev_pre_shift,
               void* stream);
+/* (eb_k_conv c8_stem: 0 = regular input, 1 = 8-channel NHWC image (gathered stem),
+ *  2 = the image already in its eb_k_stem_relayout layout; h, w stay the image's.) */
 int eb_k_resize(const void* dev_x, int ldx, void* dev_y, int ldy, int batch, int h, int w, int c,
                 int ho, int wo, void* stream);
+/* Stem layouts: eb_k_stem_layout reports the bytes of the zero-padded layout a stem conv
+ * of this geometry reads with c8_stem = 2 (stride 1: padded rows; stride 2: even/odd
+ * column planes), or EB_E_INVALID if the geometry has none; eb_k_stem_relayout writes it
+ * from the 8-channel NHWC image (bf16). */
+int eb_k_stem_layout(int batch, int h, int w, int kh, int kw, int sh, int sw, int ph, int pw,
+                     uint64_t* bytes);
+int eb_k_stem_relayout(const void* dev_x, int batch, int h, int w, int kh, int kw, int sh, int sw,
+                       int ph, int pw, void* dev_y, void* stream);
 int eb_k_pool(const void* dev_x, int ldx, void* dev_y, int ldy, int y_off, int batch, int h,
               int w, int c, int k, int s, int pad, int mode, const float* dev_scale,
               const float* dev_shift, void* stream);

@@ -100,6 +100,10 @@ _SIGS = {
                           c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
                           c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                           c_void_p, c_void_p, c_void_p, c_void_p]),
+    "eb_k_stem_layout": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                 POINTER(c_uint64)]),
+    "eb_k_stem_relayout": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                   c_int, c_int, c_void_p, c_void_p]),
     "eb_k_resize": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
                             c_int, c_void_p]),
     "eb_k_pool": (c_int, [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
@@ -125,7 +129,9 @@ def load(path: str | os.PathLike | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # EB_LIB_PATH: load another build of the library (A/B timing experiments only)
+        override = os.environ.get("EB_LIB_PATH")
+        p = Path(path) if path else Path(override) if override else LIB_PATH
         if not p.exists():
             raise ImportError(
                 f"native library {p} is missing: run `python -m paper_2003_01538_b200.build` "
@@ -133,6 +139,8 @@ def load(path: str | os.PathLike | None = None):
             )
         lib = ctypes.CDLL(str(p))
         for name, (res, args) in _SIGS.items():
+            if override and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

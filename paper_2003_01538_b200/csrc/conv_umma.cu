@@ -73,9 +73,10 @@ struct ConvSmem {
   static constexpr int kEpiBytes = kRingArea + 8 * BN * 4 + 2 * kPreMax * 4;
   // dynamic smem: everything (one CTA per SM); 1 KiB alignment slack + barrier block
   static constexpr int kBytes = 232448;
-  static constexpr int kBarBytes = 512;
+  static constexpr int kBarBytes = 1024;
   static constexpr int kBudget = kBytes - 1024 - kBarBytes;
-  static constexpr int kMaxStages = 12;  // barrier block: 3 x 12 + 20 mbarriers + slot
+  // barrier block: 3 x 32 + 21 mbarriers + TMEM slot; small stages (stems) run deep rings
+  static constexpr int kMaxStages = 32;
   static_assert((kBudget - kEpiBytes) / (kABytes + kBBytes) >= 2, "pipeline needs two stages");
 };
 
@@ -86,11 +87,17 @@ struct ConvSmem {
 struct SmemLayout {
   int resb_bytes, stage_bytes, stages, out_off, bias_off, pre_off, bar_off;
 };
+// A bytes per stage: the stem modes stage one (rows) or two (planes) 136-pixel runs
+__host__ __device__ inline int stem_a_bytes(int a_mode) {
+  return a_mode == kAModeStemRows ? 3072 : a_mode == kAModeStemPlanes ? 5120 : 0;
+}
+constexpr int kStemPlaneOff = 2304;  // planes mode: the odd-column run's offset in the stage
 template <class S>
-__host__ __device__ inline SmemLayout make_layout(int resb, int num_kb) {
+__host__ __device__ inline SmemLayout make_layout(int resb, int num_kb, int a_mode) {
   SmemLayout L;
+  const int ab = stem_a_bytes(a_mode);
   L.resb_bytes = resb ? num_kb * S::kBBytes : 0;
-  L.stage_bytes = S::kABytes + (resb ? 0 : S::kBBytes);
+  L.stage_bytes = (ab ? ab : S::kABytes) + (resb ? 0 : S::kBBytes);
   int st = (S::kBudget - S::kEpiBytes - L.resb_bytes) / L.stage_bytes;
   L.stages = st > S::kMaxStages ? S::kMaxStages : st;
   L.out_off = L.resb_bytes + L.stages * L.stage_bytes;
@@ -136,24 +143,41 @@ struct TileWalk {
 // its row (4 x 16 B, XOR-swizzled against bank conflicts), then the warp writes 8 rows
 // x 64 B per instruction using the row addresses of the lanes that own them (null =
 // row not stored).
+// base: the warp's column origin (out + out_off + n); my_row: this lane's output row
+// (pixel index) or -1 when the row is not stored.
 __device__ __forceinline__ void stage_store_rows32(uint8_t* buf, const uint32_t* pk, int lane,
-                                                   __nv_bfloat16* dst) {
+                                                   __nv_bfloat16* base, int ld, int my_row) {
   const int sw = (lane >> 1) & 3;
 #pragma unroll
   for (int u = 0; u < 4; ++u)
     *reinterpret_cast<uint4*>(buf + lane * 64 + ((u ^ sw) * 16)) =
         make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
   __syncwarp();
-  const unsigned long long d = reinterpret_cast<unsigned long long>(dst);
 #pragma unroll
   for (int it = 0; it < 4; ++it) {
     const int row = it * 8 + (lane >> 2);
     const int u = lane & 3;
-    const unsigned long long rd = __shfl_sync(0xffffffffu, d, row);
+    const int orow = __shfl_sync(0xffffffffu, my_row, row);
     const uint4 q = *reinterpret_cast<const uint4*>(buf + row * 64 + ((u ^ ((row >> 1) & 3)) * 16));
-    if (rd) *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(rd) + u * 8) = q;
+    if (orow >= 0) {
+      uint4* dst = reinterpret_cast<uint4*>(base + static_cast<size_t>(orow) * ld + u * 8);
+      asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(q.x), "r"(q.y),
+                   "r"(q.z), "r"(q.w)
+                   : "memory");
+    }
   }
   __syncwarp();
+}
+
+// EB_TRACE timing probe: role r (0 producer, 1 MMA, 2 epilogue warp 2) of CTA 0 records
+// up to 1024 (tag, clock) events
+__device__ __forceinline__ void trace_ev(long long* tr, int role, int& n, int tag) {
+  if (tr && blockIdx.x == 0 && n < 1024) {
+    const long long clk = clock64();
+    tr[(role * 1024 + n) * 2] = (static_cast<long long>(tag) << 48) | (clk & 0xFFFFFFFFFFFFll);
+    tr[(role * 1024 + n) * 2 + 1] = 0;
+    ++n;
+  }
 }
 
 __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
@@ -174,7 +198,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (offset arithmetic on the __shared__ array keeps the address space visible to the
   // compiler, so staging accesses compile to STS/LDS rather than generic ST/LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const SmemLayout L = make_layout<S>(p.resb, p.num_kb);
+  const SmemLayout L = make_layout<S>(p.resb, p.num_kb, p.a_mode);
+  const bool stem_direct = p.a_mode == kAModeStemRows || p.a_mode == kAModeStemPlanes;
+  const int a_stage = stem_direct ? stem_a_bytes(p.a_mode) : S::kABytes;  // B follows A
   uint8_t* const ring_base = smem + L.resb_bytes;  // stage s at ring_base + s * stage_bytes
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + L.stages;
@@ -261,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
+      int tr_n = 0;
       if (p.resb) {
         // resident B (single N tile): every K block's weights, once per CTA
         mbar_arrive_expect_tx(bres, L.resb_bytes);
@@ -287,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
         const int m0 = tile_m * kBlockM;
         int img = 0, oh = 0, ow = 0;
-        if (p.a_mode != kAModeTiled) {
+        if (p.a_mode != kAModeTiled && !stem_direct && !TAPN) {
           const int gw = TS > 1 ? p.Wp : p.Wo;  // tap-shift tiles walk the padded grid
           const int hw = p.Ho * gw;
           img = m0 / hw;
@@ -300,6 +327,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n0 = tile_n * BN;
         // grouped conv (block-diagonal weights): this N tile's input channel window
         const int c_base = p.grouped ? n0 : 0;
+        // stem rows / planes: first 128-byte line of this tile's filter row 0 (per tile)
+        int stem_line0 = 0;
+        const int stem_plane_lines = static_cast<int>(p.plane_px >> 3);
+        if (stem_direct) {
+          const int b = m0 / p.Mi;
+          const int local = m0 - b * p.Mi;
+          long long px;
+          if (p.a_mode == kAModeStemRows) {
+            px = static_cast<long long>(b) * p.Hq * p.Wq + local;
+          } else {
+            const int oh = local / p.Wg;
+            px = (static_cast<long long>(b) * p.Hq + 2 * oh) * p.Wq + (local - oh * p.Wg);
+          }
+          stem_line0 = static_cast<int>(px >> 3);
+        }
         // taps-in-N: receptive-field origins of the four 32-row quarter loads (per tile)
         int qw[4] = {0, 0, 0, 0}, qh[4] = {0, 0, 0, 0}, qi[4] = {0, 0, 0, 0};
         if constexpr (TAPN) {
@@ -332,8 +374,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         for (int kb = kb0; kb < kb1; ++kb, next_k()) {
           mbar_wait(&empty[stage], phase ^ 1);
+          trace_ev(p.trace, 0, tr_n, 1);
           uint8_t* sa = ring_base + stage * L.stage_bytes;
-          uint8_t* sb = p.resb ? smem + kb * S::kBBytes : sa + S::kABytes;
+          uint8_t* sb = p.resb ? smem + kb * S::kBBytes : sa + a_stage;
           if constexpr (TAPN) {
             // filter row r, channel chunk cc: lane quarter q's 32 rows are the padded-grid
             // pixels m0 + 30q ..; B = the row's 3 taps stacked along N
@@ -388,7 +431,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t abytes = p.a_mode == kAModeGatherC8 ? 0u
                                     : p.a_mode == kAModeTapC8
                                         ? static_cast<uint32_t>(p.kw * kTapC8Bytes)
-                                        : static_cast<uint32_t>(S::kALoadBytes);
+                                    : p.a_mode == kAModeStemRows   ? 2176u
+                                    : p.a_mode == kAModeStemPlanes ? 4352u
+                                                                   : static_cast<uint32_t>(S::kALoadBytes);
             // (gather mode with resident B: this stage only waits for the cp.async arrivals)
             mbar_arrive_expect_tx(&full[stage], abytes + bbytes);
           }
@@ -409,13 +454,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if (p.a_mode == kAModeIm2col) {
             tma_load_im2col_4d(sa, &map_a, &full[stage], c_base + cc * kBlockK, base_w, base_h,
                                img, static_cast<uint16_t>(ss), static_cast<uint16_t>(rr));
+          } else if (stem_direct) {
+            // filter row kb of a 128-position tile: contiguous 136-pixel runs (17 lines of
+            // 8 pixels x 8 channels) of the padded layout; the next filter row is Wq
+            // pixels further in both layouts
+            const int line = stem_line0 + kb * (p.Wq >> 3);
+            tma_load_2d(sa, &map_a, &full[stage], 0, line);
+            if (p.a_mode == kAModeStemPlanes)
+              tma_load_2d(sa + kStemPlaneOff, &map_a, &full[stage], 0, line + stem_plane_lines);
           } else if (p.a_mode == kAModeTapC8) {
             // filter row kb: tap s brings 128 pixels x 8 channels (16 B) = the K group s
             // column of core matrices (2 KiB, no swizzle); groups s >= kw keep stale
             // finite data that meets zero weights
-            for (int s = 0; s < p.kw; ++s)
-              tma_load_im2col_4d(sa + s * kTapC8Bytes, &map_a, &full[stage], 0, base_w, base_h, img,
+            for (int s = 0; s < p.kw; ++s) {
+              const int g = p.sw == 2 ? ((s & 1) ? 4 + (s >> 1) : (s >> 1)) : s;
+              tma_load_im2col_4d(sa + g * kTapC8Bytes, &map_a, &full[stage], 0, base_w, base_h, img,
                                  static_cast<uint16_t>(s), static_cast<uint16_t>(kb));
+            }
           }  // kAModeGatherC8: A is gathered by warps 6..9
           if (TS == 1 && !p.resb) {
             if (p.mcast)  // our half of B, written into both CTAs
@@ -451,8 +506,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     // PAIR: the peer's MMA warp idles; the leader issues for both CTAs
     const int t_mma_end = (PAIR && crank != 0) ? 0 : total;
     if (p.resb && t_first < t_mma_end) mbar_wait(bres, 0);
+    // K16 steps per K block that carry nonzero weights (step 0 always does), and the A
+    // start-address offset of each step (16-byte units):
+    //   128B-swizzled tiles: 32 B per step;  tap-C8: 2 KiB K groups, 4 KiB per step;
+    //   stem rows/planes: taps are core matrices 16 B apart (overlapping, LBO = 16), the
+    //   planes mode's odd-column run starts kStemPlaneOff into the stage.
+    uint32_t kmask = 0xFu;
+    uint32_t a_koff[4] = {0, 2, 4, 6};
+    uint64_t a_desc_hi = umma_desc_sw128(0);
+    const uint64_t b_desc_hi = umma_desc_sw128(0);
+    if (p.a_mode == kAModeTapC8) {
+      a_desc_hi = umma_desc(0, kTapC8Bytes, 128, 0);
+      for (int k = 0; k < 4; ++k) a_koff[k] = k * 2 * kTapC8Bytes / 16;
+    } else if (p.a_mode == kAModeStemRows) {
+      a_desc_hi = umma_desc(0, 16, 128, 0);
+      kmask = (1u << ((p.kw + 1) / 2)) - 1u;
+    } else if (p.a_mode == kAModeStemPlanes) {
+      a_desc_hi = umma_desc(0, 16, 128, 0);
+      const int ne = ((p.kw + 1) / 2 + 1) / 2;  // even taps -> K groups 0..3
+      const int no = (p.kw / 2 + 1) / 2;        // odd taps  -> K groups 4..7
+      kmask = ((1u << ne) - 1u) | (((1u << no) - 1u) << 2);
+      a_koff[2] = kStemPlaneOff / 16;
+      a_koff[3] = kStemPlaneOff / 16 + 2;
+    }
     TileWalk tw;
     tw.init(t_first, t_step, nt, mtp);
+    int tr_n = 0;
     for (int t = t_first; t < t_mma_end; t += t_step, ++j, tw.next()) {
       const int z = tw.z;
       const int kb0 = z * p.kb_per_split;
@@ -460,14 +539,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = j & 1;
       const uint32_t tmem_d = tmem_base + acc * kAccCols;
       mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      if (lane_id() == 0) trace_ev(p.trace, 1, tr_n, 10);
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(p.pre_scale ? &xfull[stage] : &full[stage], phase);
         if (p.a_mode == kAModeGatherC8) mbar_wait(&xfull[stage], phase);
+        if (lane_id() == 0) trace_ev(p.trace, 1, tr_n, 11);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(ring_base + stage * L.stage_bytes);
-          const uint32_t sb = p.resb ? smem_u32(smem + kb * S::kBBytes) : sa + S::kABytes;
+          const uint32_t sb = p.resb ? smem_u32(smem + kb * S::kBBytes) : sa + a_stage;
+          // descriptors: the per-kernel fields (LBO/SBO/layout) are fixed, so a K step or
+          // a row shift only adds to the 14-bit start-address field (16-byte units)
+          const uint64_t a0 = a_desc_hi | ((sa >> 4) & 0x3FFF);
+          const uint64_t b0 = b_desc_hi | ((sb >> 4) & 0x3FFF);
 #pragma unroll
           for (int s2 = 0; s2 < TS; ++s2) {
 #pragma unroll
@@ -475,12 +560,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               // a shift of s2 rows is a start address 128 B further: the 128B swizzle is
               // applied on absolute smem address bits (base offset field stays 0), which
               // is also what the TMA used when it wrote the tile (verified on B200)
-              // tap-C8 tiles: K-major, no swizzle, core matrices 8 rows x 16 B; K groups
-              // (taps) 2 KiB apart (LBO), 8-row groups 128 B apart (SBO)
-              const uint64_t adesc = p.a_mode == kAModeTapC8
-                                         ? umma_desc(sa + k * 2 * kTapC8Bytes, kTapC8Bytes, 128, 0)
-                                         : umma_desc_sw128(sa + s2 * 128 + k * 32);
-              const uint64_t bdesc = umma_desc_sw128(sb + s2 * S::kBTapBytes + k * 32);
+              if (!((kmask >> k) & 1u)) continue;  // (stems: all-zero weight steps)
+              const uint64_t adesc = a0 + s2 * 8 + a_koff[k];
+              const uint64_t bdesc = b0 + s2 * (S::kBTapBytes >> 4) + 2 * k;
               const uint32_t accum = (kb > kb0 || s2 > 0 || k > 0) ? 1u : 0u;
               if constexpr (PAIR)
                 umma_bf16_pair(tmem_d, adesc, bdesc, idesc, accum);
@@ -522,11 +604,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int hw = p.Ho * p.Wp;
     float* bias_s = reinterpret_cast<float*>(smem + L.bias_off) + ew * BN;
     int cached_n = -1;
-    int j = 0;
+    const int j0 = alt ? half : 0;
+    const int jstep = alt ? 2 : 1;
+    int j = j0;
     TileWalk tw;
-    tw.init(t_first, t_step, nt, mtp);
-    for (int t = t_first; t < total; t += t_step, ++j, tw.next()) {
-      if (alt && (j & 1) != half) continue;
+    tw.init(t_first + j0 * t_step, jstep * t_step, nt, mtp);
+    for (int t = t_first + j0 * t_step; t < total; t += jstep * t_step, j += jstep, tw.next()) {
       if (tw.tn != cached_n) {
         __syncwarp();
         for (int i = lane; i < BN; i += 32)
@@ -536,9 +619,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int acc = j & 1;
       const int m = tw.pm * kTileRows + static_cast<int>(quarter) * 30 + lane;
-      const int img = m / hw;
+      const int img = fdiv(m, p.fd_img);
       const int rem = m - img * hw;
-      const int oh = rem / p.Wp;
+      const int oh = fdiv(rem, p.fd_row);
       const int owp = rem - oh * p.Wp;
       const bool ok = lane < 30 && m < p.M && owp < p.Wo;
       const size_t orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + owp;
@@ -554,6 +637,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tb + BN + c, r1);
         tmem_ld32(tb + 2 * BN + c, r2);
         tmem_ld_wait();
+        if (c + 32 >= BN && p.early_release) {  // last TMEM read of the tile: hand it back now
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
@@ -571,14 +659,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-          if (p.relu) h2 = __hmax2(h2, zero2);
-          pk[i] = *reinterpret_cast<uint32_t*>(&h2);
-        }
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
+        for (int i = 0; i < 16; ++i)
+          pk[i] = p.relu ? pack_bf16x2_relu(v[2 * i], v[2 * i + 1]) : pack_bf16x2(v[2 * i], v[2 * i + 1]);
+        __nv_bfloat16* const col0 = reinterpret_cast<__nv_bfloat16*>(p.out) + p.out_off + n;
+        __nv_bfloat16* o = col0 + orow * p.ldo;
         if (p.vec_ok && n + 32 <= p.N) {
-          stage_store_rows32(smem + L.out_off + ew * S::kRowStageBytes, pk, lane, ok ? o : nullptr);
+          stage_store_rows32(smem + L.out_off + ew * S::kRowStageBytes, pk, lane, col0, p.ldo,
+                             ok ? static_cast<int>(orow) : -1);
         } else if (ok && n < p.N) {
           {
             const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(pk);
@@ -588,9 +675,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (!p.early_release) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
     }
   } else if (warp < 2 + n_epi) {
     // ------------------------------------------------------------ epilogue
@@ -621,14 +710,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* rbar = rfull + ew * nb;
     uint32_t rphase = 0;  // bit b: parity of ring buffer b's residual barrier
     uint32_t seq = 0;     // chunks this warp has staged so far (ring position)
+    int tr_n = 0;
     const bool has_res = p.res != nullptr && p.out_mode == kOutBF16;
     const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
     int cached_n = -1;
-    int j = 0;
+    // alternate-tile groups walk every other tile of the CTA directly
+    const int j0 = alt_tiles ? half : 0;
+    const int jstep = alt_tiles ? 2 : 1;
+    int j = j0;
     TileWalk tw;
-    tw.init(t_first, t_step, nt, mtp);
-    for (int t = t_first; t < total; t += t_step, ++j, tw.next()) {
-      if (alt_tiles && (j & 1) != half) continue;
+    tw.init(t_first + j0 * t_step, jstep * t_step, nt, mtp);
+    for (int t = t_first + j0 * t_step; t < total; t += jstep * t_step, j += jstep, tw.next()) {
       const int tile_n = tw.tn;
       const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
       const int z = tw.z;
@@ -636,14 +728,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m = tile_m * kBlockM + row;
       bool row_ok = m < p.M;
       size_t orow = static_cast<size_t>(m);
-      if (TS > 1) {  // padded-grid row -> output pixel; the kw-1 junk columns are dropped
-        const int hw = p.Ho * p.Wp;
-        const int img = m / hw;
-        const int rem = m - img * hw;
-        const int oh = rem / p.Wp;
-        const int owp = rem - oh * p.Wp;
-        row_ok = row_ok && owp < p.Wo;
-        orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + owp;
+      if (TS > 1 || stem_direct) {
+        // padded grid position -> output pixel (tap-shift: Ho x (Wo + kw - 1) per image, the
+        // kw-1 junk columns dropped; stems: Mi positions per image, rows of Wg)
+        const int img = fdiv(m, p.fd_img);
+        const int local = m - img * static_cast<int>(p.fd_img.d);
+        const int oh = fdiv(local, p.fd_row);
+        const int ow = local - oh * static_cast<int>(p.fd_row.d);
+        row_ok = row_ok && oh < p.Ho && ow < p.Wo;
+        orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + ow;
       }
       const int n_tile0 = tile_n * BN;
       const int m_slab = tile_m * kBlockM + static_cast<int>(quarter) * 32;
@@ -664,9 +757,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(ring + b * S::kStageOutBytes, &map_res, &rbar[b], n_tile0 + ci * CW, m_slab);
         }
       }
+      if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 20);
       mbar_wait(&tfull[acc], (j >> 1) & 1);
+      if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 21);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + ((quarter * 32) << 16);
+      // The accumulator is released as soon as this warp's last TMEM load of the tile
+      // has completed -- before its math and stores -- so the MMAs of tile j+2 overlap
+      // the epilogue of tile j.
+      bool released = false;
+      auto release = [&] {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR && crank != 0)  // the leader's MMAs write our TMEM: release it there
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          else
+            mbar_arrive(&tempty[acc]);
+        }
+        released = true;
+      };
+      int last_ci = c_first;
+      while (last_ci + c_step < NCH && n_tile0 + (last_ci + c_step) * CW < p.N) last_ci += c_step;
 #pragma unroll 1
       for (int ci = c_first; ci < NCH; ci += c_step) {
         const int c = ci * CW;
@@ -677,6 +789,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int q = 0; q < CW; q += 32) tmem_ld32(tbase + c + q, r + q);
         tmem_ld_wait();
+        if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 23);
+        if (ci == last_ci && p.early_release) release();
         if (p.out_mode != kOutBF16) {
           // fp32 logits or a split-K partial slice: direct stores (small outputs)
           if (row_ok) {
@@ -735,19 +849,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         uint32_t pk[CW / 2];
 #pragma unroll
-        for (int i = 0; i < CW / 2; ++i) {
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(v2[i].x, v2[i].y);
-          if (p.relu) h2 = __hmax2(h2, zero2);
-          pk[i] = *reinterpret_cast<uint32_t*>(&h2);
-        }
-        if (TS > 1) {
-          // tap-shift tiles are not contiguous in the output (padded grid): row stores
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + orow * p.ldo + p.out_off + n;
+        for (int i = 0; i < CW / 2; ++i)
+          pk[i] = p.relu ? pack_bf16x2_relu(v2[i].x, v2[i].y) : pack_bf16x2(v2[i].x, v2[i].y);
+        if (TS > 1 || stem_direct) {
+          // tap-shift / stem tiles are not contiguous in the output (padded grids): row
+          // stores; a grouped stem launch sends columns >= n_split to the second tensor
+          const bool second = p.n_split > 0 && n >= p.n_split;
+          __nv_bfloat16* const col0 =
+              second ? reinterpret_cast<__nv_bfloat16*>(p.out2) + p.out2_off + (n - p.n_split)
+                     : reinterpret_cast<__nv_bfloat16*>(p.out) + p.out_off + n;
+          const int ldd = second ? p.ldo2 : p.ldo;
+          __nv_bfloat16* o = col0 + orow * ldd;
+          if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 24);
           if (full_chunk && p.vec_ok && CW % 32 == 0) {
             uint8_t* stg = smem + L.out_off + ew * S::kRowStageBytes;
 #pragma unroll
             for (int h = 0; h < CW / 32; ++h)
-              stage_store_rows32(stg, pk + 16 * h, lane, row_ok ? o + 32 * h : nullptr);
+              stage_store_rows32(stg, pk + 16 * h, lane, col0 + 32 * h, ldd,
+                                 row_ok ? static_cast<int>(orow) : -1);
           } else if (row_ok) {
             {
               const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(pk);
@@ -786,15 +905,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ++seq;
       }
-      // accumulator drained (all tcgen05.ld of this tile completed above)
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (PAIR && crank != 0)  // the leader's MMAs write our TMEM: release it there
-          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
-        else
-          mbar_arrive(&tempty[acc]);
-      }
+      if (!released) release();  // (no chunk of this tile fell inside N)
+      if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 22);
     }
     if (lane == 0) bulk_wait<0>();
   } else if (p.a_mode == kAModeGatherC8) {
@@ -831,7 +943,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const __nv_bfloat16* src = p.x + ((static_cast<int64_t>(img) * p.H + (hok ? ih : 0)) * p.W) * 8;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int iw = iw0 + j;
+          // stride-2 stem weights list the even taps first (K groups 0..3), then the odd
+          const int tap = p.sw == 2 ? (j < 4 ? 2 * j : 2 * (j - 4) + 1) : j;
+          const int iw = iw0 + tap;
           const bool ok = hok && iw >= 0 && iw < p.W;
           cp_async_16(rowp + ((j ^ (r & 7)) * 16), src + (ok ? iw : 0) * 8, ok ? 16u : 0u);
         }
@@ -951,7 +1065,7 @@ int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
 
 template <int BN, int TS, bool PAIR, bool TAPN = false>
 static int stages_of(const ConvParams& p) {
-  return make_layout<ConvSmem<BN, TS, PAIR, TAPN>>(p.resb, p.num_kb).stages;
+  return make_layout<ConvSmem<BN, TS, PAIR, TAPN>>(p.resb, p.num_kb, p.a_mode).stages;
 }
 int conv_umma_stages(const ConvParams& p, int block_n) {
   const bool ts = p.a_mode == kAModeTapShift;

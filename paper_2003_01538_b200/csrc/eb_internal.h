@@ -17,13 +17,77 @@ enum AMode : int {
   kAModeTapC8 = 4,     // stem (Cin <= 8): per filter row, one TMA im2col load of 8-channel
                        // pixels per horizontal tap into a no-swizzle K-major tile
   kAModeTapN = 5,      // 3-wide stride-1 filters, Cout <= 64: the 3 taps stacked along N
+  kAModeStemRows = 6,  // stem, stride 1: zero-padded 8-channel image, one contiguous load
+                       // of 136 pixels per filter row; taps = overlapping core matrices
+  kAModeStemPlanes = 7,  // stem, stride 2: even/odd padded column planes, two such loads
 };
+
+// Padded source layouts for the stem modes (written by k_stem_relayout).  A tile is 128
+// consecutive positions of a per-image output grid of width Wg; rows of the grid with
+// ow >= Wo (and positions past Ho) are computed and dropped.
+//   rows   (stride 1): buffer [B][Hq][Wq][8], padded pixel (ih + ph, iw + pw); Wg = Wq
+//   planes (stride 2): buffer [2][B][Hq][Wq][8], plane q holds padded columns 2j + q;
+//                      Wg = 128 * ceil(Wo / 128)
+struct StemGeom {
+  int mode;        // kAModeStemRows / kAModeStemPlanes
+  int Hq, Wq, Wg;  // padded rows / width per image, output grid width
+  int Mi;          // output grid positions per image (multiple of 128)
+  int64_t plane_px;  // pixels per plane (planes mode)
+  int64_t bytes;
+};
+inline bool stem_geom(int B, int H, int W, int kh, int kw, int sh, int sw, int ph, int pw,
+                      StemGeom* g) {
+  if (kw > 8 || sh != sw || (sh != 1 && sh != 2)) return false;
+  const int Ho = (H + 2 * ph - kh) / sh + 1;
+  const int Wo = (W + 2 * pw - kw) / sw + 1;
+  if (Ho <= 0 || Wo <= 0) return false;
+  if (sh == 1) {
+    g->mode = kAModeStemRows;
+    g->Wq = (W + 2 * pw + 7) / 8 * 8;  // (taps >= kw meet zero weights; may read the next row)
+    g->Wg = g->Wq;
+    g->Mi = (Ho * g->Wg + 127) / 128 * 128;
+    // the last tile's loads reach Mi - 1 + 7 + (kh - 1) * Wq
+    g->Hq = (g->Mi + 8 + (kh - 1) * g->Wq + g->Wq - 1) / g->Wq;
+    if (g->Hq < H + 2 * ph) g->Hq = H + 2 * ph;
+    g->plane_px = static_cast<int64_t>(B) * g->Hq * g->Wq;
+    g->bytes = g->plane_px * 16;
+  } else {
+    g->mode = kAModeStemPlanes;
+    g->Wg = (Wo + 127) / 128 * 128;
+    g->Wq = g->Wg + 8;                       // plane columns reach Wg - 1 + (kw - 1) / 2
+    g->Mi = Ho * g->Wg;
+    g->Hq = 2 * (Ho - 1) + kh;               // plane rows reach 2 (Ho - 1) + kh - 1
+    if (g->Hq < H + 2 * ph) g->Hq = H + 2 * ph;
+    g->plane_px = static_cast<int64_t>(B) * g->Hq * g->Wq;
+    g->bytes = 2 * g->plane_px * 16;
+  }
+  return true;
+}
 
 enum OutMode : int {
   kOutBF16 = 0,       // bf16 NHWC slice, bias/residual/ReLU fused
   kOutF32 = 1,        // fp32 (logits), bias/ReLU fused
   kOutPartialF32 = 2,  // fp32 split-K partial of slice blockIdx.z (deterministic reduce after)
 };
+
+// Division by a run-time constant for 0 <= n < 2^31 (multiply-high + add + shift):
+// s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1, q = (umulhi(n, m) + n) >> s.
+struct FastDiv {
+  uint32_t d, m, s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  if (d == 0) return f;
+  while ((1ull << f.s) < d) ++f.s;
+  f.m = static_cast<uint32_t>(((1ull << 32) * ((1ull << f.s) - d)) / d + 1);
+  return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
+  const uint32_t t = __umulhi(static_cast<uint32_t>(n), f.m);
+  return static_cast<int>((t + static_cast<uint32_t>(n)) >> f.s);
+}
+#endif
 
 struct ConvParams {
   int M, N;
@@ -37,7 +101,17 @@ struct ConvParams {
   int mcast;                 // 2-CTA cluster: M-tile pairs share the B tile via TMA multicast
   int pair;                  // with mcast: 2-SM MMA (cta_group::2), M = 256 per CTA pair
   int resb;                  // single N tile: all K blocks of B resident in smem (loaded once)
+  int early_release;         // epilogue frees the accumulator right after its TMEM loads
+  int dbg;                   // timing experiments only (EB_DBG); 0 in production
+  long long* trace;          // timing experiments only (EB_TRACE): per-role event clocks of CTA 0
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels
+  int Wg, Mi, Hq, Wq;        // stem rows / planes modes (see StemGeom)
+  // epilogue row decode, padded-grid modes: grid positions per image and per grid row
+  // (tap-shift / taps-in-N: Ho * Wp and Wp; stems: Mi and Wg)
+  FastDiv fd_img, fd_row;
+  long long plane_px;
+  void* out2;                // grouped launch, direct-store modes: columns >= n_split
+  int ldo2, out2_off;
   void* out;
   int ldo, out_off;
   const __nv_bfloat16* res;

@@ -17,6 +17,11 @@ cudaError_t k_preprocess_u8hwc_to_nhwc(const uint8_t* x, __nv_bfloat16* y, int B
 cudaError_t k_preprocess_u8hwc_to_f32chw(const uint8_t* x, float* y, int B, int C, int64_t plane,
                                          const float* lut, cudaStream_t s);
 
+// 8-channel NHWC image -> the zero-padded stem layout described by StemGeom (eb_internal.h):
+// mode kAModeStemRows (stride 1) or kAModeStemPlanes (stride 2, even/odd column planes).
+cudaError_t k_stem_relayout(const __nv_bfloat16* x, int B, int H, int W, int ph, int pw, int mode,
+                            int Hq, int Wq, __nv_bfloat16* y, cudaStream_t s);
+
 cudaError_t k_pool(const __nv_bfloat16* x, int ldx, __nv_bfloat16* y, int ldy, int y_off, int B,
                    int H, int W, int C, int Ho, int Wo, int k, int s, int pad, int mode,
                    const float* scale, const float* shift, cudaStream_t st);

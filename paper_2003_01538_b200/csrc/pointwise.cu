@@ -9,6 +9,7 @@
 
 #include <cstdint>
 
+#include "eb_internal.h"
 #include "eb_kernels.h"
 
 namespace eb {
@@ -130,6 +131,39 @@ cudaError_t k_preprocess_u8hwc_to_f32chw(const uint8_t* x, float* y, int B, int 
   if (pixels == 0) return cudaSuccess;
   preprocess_u8hwc_to_f32chw_kernel<<<grid_for(pixels, 256), 256, 0, s>>>(x, y, pixels, C,
                                                                           plane, lut);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ stem relayout
+// One thread per 16-byte output pixel (8 bf16 channels); borders are written as zeros
+// every time, so the destination needs no initialisation.
+__global__ void stem_relayout_kernel(const uint4* __restrict__ x, int B, int H, int W, int ph,
+                                     int pw, int planes, int Hq, int Wq, uint4* __restrict__ y,
+                                     int64_t total) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i % Wq);
+    const int64_t t = i / Wq;
+    const int hq = static_cast<int>(t % Hq);
+    const int bq = static_cast<int>(t / Hq);  // q * B + b
+    const int q = bq / B;                     // plane (planes mode)
+    const int b = bq - q * B;
+    const int ih = hq - ph;
+    const int iw = planes ? 2 * j + q - pw : j - pw;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[(static_cast<int64_t>(b) * H + ih) * W + iw];
+    y[i] = v;
+  }
+}
+
+cudaError_t k_stem_relayout(const __nv_bfloat16* x, int B, int H, int W, int ph, int pw, int mode,
+                            int Hq, int Wq, __nv_bfloat16* y, cudaStream_t s) {
+  const int planes = mode == kAModeStemPlanes ? 1 : 0;
+  const int64_t total = static_cast<int64_t>(planes ? 2 : 1) * B * Hq * Wq;
+  if (total == 0) return cudaSuccess;
+  stem_relayout_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(x), B, H, W, ph, pw, planes, Hq, Wq, reinterpret_cast<uint4*>(y),
+      total);
   return cudaGetLastError();
 }
 

@@ -137,6 +137,10 @@ bool tapn_enabled() {
   static const bool on = env_flag("EB_TAPN", true);
   return on;
 }
+bool stem_rows_enabled() {
+  static const bool on = env_flag("EB_STEM_ROWS", true);
+  return on;
+}
 bool stem_tma_enabled() {
   // measured on B200: the cp.async gather is as fast for the 3x3/s1 stem and 1.6x faster
   // for the 7x7/s2 one (16-byte im2col elements are TMA-request bound)
@@ -194,7 +198,13 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // 3x3 64->64 at 56x56 92 -> 83 us.
   const bool tapn = tap_shift && a.cout <= tapn_max_cout() && a.groups == 1 && !a.pre_scale && a.n_split == 0 &&
                     tapn_enabled();
-  const int64_t M64 = static_cast<int64_t>(a.B) * Ho * (tap_shift ? Wo + a.kw - 1 : Wo);
+  // stem rows / planes: x is the padded layout of an 8-channel image (k_stem_relayout)
+  const bool stem_direct = a.c8_stem == 2;
+  StemGeom sg{};
+  if (stem_direct && !stem_geom(a.B, a.H, a.W, a.kh, a.kw, a.sh, a.sw, a.ph, a.pw, &sg))
+    EB_FAIL(EB_E_INVALID, "unsupported stem layout geometry");
+  const int64_t M64 = stem_direct ? static_cast<int64_t>(a.B) * sg.Mi
+                                  : static_cast<int64_t>(a.B) * Ho * (tap_shift ? Wo + a.kw - 1 : Wo);
   if (M64 > (1ll << 31) - 1) EB_FAIL(EB_E_INVALID, "conv M too large");
   const int M = static_cast<int>(M64);
   const int64_t kpad =
@@ -219,7 +229,18 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     pl.p.x = static_cast<const __nv_bfloat16*>(a.x);
     pl.p.H = a.H;
     pl.p.W = a.W;
-    if (stem_tma_enabled()) {
+    if (stem_direct) {
+      // the layout as rows of 128 bytes (8 pixels x 8 channels); a load = 17 such lines
+      if (!encode_tiled_2d_bf16(&pl.ma, a.x, 64, static_cast<uint64_t>(sg.bytes / 128), 64, 64, 17,
+                                &err, 0))
+        EB_FAIL(EB_E_INVALID, err);
+      pl.p.a_mode = sg.mode;
+      pl.p.Wg = sg.Wg;
+      pl.p.Mi = sg.Mi;
+      pl.p.Hq = sg.Hq;
+      pl.p.Wq = sg.Wq;
+      pl.p.plane_px = sg.plane_px;
+    } else if (stem_tma_enabled()) {
       // per filter row: one TMA im2col load per horizontal tap, 128 pixels x 8 channels
       if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, 8, 8, a.kh, a.kw, a.sh, a.sw, a.ph,
                               a.pw, 8, 128, false, &err))
@@ -317,6 +338,17 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
                               num_kb >= 8 && !a.pre_scale && plain_a);
   pl.p.mcast = mcast ? 1 : 0;
   pl.p.pair = pair ? 1 : 0;
+  if (stem_direct) {
+    pl.p.fd_img = make_fastdiv(sg.Mi);
+    pl.p.fd_row = make_fastdiv(sg.Wg);
+  } else if (tap_shift) {
+    pl.p.fd_img = make_fastdiv(static_cast<uint32_t>(Ho) * (Wo + a.kw - 1));
+    pl.p.fd_row = make_fastdiv(Wo + a.kw - 1);
+  }
+  static const bool early = env_flag("EB_EARLY_REL", true);
+  pl.p.early_release = early ? 1 : 0;
+  static const int dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
+  pl.p.dbg = dbg;
   // Resident B: with a single N tile every CTA re-streams the same weights per tile; keep
   // them in smem instead when they fit and the A ring stays deep (it gets all the space).
   if (resb_enabled() && nt == 1 && splits == 1 && !mcast) {
@@ -340,7 +372,13 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
                         a.n_split % conv_umma_chunk(bn) != 0 || a.n_split >= a.cout))
     EB_FAIL(EB_E_INVALID, "unsupported grouped-launch split");
   pl.p.n_split = a.n_split;
-  if (!a.out_f32 && splits == 1 && !tap_shift) {
+  if (a.n_split > 0) {  // direct-store modes write the second column range themselves
+    pl.p.out2 = a.y2;
+    pl.p.ldo2 = a.ldy2;
+    pl.p.out2_off = a.y2_off;
+    if (a.ldy2 % 8 != 0 || a.y2_off % 8 != 0) pl.p.vec_ok = 0;
+  }
+  if (!a.out_f32 && splits == 1 && !tap_shift && !stem_direct) {
     const int cw = conv_umma_chunk(bn);
     const int n1 = a.n_split > 0 ? a.n_split : a.cout;
     if (!encode_tiled_2d_bf16(&pl.mo, static_cast<const __nv_bfloat16*>(a.y) + a.y_off, n1, M64,
@@ -429,6 +467,8 @@ struct eb_engine {
   std::mutex mu;
   // profiling: when set, every op runs on the main stream bracketed by events
   std::vector<cudaEvent_t>* prof = nullptr;
+  // stem convs reading an 8-channel image: padded-layout scratch (stem rows / planes modes)
+  std::map<const eb_op_desc*, void*> stem_buf;
 };
 
 namespace {
@@ -479,8 +519,21 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
       a.pw = op.pw;
       a.relu = op.relu;
       a.out_f32 = dst.dtype == EB_F32;
-      // an 8-channel source is a (possibly resized) K1 image: gathered stem mode
+      // an 8-channel source is a (possibly resized) K1 image: stem mode -- relaid out into
+      // the padded rows / planes layout when this op owns such a scratch, else gathered
       a.c8_stem = src.c == 8 && op.src_c == 8 && op.src_c_off == 0;
+      if (a.c8_stem) {
+        auto it = e->stem_buf.find(&op);
+        StemGeom g;
+        if (it != e->stem_buf.end() &&
+            stem_geom(B, src.h, src.w, op.kh, op.kw, op.sh, op.sw, op.ph, op.pw, &g)) {
+          EB_CUDA(k_stem_relayout(static_cast<const __nv_bfloat16*>(x), B, src.h, src.w, op.ph, op.pw,
+                                  g.mode, g.Hq, g.Wq, static_cast<__nv_bfloat16*>(it->second), ls));
+          ++*launches;
+          a.x = it->second;
+          a.c8_stem = 2;
+        }
+      }
       a.flatten = op.flatten;
       a.groups = op.groups > 1 ? op.groups : 1;
       a.pre_scale = static_cast<const float*>(P(op.scale_off));
@@ -728,6 +781,7 @@ int eb_engine_destroy(eb_engine* e) {
   cudaStreamSynchronize(e->stream);
   for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
   for (auto& t : e->tensors) cudaFree(t.dev);
+  for (auto& kv : e->stem_buf) cudaFree(kv.second);
   cudaFree(e->pool);
   cudaFree(e->d_mean);
   cudaFree(e->d_std);
@@ -913,6 +967,21 @@ int eb_finalize(eb_engine* e) {
   const size_t img = static_cast<size_t>(mb) * e->C * e->H * e->W;
   EB_CUDA(cudaMalloc(&e->d_in_u8, img));
   EB_CUDA(cudaMalloc(&e->d_in_f32, img * sizeof(float)));
+  if (stem_rows_enabled()) {
+    for (const auto& op : e->ops) {
+      if (op.kind != EB_OP_CONV) continue;
+      const Tensor& src = e->tensors[op.src];
+      StemGeom g;
+      if (!(src.c == 8 && op.src_c == 8 && op.src_c_off == 0)) continue;
+      if (!stem_geom(mb, src.h, src.w, op.kh, op.kw, op.sh, op.sw, op.ph, op.pw, &g)) continue;
+      void* buf = nullptr;
+      if (cudaMalloc(&buf, static_cast<size_t>(g.bytes)) != cudaSuccess) {
+        cudaGetLastError();
+        EB_FAIL(EB_E_NOMEM, "stem layout allocation failed");
+      }
+      e->stem_buf[&op] = buf;
+    }
+  }
   bool used[kLanes] = {};
   for (const auto& op : e->ops) used[op.stream] = true;
   for (int l = 0; l < kLanes; ++l)
@@ -1142,8 +1211,30 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
   ConvPlan pl;
   int rc = plan_conv(a, &pl);
   if (rc != EB_OK) return rc;
-  return run_conv_plan(pl, static_cast<float*>(dev_workspace), kSplitWsFloats, a,
-                       static_cast<cudaStream_t>(stream), nullptr);
+  // EB_TRACE=<file>: timing probe (per-role event clocks of CTA 0, appended as text)
+  static const char* trace_path = getenv("EB_TRACE");
+  static long long* d_trace = nullptr;
+  if (trace_path) {
+    if (!d_trace) EB_CUDA(cudaMalloc(&d_trace, 3 * 1024 * 2 * sizeof(long long)));
+    EB_CUDA(cudaMemset(d_trace, 0, 3 * 1024 * 2 * sizeof(long long)));
+    pl.p.trace = d_trace;
+  }
+  rc = run_conv_plan(pl, static_cast<float*>(dev_workspace), kSplitWsFloats, a,
+                     static_cast<cudaStream_t>(stream), nullptr);
+  if (rc == EB_OK && trace_path) {
+    std::vector<long long> h(3 * 1024 * 2);
+    EB_CUDA(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(trace_path, "w")) {
+      for (int r = 0; r < 3; ++r)
+        for (int i = 0; i < 1024; ++i) {
+          const long long v = h[(r * 1024 + i) * 2];
+          if (v == 0) break;
+          fprintf(f, "%d %lld %lld %lld\n", r, v >> 48, v & 0xFFFFFFFFFFFFll, h[(r * 1024 + i) * 2 + 1]);
+        }
+      fclose(f);
+    }
+  }
+  return rc;
 }
 
 int eb_k_resize(const void* dev_x, int ldx, void* dev_y, int ldy, int batch, int h, int w, int c,
@@ -1151,6 +1242,24 @@ int eb_k_resize(const void* dev_x, int ldx, void* dev_y, int ldy, int batch, int
   EB_CUDA(k_resize_bilinear(static_cast<const __nv_bfloat16*>(dev_x), ldx,
                             static_cast<__nv_bfloat16*>(dev_y), ldy, batch, h, w, c, ho, wo,
                             static_cast<cudaStream_t>(stream)));
+  return EB_OK;
+}
+
+int eb_k_stem_layout(int batch, int h, int w, int kh, int kw, int sh, int sw, int ph, int pw,
+                     uint64_t* bytes) {
+  StemGeom g;
+  if (!stem_geom(batch, h, w, kh, kw, sh, sw, ph, pw, &g)) EB_FAIL(EB_E_INVALID, "no stem layout");
+  if (bytes) *bytes = static_cast<uint64_t>(g.bytes);
+  return EB_OK;
+}
+
+int eb_k_stem_relayout(const void* dev_x, int batch, int h, int w, int kh, int kw, int sh, int sw,
+                       int ph, int pw, void* dev_y, void* stream) {
+  StemGeom g;
+  if (!stem_geom(batch, h, w, kh, kw, sh, sw, ph, pw, &g)) EB_FAIL(EB_E_INVALID, "no stem layout");
+  EB_CUDA(k_stem_relayout(static_cast<const __nv_bfloat16*>(dev_x), batch, h, w, ph, pw, g.mode,
+                          g.Hq, g.Wq, static_cast<__nv_bfloat16*>(dev_y),
+                          static_cast<cudaStream_t>(stream)));
   return EB_OK;
 }
 

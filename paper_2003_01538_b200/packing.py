@@ -28,7 +28,8 @@ def _round_up(x: int, m: int) -> int:
 
 def conv_mode(kh: int, kw: int, sh: int, sw: int, ph: int, pw: int, cin: int, stem: bool) -> str:
     if stem:
-        return "c8"
+        # stride-2 stems read even/odd column planes: their K groups list even taps first
+        return "c8s2" if sw == 2 else "c8"
     if kh == kw == 1 and sh == sw == 1 and ph == pw == 0:
         return "tiled"
     return "im2col"
@@ -48,11 +49,17 @@ def pack_conv_weight(w: torch.Tensor, mode: str, hw: tuple[int, int] | None = No
     cout, cin, kh, kw = w.shape
     taps = kh * kw
     wt = w.permute(0, 2, 3, 1).reshape(cout, taps, cin)  # (Cout, tap, Cin)
-    if mode == "c8":
+    if mode in ("c8", "c8s2"):
+        # one 64-wide K block per filter row: 8 K groups (taps) x 8 channels; "c8s2" orders
+        # the groups as taps 0, 2, 4, 6, 1, 3, 5, 7 (csrc/conv_umma.cu, stem planes mode)
         if cin > 8 or kw > 8:
             raise ValueError("c8 packing needs Cin <= 8 and kw <= 8")
         out = torch.zeros(cout, kh, 8, 8, dtype=torch.float32)
-        out[:, :, :kw, :cin] = wt.reshape(cout, kh, kw, cin)
+        wr = wt.reshape(cout, kh, kw, cin)
+        for g in range(8):
+            tap = (2 * g if g < 4 else 2 * (g - 4) + 1) if mode == "c8s2" else g
+            if tap < kw:
+                out[:, :, g, :cin] = wr[:, :, tap, :]
     else:
         cpad = _round_up(cin, 64)
         out = torch.zeros(cout, taps, cpad, dtype=torch.float32)

@@ -373,7 +373,7 @@ def grouped_stem(eng: Engine, image: TRef, stems) -> list[TRef]:
             "shape": (ho, wo, sum(couts), kh, kw, sh, image.c), "weight_bytes": 2 * w[0].numel() * len(w),
             "grouped_members": len(stems)}
     eng.op(_lib.EB_OP_CONV, image, out, cout=sum(couts), kh=kh, kw=kw, sh=sh, sw=sw, ph=ph, pw=pw,
-           relu=True, lane=0, w_off=eng.weight(pack_conv_weight(w, "c8")),
+           relu=True, lane=0, w_off=eng.weight(pack_conv_weight(w, conv_mode(kh, kw, sh, sw, ph, pw, 8, True))),
            b_off=eng.weight(b.contiguous()), meta=meta, prefork=True)
     slices, off = [], 0
     for c in couts:

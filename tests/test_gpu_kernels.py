@@ -114,6 +114,49 @@ def test_conv_stem_c8():
     assert err <= 0.02 * r.abs().max().item() + 1e-2, err
 
 
+STEM_CASES = [
+    # name, B, H, W, cout, kh, kw, s, p  (the image has 3 real channels, padded to 8)
+    ("vgg_rows", 2, 30, 26, 64, 3, 3, 1, 1),
+    ("resnet_planes", 3, 57, 61, 64, 7, 7, 2, 3),
+    ("grouped_planes", 2, 40, 44, 128, 7, 7, 2, 3),
+    ("inception_planes", 2, 37, 41, 32, 3, 3, 2, 0),
+    ("wide_planes", 1, 20, 300, 64, 7, 7, 2, 3),   # Wo > 128: two tiles per output row
+]
+
+
+@pytest.mark.parametrize("case", STEM_CASES, ids=[c[0] for c in STEM_CASES])
+@pytest.mark.parametrize("layout", [1, 2], ids=["gather", "relayout"])
+def test_stem_layouts(case, layout):
+    """Stems through the cp.async gather (c8_stem = 1) and through the padded rows /
+    even-odd planes layouts (c8_stem = 2 after eb_k_stem_relayout)."""
+    lib = _lib.load()
+    _, B, H, W, cout, kh, kw, st, pd = case
+    g = torch.Generator().manual_seed(H * W + cout)
+    x = torch.zeros(B, H, W, 8)
+    x[..., :3] = torch.randn(B, H, W, 3, generator=g)
+    x = x.to(torch.bfloat16).to(DEV)
+    w = torch.randn(cout, 3, kh, kw, generator=g) / np.sqrt(3 * kh * kw)
+    bias = torch.randn(cout, generator=g) * 0.1
+    Ho, Wo = (H + 2 * pd - kh) // st + 1, (W + 2 * pd - kw) // st + 1
+    wp = pack_conv_weight(w, conv_mode(kh, kw, st, st, pd, pd, 3, True)).to(DEV)
+    src = x
+    if layout == 2:
+        nbytes = ctypes.c_uint64(0)
+        _lib.check(lib.eb_k_stem_layout(B, H, W, kh, kw, st, st, pd, pd, ctypes.byref(nbytes)))
+        src = torch.full((nbytes.value // 2,), float("nan"), device=DEV).to(torch.bfloat16)
+        _lib.check(lib.eb_k_stem_relayout(_p(x), B, H, W, kh, kw, st, st, pd, pd, _p(src), None))
+    y = torch.full((B, Ho, Wo, cout), float("nan"), device=DEV).to(torch.bfloat16)
+    _lib.check(lib.eb_k_conv(
+        _p(src), B, H, W, 8, 8, _p(wp), _p(bias.to(DEV)), None, 0, _p(y), cout, 0, cout, kh, kw,
+        st, st, pd, pd, 1, 0, layout, 0, 0, 1, None, None, None, None))
+    torch.cuda.synchronize()
+    r = ref_conv(x, 3, w, bias, None, True, kh, kw, st, st, pd, pd)
+    yy = y.float().cpu()
+    assert torch.isfinite(yy).all()
+    err = (yy - r).abs().max().item()
+    assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+
+
 def test_conv_slices_residual():
     # DenseNet-style: read a channel prefix of a wider buffer, write into a slice.
     g = torch.Generator().manual_seed(3)
