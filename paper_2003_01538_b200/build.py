@@ -24,6 +24,13 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include"), "-I", str(CSRC)]
 
+# EB_BUILD_TRACE=1: build the EB_TRACE timing probes into a separate library
+# (tools/_ab/libtrace.so, loaded with EB_LIB_PATH); the production build has none.
+if os.environ.get("EB_BUILD_TRACE"):
+    FLAGS = FLAGS + ["-DEB_ENABLE_TRACE"]
+    BUILD = ROOT / "build_trace"
+    LIB = ROOT / "tools" / "_ab" / "libtrace.so"
+
 SOURCES = ["conv_umma.cu", "pointwise.cu", "combine.cu", "runtime.cu", "tmap.cpp", "wire_decode.cpp"]
 
 
@@ -54,6 +61,7 @@ def _compile(src: Path, verbose: bool) -> Path:
 
 def build(verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
+    LIB.parent.mkdir(exist_ok=True)
     srcs = [CSRC / s for s in SOURCES]
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))

@@ -50,7 +50,9 @@ constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels 
 // with the 3 horizontal taps' weights stacked along N (N = 3 x BN); the epilogue adds the
 // tap planes shifted by 0/1/2 rows.  The A tile is 4 x 32 rows overlapping by 2, so each
 // lane quarter can form its 30 outputs with warp shuffles; tiles advance 120 rows.
-template <int BN, int TS, bool PAIR, bool TAPN = false>
+// STEM: the stem rows / planes modes (direct row stores; separate instances so the
+// other kernels do not carry their code)
+template <int BN, int TS, bool PAIR, bool TAPN = false, bool STEM = false>
 struct ConvSmem {
   static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "tile width");
   static constexpr int kBN = BN;
@@ -62,13 +64,13 @@ struct ConvSmem {
   static constexpr int kBBytes = (TAPN ? 3 : TS) * kBTapBytes;
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
   // one warp's 32-row chunk; tap-shift tiles store directly (no staging, no residual)
-  static constexpr int kStageOutBytes = (TS == 1 && !TAPN) ? 32 * kCW * 2 : 0;
+  static constexpr int kStageOutBytes = (TS == 1 && !TAPN && !STEM) ? 32 * kCW * 2 : 0;
   // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
-  static constexpr int kPreMax = (BN == 128 && TS == 1 && !PAIR && !TAPN) ? 2048 : 0;
+  static constexpr int kPreMax = (BN == 128 && TS == 1 && !PAIR && !TAPN && !STEM) ? 2048 : 0;
   // ring: 16 chunk buffers (4 warps x 4 or 8 warps x 2); tap-shift / taps-in-N tiles
   // instead stage 32 rows x 32 columns per warp for coalesced row stores
   static constexpr int kRowStageBytes = 32 * 32 * 2;
-  static constexpr int kRingArea = (TS == 1 && !TAPN) ? 16 * kStageOutBytes : 8 * kRowStageBytes;
+  static constexpr int kRingArea = (TS == 1 && !TAPN && !STEM) ? 16 * kStageOutBytes : 8 * kRowStageBytes;
   // bias cache: 8 warps x BN floats
   static constexpr int kEpiBytes = kRingArea + 8 * BN * 4 + 2 * kPreMax * 4;
   // dynamic smem: everything (one CTA per SM); 1 KiB alignment slack + barrier block
@@ -171,7 +173,12 @@ __device__ __forceinline__ void stage_store_rows32(uint8_t* buf, const uint32_t*
 
 // EB_TRACE timing probe: role r (0 producer, 1 MMA, 2 epilogue warp 2) of CTA 0 records
 // up to 1024 (tag, clock) events
+// Compiled in only with -DEB_ENABLE_TRACE (EB_BUILD_TRACE=1 python -m ...build): the
+// probes cost instruction-cache space in the hot loops.
 __device__ __forceinline__ void trace_ev(long long* tr, int role, int& n, int tag) {
+#ifndef EB_ENABLE_TRACE
+  return;
+#endif
   if (tr && blockIdx.x == 0 && n < 1024) {
     const long long clk = clock64();
     tr[(role * 1024 + n) * 2] = (static_cast<long long>(tag) << 48) | (clk & 0xFFFFFFFFFFFFll);
@@ -186,20 +193,20 @@ __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
   return cw == 64 ? (chunk ^ (row & 7)) : (chunk ^ ((row >> 1) & 3));
 }
 
-template <int BN, int TS, bool PAIR, bool TAPN>
+template <int BN, int TS, bool PAIR, bool TAPN, bool STEM>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_umma_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ CUtensorMap map_out,
                      const __grid_constant__ CUtensorMap map_res, const ConvParams p) {
-  using S = ConvSmem<BN, TS, PAIR, TAPN>;
+  using S = ConvSmem<BN, TS, PAIR, TAPN, STEM>;
   extern __shared__ uint8_t smem_raw[];
   // 128B swizzle needs 1024-byte aligned tiles
   // (offset arithmetic on the __shared__ array keeps the address space visible to the
   // compiler, so staging accesses compile to STS/LDS rather than generic ST/LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const SmemLayout L = make_layout<S>(p.resb, p.num_kb, p.a_mode);
-  const bool stem_direct = p.a_mode == kAModeStemRows || p.a_mode == kAModeStemPlanes;
+  constexpr bool stem_direct = STEM;  // a_mode is kAModeStemRows / kAModeStemPlanes
   const int a_stage = stem_direct ? stem_a_bytes(p.a_mode) : S::kABytes;  // B follows A
   uint8_t* const ring_base = smem + L.resb_bytes;  // stage s at ring_base + s * stage_bytes
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // stem rows / planes: first 128-byte line of this tile's filter row 0 (per tile)
         int stem_line0 = 0;
         const int stem_plane_lines = static_cast<int>(p.plane_px >> 3);
-        if (stem_direct) {
+        if constexpr (stem_direct) {
           const int b = m0 / p.Mi;
           const int local = m0 - b * p.Mi;
           long long px;
@@ -935,20 +942,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int oh = rem / p.Wo;
       const int ow = rem - oh * p.Wo;
       const int iw0 = ow * p.sw - p.pw;
+      // per tile: the 8 pixel columns of this row (K group j <- tap; stride-2 stem weights
+      // list the even taps first, then the odd) and which of them lie inside the image
+      uint32_t wmask = 0;
+      int coff[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int tap = p.sw == 2 ? (j < 4 ? 2 * j : 2 * (j - 4) + 1) : j;
+        const int iw = iw0 + tap;
+        const bool ok = iw >= 0 && iw < p.W;
+        wmask |= (ok ? 1u : 0u) << j;
+        coff[j] = (ok ? iw : 0) * 8;
+      }
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* rowp = ring_base + stage * L.stage_bytes + r * 128;
         const int ih = oh * p.sh - p.ph + kb;
         const bool hok = row_ok && ih >= 0 && ih < p.H;
         const __nv_bfloat16* src = p.x + ((static_cast<int64_t>(img) * p.H + (hok ? ih : 0)) * p.W) * 8;
+        const uint32_t m8 = hok ? wmask : 0u;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          // stride-2 stem weights list the even taps first (K groups 0..3), then the odd
-          const int tap = p.sw == 2 ? (j < 4 ? 2 * j : 2 * (j - 4) + 1) : j;
-          const int iw = iw0 + tap;
-          const bool ok = hok && iw >= 0 && iw < p.W;
-          cp_async_16(rowp + ((j ^ (r & 7)) * 16), src + (ok ? iw : 0) * 8, ok ? 16u : 0u);
-        }
+        for (int j = 0; j < 8; ++j)
+          cp_async_16(rowp + ((j ^ (r & 7)) * 16), src + coff[j], ((m8 >> j) & 1u) ? 16u : 0u);
         cp_async_arrive_noinc(&xfull[stage]);
         if (++stage == L.stages) {
           stage = 0;
@@ -1032,14 +1047,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------- host side
 
-template <int BN, int TS, bool PAIR, bool TAPN = false>
+template <int BN, int TS, bool PAIR, bool TAPN = false, bool STEM = false>
 static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int grid,
                              cudaStream_t stream) {
-  using S = ConvSmem<BN, TS, PAIR, TAPN>;
+  using S = ConvSmem<BN, TS, PAIR, TAPN, STEM>;
   static bool configured = false;  // attribute is per-function; idempotent
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<BN, TS, PAIR, TAPN>,
+    cudaError_t e = cudaFuncSetAttribute(conv_umma_kernel<BN, TS, PAIR, TAPN, STEM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes);
     if (e != cudaSuccess) return e;
     configured = true;
@@ -1058,17 +1073,22 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, conv_umma_kernel<BN, TS, PAIR, TAPN>, ma, mb, mo, mr, p);
+  return cudaLaunchKernelEx(&cfg, conv_umma_kernel<BN, TS, PAIR, TAPN, STEM>, ma, mb, mo, mr, p);
 }
 
 int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
 
-template <int BN, int TS, bool PAIR, bool TAPN = false>
+template <int BN, int TS, bool PAIR, bool TAPN = false, bool STEM = false>
 static int stages_of(const ConvParams& p) {
-  return make_layout<ConvSmem<BN, TS, PAIR, TAPN>>(p.resb, p.num_kb, p.a_mode).stages;
+  return make_layout<ConvSmem<BN, TS, PAIR, TAPN, STEM>>(p.resb, p.num_kb, p.a_mode).stages;
 }
 int conv_umma_stages(const ConvParams& p, int block_n) {
   const bool ts = p.a_mode == kAModeTapShift;
+  if (p.a_mode == kAModeStemRows || p.a_mode == kAModeStemPlanes)
+    return block_n == 32 ? stages_of<32, 1, false, false, true>(p)
+           : block_n == 64 ? stages_of<64, 1, false, false, true>(p)
+           : block_n == 128 ? stages_of<128, 1, false, false, true>(p)
+                            : stages_of<256, 1, false, false, true>(p);
   if (p.a_mode == kAModeTapN) return block_n == 32 ? stages_of<32, 1, false, true>(p) : stages_of<64, 1, false, true>(p);
   if (p.pair) {
     if (ts) return block_n == 64 ? stages_of<64, 3, true>(p) : stages_of<128, 3, true>(p);
@@ -1094,6 +1114,16 @@ bool pdl_enabled() {
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
                              cudaStream_t stream) {
+  if (p.a_mode == kAModeStemRows || p.a_mode == kAModeStemPlanes) {
+    if (p.mcast || p.pair) return cudaErrorInvalidValue;
+    switch (block_n) {
+      case 32: return launch_bn<32, 1, false, false, true>(ma, mb, mo, mr, p, grid, stream);
+      case 64: return launch_bn<64, 1, false, false, true>(ma, mb, mo, mr, p, grid, stream);
+      case 128: return launch_bn<128, 1, false, false, true>(ma, mb, mo, mr, p, grid, stream);
+      case 256: return launch_bn<256, 1, false, false, true>(ma, mb, mo, mr, p, grid, stream);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (p.a_mode == kAModeTapN) {
     if (p.mcast || p.pair) return cudaErrorInvalidValue;
     switch (block_n) {
