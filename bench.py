@@ -17,6 +17,8 @@ Reported on one JSON line (rank 0):
              pinned host input, H2D + forward + D2H of labels inside the timing
   roofline   the tcgen05 conv/GEMM kernel class: algorithmic FLOPs of every conv
              launch / its CUDA-event time (serialised per-op profile)
+  hbm_kernels   achieved GB/s of the memory-bound kernels (K1 preprocess, K5 combine)
+             against the measured HBM peak, timed alone through the kernel-level ABI
   cpu_baseline  the oracle (torchvision fp32 eager on all host cores) on a
              bounded sample of the same workload
 """
@@ -44,6 +46,69 @@ GFLOP_PER_IMG = 44.787  # SURVEY.md §2.4 (conv + linear, 2*MAC, torchvision flo
 MEAN = (0.485, 0.456, 0.406)
 STD = (0.229, 0.224, 0.225)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def _event_time(fn, iters: int = 50) -> float:
+    """Mean ms per call of fn() on the current stream (CUDA events, after warm-up)."""
+    import torch
+
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def hbm_kernels(B: int, hbm_peak: float, src: str) -> dict:
+    """Achieved HBM bandwidth of the two memory-bound kernels of the path, through the
+    kernel-level C-ABI on device buffers (north_star: preprocess and combine vs HBM peak).
+
+    K1 preprocess: u8 HWC (3 B/px) -> bf16 NHWC8 (16 B/px): 19 algorithmic bytes per pixel.
+    K5 combine: 3 members x 1000 fp32 logits per image read, labels + top-5 written; at the
+    bench batch it is latency-bound (a few MB), so it is also reported at B = 4096 (C4).
+    """
+    import ctypes
+
+    import torch
+
+    from paper_2003_01538_b200 import _lib
+
+    lib = _lib.load()
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    out = {}
+    hw = 224 * 224
+    x = torch.randint(0, 256, (B, hw * 3), dtype=torch.uint8, device="cuda")
+    y = torch.empty(B * hw * 8, dtype=torch.bfloat16, device="cuda")
+    lut = torch.rand(3 * 256, device="cuda")
+    ms = _event_time(lambda: _lib.check(lib.eb_k_preprocess_u8_nhwc8(P(x), P(y), B, 3, hw, P(lut), None)))
+    bytes_ = B * hw * (3 + 16)
+    out["preprocess_k1"] = {"batch": B, "us": ms * 1e3, "bytes": bytes_, "achieved_gbs": bytes_ / ms / 1e6,
+                            "frac_of_hbm": bytes_ / ms / 1e6 / hbm_peak}
+    for b in (B, 4096):
+        K, n, tk = 1000, 3, 5
+        l32 = torch.randn(b, n * K, device="cuda")
+        l64 = torch.zeros(1, 1, dtype=torch.float64, device="cuda")
+        kind = torch.zeros(n, dtype=torch.int32, device="cuda")
+        koff = torch.arange(0, n * K, K, dtype=torch.int32, device="cuda")
+        kcnt = torch.full((n,), K, dtype=torch.int32, device="cuda")
+        lab = torch.empty(n, b, dtype=torch.int32, device="cuda")
+        tki = torch.empty(n, b, tk, dtype=torch.int32, device="cuda")
+        tkp = torch.empty(n, b, tk, dtype=torch.float32, device="cuda")
+        comb = torch.empty(b, dtype=torch.int32, device="cuda")
+        ms = _event_time(lambda: _lib.check(lib.eb_k_combine(
+            P(l32), n * K, P(l64), 1, P(kind), P(koff), P(kcnt), n, b, P(lab), tk, P(tki), P(tkp), 0, 0,
+            P(comb), None)))
+        bytes_ = b * (n * K * 4 + n * 4 + n * tk * 8)
+        out[f"combine_k5_b{b}"] = {"batch": b, "us": ms * 1e3, "bytes": bytes_,
+                                   "achieved_gbs": bytes_ / ms / 1e6, "frac_of_hbm": bytes_ / ms / 1e6 / hbm_peak}
+    out["peak_gbs"] = hbm_peak
+    out["peak_source"] = f"{src} hbm_gbs"
+    return out
 
 
 def peaks() -> tuple[dict, str]:
@@ -343,6 +408,8 @@ def main() -> None:
             [{"i": i, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in m.items()}, "ms": float(t)}
              for i, (m, t) in enumerate(zip(eng.op_meta, ms))], indent=0))
 
+    hbm = hbm_kernels(B, pk["hbm_gbs"], pk_src) if rank == 0 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -377,6 +444,7 @@ def main() -> None:
                          "step_frac_of_peak": GFLOP_PER_IMG * 1e9 * B * world / (dev_ms / args.steps / 1e3) / 1e12 / peak / world,
                          "top_launch": {"shape(ho,wo,cout,kh,kw,s,cin)": list(top[0]["shape"]), "ms": top[1]} if top else None},
             "clocks": clk.summary(),
+            "hbm_kernels": hbm,
             "cpu_baseline": cpu,
         }
         if sweep:

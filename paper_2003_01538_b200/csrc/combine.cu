@@ -86,6 +86,84 @@ __device__ void member_outputs(const T* row, int K, int lane, int mem, int B, in
   }
 }
 
+// Fast path for fp32 members with K <= 32 * VPL: the warp reads the row ONCE into
+// registers (lane l holds elements l, l + 32, ...; each load instruction is one
+// coalesced 128-byte line), then argmax, the softmax denominator and the top-k rounds
+// all run on registers.  Each top-k round: every lane offers its best remaining
+// (value, index), a 5-step shuffle reduction picks the winner (value desc, index asc),
+// and the owning lane retires that slot.
+template <int VPL>
+__device__ void member_outputs_reg(const float* row, int K, int lane, int mem, int B, int b,
+                                   int32_t* labels, int* s_lab, int topk, int32_t* topk_idx,
+                                   float* topk_prob) {
+  float v[VPL];
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int i = lane + 32 * j;
+    v[j] = i < K ? __ldg(row + i) : -INFINITY;
+  }
+  auto local_best = [&](float& bv, int& bj) {
+    bv = v[0];
+    bj = 0;
+#pragma unroll
+    for (int j = 1; j < VPL; ++j)
+      if (v[j] > bv) {  // strict: equal values keep the lower j (= lower index)
+        bv = v[j];
+        bj = j;
+      }
+  };
+  auto warp_best = [&](float bv, int bi, float& wv, int& wi) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    wv = bv;
+    wi = bi;
+  };
+  float bv;
+  int bj;
+  local_best(bv, bj);
+  int bi = (bv == -INFINITY) ? -1 : lane + 32 * bj;
+  float wv;
+  int wi;
+  warp_best(bv, bi, wv, wi);
+  if (lane == 0) {
+    labels[static_cast<int64_t>(mem) * B + b] = wi;
+    s_lab[mem] = wi;
+  }
+  if (topk <= 0) return;
+  const float mx = wv;
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < VPL; ++j)
+    if (lane + 32 * j < K) sum += __expf(v[j] - mx);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  const float inv = 1.f / sum;
+  const int64_t base = (static_cast<int64_t>(mem) * B + b) * topk;
+  for (int r = 0; r < topk; ++r) {
+    if (lane == 0) {
+      topk_idx[base + r] = wi;
+      topk_prob[base + r] = (wi >= 0) ? __expf(wv - mx) * inv : 0.f;
+    }
+    if (r + 1 == topk) break;
+    if (wi >= 0 && (wi & 31) == lane) {  // the winner retires its slot
+      const int wj = wi >> 5;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j)
+        if (j == wj) v[j] = -INFINITY;
+      local_best(bv, bj);
+      bi = (bv == -INFINITY) ? -1 : lane + 32 * bj;
+    }
+    warp_best(bv, bi, wv, wi);
+  }
+}
+
 // Member m reads logits from the fp32 buffer (CNN members) when kind[m] == 0,
 // else from the fp64 buffer (LIN1 members); koff[m] is its column offset.
 __global__ void combine_kernel(const float* __restrict__ l32, int ld32,
@@ -100,7 +178,10 @@ __global__ void combine_kernel(const float* __restrict__ l32, int ld32,
   const int nwarps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int mem = warp; mem < N; mem += nwarps) {
-    if (kind[mem] == 0)
+    if (kind[mem] == 0 && kcnt[mem] <= 1024)
+      member_outputs_reg<32>(l32 + static_cast<int64_t>(b) * ld32 + koff[mem], kcnt[mem], lane, mem,
+                             B, b, labels, s_lab, topk, topk_idx, topk_prob);
+    else if (kind[mem] == 0)
       member_outputs(l32 + static_cast<int64_t>(b) * ld32 + koff[mem], kcnt[mem], lane, mem, B, b,
                      labels, s_lab, topk, topk_idx, topk_prob);
     else
