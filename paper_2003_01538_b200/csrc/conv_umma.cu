@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(p.pre_scale ? &xfull[stage] : &full[stage], phase);
-        if (p.a_mode == kAModeGatherC8) mbar_wait(&xfull[stage], phase);
+        if (p.a_mode == kAModeGatherC8 && p.dbg != 2) mbar_wait(&xfull[stage], phase);
         if (lane_id() == 0) trace_ev(p.trace, 1, tr_n, 11);
         tc_fence_after();
         if (elect_one()) {
@@ -884,6 +884,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           continue;
         }
+        if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 25);
         if (!has_res) {
           // the store that last used this ring buffer (nb chunks ago) has read it
           if (lane == 0) {
@@ -899,8 +900,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ch = 0; ch < CW / 8; ++ch)
           *reinterpret_cast<uint4*>(rowp + swz_chunk(ch, lane, CW) * 16) =
               make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+        if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 26);
         fence_proxy_async_smem();
         __syncwarp();
+        if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 27);
         if (lane == 0) {
           // a grouped launch (members sharing a stem) writes its second column range
           // to another tensor through the residual map slot
