@@ -986,12 +986,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int t = static_cast<int>(threadIdx.x) - 192;  // 0..127
       const int j = t & 7;
       const int r0 = (t >> 3) * 8;
-      float* sc_s = reinterpret_cast<float*>(smem + L.pre_off);
-      float* sh_s = sc_s + S::kPreMax;
+      // scale/shift rounded to bf16 once (the math is bf16x2 FMA anyway)
+      __nv_bfloat16* sc_s = reinterpret_cast<__nv_bfloat16*>(smem + L.pre_off);
+      __nv_bfloat16* sh_s = sc_s + S::kPreMax;
       const int kpad = p.num_kb * kBlockK;
       for (int i = t; i < kpad; i += 128) {
-        sc_s[i] = __ldg(p.pre_scale + i);
-        sh_s[i] = __ldg(p.pre_shift + i);
+        sc_s[i] = __float2bfloat16_rn(__ldg(p.pre_scale + i));
+        sh_s[i] = __float2bfloat16_rn(__ldg(p.pre_shift + i));
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");  // the four transform warps only
       int stage = 0;
@@ -1004,26 +1005,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
         for (int kb = kb0; kb < kb1; ++kb) {
           const int c0 = kb * kBlockK + j * 8;
-          const float4 s0 = *reinterpret_cast<const float4*>(sc_s + c0);
-          const float4 s1 = *reinterpret_cast<const float4*>(sc_s + c0 + 4);
-          const float4 t0 = *reinterpret_cast<const float4*>(sh_s + c0);
-          const float4 t1 = *reinterpret_cast<const float4*>(sh_s + c0 + 4);
-          // packed bf16x2 math: one HFMA2 + one HMNMX2 per channel pair
-          const __nv_bfloat162 sc2[4] = {__floats2bfloat162_rn(s0.x, s0.y), __floats2bfloat162_rn(s0.z, s0.w),
-                                         __floats2bfloat162_rn(s1.x, s1.y), __floats2bfloat162_rn(s1.z, s1.w)};
-          const __nv_bfloat162 sh2[4] = {__floats2bfloat162_rn(t0.x, t0.y), __floats2bfloat162_rn(t0.z, t0.w),
-                                         __floats2bfloat162_rn(t1.x, t1.y), __floats2bfloat162_rn(t1.z, t1.w)};
-          const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
+          // one HFMA2.RELU per channel pair
+          const uint4 sq = *reinterpret_cast<const uint4*>(sc_s + c0);
+          const uint4 tq = *reinterpret_cast<const uint4*>(sh_s + c0);
+          const __nv_bfloat162* sc2 = reinterpret_cast<const __nv_bfloat162*>(&sq);
+          const __nv_bfloat162* sh2 = reinterpret_cast<const __nv_bfloat162*>(&tq);
           mbar_wait(&full[stage], phase);
           uint8_t* tile = ring_base + stage * L.stage_bytes;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < (p.dbg == 3 ? 0 : 8); ++i) {  // (dbg 3: timing probe, no transform)
             const int r = r0 + i;  // r & 7 == i
             uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + ((j ^ i) * 16));
             uint4 x = *q;
             __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) h[e] = __hmax2(__hfma2(h[e], sc2[e], sh2[e]), zero2);
+            for (int e = 0; e < 4; ++e) h[e] = __hfma2_relu(h[e], sc2[e], sh2[e]);
             *q = x;
           }
           fence_proxy_async_smem();
