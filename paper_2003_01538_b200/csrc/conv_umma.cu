@@ -90,16 +90,23 @@ struct SmemLayout {
   int resb_bytes, stage_bytes, stages, out_off, bias_off, pre_off, bar_off;
 };
 // A bytes per stage: the stem modes stage one (rows) or two (planes) 136-pixel runs
-__host__ __device__ inline int stem_a_bytes(int a_mode) {
-  return a_mode == kAModeStemRows ? 3072 : a_mode == kAModeStemPlanes ? 5120 : 0;
+// A bytes per stage: the stem modes stage one (rows) or two (planes) 136-pixel runs per
+// filter row, kbs filter rows per stage
+constexpr int kStemPlaneOff = 2304;  // planes mode: the odd-column run's offset in a row block
+__host__ __device__ inline int stem_run_bytes(int a_mode) {
+  return a_mode == kAModeStemRows ? 2304 : a_mode == kAModeStemPlanes ? 4608 : 0;
 }
-constexpr int kStemPlaneOff = 2304;  // planes mode: the odd-column run's offset in the stage
+__host__ __device__ inline int stem_a_bytes(int a_mode, int kbs) {
+  const int b = stem_run_bytes(a_mode) * (kbs > 0 ? kbs : 1);
+  return (b + 1023) / 1024 * 1024;
+}
 template <class S>
-__host__ __device__ inline SmemLayout make_layout(int resb, int num_kb, int a_mode) {
+__host__ __device__ inline SmemLayout make_layout(int resb, int num_kb, int a_mode, int kbs) {
   SmemLayout L;
-  const int ab = stem_a_bytes(a_mode);
-  L.resb_bytes = resb ? num_kb * S::kBBytes : 0;
-  L.stage_bytes = (ab ? ab : S::kABytes) + (resb ? 0 : S::kBBytes);
+  const int ab = stem_run_bytes(a_mode) ? stem_a_bytes(a_mode, kbs) : 0;
+  const int bb = S::kBBytes * (kbs > 0 ? kbs : 1);  // B bytes of one stage
+  L.resb_bytes = resb ? num_kb * bb : 0;
+  L.stage_bytes = (ab ? ab : S::kABytes) + (resb ? 0 : bb);
   int st = (S::kBudget - S::kEpiBytes - L.resb_bytes) / L.stage_bytes;
   L.stages = st > S::kMaxStages ? S::kMaxStages : st;
   L.out_off = L.resb_bytes + L.stages * L.stage_bytes;
@@ -205,9 +212,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (offset arithmetic on the __shared__ array keeps the address space visible to the
   // compiler, so staging accesses compile to STS/LDS rather than generic ST/LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const SmemLayout L = make_layout<S>(p.resb, p.num_kb, p.a_mode);
+  const SmemLayout L = make_layout<S>(p.resb, p.num_kb, p.a_mode, p.kbs);
   constexpr bool stem_direct = STEM;  // a_mode is kAModeStemRows / kAModeStemPlanes
-  const int a_stage = stem_direct ? stem_a_bytes(p.a_mode) : S::kABytes;  // B follows A
+  const int kbs = stem_direct ? p.kbs : 1;  // 64-wide K blocks per stage
+  const int a_stage = stem_direct ? stem_a_bytes(p.a_mode, kbs) : S::kABytes;  // B follows A
+  const int b_stage = S::kBBytes * kbs;
   uint8_t* const ring_base = smem + L.resb_bytes;  // stage s at ring_base + s * stage_bytes
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + L.stages;
@@ -298,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.resb) {
         // resident B (single N tile): every K block's weights, once per CTA
         mbar_arrive_expect_tx(bres, L.resb_bytes);
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = 0; kb < p.num_kb * kbs; ++kb) {  // (stems: kbs K blocks per stage)
           uint8_t* sb = smem + kb * S::kBBytes;
           if (TAPN || TS > 1) {
             const int r = kb / p.cchunks;
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           trace_ev(p.trace, 0, tr_n, 1);
           uint8_t* sa = ring_base + stage * L.stage_bytes;
-          uint8_t* sb = p.resb ? smem + kb * S::kBBytes : sa + a_stage;
+          uint8_t* sb = p.resb ? smem + kb * b_stage : sa + a_stage;
           if constexpr (TAPN) {
             // filter row r, channel chunk cc: lane quarter q's 32 rows are the padded-grid
             // pixels m0 + 30q ..; B = the row's 3 taps stacked along N
@@ -438,8 +447,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t abytes = p.a_mode == kAModeGatherC8 ? 0u
                                     : p.a_mode == kAModeTapC8
                                         ? static_cast<uint32_t>(p.kw * kTapC8Bytes)
-                                    : p.a_mode == kAModeStemRows   ? 2176u
-                                    : p.a_mode == kAModeStemPlanes ? 4352u
+                                    : p.a_mode == kAModeStemRows   ? 2176u * kbs
+                                    : p.a_mode == kAModeStemPlanes ? 4352u * kbs
                                                                    : static_cast<uint32_t>(S::kALoadBytes);
             // (gather mode with resident B: this stage only waits for the cp.async arrivals)
             mbar_arrive_expect_tx(&full[stage], abytes + bbytes);
@@ -465,10 +474,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             // filter row kb of a 128-position tile: contiguous 136-pixel runs (17 lines of
             // 8 pixels x 8 channels) of the padded layout; the next filter row is Wq
             // pixels further in both layouts
-            const int line = stem_line0 + kb * (p.Wq >> 3);
-            tma_load_2d(sa, &map_a, &full[stage], 0, line);
-            if (p.a_mode == kAModeStemPlanes)
-              tma_load_2d(sa + kStemPlaneOff, &map_a, &full[stage], 0, line + stem_plane_lines);
+            const int run = stem_run_bytes(p.a_mode);
+            for (int r = 0; r < kbs; ++r) {
+              const int line = stem_line0 + (kb * kbs + r) * (p.Wq >> 3);
+              tma_load_2d(sa + r * run, &map_a, &full[stage], 0, line);
+              if (p.a_mode == kAModeStemPlanes)
+                tma_load_2d(sa + r * run + kStemPlaneOff, &map_a, &full[stage], 0, line + stem_plane_lines);
+            }
           } else if (p.a_mode == kAModeTapC8) {
             // filter row kb: tap s brings 128 pixels x 8 channels (16 B) = the K group s
             // column of core matrices (2 KiB, no swizzle); groups s >= kw keep stale
@@ -479,7 +491,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  static_cast<uint16_t>(s), static_cast<uint16_t>(kb));
             }
           }  // kAModeGatherC8: A is gathered by warps 6..9
-          if (TS == 1 && !p.resb) {
+          if (stem_direct && !p.resb) {
+            for (int r = 0; r < kbs; ++r)
+              tma_load_2d(sb + r * S::kBBytes, &map_b, &full[stage], (kb * kbs + r) * kBlockK, n0);
+          } else if (TS == 1 && !p.resb) {
             if (p.mcast)  // our half of B, written into both CTAs
               tma_load_2d_mcast(sb + crank * (BN / 2) * 128, &map_b, &full[stage], kb * kBlockK,
                                 n0 + static_cast<int>(crank) * (BN / 2), 0x3);
@@ -555,11 +570,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(ring_base + stage * L.stage_bytes);
-          const uint32_t sb = p.resb ? smem_u32(smem + kb * S::kBBytes) : sa + a_stage;
+          const uint32_t sb = p.resb ? smem_u32(smem + kb * b_stage) : sa + a_stage;
           // descriptors: the per-kernel fields (LBO/SBO/layout) are fixed, so a K step or
           // a row shift only adds to the 14-bit start-address field (16-byte units)
           const uint64_t a0 = a_desc_hi | ((sa >> 4) & 0x3FFF);
           const uint64_t b0 = b_desc_hi | ((sb >> 4) & 0x3FFF);
+          if constexpr (stem_direct) {
+            // kbs filter rows per stage: row block r's run / B tile follow each other
+            const uint32_t run16 = stem_run_bytes(p.a_mode) >> 4;
+            for (int r = 0; r < kbs; ++r) {
+#pragma unroll
+              for (int k = 0; k < kBlockK / 16; ++k) {
+                if (!((kmask >> k) & 1u)) continue;
+                const uint64_t adesc = a0 + r * run16 + a_koff[k];
+                const uint64_t bdesc = b0 + r * (S::kBBytes >> 4) + 2 * k;
+                umma_bf16(tmem_d, adesc, bdesc, idesc, (kb > kb0 || r > 0 || k > 0) ? 1u : 0u);
+              }
+            }
+          } else {
 #pragma unroll
           for (int s2 = 0; s2 < TS; ++s2) {
 #pragma unroll
@@ -576,6 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               else
                 umma_bf16(tmem_d, adesc, bdesc, idesc, accum);
             }
+          }
           }
           if constexpr (PAIR) {
             umma_commit_pair_mcast(&empty[stage], 0x3);
@@ -1079,7 +1108,7 @@ int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
 
 template <int BN, int TS, bool PAIR, bool TAPN = false, bool STEM = false>
 static int stages_of(const ConvParams& p) {
-  return make_layout<ConvSmem<BN, TS, PAIR, TAPN, STEM>>(p.resb, p.num_kb, p.a_mode).stages;
+  return make_layout<ConvSmem<BN, TS, PAIR, TAPN, STEM>>(p.resb, p.num_kb, p.a_mode, p.kbs).stages;
 }
 int conv_umma_stages(const ConvParams& p, int block_n) {
   const bool ts = p.a_mode == kAModeTapShift;

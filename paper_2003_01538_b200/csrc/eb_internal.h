@@ -101,6 +101,7 @@ struct ConvParams {
   int mcast;                 // 2-CTA cluster: M-tile pairs share the B tile via TMA multicast
   int pair;                  // with mcast: 2-SM MMA (cta_group::2), M = 256 per CTA pair
   int resb;                  // single N tile: all K blocks of B resident in smem (loaded once)
+  int kbs;                   // stem modes: filter rows (64-wide K blocks) per pipeline stage
   int early_release;         // epilogue frees the accumulator right after its TMEM loads
   int dbg;                   // timing experiments only (EB_DBG); 0 in production
   long long* trace;          // timing experiments only (EB_TRACE): per-role event clocks of CTA 0

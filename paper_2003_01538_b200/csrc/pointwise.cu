@@ -134,6 +134,46 @@ cudaError_t k_preprocess_u8hwc_to_f32chw(const uint8_t* x, float* y, int B, int 
   return cudaGetLastError();
 }
 
+// K1 straight into a stem layout (StemGeom): u8 HWC -> LUT -> bf16 8-channel pixels of
+// the zero-padded rows / even-odd planes buffer.  Used instead of the NHWC8 image plus a
+// relayout when a stem reads the preprocessed image (one pass, no intermediate).
+__global__ void preprocess_u8_to_layout_kernel(const uint8_t* __restrict__ x, int B, int C, int H,
+                                               int W, const float* __restrict__ lut, int ph, int pw,
+                                               int planes, int Hq, int Wq, uint4* __restrict__ y,
+                                               int64_t total) {
+  __shared__ float s_lut[8 * 256];
+  for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i % Wq);
+    const int64_t t = i / Wq;
+    const int hq = static_cast<int>(t % Hq);
+    const int bq = static_cast<int>(t / Hq);
+    const int q = bq / B;
+    const int b = bq - q * B;
+    const int ih = hq - ph;
+    const int iw = planes ? 2 * j + q - pw : j - pw;
+    __align__(16) __nv_bfloat16 v[8];
+    const bool ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
+    const uint8_t* px = x + ((static_cast<int64_t>(b) * H + (ok ? ih : 0)) * W + (ok ? iw : 0)) * C;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = __float2bfloat16_rn((ok && c < C) ? s_lut[c * 256 + px[c]] : 0.f);
+    y[i] = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
+cudaError_t k_preprocess_u8_to_layout(const uint8_t* x, int B, int C, int H, int W, const float* lut,
+                                      int ph, int pw, int mode, int Hq, int Wq, __nv_bfloat16* y,
+                                      cudaStream_t s) {
+  const int planes = mode == kAModeStemPlanes ? 1 : 0;
+  const int64_t total = static_cast<int64_t>(planes ? 2 : 1) * B * Hq * Wq;
+  if (total == 0) return cudaSuccess;
+  preprocess_u8_to_layout_kernel<<<grid_for(total, 256), 256, 0, s>>>(
+      x, B, C, H, W, lut, ph, pw, planes, Hq, Wq, reinterpret_cast<uint4*>(y), total);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ stem relayout
 // One thread per 16-byte output pixel (8 bf16 channels); borders are written as zeros
 // every time, so the destination needs no initialisation.

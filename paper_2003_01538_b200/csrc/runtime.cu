@@ -137,10 +137,14 @@ bool tapn_enabled() {
   static const bool on = env_flag("EB_TAPN", true);
   return on;
 }
+bool stem_rows_per_stage_all() {
+  static const bool on = env_flag("EB_STEM_KBS", true);
+  return on;
+}
 bool stem_rows_enabled() {
-  // measured in the engine (B200, C2): relayout + rows/planes conv is not yet faster
-  // than the cp.async gather (VGG stem 1.01 vs 0.96 ms, grouped 7x7 stem 0.73 vs 0.53 ms)
-  static const bool on = env_flag("EB_STEM_ROWS", false);
+  // measured on B200 (B = 256): VGG stem 556 us (+ K1 writes the layout) vs 843 us gathered;
+  // grouped 7x7/2 stem 361 us vs 470 us; C2 step 14.8-14.9 vs 15.1 ms
+  static const bool on = env_flag("EB_STEM_ROWS", true);
   return on;
 }
 bool stem_tma_enabled() {
@@ -237,6 +241,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
                                 &err, 0))
         EB_FAIL(EB_E_INVALID, err);
       pl.p.a_mode = sg.mode;
+      pl.p.kbs = 1;  // (raised below to the whole filter when the smem ring stays deep)
       pl.p.Wg = sg.Wg;
       pl.p.Mi = sg.Mi;
       pl.p.Hq = sg.Hq;
@@ -351,13 +356,29 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.p.early_release = early ? 1 : 0;
   static const int dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
   pl.p.dbg = dbg;
+  bool stem_whole = false;
+  if (stem_direct && stem_rows_per_stage_all()) {
+    // stems: all kh filter rows of a tile in one stage (one wait / one commit per tile);
+    // prefer resident weights, accept a 2-deep ring (a stage is a whole tile of MMAs)
+    ConvParams q = pl.p;
+    q.kbs = a.kh;
+    q.num_kb = 1;
+    q.kb_per_split = 1;
+    q.resb = nt == 1 ? 1 : 0;
+    if (conv_umma_stages(q, bn) < 2) q.resb = 0;
+    if (conv_umma_stages(q, bn) >= 2) {
+      pl.p = q;
+      stem_whole = true;
+    }
+  }
   // Resident B: with a single N tile every CTA re-streams the same weights per tile; keep
   // them in smem instead when they fit and the A ring stays deep (it gets all the space).
-  if (resb_enabled() && nt == 1 && splits == 1 && !mcast) {
+  if (resb_enabled() && nt == 1 && splits == 1 && !mcast && !stem_whole) {
     const int s_stream = conv_umma_stages(pl.p, bn);
     pl.p.resb = 1;
     const int s_res = conv_umma_stages(pl.p, bn);
-    const int64_t rb = static_cast<int64_t>(num_kb) * (tap_shift ? 3 : 1) * bn * 128;
+    const int64_t rb = static_cast<int64_t>(pl.p.num_kb) * (pl.p.kbs > 1 ? pl.p.kbs : 1) *
+                       (tap_shift ? 3 : 1) * bn * 128;
     if (rb > 112 * 1024 || s_res < 4 || s_res < s_stream) pl.p.resb = 0;
   }
   if (mcast) {
@@ -471,6 +492,10 @@ struct eb_engine {
   std::vector<cudaEvent_t>* prof = nullptr;
   // stem convs reading an 8-channel image: padded-layout scratch (stem rows / planes modes)
   std::map<const eb_op_desc*, void*> stem_buf;
+  // u8 input: stems reading the preprocessed image get their layout straight from K1;
+  // the NHWC8 image itself is then written only if something else reads it
+  bool img8_needed = true;
+  bool layouts_fused = false;  // set per enqueue (u8 input)
 };
 
 namespace {
@@ -529,9 +554,12 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
         StemGeom g;
         if (it != e->stem_buf.end() &&
             stem_geom(B, src.h, src.w, op.kh, op.kw, op.sh, op.sw, op.ph, op.pw, &g)) {
-          EB_CUDA(k_stem_relayout(static_cast<const __nv_bfloat16*>(x), B, src.h, src.w, op.ph, op.pw,
-                                  g.mode, g.Hq, g.Wq, static_cast<__nv_bfloat16*>(it->second), ls));
-          ++*launches;
+          if (!(e->layouts_fused && op.src == EB_T_IMAGE_NHWC8)) {  // else K1 wrote it
+            EB_CUDA(k_stem_relayout(static_cast<const __nv_bfloat16*>(x), B, src.h, src.w, op.ph,
+                                    op.pw, g.mode, g.Hq, g.Wq,
+                                    static_cast<__nv_bfloat16*>(it->second), ls));
+            ++*launches;
+          }
           a.x = it->second;
           a.c8_stem = 2;
         }
@@ -605,11 +633,27 @@ eb_engine* e, int input_kind, int B, int* launches) {
   const int64_t plane = static_cast<int64_t>(e->H) * e->W;
   Tensor& img8 = e->tensors[EB_T_IMAGE_NHWC8];
   Tensor& imgf = e->tensors[EB_T_IMAGE_F32];
+  e->layouts_fused = false;
   if (input_kind == EB_IN_U8_HWC) {
     if (e->any_cnn) {
-      EB_CUDA(k_preprocess_u8hwc_to_nhwc(e->d_in_u8, static_cast<__nv_bfloat16*>(img8.dev), B,
-                                         e->C, plane, 8, e->d_lut, s));
-      ++*launches;
+      if (e->img8_needed) {
+        EB_CUDA(k_preprocess_u8hwc_to_nhwc(e->d_in_u8, static_cast<__nv_bfloat16*>(img8.dev), B,
+                                           e->C, plane, 8, e->d_lut, s));
+        ++*launches;
+      }
+      // stems on the preprocessed image: K1 writes their padded layouts directly
+      for (const auto& kv : e->stem_buf) {
+        const eb_op_desc& op = *kv.first;
+        if (op.src != EB_T_IMAGE_NHWC8) continue;
+        StemGeom g;
+        if (!stem_geom(B, e->H, e->W, op.kh, op.kw, op.sh, op.sw, op.ph, op.pw, &g))
+          EB_FAIL(EB_E_INVALID, "stem layout geometry");
+        EB_CUDA(k_preprocess_u8_to_layout(e->d_in_u8, B, e->C, e->H, e->W, e->d_lut, op.ph, op.pw,
+                                          g.mode, g.Hq, g.Wq, static_cast<__nv_bfloat16*>(kv.second),
+                                          s));
+        ++*launches;
+        e->layouts_fused = true;
+      }
     }
     if (e->any_lin) {
       EB_CUDA(k_preprocess_u8hwc_to_f32chw(e->d_in_u8, static_cast<float*>(imgf.dev), B, e->C,
@@ -984,6 +1028,9 @@ int eb_finalize(eb_engine* e) {
       e->stem_buf[&op] = buf;
     }
   }
+  e->img8_needed = false;
+  for (const auto& op : e->ops)
+    if (op.src == EB_T_IMAGE_NHWC8 && !e->stem_buf.count(&op)) e->img8_needed = true;
   bool used[kLanes] = {};
   for (const auto& op : e->ops) used[op.stream] = true;
   for (int l = 0; l < kLanes; ++l)
