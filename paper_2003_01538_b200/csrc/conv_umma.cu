@@ -106,7 +106,7 @@ __host__ __device__ inline SmemLayout make_layout(int resb, int num_kb, int a_mo
   const int ab = stem_run_bytes(a_mode) ? stem_a_bytes(a_mode, kbs) : 0;
   const int bb = S::kBBytes * (kbs > 0 ? kbs : 1);  // B bytes of one stage
   L.resb_bytes = resb ? num_kb * bb : 0;
-  L.stage_bytes = (ab ? ab : S::kABytes) + (resb ? 0 : bb);
+  L.stage_bytes = (ab ? ab : S::kABytes * (kbs > 0 ? kbs : 1)) + (resb ? 0 : bb);
   int st = (S::kBudget - S::kEpiBytes - L.resb_bytes) / L.stage_bytes;
   L.stages = st > S::kMaxStages ? S::kMaxStages : st;
   L.out_off = L.resb_bytes + L.stages * L.stage_bytes;
@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const SmemLayout L = make_layout<S>(p.resb, p.num_kb, p.a_mode, p.kbs);
   constexpr bool stem_direct = STEM;  // a_mode is kAModeStemRows / kAModeStemPlanes
-  const int kbs = stem_direct ? p.kbs : 1;  // 64-wide K blocks per stage
-  const int a_stage = stem_direct ? stem_a_bytes(p.a_mode, kbs) : S::kABytes;  // B follows A
+  const int kbs = p.kbs > 0 ? p.kbs : 1;  // 64-wide K blocks per stage (stems, taps-in-N)
+  const int a_stage = stem_direct ? stem_a_bytes(p.a_mode, kbs) : S::kABytes * kbs;  // B follows A
   const int b_stage = S::kBBytes * kbs;
   uint8_t* const ring_base = smem + L.resb_bytes;  // stage s at ring_base + s * stage_bytes
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -396,17 +396,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (TAPN) {
             // filter row r, channel chunk cc: lane quarter q's 32 rows are the padded-grid
             // pixels m0 + 30q ..; B = the row's 3 taps stacked along N
-            const int r = outer;
-            mbar_arrive_expect_tx(&full[stage], 4 * 32 * 128 + (p.resb ? 0 : S::kBBytes));
+            // (kbs K blocks per stage: block g = kb * kbs + sub)
+            mbar_arrive_expect_tx(&full[stage], kbs * (4 * 32 * 128 + (p.resb ? 0 : S::kBBytes)));
+            for (int sub = 0; sub < kbs; ++sub) {
+              const int g = kb * kbs + sub;
+              const int r = g / p.cchunks;
+              const int gc = g - r * p.cchunks;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              tma_load_im2col_4d(sa + q * 4096, &map_a, &full[stage], cc * kBlockK, qw[q], qh[q], qi[q],
-                                 0, static_cast<uint16_t>(r));
-            if (!p.resb) {
+              for (int q = 0; q < 4; ++q)
+                tma_load_im2col_4d(sa + sub * S::kABytes + q * 4096, &map_a, &full[stage], gc * kBlockK,
+                                   qw[q], qh[q], qi[q], 0, static_cast<uint16_t>(r));
+              if (!p.resb) {
 #pragma unroll
-              for (int s2 = 0; s2 < 3; ++s2)
-                tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, &full[stage],
-                            ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, n0);
+                for (int s2 = 0; s2 < 3; ++s2)
+                  tma_load_2d(sb + sub * S::kBBytes + s2 * S::kBTapBytes, &map_b, &full[stage],
+                              ((r * p.kw + s2) * p.cchunks + gc) * kBlockK, n0);
+              }
             }
             if (++stage == L.stages) {
               stage = 0;
@@ -588,6 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           } else {
+          for (int sub = 0; sub < kbs; ++sub) {  // (kbs > 1: taps-in-N only)
 #pragma unroll
           for (int s2 = 0; s2 < TS; ++s2) {
 #pragma unroll
@@ -596,14 +602,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               // applied on absolute smem address bits (base offset field stays 0), which
               // is also what the TMA used when it wrote the tile (verified on B200)
               if (!((kmask >> k) & 1u)) continue;  // (stems: all-zero weight steps)
-              const uint64_t adesc = a0 + s2 * 8 + a_koff[k];
-              const uint64_t bdesc = b0 + s2 * (S::kBTapBytes >> 4) + 2 * k;
-              const uint32_t accum = (kb > kb0 || s2 > 0 || k > 0) ? 1u : 0u;
+              const uint64_t adesc = a0 + sub * (S::kABytes >> 4) + s2 * 8 + a_koff[k];
+              const uint64_t bdesc = b0 + sub * (S::kBBytes >> 4) + s2 * (S::kBTapBytes >> 4) + 2 * k;
+              const uint32_t accum = (kb > kb0 || sub > 0 || s2 > 0 || k > 0) ? 1u : 0u;
               if constexpr (PAIR)
                 umma_bf16_pair(tmem_d, adesc, bdesc, idesc, accum);
               else
                 umma_bf16(tmem_d, adesc, bdesc, idesc, accum);
             }
+          }
           }
           }
           if constexpr (PAIR) {

@@ -356,6 +356,27 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.p.early_release = early ? 1 : 0;
   static const int dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
   pl.p.dbg = dbg;
+  if (tapn) {
+    // taps-in-N: several K blocks per stage (one 4-MMA K block at N = 3*Cout is only a few
+    // hundred cycles of tensor work, less than a stage's fixed sync cost); kbs divides
+    // the kh*cchunks K blocks
+    static const int kbs_env = getenv("EB_KBS") ? atoi(getenv("EB_KBS")) : 0;
+    // measured on B200 (B = 256): Cout 32, Cin 128 (6 K blocks): kbs 1/2/3 = 101/77/85 us at
+    // 56x56; Cout 64, Cin 64 (3 K blocks): kbs 1/3 = 1197/1028 us at 224x224, 71/64 at 56x56
+    int want = kbs_env > 0 ? kbs_env : (bn <= 32 ? 2 : 3);
+    while (want > 1 && num_kb % want != 0) --want;
+    if (want > 1) {
+      ConvParams q = pl.p;
+      q.kbs = want;
+      q.num_kb = num_kb / want;
+      q.kb_per_split = q.num_kb;
+      q.resb = 1;
+      if (conv_umma_stages(q, bn) >= 2) {
+        q.resb = 0;  // (decided below)
+        pl.p = q;
+      }
+    }
+  }
   bool stem_whole = false;
   if (stem_direct && stem_rows_per_stage_all()) {
     // stems: all kh filter rows of a tile in one stage (one wait / one commit per tile);
@@ -379,7 +400,8 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     const int s_res = conv_umma_stages(pl.p, bn);
     const int64_t rb = static_cast<int64_t>(pl.p.num_kb) * (pl.p.kbs > 1 ? pl.p.kbs : 1) *
                        (tap_shift ? 3 : 1) * bn * 128;
-    if (rb > 112 * 1024 || s_res < 4 || s_res < s_stream) pl.p.resb = 0;
+    const int min_stages = pl.p.kbs > 1 ? 2 : 4;  // (multi-block stages are long)
+    if (rb > 112 * 1024 || s_res < min_stages || s_res < s_stream) pl.p.resb = 0;
   }
   if (mcast) {
     if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn / 2, &err))
