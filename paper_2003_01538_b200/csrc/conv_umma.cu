@@ -194,6 +194,16 @@ __device__ __forceinline__ void trace_ev(long long* tr, int role, int& n, int ta
   }
 }
 
+// EB_DBG timing probes (trace build only): 2 = MMA does not wait for the stem gather,
+// 3 = no pre-activation transform.  Results are wrong under a probe; timing only.
+__device__ __forceinline__ bool dbg_probe(const ConvParams& p, int which) {
+#ifdef EB_ENABLE_TRACE
+  return p.dbg == which;
+#else
+  return false;
+#endif
+}
+
 __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
   // TMA SWIZZLE_128B (128 B rows): 16 B chunk ^= row % 8
   // TMA SWIZZLE_64B  (64 B rows):  16 B chunk ^= (row / 2) % 4
@@ -570,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(p.pre_scale ? &xfull[stage] : &full[stage], phase);
-        if (p.a_mode == kAModeGatherC8 && p.dbg != 2) mbar_wait(&xfull[stage], phase);
+        if (p.a_mode == kAModeGatherC8 && !dbg_probe(p, 2)) mbar_wait(&xfull[stage], phase);
         if (lane_id() == 0) trace_ev(p.trace, 1, tr_n, 11);
         tc_fence_after();
         if (elect_one()) {
@@ -645,6 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool alt = n_epi == 8;
     const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
     const int hw = p.Ho * p.Wp;
+    int tr_n = 0;
     float* bias_s = reinterpret_cast<float*>(smem + L.bias_off) + ew * BN;
     int cached_n = -1;
     const int j0 = alt ? half : 0;
@@ -669,7 +680,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool ok = lane < 30 && m < p.M && owp < p.Wo;
       const size_t orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + owp;
       const int n_tile0 = tw.tn * BN;
+      if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 20);
       mbar_wait(&tfull[acc], (j >> 1) & 1);
+      if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 21);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * kAccCols + ((quarter * 32) << 16);
 #pragma unroll
@@ -685,25 +698,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        float v[32];
+        // ((D0 + D1') + D2') + bias on fp32 pairs (FADD2), the shifted planes by shuffle
+        float2 v2[16];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float d1 = __shfl_down_sync(0xffffffffu, __uint_as_float(r1[i]), 1);
-          const float d2 = __shfl_down_sync(0xffffffffu, __uint_as_float(r2[i]), 2);
-          v[i] = (__uint_as_float(r0[i]) + d1) + d2;
+        for (int i = 0; i < 16; ++i) {
+          const float2 d1 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * i]), 1),
+                                        __shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * i + 1]), 1));
+          const float2 d2 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r2[2 * i]), 2),
+                                        __shfl_down_sync(0xffffffffu, __uint_as_float(r2[2 * i + 1]), 2));
+          v2[i] = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(r0[2 * i]), __uint_as_float(r0[2 * i + 1])),
+                                        d1),
+                             d2);
         }
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c + i);
-          v[i] += b4.x;
-          v[i + 1] += b4.y;
-          v[i + 2] += b4.z;
-          v[i + 3] += b4.w;
+        for (int i = 0; i < 8; ++i) {
+          const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c + 4 * i);
+          v2[2 * i] = __fadd2_rn(v2[2 * i], make_float2(b4.x, b4.y));
+          v2[2 * i + 1] = __fadd2_rn(v2[2 * i + 1], make_float2(b4.z, b4.w));
         }
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          pk[i] = p.relu ? pack_bf16x2_relu(v[2 * i], v[2 * i + 1]) : pack_bf16x2(v[2 * i], v[2 * i + 1]);
+          pk[i] = p.relu ? pack_bf16x2_relu(v2[i].x, v2[i].y) : pack_bf16x2(v2[i].x, v2[i].y);
         __nv_bfloat16* const col0 = reinterpret_cast<__nv_bfloat16*>(p.out) + p.out_off + n;
         __nv_bfloat16* o = col0 + orow * p.ldo;
         if (p.vec_ok && n + 32 <= p.N) {
@@ -723,6 +739,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
       }
+      if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 22);
     }
   } else if (warp < 2 + n_epi) {
     // ------------------------------------------------------------ epilogue
@@ -1049,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[stage], phase);
           uint8_t* tile = ring_base + stage * L.stage_bytes;
 #pragma unroll
-          for (int i = 0; i < (p.dbg == 3 ? 0 : 8); ++i) {  // (dbg 3: timing probe, no transform)
+          for (int i = 0; i < (dbg_probe(p, 3) ? 0 : 8); ++i) {
             const int r = r0 + i;  // r & 7 == i
             uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + ((j ^ i) * 16));
             uint4 x = *q;
