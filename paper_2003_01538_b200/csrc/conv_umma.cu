@@ -283,7 +283,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // arrivals that drain one accumulator: the epilogue warps that read it (8 when the
       // two epilogue groups split each tile's chunks), doubled in PAIR mode where the
       // leader waits for both CTAs' epilogues
-      const uint32_t drain = (n_epi == 8 && BN / S::kCW > 1) ? 8u : 4u;
+      const uint32_t drain =
+          (n_epi == 8 && (BN / S::kCW > 1 || (TAPN && BN == 64))) ? 8u : 4u;
       mbar_init(&tempty[a], PAIR ? 2 * drain : drain);
     }
     for (int a = 0; a < 16; ++a) mbar_init(&rfull[a], 1);
@@ -646,13 +647,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Lane l of quarter q owns padded-grid row m = tile*120 + 30q + l; its output is
     //   out[m] = D0[m] + D1[m+1] + D2[m+2]   (D_s = the tap-s column block)
     // and rows m+1, m+2 live in lanes l+1, l+2 of the same warp (quarters overlap by 2
-    // rows, lanes 30/31 only feed their neighbours).  Two epilogue groups take
-    // alternate tiles.  Direct 16-byte stores (rows are not contiguous in the output).
+    // rows, lanes 30/31 only feed their neighbours).  With 64 output channels the two
+    // epilogue groups split every tile's columns (32 each: the accumulator is released as
+    // soon as both have loaded their half); with 32 they take alternate tiles.  Row
+    // stores are staged per warp (rows are not contiguous in the output).
     const int ew = static_cast<int>(warp) - 2;
     const int half = ew >> 2;
     const uint32_t quarter = warp & 3;
     const int lane = static_cast<int>(lane_id());
-    const bool alt = n_epi == 8;
+    const bool split_cols = n_epi == 8 && BN == 64;
+    const bool alt = n_epi == 8 && !split_cols;
+    const int c_lo = split_cols ? 32 * half : 0;
+    const int c_hi = split_cols ? c_lo + 32 : BN;
     const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.f, 0.f);
     const int hw = p.Ho * p.Wp;
     int tr_n = 0;
@@ -686,14 +692,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * kAccCols + ((quarter * 32) << 16);
 #pragma unroll
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_lo; c < c_hi; c += 32) {
         const int n = n_tile0 + c;
         uint32_t r0[32], r1[32], r2[32];
         tmem_ld32(tb + c, r0);
         tmem_ld32(tb + BN + c, r1);
         tmem_ld32(tb + 2 * BN + c, r2);
         tmem_ld_wait();
-        if (c + 32 >= BN && p.early_release) {  // last TMEM read of the tile: hand it back now
+        if (c + 32 >= c_hi && p.early_release) {  // last TMEM read of the tile: hand it back now
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
