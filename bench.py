@@ -402,6 +402,14 @@ def main() -> None:
                 top = (m, float(t))
     pk, pk_src = peaks()
     achieved = conv_flops / (conv_ms / 1e3) / 1e12
+    # DRAM traffic of the top launch from the committed ncu capture of the same layer
+    traffic = None
+    tl = ROOT / "profiles" / "round1" / "top_launch_ncu.json"
+    if top is not None and tl.exists():
+        t = json.loads(tl.read_text())
+        if list(t["shape(ho,wo,cout,kh,kw,s,cin)"]) == list(top[0]["shape"]) and t["batch"] == B:
+            traffic = {"dram_bytes_per_launch": t["dram_bytes_read"] + t["dram_bytes_write"],
+                       "algorithmic_bytes_per_launch": t["algorithmic_bytes"], "source": t["source"]}
     peak = pk["bf16_tflops_sustained"]
     if args.profile_json and rank == 0:
         Path(args.profile_json).write_text(json.dumps(
@@ -438,7 +446,7 @@ def main() -> None:
             "gpu_launches": int(n_launch * args.steps),
             "roofline": {"bound": "tensor", "kernel": "conv_umma_kernel (all conv/FC launches)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{pk_src} bf16_tflops_sustained",
                          "flops_per_step": conv_flops, "kernel_ms_per_step_serialised": conv_ms,
                          "step_frac_of_peak": GFLOP_PER_IMG * 1e9 * B * world / (dev_ms / args.steps / 1e3) / 1e12 / peak / world,
