@@ -137,29 +137,31 @@ cudaError_t k_preprocess_u8hwc_to_f32chw(const uint8_t* x, float* y, int B, int 
 // K1 straight into a stem layout (StemGeom): u8 HWC -> LUT -> bf16 8-channel pixels of
 // the zero-padded rows / even-odd planes buffer.  Used instead of the NHWC8 image plus a
 // relayout when a stem reads the preprocessed image (one pass, no intermediate).
-__global__ void preprocess_u8_to_layout_kernel(const uint8_t* __restrict__ x, int B, int C, int H,
-                                               int W, const float* __restrict__ lut, int ph, int pw,
-                                               int planes, int Hq, int Wq, uint4* __restrict__ y,
-                                               int64_t total) {
+__global__ void __launch_bounds__(256)
+    preprocess_u8_to_layout_kernel(const uint8_t* __restrict__ x, int B, int C, int H, int W,
+                                   const float* __restrict__ lut, int ph, int pw, int planes, int Hq,
+                                   int Wq, uint4* __restrict__ y) {
+  // one CTA per padded row (plane q, image b, row hq); threads walk its Wq pixels
   __shared__ float s_lut[8 * 256];
   for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
   __syncthreads();
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(i % Wq);
-    const int64_t t = i / Wq;
-    const int hq = static_cast<int>(t % Hq);
-    const int bq = static_cast<int>(t / Hq);
-    const int q = bq / B;
-    const int b = bq - q * B;
-    const int ih = hq - ph;
+  const int row = blockIdx.x;  // (q * B + b) * Hq + hq
+  const int hq = row % Hq;
+  const int bq = row / Hq;
+  const int q = bq / B;
+  const int b = bq - q * B;
+  const int ih = hq - ph;
+  uint4* yr = y + static_cast<int64_t>(row) * Wq;
+  const bool hok = ih >= 0 && ih < H;
+  const uint8_t* xr = x + (static_cast<int64_t>(b) * H + (hok ? ih : 0)) * W * C;
+  for (int j = threadIdx.x; j < Wq; j += blockDim.x) {
     const int iw = planes ? 2 * j + q - pw : j - pw;
+    const bool ok = hok && iw >= 0 && iw < W;
     __align__(16) __nv_bfloat16 v[8];
-    const bool ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
-    const uint8_t* px = x + ((static_cast<int64_t>(b) * H + (ok ? ih : 0)) * W + (ok ? iw : 0)) * C;
+    const uint8_t* px = xr + (ok ? iw : 0) * C;
 #pragma unroll
     for (int c = 0; c < 8; ++c) v[c] = __float2bfloat16_rn((ok && c < C) ? s_lut[c * 256 + px[c]] : 0.f);
-    y[i] = *reinterpret_cast<const uint4*>(v);
+    yr[j] = *reinterpret_cast<const uint4*>(v);
   }
 }
 
@@ -167,43 +169,42 @@ cudaError_t k_preprocess_u8_to_layout(const uint8_t* x, int B, int C, int H, int
                                       int ph, int pw, int mode, int Hq, int Wq, __nv_bfloat16* y,
                                       cudaStream_t s) {
   const int planes = mode == kAModeStemPlanes ? 1 : 0;
-  const int64_t total = static_cast<int64_t>(planes ? 2 : 1) * B * Hq * Wq;
-  if (total == 0) return cudaSuccess;
-  preprocess_u8_to_layout_kernel<<<grid_for(total, 256), 256, 0, s>>>(
-      x, B, C, H, W, lut, ph, pw, planes, Hq, Wq, reinterpret_cast<uint4*>(y), total);
+  const int rows = (planes ? 2 : 1) * B * Hq;
+  if (rows == 0 || Wq == 0) return cudaSuccess;
+  preprocess_u8_to_layout_kernel<<<rows, 256, 0, s>>>(x, B, C, H, W, lut, ph, pw, planes, Hq, Wq,
+                                                      reinterpret_cast<uint4*>(y));
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ stem relayout
 // One thread per 16-byte output pixel (8 bf16 channels); borders are written as zeros
 // every time, so the destination needs no initialisation.
-__global__ void stem_relayout_kernel(const uint4* __restrict__ x, int B, int H, int W, int ph,
-                                     int pw, int planes, int Hq, int Wq, uint4* __restrict__ y,
-                                     int64_t total) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(i % Wq);
-    const int64_t t = i / Wq;
-    const int hq = static_cast<int>(t % Hq);
-    const int bq = static_cast<int>(t / Hq);  // q * B + b
-    const int q = bq / B;                     // plane (planes mode)
-    const int b = bq - q * B;
-    const int ih = hq - ph;
+__global__ void __launch_bounds__(256)
+    stem_relayout_kernel(const uint4* __restrict__ x, int B, int H, int W, int ph, int pw,
+                         int planes, int Hq, int Wq, uint4* __restrict__ y) {
+  // one CTA per padded row (plane q, image b, row hq); threads walk its Wq pixels
+  const int row = blockIdx.x;  // (q * B + b) * Hq + hq
+  const int hq = row % Hq;
+  const int bq = row / Hq;
+  const int q = bq / B;
+  const int b = bq - q * B;
+  const int ih = hq - ph;
+  const bool hok = ih >= 0 && ih < H;
+  const uint4* xr = x + (static_cast<int64_t>(b) * H + (hok ? ih : 0)) * W;
+  uint4* yr = y + static_cast<int64_t>(row) * Wq;
+  for (int j = threadIdx.x; j < Wq; j += blockDim.x) {
     const int iw = planes ? 2 * j + q - pw : j - pw;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = x[(static_cast<int64_t>(b) * H + ih) * W + iw];
-    y[i] = v;
+    yr[j] = (hok && iw >= 0 && iw < W) ? xr[iw] : make_uint4(0, 0, 0, 0);
   }
 }
 
 cudaError_t k_stem_relayout(const __nv_bfloat16* x, int B, int H, int W, int ph, int pw, int mode,
                             int Hq, int Wq, __nv_bfloat16* y, cudaStream_t s) {
   const int planes = mode == kAModeStemPlanes ? 1 : 0;
-  const int64_t total = static_cast<int64_t>(planes ? 2 : 1) * B * Hq * Wq;
-  if (total == 0) return cudaSuccess;
-  stem_relayout_kernel<<<grid_for(total, 256), 256, 0, s>>>(
-      reinterpret_cast<const uint4*>(x), B, H, W, ph, pw, planes, Hq, Wq, reinterpret_cast<uint4*>(y),
-      total);
+  const int rows = (planes ? 2 : 1) * B * Hq;
+  if (rows == 0 || Wq == 0) return cudaSuccess;
+  stem_relayout_kernel<<<rows, 256, 0, s>>>(reinterpret_cast<const uint4*>(x), B, H, W, ph, pw,
+                                            planes, Hq, Wq, reinterpret_cast<uint4*>(y));
   return cudaGetLastError();
 }
 
