@@ -91,3 +91,16 @@ def test_variable_batch_masking(tmp_path):
         _, _, part = E.predict_u8(ens, px[:b], want_logits=True)
         scale = np.abs(full["logits"]).max()
         np.testing.assert_allclose(part["logits"], full["logits"][:, :b], rtol=0, atol=0.01 * scale)
+
+
+def test_variable_batch_masking_vgg_resnet50(tmp_path):
+    """Same property through the VGG stem (padded-rows layout), taps-in-N with 64
+    channels (VGG conv1_2, ResNet-50 layer1) and the 2-SM MMA layers, at odd batches."""
+    docs = [cnn1_doc("v11", "vgg11", 4), cnn1_doc("r50", "resnet50", 3)]
+    ens = build(tmp_path, docs, max_batch=36, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    px = synth.images(33, 224, 224, 3, seed0=700)
+    _, _, full = E.predict_u8(ens, px, want_logits=True)
+    for b in (1, 5, 33):
+        _, _, part = E.predict_u8(ens, px[:b], want_logits=True)
+        scale = np.abs(full["logits"]).max()
+        np.testing.assert_allclose(part["logits"], full["logits"][:, :b], rtol=0, atol=0.01 * scale)
