@@ -315,7 +315,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int tr_n = 0;
-      if (p.resb) {
+      if (p.resb && PAIR) {
+        // 2-SM taps-in-N: each CTA keeps its half of the stacked [tap0; tap1; tap2] rows
+        // (rows 1.5*BN*crank .. +1.5*BN, as three BN/2-row boxes); both halves complete
+        // on the leader's barrier
+        const uint32_t rb = mapa_shared(smem_u32(bres), 0);
+        if (crank == 0) mbar_arrive_expect_tx(bres, 2u * L.resb_bytes);
+        for (int kb = 0; kb < p.num_kb * kbs; ++kb) {
+          uint8_t* sb = smem + kb * S::kBBytes;
+          const int r = kb / p.cchunks;
+          const int cc = kb - r * p.cchunks;
+          for (int box = 0; box < 3; ++box) {
+            const int R = (3 * static_cast<int>(crank) + box) * (BN / 2);  // stacked row
+            const int tap = R / BN;
+            tma_load_2d_pair(sb + box * S::kBTapBytes, &map_b, rb,
+                             ((r * p.kw + tap) * p.cchunks + cc) * kBlockK, R - tap * BN);
+          }
+        }
+      } else if (p.resb) {
         // resident B (single N tile): every K block's weights, once per CTA
         mbar_arrive_expect_tx(bres, L.resb_bytes);
         for (int kb = 0; kb < p.num_kb * kbs; ++kb) {  // (stems: kbs K blocks per stage)
@@ -408,6 +425,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             // filter row r, channel chunk cc: lane quarter q's 32 rows are the padded-grid
             // pixels m0 + 30q ..; B = the row's 3 taps stacked along N
             // (kbs K blocks per stage: block g = kb * kbs + sub)
+            if constexpr (PAIR) {
+              // 2-SM: each CTA stages its own tile's A; B is resident (halves per CTA);
+              // both CTAs' loads complete on the leader's barrier
+              const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+              if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2u * kbs * (4 * 32 * 128));
+              for (int sub = 0; sub < kbs; ++sub) {
+                const int g = kb * kbs + sub;
+                const int r = g / p.cchunks;
+                const int gc = g - r * p.cchunks;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  tma_load_im2col_4d_pair(sa + sub * S::kABytes + q * 4096, &map_a, fb, gc * kBlockK,
+                                          qw[q], qh[q], qi[q], 0, static_cast<uint16_t>(r));
+              }
+            } else {
             mbar_arrive_expect_tx(&full[stage], kbs * (4 * 32 * 128 + (p.resb ? 0 : S::kBBytes)));
             for (int sub = 0; sub < kbs; ++sub) {
               const int g = kb * kbs + sub;
@@ -423,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   tma_load_2d(sb + sub * S::kBBytes + s2 * S::kBTapBytes, &map_b, &full[stage],
                               ((r * p.kw + s2) * p.cchunks + gc) * kBlockK, n0);
               }
+            }
             }
             if (++stage == L.stages) {
               stage = 0;
@@ -678,7 +711,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         cached_n = tw.tn;
       }
       const int acc = j & 1;
-      const int m = tw.pm * kTileRows + static_cast<int>(quarter) * 30 + lane;
+      const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
+      const int m = tile_m * kTileRows + static_cast<int>(quarter) * 30 + lane;
       const int img = fdiv(m, p.fd_img);
       const int rem = m - img * hw;
       const int oh = fdiv(rem, p.fd_row);
@@ -702,7 +736,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c + 32 >= c_hi && p.early_release) {  // last TMEM read of the tile: hand it back now
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if (PAIR && crank != 0)  // the leader's MMAs write our TMEM: release it there
+              mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            else
+              mbar_arrive(&tempty[acc]);
+          }
         }
         // ((D0 + D1') + D2') + bias on fp32 pairs (FADD2), the shifted planes by shuffle
         float2 v2[16];
@@ -743,7 +782,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!p.early_release) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if (PAIR && crank != 0)
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+          else
+            mbar_arrive(&tempty[acc]);
+        }
       }
       if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 22);
     }
@@ -1147,7 +1191,10 @@ int conv_umma_stages(const ConvParams& p, int block_n) {
            : block_n == 64 ? stages_of<64, 1, false, false, true>(p)
            : block_n == 128 ? stages_of<128, 1, false, false, true>(p)
                             : stages_of<256, 1, false, false, true>(p);
-  if (p.a_mode == kAModeTapN) return block_n == 32 ? stages_of<32, 1, false, true>(p) : stages_of<64, 1, false, true>(p);
+  if (p.a_mode == kAModeTapN) {
+    if (p.pair) return block_n == 32 ? stages_of<32, 1, true, true>(p) : stages_of<64, 1, true, true>(p);
+    return block_n == 32 ? stages_of<32, 1, false, true>(p) : stages_of<64, 1, false, true>(p);
+  }
   if (p.pair) {
     if (ts) return block_n == 64 ? stages_of<64, 3, true>(p) : stages_of<128, 3, true>(p);
     return block_n == 64 ? stages_of<64, 1, true>(p) : block_n == 128 ? stages_of<128, 1, true>(p) : stages_of<256, 1, true>(p);
@@ -1183,7 +1230,15 @@ cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const
     }
   }
   if (p.a_mode == kAModeTapN) {
-    if (p.mcast || p.pair) return cudaErrorInvalidValue;
+    if (p.pair) {
+      if (!p.mcast || !p.resb) return cudaErrorInvalidValue;
+      switch (block_n) {
+        case 32: return launch_bn<32, 1, true, true>(ma, mb, mo, mr, p, grid, stream);
+        case 64: return launch_bn<64, 1, true, true>(ma, mb, mo, mr, p, grid, stream);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+    if (p.mcast) return cudaErrorInvalidValue;
     switch (block_n) {
       case 32: return launch_bn<32, 1, false, true>(ma, mb, mo, mr, p, grid, stream);
       case 64: return launch_bn<64, 1, false, true>(ma, mb, mo, mr, p, grid, stream);

@@ -129,6 +129,13 @@ int tapn_max_cout() {
   }();
   return v;
 }
+bool pair_tapn_enabled() {
+  // correct but slower (B200, B = 256): 224x224 64->64 1600 vs 1120 us, 56x56 107 vs 65 us,
+  // growth conv 76.4 vs 77.1 us -- the pair's lock-step per one-stage tile costs more than
+  // the halved B reads save.  Opt-in.
+  static const bool on = env_flag("EB_PAIR_TAPN", false);
+  return on;
+}
 bool resb_enabled() {
   static const bool on = env_flag("EB_RESB", true);
   return on;
@@ -338,10 +345,10 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   const bool plain_a = pl.p.a_mode == kAModeTiled || pl.p.a_mode == kAModeIm2col;
   // (short K loops stay unpaired: the pair's lock-step costs more than it saves when the
   // layer is memory-bound -- measured on B200, 1x1 256->64 at 56x56: 79 us single vs 107 us)
-  const bool pair = pair_enabled() && splits == 1 && mt >= 2 && !a.pre_scale && !tapn &&
+  bool pair = pair_enabled() && splits == 1 && mt >= 2 && !a.pre_scale && !tapn &&
                     (tap_shift ? ((bn == 64 || bn == 128) && num_kb >= pair_min_kb_ts())
                                : (plain_a && bn >= 64 && num_kb >= 8));
-  const bool mcast = pair || (mcast_enabled() && splits == 1 && bn >= 128 && mt >= 2 &&
+  bool mcast = pair || (mcast_enabled() && splits == 1 && bn >= 128 && mt >= 2 &&
                               num_kb >= 8 && !a.pre_scale && plain_a);
   pl.p.mcast = mcast ? 1 : 0;
   pl.p.pair = pair ? 1 : 0;
@@ -365,11 +372,24 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     // 56x56; Cout 64, Cin 64 (3 K blocks): kbs 1/3 = 1197/1028 us at 224x224, 71/64 at 56x56
     int want = kbs_env > 0 ? kbs_env : (bn <= 32 ? 2 : 3);
     while (want > 1 && num_kb % want != 0) --want;
-    if (want > 1) {
-      ConvParams q = pl.p;
-      q.kbs = want;
-      q.num_kb = num_kb / want;
-      q.kb_per_split = q.num_kb;
+    ConvParams q = pl.p;
+    q.kbs = want;
+    q.num_kb = num_kb / want;
+    q.kb_per_split = q.num_kb;
+    // 2-SM taps-in-N: the MMA re-reads the stacked 3-tap B for every K step; a CTA pair
+    // halves that per SM.  Requires resident B (each CTA keeps its half).
+    bool tp = pair_tapn_enabled() && splits == 1 && mt >= 2 && nt == 1 && resb_enabled();
+    if (tp) {
+      q.pair = 1;
+      q.mcast = 1;
+      q.resb = 1;
+      if (conv_umma_stages(q, bn) < 2) tp = false;
+    }
+    if (tp) {
+      pl.p = q;  // resident B decided here (the generic pass below skips cluster modes)
+      pair = mcast = true;
+    } else if (want > 1) {
+      q.pair = q.mcast = 0;
       q.resb = 1;
       if (conv_umma_stages(q, bn) >= 2) {
         q.resb = 0;  // (decided below)
