@@ -378,3 +378,65 @@ def test_resize_bilinear_matches_interpolate(hw, out):
     r = F.interpolate(x.float().cpu().permute(0, 3, 1, 2), size=out, mode="bilinear",
                       align_corners=False).permute(0, 2, 3, 1)
     assert (y.float().cpu() - r).abs().max().item() < 0.03
+
+
+GUARD_CASES = [
+    # name, B, H, W, cin, cout, kh, kw, s, p, stem   (exercise every store path at odd sizes)
+    ("tapn32", 3, 13, 11, 128, 32, 3, 3, 1, 1, False),
+    ("tapn64", 2, 17, 9, 64, 64, 3, 3, 1, 1, False),
+    ("tapshift96", 2, 15, 13, 64, 96, 3, 3, 1, 1, False),
+    ("pair256", 2, 14, 14, 512, 256, 3, 3, 1, 1, False),
+    ("im2col_s2", 3, 15, 15, 64, 128, 3, 3, 2, 1, False),
+    ("tiled", 3, 9, 7, 192, 64, 1, 1, 1, 0, False),
+    ("stem_rows", 2, 19, 23, 8, 64, 3, 3, 1, 1, True),
+    ("stem_planes", 2, 21, 25, 8, 128, 7, 7, 2, 3, True),
+]
+
+
+@pytest.mark.parametrize("case", GUARD_CASES, ids=[c[0] for c in GUARD_CASES])
+def test_conv_writes_stay_inside_output(case):
+    """Bounds check without a sanitizer: the output lives inside a larger buffer filled with
+    a sentinel; after the conv every element outside the [B, Ho, Wo, cout] slice (guard
+    rows before/after, and the channels past cout in a wider row) must be untouched, and
+    the slice must match the fp32 reference."""
+    lib = _lib.load()
+    _, B, H, W, cin, cout, kh, kw, st, pd, stem = case
+    g = torch.Generator().manual_seed(sum(map(ord, case[0])))
+    if stem:
+        x = torch.zeros(B, H, W, 8)
+        x[..., :3] = torch.randn(B, H, W, 3, generator=g)
+        cin_real = 3
+    else:
+        x = torch.randn(B, H, W, cin, generator=g)
+        cin_real = cin
+    x = x.to(torch.bfloat16).to(DEV)
+    w = torch.randn(cout, cin_real, kh, kw, generator=g) / np.sqrt(cin_real * kh * kw)
+    bias = torch.randn(cout, generator=g) * 0.1
+    Ho, Wo = (H + 2 * pd - kh) // st + 1, (W + 2 * pd - kw) // st + 1
+    wp = pack_conv_weight(w, conv_mode(kh, kw, st, st, pd, pd, cin_real, stem)).to(DEV)
+    ld = cout + 24                       # wider rows: channels [cout, ld) must stay untouched
+    guard = 4096                         # elements before and after the tensor
+    n = B * Ho * Wo * ld
+    SENT = -12352.0  # exactly representable in bf16
+    buf = torch.full((guard + n + guard,), SENT, device=DEV).to(torch.bfloat16)
+    y = buf[guard:guard + n].view(B, Ho, Wo, ld)
+    src = x
+    layout = 1 if stem else 0
+    if stem:
+        nbytes = ctypes.c_uint64(0)
+        _lib.check(lib.eb_k_stem_layout(B, H, W, kh, kw, st, st, pd, pd, ctypes.byref(nbytes)))
+        src = torch.zeros(nbytes.value // 2, device=DEV, dtype=torch.bfloat16)
+        _lib.check(lib.eb_k_stem_relayout(_p(x), B, H, W, kh, kw, st, st, pd, pd, _p(src), None))
+        layout = 2
+    ws = torch.zeros(4 << 20, device=DEV)
+    _lib.check(lib.eb_k_conv(
+        _p(src), B, H, W, x.shape[-1], x.shape[-1] if stem else cin, _p(wp), _p(bias.to(DEV)), None, 0,
+        _p(y), ld, 0, cout, kh, kw, st, st, pd, pd, 1, 0, layout, 0, 0, 1, _p(ws), None, None, None))
+    torch.cuda.synchronize()
+    b = buf.float().cpu()
+    assert (b[:guard] == SENT).all() and (b[guard + n:] == SENT).all(), "write before/after the tensor"
+    yy = y.float().cpu()
+    assert (yy[..., cout:] == SENT).all(), "write past cout in a row"
+    r = ref_conv(x, cin_real, w, bias, None, True, kh, kw, st, st, pd, pd)
+    err = (yy[..., :cout] - r).abs().max().item()
+    assert err <= 0.02 * r.abs().max().item() + 1e-2, err
