@@ -64,13 +64,17 @@ struct ConvSmem {
   static constexpr int kBBytes = (TAPN ? 3 : TS) * kBTapBytes;
   static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
   // one warp's 32-row chunk; tap-shift tiles store directly (no staging, no residual)
-  static constexpr int kStageOutBytes = (TS == 1 && !TAPN && !STEM) ? 32 * kCW * 2 : 0;
+  static constexpr int kStageOutBytes = (TS == 1 && !TAPN) ? 32 * kCW * 2 : 0;
   // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
   static constexpr int kPreMax = (BN == 128 && TS == 1 && !PAIR && !TAPN && !STEM) ? 2048 : 0;
   // ring: 16 chunk buffers (4 warps x 4 or 8 warps x 2); tap-shift / taps-in-N tiles
   // instead stage 32 rows x 32 columns per warp for coalesced row stores
   static constexpr int kRowStageBytes = 32 * 32 * 2;
-  static constexpr int kRingArea = (TS == 1 && !TAPN && !STEM) ? 16 * kStageOutBytes : 8 * kRowStageBytes;
+  // (stems: one chunk buffer per warp -- their whole-filter stages need the space)
+  static constexpr int kRingArea = STEM ? (8 * kStageOutBytes > 8 * kRowStageBytes ? 8 * kStageOutBytes
+                                                                                    : 8 * kRowStageBytes)
+                                   : (TS == 1 && !TAPN) ? 16 * kStageOutBytes
+                                                        : 8 * kRowStageBytes;
   // bias cache: 8 warps x BN floats
   static constexpr int kEpiBytes = kRingArea + 8 * BN * 4 + 2 * kPreMax * 4;
   // dynamic smem: everything (one CTA per SM); 1 KiB alignment slack + barrier block
@@ -814,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool alt_tiles = wide && NCH == 1;
     const int c_first = (wide && NCH > 1) ? half : 0;
     const int c_step = (wide && NCH > 1) ? 2 : 1;
-    const int nb = wide ? 2 : 4;  // ring buffers per warp (>= chunks this warp owns per tile)
+    const int nb = STEM ? 1 : wide ? 2 : 4;  // ring buffers per warp
     uint8_t* ring = smem + L.out_off + ew * nb * S::kStageOutBytes;
     float* bias_s = reinterpret_cast<float*>(smem + L.bias_off) + ew * BN;
     uint64_t* rbar = rfull + ew * nb;
@@ -961,7 +965,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < CW / 2; ++i)
           pk[i] = p.relu ? pack_bf16x2_relu(v2[i].x, v2[i].y) : pack_bf16x2(v2[i].x, v2[i].y);
-        if (TS > 1 || stem_direct) {
+        if (TS > 1 || (stem_direct && !p.stem_tma)) {
           // tap-shift / stem tiles are not contiguous in the output (padded grids): row
           // stores; a grouped stem launch sends columns >= n_split to the second tensor
           const bool second = p.n_split > 0 && n >= p.n_split;
@@ -971,6 +975,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ldd = second ? p.ldo2 : p.ldo;
           __nv_bfloat16* o = col0 + orow * ldd;
           if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 24);
+          if (dbg_probe(p, 1)) continue;  // (trace build: no stores)
           if (full_chunk && p.vec_ok && CW % 32 == 0) {
             uint8_t* stg = smem + L.out_off + ew * S::kRowStageBytes;
 #pragma unroll
@@ -991,7 +996,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!has_res) {
           // the store that last used this ring buffer (nb chunks ago) has read it
           if (lane == 0) {
-            if (wide)
+            if (nb == 1)
+              bulk_wait_read<0>();
+            else if (wide)
               bulk_wait_read<1>();
             else
               bulk_wait_read<3>();
@@ -1010,10 +1017,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           // a grouped launch (members sharing a stem) writes its second column range
           // to another tensor through the residual map slot
-          if (p.n_split > 0 && n >= p.n_split)
+          if (stem_direct) {
+            // the warp's 32 grid positions lie in one output row: a 3-D (C, Wo, B*Ho) store
+            // clipped at Wo drops the junk columns; slabs wholly past Wo / Ho are skipped
+            const int img = fdiv(m_slab, p.fd_img);
+            const int local = m_slab - img * static_cast<int>(p.fd_img.d);
+            const int oh = fdiv(local, p.fd_row);
+            const int ow0 = local - oh * static_cast<int>(p.fd_row.d);
+            if (m_slab < p.M && oh < p.Ho) {
+              if (ow0 < p.Wo) tma_store_3d(&map_out, buf, n, ow0, img * p.Ho + oh);
+              const int k = static_cast<int>(p.fd_row.d) - ow0;  // rows left in this grid row
+              if (k < 32 && oh + 1 < p.Ho) {
+                // the slab's tail starts the next output row: 8-row boxes (map_res slot)
+                for (int r8 = k; r8 < 32; r8 += 8)
+                  tma_store_3d(&map_res, buf + r8 * (CW * 2), n, r8 - k, img * p.Ho + oh + 1);
+              }
+            }
+          } else if (p.n_split > 0 && n >= p.n_split) {
             tma_store_2d(&map_res, buf, n - p.n_split, m_slab);
-          else
+          } else {
             tma_store_2d(&map_out, buf, n, m_slab);
+          }
           bulk_commit();
         }
         ++seq;

@@ -43,7 +43,10 @@ inline bool stem_geom(int B, int H, int W, int kh, int kw, int sh, int sw, int p
   if (Ho <= 0 || Wo <= 0) return false;
   if (sh == 1) {
     g->mode = kAModeStemRows;
-    g->Wq = (W + 2 * pw + 7) / 8 * 8;  // (taps >= kw meet zero weights; may read the next row)
+    // a multiple of 8: an epilogue warp's 32-row slab meets at most one grid-row boundary,
+    // at an 8-row-aligned offset (the second part is stored in 8-row boxes); taps >= kw
+    // meet zero weights
+    g->Wq = (W + 2 * pw + 7) / 8 * 8;
     g->Wg = g->Wq;
     g->Mi = (Ho * g->Wg + 127) / 128 * 128;
     // the last tile's loads reach Mi - 1 + 7 + (kh - 1) * Wq
@@ -101,6 +104,7 @@ struct ConvParams {
   int mcast;                 // 2-CTA cluster: M-tile pairs share the B tile via TMA multicast
   int pair;                  // with mcast: 2-SM MMA (cta_group::2), M = 256 per CTA pair
   int resb;                  // single N tile: all K blocks of B resident in smem (loaded once)
+  int stem_tma;              // stem modes: epilogue stores 32-pixel slabs with a clipped 3-D map
   int kbs;                   // stem modes: filter rows (64-wide K blocks) per pipeline stage
   int early_release;         // epilogue frees the accumulator right after its TMEM loads
   int dbg;                   // timing experiments only (EB_DBG); 0 in production
@@ -139,6 +143,10 @@ int conv_umma_stages(const ConvParams& p, int block_n);
 bool encode_tiled_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                           uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer,
                           std::string* err, int swizzle_bytes = 128);
+// 3-D tiled map (d0 innermost, contiguous); strides in elements
+bool encode_tiled_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                          uint64_t stride1_elems, uint64_t stride2_elems, uint32_t b0, uint32_t b1,
+                          uint32_t b2, std::string* err, int swizzle_bytes = 128);
 bool encode_im2col_bf16(CUtensorMap* map, const void* base, int n, int h, int w, int c, int ldc,
                         int kh, int kw, int sh, int sw, int ph, int pw, int chans_per_pixel,
                         int pixels, bool swizzle128, std::string* err, int upper_w_extra = 0);

@@ -148,6 +148,10 @@ bool stem_rows_per_stage_all() {
   static const bool on = env_flag("EB_STEM_KBS", true);
   return on;
 }
+bool stem_tma_store_enabled() {
+  static const bool on = env_flag("EB_STEM_TMA_STORE", true);
+  return on;
+}
 bool stem_rows_enabled() {
   // measured on B200 (B = 256): VGG stem 556 us (+ K1 writes the layout) vs 843 us gathered;
   // grouped 7x7/2 stem 361 us vs 470 us; C2 step 14.8-14.9 vs 15.1 ms
@@ -443,7 +447,18 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     pl.p.out2_off = a.y2_off;
     if (a.ldy2 % 8 != 0 || a.y2_off % 8 != 0) pl.p.vec_ok = 0;
   }
-  if (!a.out_f32 && splits == 1 && !tap_shift && !stem_direct) {
+  if (stem_direct && !a.out_f32 && a.n_split == 0 && pl.p.vec_ok && stem_tma_store_enabled()) {
+    // stems: 32-pixel slabs stored through a (C, Wo, B*Ho) map that clips the junk columns
+    const int cw = conv_umma_chunk(bn);
+    for (int box : {32, 8}) {  // (8-row boxes: a slab's part in the next output row)
+      if (!encode_tiled_3d_bf16(box == 32 ? &pl.mo : &pl.mr,
+                                static_cast<const __nv_bfloat16*>(a.y) + a.y_off, a.cout, Wo,
+                                static_cast<uint64_t>(a.B) * Ho, a.ldy,
+                                static_cast<uint64_t>(a.ldy) * Wo, cw, box, 1, &err, cw * 2))
+        EB_FAIL(EB_E_INVALID, err);
+    }
+    pl.p.stem_tma = 1;
+  } else if (!a.out_f32 && splits == 1 && !tap_shift && !stem_direct) {
     const int cw = conv_umma_chunk(bn);
     const int n1 = a.n_split > 0 ? a.n_split : a.cout;
     if (!encode_tiled_2d_bf16(&pl.mo, static_cast<const __nv_bfloat16*>(a.y) + a.y_off, n1, M64,
@@ -452,7 +467,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   } else {
     pl.mo = pl.mb;  // unused: fp32 outputs are stored directly
   }
-  pl.mr = pl.mb;
+  if (!pl.p.stem_tma) pl.mr = pl.mb;  // (stems with 3-D stores use the slot for 8-row boxes)
   if (a.n_split > 0) {
     const int cw = conv_umma_chunk(bn);
     if (!encode_tiled_2d_bf16(&pl.mr, static_cast<const __nv_bfloat16*>(a.y2) + a.y2_off,

@@ -270,6 +270,12 @@ EB_DEVICE void tma_store_2d(const void* map, const void* src, int c0, int c1) {
       "r"(smem_u32(src)), "r"(c0), "r"(c1)
       : "memory");
 }
+EB_DEVICE void tma_store_3d(const void* map, const void* src, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 EB_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until at most N committed bulk groups are still reading shared memory
 template <int N>
