@@ -39,7 +39,11 @@ bool pdl_enabled();
 
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // one 128-byte swizzle atom of bf16
-constexpr int kThreads = 320;  // 2 control warps + 4 epilogue warps + 4 A-transform warps
+// 2 control warps + 8 epilogue warps (or 4 epilogue + 4 stem-gather / 6 pre-activation
+// warps).  Twelve warps cost no registers over ten: three warps per SM sub-partition
+// either way caps a thread at 168 registers.
+constexpr int kThreads = 384;
+constexpr int kXformThreads = 192;  // pre-activation transform: warps 6..11
 constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels x 8 bf16
 
 // TS = filter taps consumed per pipeline stage: 1 (one TMA im2col load per tap)
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 16; ++a) mbar_init(&rfull[a], 1);
     // A-gather mode: 128 per-thread cp.async arrivals; A-transform mode: one arrive per warp
-    const uint32_t xcount = p.a_mode == kAModeGatherC8 ? 128u : 4u;
+    const uint32_t xcount = p.a_mode == kAModeGatherC8 ? 128u : kXformThreads / 32;
     for (int s = 0; s < L.stages; ++s) mbar_init(&xfull[s], xcount);
     fence_mbar_init();
   }
@@ -1046,7 +1050,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 22);
     }
     if (lane == 0) bulk_wait<0>();
-  } else if (p.a_mode == kAModeGatherC8) {
+  } else if (p.a_mode == kAModeGatherC8 && warp < 10) {
     // ------------------------------------------------------------ A gather (stem)
     // Thread r builds A row r: for filter row kb, the 8 consecutive input pixels
     // starting at the receptive field's left edge are 8 x 16 B = one 128-byte
@@ -1106,22 +1110,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ A transform
     // relu(a * scale[k] + shift[k]) in place on the swizzled A tile, then a proxy
     // fence so the tensor core sees the result.  Thread t owns logical 16-byte chunk
-    // j = t % 8 (8 channels) of rows 8*(t/8) .. +7: its scale/shift are read once
+    // j = t % 8 (8 channels) of rows t/8, t/8 + 24, ...: its scale/shift are read once
     // per stage (from an smem copy of the whole vector), and each warp's accesses
     // cover whole 128-byte rows (conflict-free).
     if constexpr (S::kPreMax > 0) {
-      const int t = static_cast<int>(threadIdx.x) - 192;  // 0..127
+      const int t = static_cast<int>(threadIdx.x) - 192;  // 0 .. kXformThreads-1
       const int j = t & 7;
-      const int r0 = (t >> 3) * 8;
+      constexpr int kRowStep = kXformThreads / 8;         // 24 rows apart
       // scale/shift rounded to bf16 once (the math is bf16x2 FMA anyway)
       __nv_bfloat16* sc_s = reinterpret_cast<__nv_bfloat16*>(smem + L.pre_off);
       __nv_bfloat16* sh_s = sc_s + S::kPreMax;
       const int kpad = p.num_kb * kBlockK;
-      for (int i = t; i < kpad; i += 128) {
+      for (int i = t; i < kpad; i += kXformThreads) {
         sc_s[i] = __float2bfloat16_rn(__ldg(p.pre_scale + i));
         sh_s[i] = __float2bfloat16_rn(__ldg(p.pre_shift + i));
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the four transform warps only
+      asm volatile("bar.sync 1, %0;" ::"n"(kXformThreads) : "memory");  // transform warps only
       int stage = 0;
       uint32_t phase = 0;
       TileWalk tw;
@@ -1140,9 +1144,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[stage], phase);
           uint8_t* tile = ring_base + stage * L.stage_bytes;
 #pragma unroll
-          for (int i = 0; i < (dbg_probe(p, 3) ? 0 : 8); ++i) {
-            const int r = r0 + i;  // r & 7 == i
-            uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + ((j ^ i) * 16));
+          for (int i = 0; i < (dbg_probe(p, 3) ? 0 : (kBlockM + kRowStep - 1) / kRowStep); ++i) {
+            const int r = (t >> 3) + i * kRowStep;
+            if (r >= kBlockM) break;
+            uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + ((j ^ (r & 7)) * 16));
             uint4 x = *q;
             __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
 #pragma unroll
