@@ -687,6 +687,7 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
 int enqueue_layers(
 eb_engine* e, int input_kind, int B, int* launches) {
   cudaStream_t s = e->stream;
+  set_pdl_batch(B);
   const int64_t plane = static_cast<int64_t>(e->H) * e->W;
   Tensor& img8 = e->tensors[EB_T_IMAGE_NHWC8];
   Tensor& imgf = e->tensors[EB_T_IMAGE_F32];
@@ -1314,6 +1315,7 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
   a.flatten = 0;
   a.split_k = split_k;
   a.block_n = block_n;
+  set_pdl_batch(batch);  // (same PDL policy as the engine)
   ConvPlan pl;
   int rc = plan_conv(a, &pl);
   if (rc != EB_OK) return rc;
