@@ -764,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              d2);
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < (dbg_probe(p, 4) ? 0 : 8); ++i) {
           const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c + 4 * i);
           v2[2 * i] = __fadd2_rn(v2[2 * i], make_float2(b4.x, b4.y));
           v2[2 * i + 1] = __fadd2_rn(v2[2 * i + 1], make_float2(b4.z, b4.w));
@@ -941,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 v2[CW / 2];
 #pragma unroll
         for (int i = 0; i < CW / 2; ++i) v2[i] = make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-        if (p.bias) {
+        if (p.bias && !dbg_probe(p, 4)) {
 #pragma unroll
           for (int i = 0; i < CW; i += 4) {
             const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c + i);
