@@ -869,7 +869,15 @@ int eb_engine_create(int device, int max_batch, int in_c, int in_h, int in_w, eb
     delete e;
     EB_FAIL(EB_E_CUDA, "stream create failed");
   }
-  for (int l = 1; l < kLanes; ++l) cudaStreamCreateWithFlags(&e->lanes[l], cudaStreamNonBlocking);
+  {
+    // EB_LANE_PRIO=<lane>: that lane's stream gets the highest priority (experiment)
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char* pr = getenv("EB_LANE_PRIO");
+    const int prio_lane = (pr && *pr) ? atoi(pr) : -1;
+    for (int l = 1; l < kLanes; ++l)
+      cudaStreamCreateWithPriority(&e->lanes[l], cudaStreamNonBlocking, l == prio_lane ? hi : lo);
+  }
   e->lanes[0] = e->stream;
   cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming);
   for (int l = 0; l < kLanes; ++l) cudaEventCreateWithFlags(&e->ev_join[l], cudaEventDisableTiming);
