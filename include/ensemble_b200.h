@@ -138,6 +138,13 @@ int eb_finalize(eb_engine* e);
  * layout).  Optional outputs (NULL to skip): host_logits fp32 [N][batch][Kmax]
  * (zero padded), top-k indices/probabilities [N][batch][topk], combined policy
  * output [batch].  Host<->device copies are inside this call. */
+/* A pipelined sequence of forwards (bulk serving; bench.py's end-to-end figure): batch
+ * i (host_inputs[i], `batch` samples, one encoding) is copied host->device on a
+ * separate copy stream while batch i-1 computes; its labels ([N][batch] int32) land
+ * in host_labels[i].  Every batch's transfers are inside the call, which returns when
+ * all batches are done.  Same validation and errors as eb_forward. */
+int eb_forward_batches(eb_engine* e, const void* const* host_inputs, int n_batches, int input_kind,
+                       int batch, int32_t* const* host_labels);
 int eb_forward(eb_engine* e, const void* host_input, int input_kind, int batch,
                int32_t* host_labels, float* host_logits, int topk, int32_t* host_topk_idx,
                float* host_topk_prob, int policy, int policy_k, int32_t* host_combined);

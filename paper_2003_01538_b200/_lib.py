@@ -83,6 +83,8 @@ _SIGS = {
     "eb_forward": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int,
                            c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "eb_forward_device": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int]),
+    "eb_forward_batches": (c_int, [c_void_p, POINTER(c_void_p), c_int, c_int, c_int,
+                                   POINTER(c_void_p)]),
     "eb_input_buffer": (c_int, [c_void_p, c_int, POINTER(c_void_p)]),
     "eb_output_labels": (c_int, [c_void_p, POINTER(c_void_p)]),
     "eb_tensor_ptr": (c_int, [c_void_p, c_int, POINTER(c_void_p), POINTER(c_int), POINTER(c_int),

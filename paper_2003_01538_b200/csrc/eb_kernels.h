@@ -19,6 +19,7 @@ cudaError_t k_preprocess_u8hwc_to_f32chw(const uint8_t* x, float* y, int B, int 
 
 // 8-channel NHWC image -> the zero-padded stem layout described by StemGeom (eb_internal.h):
 // mode kAModeStemRows (stride 1) or kAModeStemPlanes (stride 2, even/odd column planes).
+cudaError_t k_copy(const void* src, void* dst, size_t bytes, cudaStream_t s);
 cudaError_t k_preprocess_u8_to_layout(const uint8_t* x, int B, int C, int H, int W, const float* lut,
                                       int ph, int pw, int mode, int Hq, int Wq, __nv_bfloat16* y,
                                       cudaStream_t s);

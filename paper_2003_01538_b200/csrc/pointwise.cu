@@ -176,6 +176,25 @@ cudaError_t k_preprocess_u8_to_layout(const uint8_t* x, int B, int C, int H, int
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ device copy
+// SM copy for the pipelined forward's staging -> input move (a copy-engine D2D of a
+// batch of images runs far below HBM bandwidth).
+__global__ void copy16_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t k_copy(const void* src, void* dst, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | bytes) & 15)
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s);
+  const int64_t n16 = static_cast<int64_t>(bytes / 16);
+  copy16_kernel<<<grid_for(n16, 256), 256, 0, s>>>(static_cast<const uint4*>(src),
+                                                   static_cast<uint4*>(dst), n16);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ stem relayout
 // One thread per 16-byte output pixel (8 bf16 channels); borders are written as zeros
 // every time, so the destination needs no initialisation.

@@ -529,6 +529,12 @@ struct eb_engine {
   int nms = 1;
   uint8_t* d_in_u8 = nullptr;
   float* d_in_f32 = nullptr;
+  // eb_forward_batches: a staging buffer filled on a copy stream while the previous
+  // batch computes
+  void* d_stage = nullptr;
+  size_t d_stage_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_staged = nullptr, ev_stage_free = nullptr;
   float* ws[kLanes] = {};
   double* lin_part = nullptr;
   int lin_nsplit = 1;
@@ -900,6 +906,10 @@ int eb_engine_destroy(eb_engine* e) {
   cudaFree(e->d_lut);
   cudaFree(e->d_in_u8);
   cudaFree(e->d_in_f32);
+  cudaFree(e->d_stage);
+  if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
+  if (e->ev_staged) cudaEventDestroy(e->ev_staged);
+  if (e->ev_stage_free) cudaEventDestroy(e->ev_stage_free);
   for (int l = 0; l < kLanes; ++l) cudaFree(e->ws[l]);
   cudaFree(e->lin_part);
   cudaFree(e->d_labels);
@@ -1201,6 +1211,65 @@ int eb_forward(eb_engine* e, const void* host_input, int input_kind, int batch,
                                 static_cast<const float*>(t.dev) + m.koff, t.c * sizeof(float),
                                 m.k * sizeof(float), batch, cudaMemcpyDeviceToHost, e->stream));
     }
+  }
+  EB_CUDA(cudaStreamSynchronize(e->stream));
+  return EB_OK;
+}
+
+int eb_forward_batches(eb_engine* e, const void* const* host_inputs, int n_batches, int input_kind,
+                       int batch, int32_t* const* host_labels) {
+  int rc = check_batch(e, batch);
+  if (rc != EB_OK) return rc;
+  if (n_batches < 0 || (n_batches > 0 && (!host_inputs || !host_labels)))
+    EB_FAIL(EB_E_INVALID, "null inputs/labels");
+  if (input_kind != EB_IN_U8_HWC && input_kind != EB_IN_F32_CHW)
+    EB_FAIL(EB_E_INVALID, "unknown input encoding");
+  for (int i = 0; i < n_batches; ++i)
+    if (!host_inputs[i] || !host_labels[i]) EB_FAIL(EB_E_INVALID, "null input/labels entry");
+  std::lock_guard<std::mutex> lock(e->mu);
+  cudaSetDevice(e->device);
+  const size_t bytes = static_cast<size_t>(batch) * e->C * e->H * e->W *
+                       (input_kind == EB_IN_U8_HWC ? 1 : sizeof(float));
+  void* d_in = input_kind == EB_IN_U8_HWC ? static_cast<void*>(e->d_in_u8) : static_cast<void*>(e->d_in_f32);
+  if (e->d_stage_bytes < bytes) {
+    cudaFree(e->d_stage);
+    e->d_stage = nullptr;
+    e->d_stage_bytes = 0;
+    const size_t cap = static_cast<size_t>(e->max_batch) * e->C * e->H * e->W * sizeof(float);
+    if (cudaMalloc(&e->d_stage, cap) != cudaSuccess) {
+      cudaGetLastError();
+      EB_FAIL(EB_E_NOMEM, "staging buffer allocation failed");
+    }
+    e->d_stage_bytes = cap;
+  }
+  if (!e->copy_stream) {
+    EB_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+
+    EB_CUDA(cudaEventCreateWithFlags(&e->ev_staged, cudaEventDisableTiming));
+    EB_CUDA(cudaEventCreateWithFlags(&e->ev_stage_free, cudaEventDisableTiming));
+  }
+  const int n = static_cast<int>(e->members.size());
+  // copy stream: H2D of batch i into the staging buffer (after batch i-1 left it);
+  // engine stream: staging -> input buffer, forward, D2H of labels.  So batch i+1's
+  // transfer overlaps batch i's forward.
+  if (n_batches > 0) {
+    EB_CUDA(cudaMemcpyAsync(e->d_stage, host_inputs[0], bytes, cudaMemcpyHostToDevice, e->copy_stream));
+    EB_CUDA(cudaEventRecord(e->ev_staged, e->copy_stream));
+  }
+  for (int i = 0; i < n_batches; ++i) {
+    EB_CUDA(cudaStreamWaitEvent(e->stream, e->ev_staged, 0));
+    EB_CUDA(k_copy(e->d_stage, d_in, bytes, e->stream));
+    EB_CUDA(cudaEventRecord(e->ev_stage_free, e->stream));
+    if (i + 1 < n_batches) {
+      EB_CUDA(cudaStreamWaitEvent(e->copy_stream, e->ev_stage_free, 0));
+      EB_CUDA(cudaMemcpyAsync(e->d_stage, host_inputs[i + 1], bytes, cudaMemcpyHostToDevice,
+                              e->copy_stream));
+      EB_CUDA(cudaEventRecord(e->ev_staged, e->copy_stream));
+    }
+    rc = eb_forward_device(e, input_kind, batch, 0, EB_POLICY_NONE, 0);
+    if (rc != EB_OK) return rc;
+    EB_CUDA(cudaMemcpyAsync(host_labels[i], e->d_labels, static_cast<size_t>(n) * batch * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, e->stream));
   }
   EB_CUDA(cudaStreamSynchronize(e->stream));
   return EB_OK;

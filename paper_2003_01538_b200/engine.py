@@ -155,6 +155,30 @@ class Engine:
             out["combined"] = comb[:b]
         return out
 
+    def forward_batches(self, xs, input_kind: int) -> list:
+        """One native eb_forward_batches call: a pipelined sequence of equal-size host
+        batches (each batch's H2D overlaps the previous batch's forward).  Returns the
+        labels ([N][B] int32) of every batch."""
+        import ctypes
+
+        if not xs:
+            return []
+        b = int(xs[0].shape[0])
+        n = len(self.members)
+        arrs = [np.ascontiguousarray(x) for x in xs]
+        if any(int(a.shape[0]) != b for a in arrs):
+            raise ValueError("eb_forward_batches needs equal batch sizes")
+        # pinned label buffers: the device->host copies stay asynchronous, so the host
+        # enqueues every batch without waiting on the previous one
+        need = len(arrs) * n * b
+        if getattr(self, "_pinned_labels", None) is None or self._pinned_labels.numel() < need:
+            self._pinned_labels = torch.empty(need, dtype=torch.int32, pin_memory=True)  # reused
+        pinned = self._pinned_labels[:need].view(len(arrs), n, b)
+        ins = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        outs = (ctypes.c_void_p * len(arrs))(*[pinned[i].data_ptr() for i in range(len(arrs))])
+        check(self.lib.eb_forward_batches(self._h, ins, len(arrs), input_kind, b, outs))
+        return [pinned[i].numpy().copy() for i in range(len(arrs))]
+
     def forward_device(self, batch: int, input_kind: int, topk: int = 0, policy: int = 0,
                        policy_k: int = 0):
         check(self.lib.eb_forward_device(self._h, input_kind, batch, topk, policy, policy_k))

@@ -104,3 +104,22 @@ def test_variable_batch_masking_vgg_resnet50(tmp_path):
         _, _, part = E.predict_u8(ens, px[:b], want_logits=True)
         scale = np.abs(full["logits"]).max()
         np.testing.assert_allclose(part["logits"], full["logits"][:, :b], rtol=0, atol=0.01 * scale)
+
+
+def test_pipelined_batches_equal_single_calls(tmp_path):
+    """eb_forward_batches (copy of batch i+1 overlapping the forward of batch i) returns
+    exactly the labels of one eb_forward call per batch, for u8 and f32 inputs."""
+    from paper_2003_01538_b200 import _lib
+    from paper_2003_01538_b200.ensemble import engine_for
+
+    docs = [cnn1_doc("r18", "resnet18", 1), cnn1_doc("d121", "densenet121", 2)]
+    ens = build(tmp_path, docs, max_batch=8, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    eng = engine_for(ens)
+    batches = [synth.images(6, 224, 224, 3, seed0=900 + 10 * i) for i in range(4)]
+    got = eng.forward_batches(batches, _lib.EB_IN_U8_HWC)
+    for x, lab in zip(batches, got):
+        assert np.array_equal(lab, eng.forward(x, _lib.EB_IN_U8_HWC)["labels"])
+    f32 = [(x.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0)).reshape(6, -1) for x in batches]
+    got32 = eng.forward_batches(f32, _lib.EB_IN_F32_CHW)
+    for x, lab in zip(f32, got32):
+        assert np.array_equal(lab, eng.forward(x, _lib.EB_IN_F32_CHW)["labels"])
