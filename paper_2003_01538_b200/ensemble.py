@@ -17,6 +17,8 @@ eg/ensemble.py:133; SPEC.md:178).
 
 from __future__ import annotations
 
+import os
+
 import threading
 import weakref
 from dataclasses import dataclass, field
@@ -302,7 +304,9 @@ def build_engine(models, shape, spec, max_batch: int, device: int = 0):
         k = len(m.labels)
         if _kind(m) == "cnn1":
             img = zoo.resized_image(eng, tuple(m.input_shape.dims[1:]), images)
-            zoo.lower(eng, m.arch, torch_models[m.id], logits32.slice(koffs[m.id], k), lane % 4,
+            # one concurrency lane per member (EB_ONE_LANE=1: all members on the main stream)
+            mlane = 0 if os.environ.get("EB_ONE_LANE") == "1" else lane % 4
+            zoo.lower(eng, m.arch, torch_models[m.id], logits32.slice(koffs[m.id], k), mlane,
                       image=img, stem_out=stem_out.get(m.id))
             lane += 1
             eng.member(_lib.EB_MEMBER_CNN, logits32, koffs[m.id], k)
