@@ -579,6 +579,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * kBlockM : kBlockM, TAPN ? 3 * BN : BN);
+    constexpr uint32_t idesc_2bn = umma_idesc_bf16(kBlockM, 2 * BN);
+    constexpr uint32_t idesc_bn = umma_idesc_bf16(kBlockM, BN);
     int stage = 0;
     uint32_t phase = 0;
     int j = 0;  // local tile counter
@@ -657,10 +659,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t adesc = a0 + sub * (S::kABytes >> 4) + s2 * 8 + a_koff[k];
               const uint64_t bdesc = b0 + sub * (S::kBBytes >> 4) + s2 * (S::kBTapBytes >> 4) + 2 * k;
               const uint32_t accum = (kb > kb0 || sub > 0 || s2 > 0 || k > 0) ? 1u : 0u;
-              if constexpr (PAIR)
+              if constexpr (PAIR) {
                 umma_bf16_pair(tmem_d, adesc, bdesc, idesc, accum);
-              else
+              } else if constexpr (TAPN) {
+                if (p.tapn2) {
+                  // planes 0|1 = A x [tap0; tap1]; plane 0 += (A two rows on) x tap2: the
+                  // epilogue then adds one shifted plane instead of two
+                  umma_bf16(tmem_d, adesc, bdesc, idesc_2bn, accum);
+                  umma_bf16(tmem_d, adesc + 16, bdesc + (2 * BN * 128 >> 4), idesc_bn, 1u);
+                } else {
+                  umma_bf16(tmem_d, adesc, bdesc, idesc, accum);
+                }
+              } else {
                 umma_bf16(tmem_d, adesc, bdesc, idesc, accum);
+              }
             }
           }
           }
@@ -687,6 +699,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue, taps-in-N
     // Lane l of quarter q owns padded-grid row m = tile*120 + 30q + l; its output is
     //   out[m] = D0[m] + D1[m+1] + D2[m+2]   (D_s = the tap-s column block)
+    // (tapn2: the MMA warp already accumulated D2[m+2] into plane 0 through a 2-row
+    // shifted A descriptor, so only plane 1 is shuffled)
     // and rows m+1, m+2 live in lanes l+1, l+2 of the same warp (quarters overlap by 2
     // rows, lanes 30/31 only feed their neighbours).  With 64 output channels the two
     // epilogue groups split every tile's columns (32 each: the accumulator is released as
@@ -737,9 +751,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = c_lo; c < c_hi; c += 32) {
         const int n = n_tile0 + c;
         uint32_t r0[32], r1[32], r2[32];
+        const bool two = !PAIR && p.tapn2;
         tmem_ld32(tb + c, r0);
         tmem_ld32(tb + BN + c, r1);
-        tmem_ld32(tb + 2 * BN + c, r2);
+        if (!two) tmem_ld32(tb + 2 * BN + c, r2);
         tmem_ld_wait();
         if (c + 32 >= c_hi && p.early_release) {  // last TMEM read of the tile: hand it back now
           tc_fence_before();
@@ -753,6 +768,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // ((D0 + D1') + D2') + bias on fp32 pairs (FADD2), the shifted planes by shuffle
         float2 v2[16];
+        if (two) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 d1 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * i]), 1),
+                                          __shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * i + 1]), 1));
+            v2[i] = __fadd2_rn(make_float2(__uint_as_float(r0[2 * i]), __uint_as_float(r0[2 * i + 1])), d1);
+          }
+        } else
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float2 d1 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * i]), 1),

@@ -107,6 +107,7 @@ struct ConvParams {
   int stem_tma;              // stem modes: epilogue stores 32-pixel slabs with a clipped 3-D map
   int kbs;                   // stem modes: filter rows (64-wide K blocks) per pipeline stage
   int early_release;         // epilogue frees the accumulator right after its TMEM loads
+  int tapn2;                 // taps-in-N (unpaired): tap 2 folded into plane 0 by a 2-row A shift
   int dbg;                   // timing experiments only (EB_DBG); 0 in production
   long long* trace;          // timing experiments only (EB_TRACE): per-role event clocks of CTA 0
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels

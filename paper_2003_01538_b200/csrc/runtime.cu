@@ -365,6 +365,12 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   }
   static const bool early = env_flag("EB_EARLY_REL", true);
   pl.p.early_release = early ? 1 : 0;
+  // tap 2 folded by a shifted A (2 MMAs per K step, one plane less to combine): pays
+  // where the epilogue bounds the layer (one 64-channel K block per filter row); with
+  // more K blocks the layer is MMA-issue bound and the extra MMAs cost more.
+  // EB_TAPN2: 0 off, 1 auto, 2 always
+  static const int tapn2 = getenv("EB_TAPN2") ? atoi(getenv("EB_TAPN2")) : 1;
+  pl.p.tapn2 = (tapn && !pair && (tapn2 == 2 || (tapn2 == 1 && num_kb <= a.kh))) ? 1 : 0;
   static const int dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
   pl.p.dbg = dbg;
   if (tapn) {
