@@ -187,6 +187,14 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
               void* stream);
 /* (eb_k_conv c8_stem: 0 = regular input, 1 = 8-channel NHWC image (gathered stem),
  *  2 = the image already in its eb_k_stem_relayout layout; h, w stay the image's.) */
+/* eb_k_conv_maxpool2: a stride-1 conv followed by a 2x2 / stride-2 max-pool, fused
+ * (eb_k_conv then eb_k_pool with kernel 2, stride 2, EB_POOL_MAX; bit-identical).  dev_y
+ * is the pooled NHWC tensor (Ho/2 x Wo/2, row stride ldy, channel offset y_off).  Only the
+ * taps-in-N geometry (3x3, pad 1, Cout <= 64 and a multiple of 32, even Ho and Wo, ldy and
+ * y_off multiples of 8); EB_E_INVALID otherwise. */
+int eb_k_conv_maxpool2(const void* dev_x, int batch, int h, int w, int ldx, int cin,
+                       const void* dev_w, const float* dev_bias, void* dev_y, int ldy, int y_off,
+                       int cout, int kh, int kw, int ph, int pw, int relu, void* stream);
 int eb_k_resize(const void* dev_x, int ldx, void* dev_y, int ldy, int batch, int h, int w, int c,
                 int ho, int wo, void* stream);
 /* Stem layouts: eb_k_stem_layout reports the bytes of the zero-padded layout a stem conv

@@ -202,6 +202,21 @@ __device__ __forceinline__ void trace_ev(long long* tr, int role, int& n, int ta
   }
 }
 
+// EB_TRACE CTA span probe: every CTA (< 1024) records global-timer stamps at entry (0),
+// after its prologue (1) and at exit (2)
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_cta(long long* tr, int which) {
+#ifndef EB_ENABLE_TRACE
+  return;
+#endif
+  if (tr && threadIdx.x == 0 && blockIdx.x < 1024)
+    tr[3 * 1024 * 2 + blockIdx.x * 4 + which] = static_cast<long long>(global_ns());
+}
+
 // EB_DBG timing probes (trace build only): 2 = MMA does not wait for the stem gather,
 // 3 = no pre-activation transform.  Results are wrong under a probe; timing only.
 __device__ __forceinline__ bool dbg_probe(const ConvParams& p, int which) {
@@ -245,6 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bres = xfull + L.stages;     // resident B landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
+  trace_cta(p.trace, 0);
   const uint32_t warp = warp_id();
   constexpr int kTileRows = TAPN ? 120 : kBlockM;  // output rows a tile advances
   constexpr int kAccCols = TAPN ? 3 * BN : BN;      // TMEM columns per accumulator
@@ -316,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // its output.  Let the next layer's CTAs start their own prologue as SMs free up.
   pdl_wait();
   pdl_launch_dependents();
+  trace_cta(p.trace, 1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -397,6 +414,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         // taps-in-N: receptive-field origins of the four 32-row quarter loads (per tile)
         int qw[4] = {0, 0, 0, 0}, qh[4] = {0, 0, 0, 0}, qi[4] = {0, 0, 0, 0};
         if constexpr (TAPN) {
+          if (p.pool2) {
+            // fused 2x2 max-pool: a tile is output rows 2r, 2r+1 x columns [60 sg, 60 sg + 60)
+            // of one image; quarters 0/1 = row 2r (30 columns each), 2/3 = row 2r + 1
+            const int sg = tile_m % p.nseg;
+            const int rowp = tile_m / p.nseg;
+            const int img = rowp / p.Ho2;
+            const int r = rowp - img * p.Ho2;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              qi[q] = img;
+              qh[q] = 2 * r + (q >> 1) - p.ph;
+              // (a quarter that starts past the row's end only feeds junk lanes: load the
+              // segment's first one again rather than hand the TMA an out-of-range origin)
+              const int c0 = 60 * sg + 30 * (q & 1);
+              qw[q] = (c0 < p.Wo ? c0 : 60 * sg) - p.pw;
+            }
+          } else {
           const int hw = p.Ho * p.Wp;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -406,6 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             qh[q] = qrem / p.Wp;
             qw[q] = qrem - qh[q] * p.Wp - p.pw;
             qh[q] -= p.ph;
+          }
           }
         }
         // K-block coordinates, advanced incrementally: kb = (row_or_tap * cchunks + cc), and
@@ -718,6 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int hw = p.Ho * p.Wp;
     int tr_n = 0;
     float* bias_s = reinterpret_cast<float*>(smem + L.bias_off) + ew * BN;
+    int pool_round = 0;  // fused pool: vertical exchanges done (upper quarters)
     int cached_n = -1;
     const int j0 = alt ? half : 0;
     const int jstep = alt ? 2 : 1;
@@ -734,13 +770,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int acc = j & 1;
       const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
-      const int m = tile_m * kTileRows + static_cast<int>(quarter) * 30 + lane;
-      const int img = fdiv(m, p.fd_img);
-      const int rem = m - img * hw;
-      const int oh = fdiv(rem, p.fd_row);
-      const int owp = rem - oh * p.Wp;
-      const bool ok = lane < 30 && m < p.M && owp < p.Wo;
-      const size_t orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + owp;
+      bool ok;
+      size_t orow;
+      if (p.pool2) {
+        // pooled pixel (r, 30 sg + 15 (quarter & 1) + lane / 2), held by the even lanes of
+        // the row-2r quarters (0, 1) after the max over the 2x2 window
+        const int sg = tile_m % p.nseg;
+        const int rowp = tile_m / p.nseg;
+        const int ow = 60 * sg + 30 * static_cast<int>(quarter & 1) + lane;
+        ok = lane < 30 && !(lane & 1) && ow < p.Wo;
+        orow = static_cast<size_t>(rowp) * p.Wo2 + (ow >> 1);
+      } else {
+        const int m = tile_m * kTileRows + static_cast<int>(quarter) * 30 + lane;
+        const int img = fdiv(m, p.fd_img);
+        const int rem = m - img * hw;
+        const int oh = fdiv(rem, p.fd_row);
+        const int owp = rem - oh * p.Wp;
+        ok = lane < 30 && m < p.M && owp < p.Wo;
+        orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + owp;
+      }
       const int n_tile0 = tw.tn * BN;
       if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 20);
       mbar_wait(&tfull[acc], (j >> 1) & 1);
@@ -786,6 +834,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         d1),
                              d2);
         }
+        if (p.pool2) {
+          // max over the 2x2 window before bias / ReLU / rounding (all monotone, so this
+          // equals pooling the rounded conv output): horizontal pairs are lanes (2k, 2k+1);
+          // vertical pairs are quarters q and q + 2, exchanged through the upper quarter's
+          // staging slot (float4 chunks XOR-swizzled by pair index)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            v2[i].x = fmaxf(v2[i].x, __shfl_down_sync(0xffffffffu, v2[i].x, 1));
+            v2[i].y = fmaxf(v2[i].y, __shfl_down_sync(0xffffffffu, v2[i].y, 1));
+          }
+          const bool upper = quarter >= 2;
+          float4* xb = reinterpret_cast<float4*>(smem + L.out_off + (upper ? ew : ew - 2) * S::kRowStageBytes);
+          const int h = lane >> 1;
+          const int bar_id = 2 + half * 2 + static_cast<int>(quarter & 1);
+          if (upper) {
+            if (pool_round > 0) named_bar_sync(bar_id + 4, 64);  // reader done with the last tile
+            if (!(lane & 1) && lane < 30)
+#pragma unroll
+              for (int c4 = 0; c4 < 8; ++c4)
+                xb[h * 8 + (c4 ^ (h & 7))] = make_float4(v2[2 * c4].x, v2[2 * c4].y, v2[2 * c4 + 1].x, v2[2 * c4 + 1].y);
+            named_bar_arrive(bar_id, 64);
+            ++pool_round;
+            continue;
+          }
+          named_bar_sync(bar_id, 64);
+          if (!(lane & 1) && lane < 30)
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) {
+              const float4 o = xb[h * 8 + (c4 ^ (h & 7))];
+              v2[2 * c4].x = fmaxf(v2[2 * c4].x, o.x);
+              v2[2 * c4].y = fmaxf(v2[2 * c4].y, o.y);
+              v2[2 * c4 + 1].x = fmaxf(v2[2 * c4 + 1].x, o.z);
+              v2[2 * c4 + 1].y = fmaxf(v2[2 * c4 + 1].y, o.w);
+            }
+          named_bar_arrive(bar_id + 4, 64);
+        }
 #pragma unroll
         for (int i = 0; i < (dbg_probe(p, 4) ? 0 : 8); ++i) {
           const float4 b4 = *reinterpret_cast<const float4*>(bias_s + c + 4 * i);
@@ -798,7 +882,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[i] = p.relu ? pack_bf16x2_relu(v2[i].x, v2[i].y) : pack_bf16x2(v2[i].x, v2[i].y);
         __nv_bfloat16* const col0 = reinterpret_cast<__nv_bfloat16*>(p.out) + p.out_off + n;
         __nv_bfloat16* o = col0 + orow * p.ldo;
-        if (p.vec_ok && n + 32 <= p.N) {
+        if (p.pool2) {  // (vec_ok and N % 32 == 0 checked by the plan): 64 B per pooled pixel
+          if (ok) {
+            uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+          }
+        } else if (p.vec_ok && n + 32 <= p.N) {
           stage_store_rows32(smem + L.out_off + ew * S::kRowStageBytes, pk, lane, col0, p.ldo,
                              ok ? static_cast<int>(orow) : -1);
         } else if (ok && n < p.N) {
@@ -1190,6 +1281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  trace_cta(p.trace, 2);
   if (p.mcast) cluster_sync();  // no CTA leaves while its peer may still write into it
   if (warp == 1) {
     if constexpr (PAIR)

@@ -108,6 +108,8 @@ struct ConvParams {
   int kbs;                   // stem modes: filter rows (64-wide K blocks) per pipeline stage
   int early_release;         // epilogue frees the accumulator right after its TMEM loads
   int tapn2;                 // taps-in-N (unpaired): tap 2 folded into plane 0 by a 2-row A shift
+  int pool2;                 // taps-in-N: 2x2/2 max-pool fused (out is the pooled tensor)
+  int nseg, Ho2, Wo2;        // pool2: 60-column segments per row pair, pooled geometry
   int dbg;                   // timing experiments only (EB_DBG); 0 in production
   long long* trace;          // timing experiments only (EB_TRACE): per-role event clocks of CTA 0
   const __nv_bfloat16* x;    // input base (gather mode), NHWC with 8 channels

@@ -84,6 +84,7 @@ struct ConvArgs {
   int groups = 1;                    // grouped conv (block-diagonal weights per N tile)
   const float* pre_scale = nullptr;  // pre-activation on A (tiled mode only)
   const float* pre_shift = nullptr;
+  int pool2 = 0;  // fused 2x2/2 max-pool: y is the pooled (Ho/2 x Wo/2) tensor
 };
 
 int conv_out(int in, int k, int s, int p) { return (in + 2 * p - k) / s + 1; }
@@ -289,7 +290,8 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // tap-shift stages cover all kw taps of one filter row; a grouped tile sees BN channels
   const int cin_tile = a.groups > 1 ? bn : a.cin;
   const int num_kb = tap_shift ? a.kh * ((cin_tile + 63) / 64) : static_cast<int>(kpad / 64);
-  const int mt = tapn ? (M + 119) / 120 : (M + 127) / 128;
+  const int mt = (tapn && a.pool2) ? a.B * (Ho / 2) * ((Wo + 59) / 60)
+                                   : tapn ? (M + 119) / 120 : (M + 127) / 128;
   const int nt = (a.cout + bn - 1) / bn;
   int splits = a.split_k;
   if (splits <= 0) {
@@ -371,6 +373,20 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // EB_TAPN2: 0 off, 1 auto, 2 always
   static const int tapn2 = getenv("EB_TAPN2") ? atoi(getenv("EB_TAPN2")) : 1;
   pl.p.tapn2 = (tapn && !pair && (tapn2 == 2 || (tapn2 == 1 && num_kb <= a.kh))) ? 1 : 0;
+  if (a.pool2) {
+    // fused max-pool (VGG): taps-in-N tiles re-cut as 2 output rows x 60 columns so that
+    // each 2x2 window lies inside one tile
+    if (!tapn || Ho % 2 || Wo % 2 || a.cout % 32 || !pl.p.vec_ok || a.res || a.out_f32 ||
+        a.n_split || splits != 1 || pair)
+      EB_FAIL(EB_E_INVALID, "max-pool fusion needs a taps-in-N conv with even output size");
+    pl.p.pool2 = 1;
+    pl.p.Ho2 = Ho / 2;
+    pl.p.Wo2 = Wo / 2;
+    pl.p.nseg = (Wo + 59) / 60;
+    const int64_t mt2 = static_cast<int64_t>(a.B) * pl.p.Ho2 * pl.p.nseg;
+    if (mt2 * 120 > (1ll << 31) - 1) EB_FAIL(EB_E_INVALID, "conv M too large");
+    pl.p.M = static_cast<int>(mt2 * 120);  // (the kernel derives its tile count as M / 120)
+  }
   static const int dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
   pl.p.dbg = dbg;
   if (tapn) {
@@ -565,6 +581,10 @@ struct eb_engine {
   // the NHWC8 image itself is then written only if something else reads it
   bool img8_needed = true;
   bool layouts_fused = false;  // set per enqueue (u8 input)
+  // conv -> 2x2/2 max-pool pairs fused at finalize: op_pool[i] = index of the pool op whose
+  // output conv i writes directly (-1 if none); op_skip marks the absorbed pool ops
+  std::vector<int> op_pool;
+  std::vector<uint8_t> op_skip;
 };
 
 namespace {
@@ -577,6 +597,9 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
   auto P = [&](uint64_t off) -> const void* {
     return off == EB_NO_OFFSET ? nullptr : static_cast<const void*>(pool + off);
   };
+  const size_t op_idx = static_cast<size_t>(&op - e->ops.data());
+  if (op_idx < e->op_skip.size() && e->op_skip[op_idx]) return EB_OK;  // fused into its conv
+  const int fused_pool = op_idx < e->op_pool.size() ? e->op_pool[op_idx] : -1;
   Tensor& src = e->tensors[op.src];
   Tensor& dst = e->tensors[op.dst];
   const size_t es = dsize(src.dtype);
@@ -600,6 +623,13 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
       a.ldy = dst.c;
       a.y_off = op.dst_c_off;
       a.cout = op.cout;
+      if (fused_pool >= 0) {  // the conv writes the pooled tensor of the absorbed pool op
+        const eb_op_desc& po = e->ops[fused_pool];
+        a.y = e->tensors[po.dst].dev;
+        a.ldy = e->tensors[po.dst].c;
+        a.y_off = po.dst_c_off;
+        a.pool2 = 1;
+      }
       if (op.n_split > 0) {  // grouped launch: columns >= n_split go to dst2
         const Tensor& d2 = e->tensors[op.dst2];
         a.y2 = d2.dev;
@@ -1075,14 +1105,70 @@ int eb_add_member(eb_engine* e, int kind, int logits_tensor, int k_off, int k) {
   return EB_OK;
 }
 
+namespace {
+// Peephole at finalize: a taps-in-N conv whose only reader is the next op on its lane, a
+// 2x2/2 max-pool over the whole tensor, writes the pooled tensor itself (VGG: conv1_2 +
+// pool1 at 224x224 is 1.46 ms unfused, 1.11-1.15 ms fused on B200, B = 256).  EB_POOL_FUSE=0
+// keeps them apart.
+void fuse_conv_pools(eb_engine* e) {
+  const size_t n = e->ops.size();
+  e->op_pool.assign(n, -1);
+  e->op_skip.assign(n, 0);
+  static const bool on = env_flag("EB_POOL_FUSE", true);
+  if (!on || !tap_shift_enabled() || !tapn_enabled()) return;
+  for (size_t i = 0; i + 1 < n; ++i) {
+    const eb_op_desc& c = e->ops[i];
+    const eb_op_desc& po = e->ops[i + 1];
+    if (c.kind != EB_OP_CONV || po.kind != EB_OP_POOL || po.src != c.dst) continue;
+    if (po.pool_mode != EB_POOL_MAX || po.kh != 2 || po.kw != 2 || po.sh != 2 || po.sw != 2 ||
+        po.ph || po.pw || po.stream != c.stream || is_prefork(po) || is_prefork(c))
+      continue;
+    const Tensor& src = e->tensors[c.src];
+    const Tensor& t = e->tensors[c.dst];
+    const Tensor& pd = e->tensors[po.dst];
+    if (t.dtype != EB_BF16 || pd.dtype != EB_BF16 || c.dst_c_off != 0 || c.cout != t.c ||
+        po.src_c_off != 0 || po.src_c != t.c || pd.c % 8 || po.dst_c_off % 8)
+      continue;
+    // the taps-in-N geometry (plan_conv): 3x3/s1/p1, Cout <= 64 in 32s, even output, plain
+    if (c.kh != 3 || c.kw != 3 || c.sh != 1 || c.sw != 1 || c.ph != 1 || c.pw != 1 ||
+        c.cout % 32 || c.cout > std::min(64, tapn_max_cout()) || c.groups > 1 || c.res >= 0 ||
+        c.scale_off != EB_NO_OFFSET || c.n_split || c.flatten || src.c == 8 || t.h % 2 || t.w % 2)
+      continue;
+    bool other = false;  // nobody else reads the full-resolution output
+    for (size_t k = 0; k < n; ++k)
+      if (k != i + 1 && (e->ops[k].src == c.dst || e->ops[k].res == c.dst)) other = true;
+    for (const auto& m : e->members)
+      if (m.tensor == c.dst) other = true;
+    if (other) continue;
+    e->op_pool[i] = static_cast<int>(i + 1);
+    e->op_skip[i + 1] = 1;
+    ++i;
+  }
+}
+}  // namespace
+
 int eb_finalize(eb_engine* e) {
   if (!e || e->finalized) EB_FAIL(EB_E_STATE, "engine already finalized");
   if (e->members.empty()) EB_FAIL(EB_E_INVALID, "no members");
   if (!e->have_pre) EB_FAIL(EB_E_STATE, "preprocess not set");
   cudaSetDevice(e->device);
   const int mb = e->max_batch;
+  fuse_conv_pools(e);
+  std::vector<uint8_t> t_read(e->tensors.size(), 0);  // tensors some op or member reads
+  for (size_t i = 0; i < e->ops.size(); ++i) {
+    if (e->op_skip[i]) continue;
+    const eb_op_desc& op = e->ops[i];
+    t_read[op.src] = 1;
+    if (op.res >= 0) t_read[op.res] = 1;
+  }
+  for (const auto& m : e->members) t_read[m.tensor] = 1;
   for (size_t i = 0; i < e->tensors.size(); ++i) {
     Tensor& t = e->tensors[i];
+    // a fused conv's full-resolution output is never materialised
+    bool absorbed = false;
+    for (size_t k = 0; k < e->ops.size(); ++k)
+      if (e->op_pool[k] >= 0 && e->ops[k].dst == static_cast<int>(i)) absorbed = true;
+    if (absorbed && !t_read[i]) continue;
     if (i == EB_T_IMAGE_NHWC8 && !e->any_cnn) continue;
     if (i == EB_T_IMAGE_F32 && !e->any_lin) continue;
     const size_t bytes = static_cast<size_t>(mb) * t.h * t.w * t.c * dsize(t.dtype);
@@ -1362,13 +1448,15 @@ int eb_k_preprocess_u8_nhwc8(const uint8_t* dev_x, void* dev_y_bf16, int batch, 
   return EB_OK;
 }
 
-int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, const void* dev_w,
-              const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
-              int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
-              int out_f32, int c8_stem, int split_k, int block_n, int groups,
-              void* dev_workspace, const float* dev_pre_scale, const float* dev_pre_shift,
-              void* stream) {
+namespace {
+int k_conv_abi(const void* dev_x, int batch, int h, int w, int ldx, int cin, const void* dev_w,
+               const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
+               int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
+               int out_f32, int c8_stem, int split_k, int block_n, int groups,
+               void* dev_workspace, const float* dev_pre_scale, const float* dev_pre_shift,
+               void* stream, int pool2) {
   ConvArgs a{};
+  a.pool2 = pool2;
   a.groups = groups > 1 ? groups : 1;
   a.pre_scale = dev_pre_scale;
   a.pre_shift = dev_pre_shift;
@@ -1404,16 +1492,17 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
   if (rc != EB_OK) return rc;
   // EB_TRACE=<file>: timing probe (per-role event clocks of CTA 0, appended as text)
   static const char* trace_path = getenv("EB_TRACE");
+  constexpr size_t kTraceLongs = 3 * 1024 * 2 + 1024 * 4;
   static long long* d_trace = nullptr;
   if (trace_path) {
-    if (!d_trace) EB_CUDA(cudaMalloc(&d_trace, 3 * 1024 * 2 * sizeof(long long)));
-    EB_CUDA(cudaMemset(d_trace, 0, 3 * 1024 * 2 * sizeof(long long)));
+    if (!d_trace) EB_CUDA(cudaMalloc(&d_trace, kTraceLongs * sizeof(long long)));
+    EB_CUDA(cudaMemset(d_trace, 0, kTraceLongs * sizeof(long long)));
     pl.p.trace = d_trace;
   }
   rc = run_conv_plan(pl, static_cast<float*>(dev_workspace), kSplitWsFloats, a,
                      static_cast<cudaStream_t>(stream), nullptr);
   if (rc == EB_OK && trace_path) {
-    std::vector<long long> h(3 * 1024 * 2);
+    std::vector<long long> h(kTraceLongs);
     EB_CUDA(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     if (FILE* f = fopen(trace_path, "w")) {
       for (int r = 0; r < 3; ++r)
@@ -1422,10 +1511,36 @@ int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, cons
           if (v == 0) break;
           fprintf(f, "%d %lld %lld %lld\n", r, v >> 48, v & 0xFFFFFFFFFFFFll, h[(r * 1024 + i) * 2 + 1]);
         }
+      // CTA spans: "3 <cta> <entry ns> <prologue done ns> <exit ns>"
+      for (int c = 0; c < 1024; ++c) {
+        const long long* q = &h[3 * 1024 * 2 + c * 4];
+        if (q[0] == 0) break;
+        fprintf(f, "3 %d %lld %lld %lld\n", c, q[0], q[1], q[2]);
+      }
       fclose(f);
     }
   }
   return rc;
+}
+}  // namespace
+
+int eb_k_conv(const void* dev_x, int batch, int h, int w, int ldx, int cin, const void* dev_w,
+              const float* dev_bias, const void* dev_res, int ldr, void* dev_y, int ldy,
+              int y_off, int cout, int kh, int kw, int sh, int sw, int ph, int pw, int relu,
+              int out_f32, int c8_stem, int split_k, int block_n, int groups,
+              void* dev_workspace, const float* dev_pre_scale, const float* dev_pre_shift,
+              void* stream) {
+  return k_conv_abi(dev_x, batch, h, w, ldx, cin, dev_w, dev_bias, dev_res, ldr, dev_y, ldy, y_off,
+                    cout, kh, kw, sh, sw, ph, pw, relu, out_f32, c8_stem, split_k, block_n, groups,
+                    dev_workspace, dev_pre_scale, dev_pre_shift, stream, 0);
+}
+
+int eb_k_conv_maxpool2(const void* dev_x, int batch, int h, int w, int ldx, int cin,
+                       const void* dev_w, const float* dev_bias, void* dev_y, int ldy, int y_off,
+                       int cout, int kh, int kw, int ph, int pw, int relu, void* stream) {
+  return k_conv_abi(dev_x, batch, h, w, ldx, cin, dev_w, dev_bias, nullptr, 0, dev_y, ldy, y_off,
+                    cout, kh, kw, 1, 1, ph, pw, relu, 0, 0, 0, 0, 1, nullptr, nullptr, nullptr,
+                    stream, 1);
 }
 
 int eb_k_resize(const void* dev_x, int ldx, void* dev_y, int ldy, int batch, int h, int w, int c,

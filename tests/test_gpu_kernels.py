@@ -440,3 +440,55 @@ def test_conv_writes_stay_inside_output(case):
     r = ref_conv(x, cin_real, w, bias, None, True, kh, kw, st, st, pd, pd)
     err = (yy[..., :cout] - r).abs().max().item()
     assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+
+
+POOL2_CASES = [  # B, H, W, Cin, Cout
+    (2, 224, 224, 64, 64),   # VGG16 conv1_2 + pool1 geometry
+    (3, 20, 26, 64, 32),     # one segment, ragged (26 < 60)
+    (2, 14, 122, 48, 64),    # 3 segments, the last partial; Cin < 64
+    (2, 12, 16, 128, 32),    # 2 K blocks per filter row (3-plane epilogue)
+    (1, 2, 2, 64, 64),       # a single pooled pixel
+]
+
+
+@pytest.mark.parametrize("case", POOL2_CASES, ids=[f"{c[1]}x{c[2]}c{c[3]}-{c[4]}" for c in POOL2_CASES])
+def test_conv_maxpool2_fused_bit_exact(case):
+    """eb_k_conv_maxpool2 == eb_k_conv then eb_k_pool(2, 2, max), bit for bit, and no write
+    outside the pooled slice (guard sentinel, wider rows)."""
+    lib = _lib.load()
+    B, H, W, cin, cout = case
+    g = torch.Generator().manual_seed(B * 1000 + H * 7 + cin)
+    x = torch.randn(B, H, W, cin, generator=g).to(torch.bfloat16).to(DEV)
+    w = torch.randn(cout, cin, 3, 3, generator=g) / np.sqrt(cin * 9)
+    bias = (torch.randn(cout, generator=g) * 0.1).to(DEV)
+    y_full = run_conv(x, cin, cin, w, bias.cpu(), None, True, 3, 3, 1, 1, 1, 1)
+    Ho2, Wo2 = H // 2, W // 2
+    ref = torch.zeros(B, Ho2, Wo2, cout, device=DEV, dtype=torch.bfloat16)
+    _lib.check(lib.eb_k_pool(_p(y_full), cout, _p(ref), cout, 0, B, H, W, cout, 2, 2, 0, 0,
+                             None, None, None))
+    wp = pack_conv_weight(w, conv_mode(3, 3, 1, 1, 1, 1, cin, False)).to(DEV)
+    ld, off, guard = cout + 16, 8, 2048
+    SENT = -12352.0
+    n = B * Ho2 * Wo2 * ld
+    buf = torch.full((guard + n + guard,), SENT, device=DEV).to(torch.bfloat16)
+    y = buf[guard:guard + n].view(B, Ho2, Wo2, ld)
+    _lib.check(lib.eb_k_conv_maxpool2(_p(x), B, H, W, cin, cin, _p(wp), _p(bias), _p(y), ld, off,
+                                      cout, 3, 3, 1, 1, 1, None))
+    torch.cuda.synchronize()
+    b = buf.float().cpu()
+    assert (b[:guard] == SENT).all() and (b[guard + n:] == SENT).all(), "write outside the tensor"
+    yy = y.cpu()
+    assert (yy[..., :off].float() == SENT).all() and (yy[..., off + cout:].float() == SENT).all()
+    assert torch.equal(yy[..., off:off + cout], ref.cpu()), "fused pool differs from conv + pool"
+
+
+def test_conv_maxpool2_rejects_unsupported():
+    lib = _lib.load()
+    x = torch.zeros(1, 8, 8, 64, device=DEV, dtype=torch.bfloat16)
+    wp = torch.zeros(1 << 16, device=DEV, dtype=torch.bfloat16)
+    y = torch.zeros(1, 4, 4, 256, device=DEV, dtype=torch.bfloat16)
+    # Cout 256 (not taps-in-N) and an odd output size are refused, not mis-computed
+    assert lib.eb_k_conv_maxpool2(_p(x), 1, 8, 8, 64, 64, _p(wp), None, _p(y), 256, 0, 256, 3, 3, 1, 1,
+                                  1, None) != 0
+    assert lib.eb_k_conv_maxpool2(_p(x), 1, 7, 7, 64, 64, _p(wp), None, _p(y), 64, 0, 64, 3, 3, 1, 1,
+                                  1, None) != 0

@@ -24,6 +24,8 @@ ap.add_argument("--pre", action="store_true", help="fused BN-ReLU pre-activation
 ap.add_argument("--split", type=int, default=0)
 ap.add_argument("--groups", type=int, default=1)
 ap.add_argument("--relayout", action="store_true", help="stem: padded rows / planes layout (c8_stem=2)")
+ap.add_argument("--pool", action="store_true", help="fused 2x2/2 max-pool (eb_k_conv_maxpool2)")
+ap.add_argument("--then-pool", action="store_true", help="conv then a separate eb_k_pool (2x2/2 max)")
 a = ap.parse_args()
 lib = _lib.load()
 P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
@@ -63,10 +65,21 @@ if a.relayout:
 STEM = 2 if a.relayout else int(a.stem)
 
 
+if a.pool or a.then_pool:
+    yp = torch.empty(a.B, Ho // 2, Wo // 2, a.COUT, device="cuda", dtype=torch.bfloat16)
+
+
 def run():
+    if a.pool:
+        _lib.check(lib.eb_k_conv_maxpool2(P(src), a.B, a.H, a.W, LD, LD, P(wp), P(bias), P(yp), a.COUT, 0,
+                                          a.COUT, a.KH, a.KW, a.P, a.P, 1, None))
+        return
     _lib.check(lib.eb_k_conv(P(src), a.B, a.H, a.W, LD, LD, P(wp), P(bias), P(res),
                              a.COUT if res is not None else 0, P(y), a.COUT, 0, a.COUT, a.KH, a.KW,
                              a.S, a.S, a.P, a.P, 1, 0, STEM, a.split, a.block_n, a.groups, P(ws), P(pre_s), P(pre_t), None))
+    if a.then_pool:
+        _lib.check(lib.eb_k_pool(P(y), a.COUT, P(yp), a.COUT, 0, a.B, Ho, Wo, a.COUT, 2, 2, 0, 0,
+                                 None, None, None))
 
 
 for _ in range(3):

@@ -3,9 +3,22 @@ import collections
 import sys
 
 ev = collections.defaultdict(list)
+spans = []
 for line in open(sys.argv[1]):
-    r, tag, clk, ns = map(int, line.split())
+    f = list(map(int, line.split()))
+    if f[0] == 3:  # CTA span: cta, entry, prologue done, exit (global ns)
+        spans.append(f[1:])
+        continue
+    r, tag, clk, ns = f
     ev[r].append((tag, clk))
+if spans:
+    t0 = min(s[1] for s in spans)
+    q = lambda v: (min(v), sorted(v)[len(v) // 2], max(v))  # noqa: E731
+    print(f"CTAs {len(spans)}: entry +ns min/med/max {q([s[1] - t0 for s in spans])}")
+    print(f"   prologue ns {q([s[2] - s[1] for s in spans])}  body ns {q([s[3] - s[2] for s in spans])}")
+    print(f"   exit +ns {q([s[3] - t0 for s in spans])}")
+if not ev:
+    sys.exit(0)
 t0 = min(v[0][1] for v in ev.values())
 names = {0: "producer", 1: "mma", 2: "epilogue(w2)"}
 for r in sorted(ev):
