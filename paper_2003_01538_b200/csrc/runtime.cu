@@ -333,6 +333,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.p.out_mode = a.out_f32 ? kOutF32 : kOutBF16;
   pl.p.pre_scale = a.pre_scale;
   pl.p.pre_shift = a.pre_shift;
+
   if (a.pre_scale && (pl.p.a_mode != kAModeTiled || !a.pre_shift))
     EB_FAIL(EB_E_INVALID, "pre-activation is only supported on 1x1 (tiled) convolutions");
   if (a.pre_scale && (bn != 128 || num_kb * 64 > 2048))
@@ -1490,6 +1491,10 @@ int k_conv_abi(const void* dev_x, int batch, int h, int w, int ldx, int cin, con
   ConvPlan pl;
   int rc = plan_conv(a, &pl);
   if (rc != EB_OK) return rc;
+  if (env_flag("EB_DEBUG_PLAN", false))
+    fprintf(stderr, "[eb] conv mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d kbs=%d cl=%d pair=%d resb=%d stages=%d\n",
+            pl.p.a_mode, pl.block_n, pl.grid, pl.splits, pl.p.M, pl.p.N, pl.p.num_kb, pl.p.kbs, pl.p.mcast,
+            pl.p.pair, pl.p.resb, conv_umma_stages(pl.p, pl.block_n));
   // EB_TRACE=<file>: timing probe (per-role event clocks of CTA 0, appended as text)
   static const char* trace_path = getenv("EB_TRACE");
   constexpr size_t kTraceLongs = 3 * 1024 * 2 + 1024 * 4;
