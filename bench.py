@@ -70,7 +70,8 @@ def hbm_kernels(B: int, hbm_peak: float, src: str) -> dict:
     """Achieved HBM bandwidth of the two memory-bound kernels of the path, through the
     kernel-level C-ABI on device buffers (north_star: preprocess and combine vs HBM peak).
 
-    K1 preprocess: u8 HWC (3 B/px) -> bf16 NHWC8 (16 B/px): 19 algorithmic bytes per pixel.
+    K1 preprocess: u8 HWC (3 B/px) -> bf16 NHWC8 (16 B/px): 19 algorithmic bytes per pixel;
+    and straight into the stem layouts (u8 read + the layout's bytes written).
     K5 combine: 3 members x 1000 fp32 logits per image read, labels + top-5 written; at the
     bench batch it is latency-bound (a few MB), so it is also reported at B = 4096 (C4).
     """
@@ -91,6 +92,20 @@ def hbm_kernels(B: int, hbm_peak: float, src: str) -> dict:
     bytes_ = B * hw * (3 + 16)
     out["preprocess_k1"] = {"batch": B, "us": ms * 1e3, "bytes": bytes_, "achieved_gbs": bytes_ / ms / 1e6,
                             "frac_of_hbm": bytes_ / ms / 1e6 / hbm_peak}
+    # K1 as the engine runs it for C2 (u8 request): straight into the two stem layouts
+    # (VGG 3x3/s1 padded rows, the grouped 7x7/s2 stem's even/odd column planes)
+    xr = x.view(B, 224, 224, 3)
+    for name, (kh, st, pd) in () if not hasattr(lib, "eb_k_preprocess_u8_layout") else (("rows_3x3", (3, 1, 1)), ("planes_7x7s2", (7, 2, 3))):
+        nb = ctypes.c_uint64(0)
+        _lib.check(lib.eb_k_stem_layout(B, 224, 224, kh, kh, st, st, pd, pd, ctypes.byref(nb)))
+        ly = torch.empty(nb.value // 2, dtype=torch.bfloat16, device="cuda")
+        ms = _event_time(lambda: _lib.check(lib.eb_k_preprocess_u8_layout(
+            P(xr), B, 3, 224, 224, P(lut), kh, kh, st, st, pd, pd, P(ly), None)))
+        bytes_ = B * hw * 3 + nb.value
+        out[f"preprocess_k1_{name}"] = {"batch": B, "us": ms * 1e3, "bytes": bytes_,
+                                        "achieved_gbs": bytes_ / ms / 1e6,
+                                        "frac_of_hbm": bytes_ / ms / 1e6 / hbm_peak}
+        del ly
     for b in (B, 4096):
         K, n, tk = 1000, 3, 5
         l32 = torch.randn(b, n * K, device="cuda")

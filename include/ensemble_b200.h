@@ -205,6 +205,12 @@ int eb_k_stem_layout(int batch, int h, int w, int kh, int kw, int sh, int sw, in
                      uint64_t* bytes);
 int eb_k_stem_relayout(const void* dev_x, int batch, int h, int w, int kh, int kw, int sh, int sw,
                        int ph, int pw, void* dev_y, void* stream);
+/* K1 straight into a stem layout: u8 HWC pixels (c <= 8 channels) -> per-channel LUT ->
+ * the padded layout eb_k_stem_relayout would produce from the NHWC8 image (identical
+ * bytes, one pass; what the engine runs for stems on a u8 request). */
+int eb_k_preprocess_u8_layout(const uint8_t* dev_x, int batch, int c, int h, int w,
+                              const float* dev_lut, int kh, int kw, int sh, int sw, int ph, int pw,
+                              void* dev_y, void* stream);
 int eb_k_pool(const void* dev_x, int ldx, void* dev_y, int ldy, int y_off, int batch, int h,
               int w, int c, int k, int s, int pad, int mode, const float* dev_scale,
               const float* dev_shift, void* stream);

@@ -105,6 +105,8 @@ _SIGS = {
     "eb_k_conv_maxpool2": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p,
                                    c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
                                    c_int, c_int, c_void_p]),
+    "eb_k_preprocess_u8_layout": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int,
+                                          c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p]),
     "eb_k_stem_layout": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                  POINTER(c_uint64)]),
     "eb_k_stem_relayout": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,

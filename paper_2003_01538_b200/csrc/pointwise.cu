@@ -137,31 +137,69 @@ cudaError_t k_preprocess_u8hwc_to_f32chw(const uint8_t* x, float* y, int B, int 
 // K1 straight into a stem layout (StemGeom): u8 HWC -> LUT -> bf16 8-channel pixels of
 // the zero-padded rows / even-odd planes buffer.  Used instead of the NHWC8 image plus a
 // relayout when a stem reads the preprocessed image (one pass, no intermediate).
+// A work unit is kRows consecutive padded rows hq of one image (both planes in the planes
+// mode, which read the same input rows): the unit's input rows are one contiguous run of
+// bytes, staged into smem with 16-byte loads (all in flight at once), then every output
+// pixel is formed from smem and written with one 16-byte store.
+constexpr int kK1Rows = 8;
+constexpr int kK1MaxRowBytes = 2048;  // W * C per input row staged (larger: direct loads)
+
+template <int CT>  // CT: channel count when known at compile time (3), else 0
 __global__ void __launch_bounds__(256)
-    preprocess_u8_to_layout_kernel(const uint8_t* __restrict__ x, int B, int C, int H, int W,
+    preprocess_u8_to_layout_kernel(const uint8_t* __restrict__ x, int B, int C_, int H, int W,
                                    const float* __restrict__ lut, int ph, int pw, int planes, int Hq,
                                    int Wq, uint4* __restrict__ y) {
-  // one CTA per padded row (plane q, image b, row hq); threads walk its Wq pixels
-  __shared__ float s_lut[8 * 256];
-  for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = lut[i];
-  __syncthreads();
-  const int row = blockIdx.x;  // (q * B + b) * Hq + hq
-  const int hq = row % Hq;
-  const int bq = row / Hq;
-  const int q = bq / B;
-  const int b = bq - q * B;
-  const int ih = hq - ph;
-  uint4* yr = y + static_cast<int64_t>(row) * Wq;
-  const bool hok = ih >= 0 && ih < H;
-  const uint8_t* xr = x + (static_cast<int64_t>(b) * H + (hok ? ih : 0)) * W * C;
-  for (int j = threadIdx.x; j < Wq; j += blockDim.x) {
-    const int iw = planes ? 2 * j + q - pw : j - pw;
-    const bool ok = hok && iw >= 0 && iw < W;
-    __align__(16) __nv_bfloat16 v[8];
-    const uint8_t* px = xr + (ok ? iw : 0) * C;
+  const int C = CT ? CT : C_;
+  // the LUT pre-rounded to bf16 (the value the output carries)
+  __shared__ __nv_bfloat16 s_lut[8 * 256];
+  __shared__ __align__(16) uint8_t s_in[kK1Rows * kK1MaxRowBytes];
+  for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = __float2bfloat16_rn(lut[i]);
+  const int row_bytes = W * C;
+  const bool staged = row_bytes <= kK1MaxRowBytes;
+  const int chunks = (Hq + kK1Rows - 1) / kK1Rows;
+  const int units = B * chunks;
+  const int nq = planes ? 2 : 1;
+  const int warp = static_cast<int>(threadIdx.x) >> 5;
+  const int lane = static_cast<int>(threadIdx.x) & 31;
+  const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int b = u / chunks;
+    const int hq0 = (u - b * chunks) * kK1Rows;
+    // input rows [ih0, ih1) of this unit that lie inside the image
+    const int ih0 = max(hq0 - ph, 0);
+    const int ih1 = min(hq0 + kK1Rows - ph, H);
+    const uint8_t* src = x + (static_cast<int64_t>(b) * H + ih0) * row_bytes;
+    __syncthreads();  // (previous unit done with s_in; LUT staged)
+    if (staged && ih1 > ih0) {
+      const int n = (ih1 - ih0) * row_bytes;
+      if (((reinterpret_cast<uintptr_t>(src) | static_cast<uintptr_t>(n)) & 15) == 0) {
+        for (int i = threadIdx.x; i < n / 16; i += blockDim.x)
+          reinterpret_cast<uint4*>(s_in)[i] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+      } else {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) s_in[i] = src[i];
+      }
+    }
+    __syncthreads();
+    // one warp per output row (plane q, padded row hq), 32 pixels per step
+    for (int qr = warp; qr < nq * kK1Rows; qr += 8) {
+      const int q = qr / kK1Rows;
+      const int hq = hq0 + (qr - q * kK1Rows);
+      if (hq >= Hq) continue;
+      const int ih = hq - ph;
+      const bool hok = ih >= 0 && ih < H;
+      uint4* yr = y + (static_cast<int64_t>(q * B + b) * Hq + hq) * Wq;
+      const uint8_t* rowp = staged ? s_in + (ih - ih0) * row_bytes
+                                   : x + (static_cast<int64_t>(b) * H + ih) * row_bytes;
+      for (int j = lane; j < Wq; j += 32) {
+        const int iw = planes ? 2 * j + q - pw : j - pw;
+        const bool ok = hok && iw >= 0 && iw < W;
+        const uint8_t* px = rowp + iw * C;
+        __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = __float2bfloat16_rn((ok && c < C) ? s_lut[c * 256 + px[c]] : 0.f);
-    yr[j] = *reinterpret_cast<const uint4*>(v);
+        for (int c = 0; c < 8; ++c) v[c] = (ok && c < C) ? s_lut[c * 256 + px[c]] : zero;
+        yr[j] = *reinterpret_cast<const uint4*>(v);
+      }
+    }
   }
 }
 
@@ -169,10 +207,15 @@ cudaError_t k_preprocess_u8_to_layout(const uint8_t* x, int B, int C, int H, int
                                       int ph, int pw, int mode, int Hq, int Wq, __nv_bfloat16* y,
                                       cudaStream_t s) {
   const int planes = mode == kAModeStemPlanes ? 1 : 0;
-  const int rows = (planes ? 2 : 1) * B * Hq;
-  if (rows == 0 || Wq == 0) return cudaSuccess;
-  preprocess_u8_to_layout_kernel<<<rows, 256, 0, s>>>(x, B, C, H, W, lut, ph, pw, planes, Hq, Wq,
-                                                      reinterpret_cast<uint4*>(y));
+  if (B == 0 || Hq == 0 || Wq == 0) return cudaSuccess;
+  const int64_t units = static_cast<int64_t>(B) * ((Hq + kK1Rows - 1) / kK1Rows);
+  const int grid = static_cast<int>(std::min<int64_t>(units, 148 * 8));
+  if (C == 3)
+    preprocess_u8_to_layout_kernel<3><<<grid, 256, 0, s>>>(x, B, C, H, W, lut, ph, pw, planes, Hq,
+                                                           Wq, reinterpret_cast<uint4*>(y));
+  else
+    preprocess_u8_to_layout_kernel<0><<<grid, 256, 0, s>>>(x, B, C, H, W, lut, ph, pw, planes, Hq,
+                                                           Wq, reinterpret_cast<uint4*>(y));
   return cudaGetLastError();
 }
 

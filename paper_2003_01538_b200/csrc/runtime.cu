@@ -1574,6 +1574,18 @@ int eb_k_stem_relayout(const void* dev_x, int batch, int h, int w, int kh, int k
   return EB_OK;
 }
 
+int eb_k_preprocess_u8_layout(const uint8_t* dev_x, int batch, int c, int h, int w,
+                              const float* dev_lut, int kh, int kw, int sh, int sw, int ph, int pw,
+                              void* dev_y, void* stream) {
+  StemGeom g;
+  if (c < 1 || c > 8) EB_FAIL(EB_E_INVALID, "1..8 channels");
+  if (!stem_geom(batch, h, w, kh, kw, sh, sw, ph, pw, &g)) EB_FAIL(EB_E_INVALID, "no stem layout");
+  EB_CUDA(k_preprocess_u8_to_layout(dev_x, batch, c, h, w, dev_lut, ph, pw, g.mode, g.Hq, g.Wq,
+                                    static_cast<__nv_bfloat16*>(dev_y),
+                                    static_cast<cudaStream_t>(stream)));
+  return EB_OK;
+}
+
 int eb_k_pool(const void* dev_x, int ldx, void* dev_y, int ldy, int y_off, int batch, int h,
               int w, int c, int k, int s, int pad, int mode, const float* dev_scale,
               const float* dev_shift, void* stream) {

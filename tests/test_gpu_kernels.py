@@ -217,6 +217,31 @@ def test_preprocess_u8_lut_exact():
     assert (got[..., C:].float() == 0).all()
 
 
+@pytest.mark.parametrize("geom", [(2, 224, 224, 3, 3, 1, 1), (2, 224, 224, 7, 7, 2, 3),
+                                  (3, 19, 23, 3, 3, 1, 1), (2, 21, 25, 7, 7, 2, 3),
+                                  (1, 20, 300, 7, 7, 2, 3)],
+                         ids=["vgg_rows", "grouped_planes", "rows_ragged", "planes_ragged", "wide"])
+def test_preprocess_u8_layout_equals_relayout(geom):
+    """K1 straight into a stem layout == K1 to NHWC8 then eb_k_stem_relayout, byte for byte
+    (the engine's u8 path uses the former)."""
+    lib = _lib.load()
+    B, H, W, kh, kw, st, pd = geom
+    rng = np.random.default_rng(H * W + kh)
+    px = torch.from_numpy(rng.integers(0, 256, size=(B, H, W, 3), dtype=np.uint8)).to(DEV)
+    lut = torch.from_numpy(u8_lut((0.485, 0.456, 0.406), (0.229, 0.224, 0.225), 255.0, 3)).to(DEV)
+    img8 = torch.empty(B, H, W, 8, dtype=torch.bfloat16, device=DEV)
+    _lib.check(lib.eb_k_preprocess_u8_nhwc8(_p(px), _p(img8), B, 3, H * W, _p(lut), None))
+    nbytes = ctypes.c_uint64(0)
+    _lib.check(lib.eb_k_stem_layout(B, H, W, kh, kw, st, st, pd, pd, ctypes.byref(nbytes)))
+    a = torch.full((nbytes.value // 2,), 7.0, device=DEV).to(torch.bfloat16)
+    b = torch.full((nbytes.value // 2,), -7.0, device=DEV).to(torch.bfloat16)
+    _lib.check(lib.eb_k_stem_relayout(_p(img8), B, H, W, kh, kw, st, st, pd, pd, _p(a), None))
+    _lib.check(lib.eb_k_preprocess_u8_layout(_p(px), B, 3, H, W, _p(lut), kh, kw, st, st, pd, pd,
+                                             _p(b), None))
+    torch.cuda.synchronize()
+    assert torch.equal(a.view(torch.int16).cpu(), b.view(torch.int16).cpu())
+
+
 def test_preprocess_f32_bit_exact():
     lib = _lib.load()
     rng = np.random.default_rng(1)
