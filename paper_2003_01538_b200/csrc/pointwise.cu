@@ -521,11 +521,24 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
     Vec8 acc;
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc.v[j] = 0.f;
-    for (int p = 0; p < HW; ++p) {
-      Vec8 v = load8(x + (b * HW + p) * ldx + c);
-      if (scale) bnrelu8(v, scale, shift, c);
+    // 8 pixels' loads in flight per step (the sum keeps its sequential order)
+    const __nv_bfloat16* xb = x + b * HW * ldx + c;
+    for (int p0 = 0; p0 < HW; p0 += 8) {
+      uint4 q[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc.v[j] += v.v[j];
+      for (int u = 0; u < 8; ++u)
+        if (p0 + u < HW) q[u] = __ldg(reinterpret_cast<const uint4*>(xb + static_cast<int64_t>(p0 + u) * ldx));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (p0 + u >= HW) break;
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&q[u]);
+        Vec8 v;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v.v[j] = __bfloat162float(h[j]);
+        if (scale) bnrelu8(v, scale, shift, c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc.v[j] += v.v[j];
+      }
     }
     const float inv = 1.f / static_cast<float>(HW);
 #pragma unroll
