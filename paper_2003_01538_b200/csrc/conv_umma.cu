@@ -56,7 +56,7 @@ constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels 
 // lane quarter can form its 30 outputs with warp shuffles; tiles advance 120 rows.
 // STEM: the stem rows / planes modes (direct row stores; separate instances so the
 // other kernels do not carry their code)
-template <int BN, int TS, bool PAIR, bool TAPN = false, bool STEM = false>
+template <int BN, int TS, bool PAIR, int TAPN = 0, bool STEM = false>
 struct ConvSmem {
   static_assert(BN == 32 || BN == 64 || BN == 128 || BN == 256, "tile width");
   static constexpr int kBN = BN;
@@ -233,7 +233,7 @@ __device__ __forceinline__ int swz_chunk(int chunk, int row, int cw) {
   return cw == 64 ? (chunk ^ (row & 7)) : (chunk ^ ((row >> 1) & 3));
 }
 
-template <int BN, int TS, bool PAIR, bool TAPN, bool STEM>
+template <int BN, int TS, bool PAIR, int TAPN, bool STEM>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_umma_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // two epilogue groups split each tile's chunks), doubled in PAIR mode where the
       // leader waits for both CTAs' epilogues
       const uint32_t drain =
-          (n_epi == 8 && (BN / S::kCW > 1 || (TAPN && BN == 64))) ? 8u : 4u;
+          (n_epi == 8 && (TAPN ? (BN == 64 && !p.tapn_alt) : BN / S::kCW > 1)) ? 8u : 4u;
       mbar_init(&tempty[a], PAIR ? 2 * drain : drain);
     }
     for (int a = 0; a < 16; ++a) mbar_init(&rfull[a], 1);
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // taps-in-N: receptive-field origins of the four 32-row quarter loads (per tile)
         int qw[4] = {0, 0, 0, 0}, qh[4] = {0, 0, 0, 0}, qi[4] = {0, 0, 0, 0};
         if constexpr (TAPN) {
-          if (p.pool2) {
+          if constexpr ((TAPN & 4) != 0) {
             // fused 2x2 max-pool: a tile is output rows 2r, 2r+1 x columns [60 sg, 60 sg + 60)
             // of one image; quarters 0/1 = row 2r (30 columns each), 2/3 = row 2r + 1
             const int sg = tile_m % p.nseg;
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if constexpr (PAIR) {
                 umma_bf16_pair(tmem_d, adesc, bdesc, idesc, accum);
               } else if constexpr (TAPN) {
-                if (p.tapn2) {
+                if constexpr ((TAPN & 3) == 2) {
                   // planes 0|1 = A x [tap0; tap1]; plane 0 += (A two rows on) x tap2: the
                   // epilogue then adds one shifted plane instead of two
                   umma_bf16(tmem_d, adesc, bdesc, idesc_2bn, accum);
@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;
     const uint32_t quarter = warp & 3;
     const int lane = static_cast<int>(lane_id());
-    const bool split_cols = n_epi == 8 && BN == 64;
+    const bool split_cols = n_epi == 8 && BN == 64 && !p.tapn_alt;
     const bool alt = n_epi == 8 && !split_cols;
     const int c_lo = split_cols ? 32 * half : 0;
     const int c_hi = split_cols ? c_lo + 32 : BN;
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
       bool ok;
       size_t orow;
-      if (p.pool2) {
+      if constexpr ((TAPN & 4) != 0) {
         // pooled pixel (r, 30 sg + 15 (quarter & 1) + lane / 2), held by the even lanes of
         // the row-2r quarters (0, 1) after the max over the 2x2 window
         const int sg = tile_m % p.nseg;
@@ -799,10 +799,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = c_lo; c < c_hi; c += 32) {
         const int n = n_tile0 + c;
         uint32_t r0[32], r1[32], r2[32];
-        const bool two = !PAIR && p.tapn2;
+        constexpr bool two = !PAIR && (TAPN & 3) == 2;
         tmem_ld32(tb + c, r0);
         tmem_ld32(tb + BN + c, r1);
-        if (!two) tmem_ld32(tb + 2 * BN + c, r2);
+        if constexpr (!two) tmem_ld32(tb + 2 * BN + c, r2);
         tmem_ld_wait();
         if (c + 32 >= c_hi && p.early_release) {  // last TMEM read of the tile: hand it back now
           tc_fence_before();
@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // ((D0 + D1') + D2') + bias on fp32 pairs (FADD2), the shifted planes by shuffle
         float2 v2[16];
-        if (two) {
+        if constexpr (two) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float2 d1 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * i]), 1),
@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         d1),
                              d2);
         }
-        if (p.pool2) {
+        if constexpr ((TAPN & 4) != 0) {
           // max over the 2x2 window before bias / ReLU / rounding (all monotone, so this
           // equals pooling the rounded conv output): horizontal pairs are lanes (2k, 2k+1);
           // vertical pairs are quarters q and q + 2, exchanged through the upper quarter's
@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[i] = p.relu ? pack_bf16x2_relu(v2[i].x, v2[i].y) : pack_bf16x2(v2[i].x, v2[i].y);
         __nv_bfloat16* const col0 = reinterpret_cast<__nv_bfloat16*>(p.out) + p.out_off + n;
         __nv_bfloat16* o = col0 + orow * p.ldo;
-        if (p.pool2) {  // (vec_ok and N % 32 == 0 checked by the plan): 64 B per pooled pixel
+        if constexpr ((TAPN & 4) != 0) {  // (vec_ok and N % 32 == 0 checked by the plan): 64 B per pooled pixel
           if (ok) {
             uint4* o4 = reinterpret_cast<uint4*>(o);
 #pragma unroll
@@ -1293,7 +1293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------- host side
 
-template <int BN, int TS, bool PAIR, bool TAPN = false, bool STEM = false>
+template <int BN, int TS, bool PAIR, int TAPN = 0, bool STEM = false>
 static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int grid,
                              cudaStream_t stream) {
@@ -1324,20 +1324,31 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
 
 int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
 
-template <int BN, int TS, bool PAIR, bool TAPN = false, bool STEM = false>
+template <int BN, int TS, bool PAIR, int TAPN = 0, bool STEM = false>
 static int stages_of(const ConvParams& p) {
   return make_layout<ConvSmem<BN, TS, PAIR, TAPN, STEM>>(p.resb, p.num_kb, p.a_mode, p.kbs).stages;
 }
 int conv_umma_stages(const ConvParams& p, int block_n) {
   const bool ts = p.a_mode == kAModeTapShift;
   if (p.a_mode == kAModeStemRows || p.a_mode == kAModeStemPlanes)
-    return block_n == 32 ? stages_of<32, 1, false, false, true>(p)
-           : block_n == 64 ? stages_of<64, 1, false, false, true>(p)
-           : block_n == 128 ? stages_of<128, 1, false, false, true>(p)
-                            : stages_of<256, 1, false, false, true>(p);
+    return block_n == 32 ? stages_of<32, 1, false, 0, true>(p)
+           : block_n == 64 ? stages_of<64, 1, false, 0, true>(p)
+           : block_n == 128 ? stages_of<128, 1, false, 0, true>(p)
+                            : stages_of<256, 1, false, 0, true>(p);
   if (p.a_mode == kAModeTapN) {
-    if (p.pair) return block_n == 32 ? stages_of<32, 1, true, true>(p) : stages_of<64, 1, true, true>(p);
-    return block_n == 32 ? stages_of<32, 1, false, true>(p) : stages_of<64, 1, false, true>(p);
+    if (p.pair) return block_n == 32 ? stages_of<32, 1, true, 1>(p) : stages_of<64, 1, true, 1>(p);
+    // TAPN template value: 1 = three planes, 2 = two (tap 2 folded by the MMA), +4 = fused pool
+    const int tv = (p.tapn2 ? 2 : 1) + (p.pool2 ? 4 : 0);
+    switch (tv + (block_n == 32 ? 0 : 8)) {
+      case 1: return stages_of<32, 1, false, 1>(p);
+      case 2: return stages_of<32, 1, false, 2>(p);
+      case 5: return stages_of<32, 1, false, 5>(p);
+      case 6: return stages_of<32, 1, false, 6>(p);
+      case 9: return stages_of<64, 1, false, 1>(p);
+      case 10: return stages_of<64, 1, false, 2>(p);
+      case 13: return stages_of<64, 1, false, 5>(p);
+      default: return stages_of<64, 1, false, 6>(p);
+    }
   }
   if (p.pair) {
     if (ts) return block_n == 64 ? stages_of<64, 3, true>(p) : stages_of<128, 3, true>(p);
@@ -1378,10 +1389,10 @@ cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const
   if (p.a_mode == kAModeStemRows || p.a_mode == kAModeStemPlanes) {
     if (p.mcast || p.pair) return cudaErrorInvalidValue;
     switch (block_n) {
-      case 32: return launch_bn<32, 1, false, false, true>(ma, mb, mo, mr, p, grid, stream);
-      case 64: return launch_bn<64, 1, false, false, true>(ma, mb, mo, mr, p, grid, stream);
-      case 128: return launch_bn<128, 1, false, false, true>(ma, mb, mo, mr, p, grid, stream);
-      case 256: return launch_bn<256, 1, false, false, true>(ma, mb, mo, mr, p, grid, stream);
+      case 32: return launch_bn<32, 1, false, 0, true>(ma, mb, mo, mr, p, grid, stream);
+      case 64: return launch_bn<64, 1, false, 0, true>(ma, mb, mo, mr, p, grid, stream);
+      case 128: return launch_bn<128, 1, false, 0, true>(ma, mb, mo, mr, p, grid, stream);
+      case 256: return launch_bn<256, 1, false, 0, true>(ma, mb, mo, mr, p, grid, stream);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -1389,15 +1400,27 @@ cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const
     if (p.pair) {
       if (!p.mcast || !p.resb) return cudaErrorInvalidValue;
       switch (block_n) {
-        case 32: return launch_bn<32, 1, true, true>(ma, mb, mo, mr, p, grid, stream);
-        case 64: return launch_bn<64, 1, true, true>(ma, mb, mo, mr, p, grid, stream);
+        case 32: return launch_bn<32, 1, true, 1>(ma, mb, mo, mr, p, grid, stream);
+        case 64: return launch_bn<64, 1, true, 1>(ma, mb, mo, mr, p, grid, stream);
         default: return cudaErrorInvalidValue;
       }
     }
     if (p.mcast) return cudaErrorInvalidValue;
     switch (block_n) {
-      case 32: return launch_bn<32, 1, false, true>(ma, mb, mo, mr, p, grid, stream);
-      case 64: return launch_bn<64, 1, false, true>(ma, mb, mo, mr, p, grid, stream);
+      case 32:
+      case 64: {
+        const int tv = (p.tapn2 ? 2 : 1) + (p.pool2 ? 4 : 0);
+        switch (tv + (block_n == 32 ? 0 : 8)) {
+          case 1: return launch_bn<32, 1, false, 1>(ma, mb, mo, mr, p, grid, stream);
+          case 2: return launch_bn<32, 1, false, 2>(ma, mb, mo, mr, p, grid, stream);
+          case 5: return launch_bn<32, 1, false, 5>(ma, mb, mo, mr, p, grid, stream);
+          case 6: return launch_bn<32, 1, false, 6>(ma, mb, mo, mr, p, grid, stream);
+          case 9: return launch_bn<64, 1, false, 1>(ma, mb, mo, mr, p, grid, stream);
+          case 10: return launch_bn<64, 1, false, 2>(ma, mb, mo, mr, p, grid, stream);
+          case 13: return launch_bn<64, 1, false, 5>(ma, mb, mo, mr, p, grid, stream);
+          default: return launch_bn<64, 1, false, 6>(ma, mb, mo, mr, p, grid, stream);
+        }
+      }
       default: return cudaErrorInvalidValue;
     }
   }

@@ -107,6 +107,7 @@ struct ConvParams {
   int stem_tma;              // stem modes: epilogue stores 32-pixel slabs with a clipped 3-D map
   int kbs;                   // stem modes: filter rows (64-wide K blocks) per pipeline stage
   int early_release;         // epilogue frees the accumulator right after its TMEM loads
+  int tapn_alt;              // taps-in-N, 64 columns: epilogue groups take alternate tiles
   int tapn2;                 // taps-in-N (unpaired): tap 2 folded into plane 0 by a 2-row A shift
   int pool2;                 // taps-in-N: 2x2/2 max-pool fused (out is the pooled tensor)
   int nseg, Ho2, Wo2;        // pool2: 60-column segments per row pair, pooled geometry

@@ -388,6 +388,11 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     if (mt2 * 120 > (1ll << 31) - 1) EB_FAIL(EB_E_INVALID, "conv M too large");
     pl.p.M = static_cast<int>(mt2 * 120);  // (the kernel derives its tile count as M / 120)
   }
+  // 64-column taps-in-N: the two epilogue groups take alternate tiles (each warp then has
+  // two independent 32-column chunks per tile to overlap) rather than splitting columns:
+  // B200, B = 256: 224x224 64->64 (+ fused pool) 1185 -> 1080 us, 56x56 72.6 -> 67.2 us
+  static const bool tapn_alt = env_flag("EB_TAPN_ALT", true);
+  pl.p.tapn_alt = tapn_alt ? 1 : 0;
   static const int dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
   pl.p.dbg = dbg;
   if (tapn) {
