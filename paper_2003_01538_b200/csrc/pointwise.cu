@@ -148,7 +148,7 @@ template <int CT>  // CT: channel count when known at compile time (3), else 0
 __global__ void __launch_bounds__(256)
     preprocess_u8_to_layout_kernel(const uint8_t* __restrict__ x, int B, int C_, int H, int W,
                                    const float* __restrict__ lut, int ph, int pw, int planes, int Hq,
-                                   int Wq, uint4* __restrict__ y) {
+                                   int Wq, int rpu, uint4* __restrict__ y) {
   const int C = CT ? CT : C_;
   // the LUT pre-rounded to bf16 (the value the output carries)
   __shared__ __nv_bfloat16 s_lut[8 * 256];
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256)
   for (int i = threadIdx.x; i < C * 256; i += blockDim.x) s_lut[i] = __float2bfloat16_rn(lut[i]);
   const int row_bytes = W * C;
   const bool staged = row_bytes <= kK1MaxRowBytes;
-  const int chunks = (Hq + kK1Rows - 1) / kK1Rows;
+  const int chunks = (Hq + rpu - 1) / rpu;
   const int units = B * chunks;
   const int nq = planes ? 2 : 1;
   const int warp = static_cast<int>(threadIdx.x) >> 5;
@@ -164,10 +164,10 @@ __global__ void __launch_bounds__(256)
   const __nv_bfloat16 zero = __float2bfloat16_rn(0.f);
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int b = u / chunks;
-    const int hq0 = (u - b * chunks) * kK1Rows;
+    const int hq0 = (u - b * chunks) * rpu;
     // input rows [ih0, ih1) of this unit that lie inside the image
     const int ih0 = max(hq0 - ph, 0);
-    const int ih1 = min(hq0 + kK1Rows - ph, H);
+    const int ih1 = min(hq0 + rpu - ph, H);
     const uint8_t* src = x + (static_cast<int64_t>(b) * H + ih0) * row_bytes;
     __syncthreads();  // (previous unit done with s_in; LUT staged)
     if (staged && ih1 > ih0) {
@@ -181,9 +181,9 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     // one warp per output row (plane q, padded row hq), 32 pixels per step
-    for (int qr = warp; qr < nq * kK1Rows; qr += 8) {
-      const int q = qr / kK1Rows;
-      const int hq = hq0 + (qr - q * kK1Rows);
+    for (int qr = warp; qr < nq * rpu; qr += 8) {
+      const int q = qr / rpu;
+      const int hq = hq0 + (qr - q * rpu);
       if (hq >= Hq) continue;
       const int ih = hq - ph;
       const bool hok = ih >= 0 && ih < H;
@@ -208,14 +208,17 @@ cudaError_t k_preprocess_u8_to_layout(const uint8_t* x, int B, int C, int H, int
                                       cudaStream_t s) {
   const int planes = mode == kAModeStemPlanes ? 1 : 0;
   if (B == 0 || Hq == 0 || Wq == 0) return cudaSuccess;
-  const int64_t units = static_cast<int64_t>(B) * ((Hq + kK1Rows - 1) / kK1Rows);
+  // rows per unit: kK1Rows, fewer when that would leave SMs idle (small batches)
+  int rpu = kK1Rows;
+  while (rpu > 1 && static_cast<int64_t>(B) * ((Hq + rpu - 1) / rpu) < 148 * 4) rpu /= 2;
+  const int64_t units = static_cast<int64_t>(B) * ((Hq + rpu - 1) / rpu);
   const int grid = static_cast<int>(std::min<int64_t>(units, 148 * 8));
   if (C == 3)
     preprocess_u8_to_layout_kernel<3><<<grid, 256, 0, s>>>(x, B, C, H, W, lut, ph, pw, planes, Hq,
-                                                           Wq, reinterpret_cast<uint4*>(y));
+                                                           Wq, rpu, reinterpret_cast<uint4*>(y));
   else
     preprocess_u8_to_layout_kernel<0><<<grid, 256, 0, s>>>(x, B, C, H, W, lut, ph, pw, planes, Hq,
-                                                           Wq, reinterpret_cast<uint4*>(y));
+                                                           Wq, rpu, reinterpret_cast<uint4*>(y));
   return cudaGetLastError();
 }
 
