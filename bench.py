@@ -445,7 +445,9 @@ def main() -> None:
             sweep[str(b)] = b * 10 / (s0.elapsed_time(s1) / 1e3)
 
     # ---- roofline of the tcgen05 conv/GEMM kernel class (serialised per-op profile)
-    ms = eng.profile(B, kind)
+    # per-op median of 3 serialised runs (an eager run's event times absorb any host-side
+    # launch hiccup of the op that follows it)
+    ms = np.median(np.stack([eng.profile(B, kind) for _ in range(3)]), axis=0)
     conv_ms = conv_flops = 0.0
     top = None
     for m, t in zip(eng.op_meta, ms):
