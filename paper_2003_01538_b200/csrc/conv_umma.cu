@@ -43,7 +43,10 @@ constexpr int kBlockK = 64;  // one 128-byte swizzle atom of bf16
 // warps).  Twelve warps cost no registers over ten: three warps per SM sub-partition
 // either way caps a thread at 168 registers.
 constexpr int kThreads = 384;
-constexpr int kXformThreads = 192;  // pre-activation transform: warps 6..11
+#ifndef EB_XFORM_THREADS
+#define EB_XFORM_THREADS 64
+#endif
+constexpr int kXformThreads = EB_XFORM_THREADS;  // pre-activation transform: the last warps
 constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels x 8 bf16
 
 // TS = filter taps consumed per pipeline stage: 1 (one TMA im2col load per tap)
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t_first = p.mcast ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
   const int t_step = p.mcast ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
   // warps 6..9 help with A (stem gather / pre-activation) or, otherwise, double the epilogue
-  const bool a_helper = p.a_mode == kAModeGatherC8 || p.pre_scale != nullptr;
+  const bool a_helper = p.a_mode == kAModeGatherC8 || (p.pre_scale != nullptr && kXformThreads > 64);
   const int n_epi = a_helper ? 4 : 8;
 
   if (p.a_mode == kAModeTapC8) {
@@ -1228,9 +1231,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // per stage (from an smem copy of the whole vector), and each warp's accesses
     // cover whole 128-byte rows (conflict-free).
     if constexpr (S::kPreMax > 0) {
-      const int t = static_cast<int>(threadIdx.x) - 192;  // 0 .. kXformThreads-1
+      const int t = static_cast<int>(threadIdx.x) - (kThreads - kXformThreads);  // 0 .. kXformThreads-1
       const int j = t & 7;
-      constexpr int kRowStep = kXformThreads / 8;         // 24 rows apart
+      constexpr int kRowStep = kXformThreads / 8;         // rows apart
       // scale/shift rounded to bf16 once (the math is bf16x2 FMA anyway)
       __nv_bfloat16* sc_s = reinterpret_cast<__nv_bfloat16*>(smem + L.pre_off);
       __nv_bfloat16* sh_s = sc_s + S::kPreMax;
@@ -1257,17 +1260,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           const __nv_bfloat162* sh2 = reinterpret_cast<const __nv_bfloat162*>(&tq);
           mbar_wait(&full[stage], phase);
           uint8_t* tile = ring_base + stage * L.stage_bytes;
+          // all of this thread's rows are loaded before any is stored (the loads are
+          // then in flight together; interleaved, each store fenced the next load)
+          constexpr int kRowsPer = (kBlockM + kRowStep - 1) / kRowStep;
+          static_assert(kRowStep % 8 == 0, "rows of one thread must share the 128B swizzle phase");
+          const int r0 = t >> 3;  // rows r0 + i * kRowStep share one swizzle phase
+          uint8_t* const col = tile + r0 * 128 + ((j ^ (r0 & 7)) * 16);
+          uint4 xs[kRowsPer];
 #pragma unroll
-          for (int i = 0; i < (dbg_probe(p, 3) ? 0 : (kBlockM + kRowStep - 1) / kRowStep); ++i) {
-            const int r = (t >> 3) + i * kRowStep;
-            if (r >= kBlockM) break;
-            uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + ((j ^ (r & 7)) * 16));
-            uint4 x = *q;
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&x);
+          for (int i = 0; i < kRowsPer; ++i)
+            if (r0 + i * kRowStep < kBlockM) xs[i] = *reinterpret_cast<const uint4*>(col + i * kRowStep * 128);
+#pragma unroll
+          for (int i = 0; i < kRowsPer; ++i) {
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&xs[i]);
 #pragma unroll
             for (int e = 0; e < 4; ++e) h[e] = __hfma2_relu(h[e], sc2[e], sh2[e]);
-            *q = x;
           }
+#pragma unroll
+          for (int i = 0; i < (dbg_probe(p, 3) ? 0 : kRowsPer); ++i)
+            if (r0 + i * kRowStep < kBlockM) *reinterpret_cast<uint4*>(col + i * kRowStep * 128) = xs[i];
           fence_proxy_async_smem();
           __syncwarp();
           if ((t & 31) == 0) mbar_arrive(&xfull[stage]);
