@@ -82,8 +82,11 @@ struct ConvSmem {
                                                                                     : 8 * kRowStageBytes)
                                    : (TS == 1 && !TAPN) ? 16 * kStageOutBytes
                                                         : 8 * kRowStageBytes;
+  // tall taps-in-N: per epilogue group, two tile-parity buffers of the boundary rows three
+  // lane quarters hand to the quarter above (96 floats each)
+  static constexpr int kXchBytes = (TAPN & 8) ? 2 * 2 * 3 * 96 * 4 : 0;
   // bias cache: 8 warps x BN floats
-  static constexpr int kEpiBytes = kRingArea + 8 * BN * 4 + 2 * kPreMax * 4;
+  static constexpr int kEpiBytes = kRingArea + 8 * BN * 4 + 2 * kPreMax * 4 + kXchBytes;
   // dynamic smem: everything (one CTA per SM); 1 KiB alignment slack + barrier block
   static constexpr int kBytes = 232448;
   static constexpr int kBarBytes = 1024;
@@ -98,7 +101,7 @@ struct ConvSmem {
 // (single N tile, short K) the weights are loaded once per CTA and the ring holds A only,
 // so the same space buys a deeper A pipeline.
 struct SmemLayout {
-  int resb_bytes, stage_bytes, stages, out_off, bias_off, pre_off, bar_off;
+  int resb_bytes, stage_bytes, stages, out_off, bias_off, pre_off, xch_off, bar_off;
 };
 // A bytes per stage: the stem modes stage one (rows) or two (planes) 136-pixel runs
 // A bytes per stage: the stem modes stage one (rows) or two (planes) 136-pixel runs per
@@ -112,18 +115,22 @@ __host__ __device__ inline int stem_a_bytes(int a_mode, int kbs) {
   return (b + 1023) / 1024 * 1024;
 }
 template <class S>
-__host__ __device__ inline SmemLayout make_layout(int resb, int num_kb, int a_mode, int kbs) {
+__host__ __device__ inline SmemLayout make_layout(const ConvParams& p) {
   SmemLayout L;
-  const int ab = stem_run_bytes(a_mode) ? stem_a_bytes(a_mode, kbs) : 0;
-  const int bb = S::kBBytes * (kbs > 0 ? kbs : 1);  // B bytes of one stage
-  L.resb_bytes = resb ? num_kb * bb : 0;
-  L.stage_bytes = (ab ? ab : S::kABytes * (kbs > 0 ? kbs : 1)) + (resb ? 0 : bb);
+  const int kbs = p.kbs > 0 ? p.kbs : 1;
+  // A bytes of one stage: stems their row runs; tall taps-in-N one tall_rows-row load per
+  // channel chunk (every filter row of it resident, kh B tiles per chunk)
+  const int ab = stem_run_bytes(p.a_mode) ? stem_a_bytes(p.a_mode, kbs) : p.tall_rows * 128 * kbs;
+  const int bb = S::kBBytes * kbs;  // B bytes of one stage
+  L.resb_bytes = p.resb ? p.num_kb * bb * (p.tall_rows ? p.taps / p.kw : 1) : 0;
+  L.stage_bytes = (ab ? ab : S::kABytes * kbs) + (p.resb ? 0 : bb);
   int st = (S::kBudget - S::kEpiBytes - L.resb_bytes) / L.stage_bytes;
   L.stages = st > S::kMaxStages ? S::kMaxStages : st;
   L.out_off = L.resb_bytes + L.stages * L.stage_bytes;
   L.bias_off = L.out_off + S::kRingArea;
   L.pre_off = L.bias_off + 8 * S::kBN * 4;
-  L.bar_off = L.pre_off + 2 * S::kPreMax * 4;
+  L.xch_off = L.pre_off + 2 * S::kPreMax * 4;
+  L.bar_off = L.xch_off + S::kXchBytes;
   return L;
 }
 // Persistent tile walk t = t_first, t_first + t_step, ...; t = (z * mtp + pm) * nt + tn.
@@ -248,10 +255,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (offset arithmetic on the __shared__ array keeps the address space visible to the
   // compiler, so staging accesses compile to STS/LDS rather than generic ST/LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const SmemLayout L = make_layout<S>(p.resb, p.num_kb, p.a_mode, p.kbs);
+  const SmemLayout L = make_layout<S>(p);
   constexpr bool stem_direct = STEM;  // a_mode is kAModeStemRows / kAModeStemPlanes
   const int kbs = p.kbs > 0 ? p.kbs : 1;  // 64-wide K blocks per stage (stems, taps-in-N)
-  const int a_stage = stem_direct ? stem_a_bytes(p.a_mode, kbs) : S::kABytes * kbs;  // B follows A
+  constexpr bool tall = (TAPN & 8) != 0;  // tall taps-in-N (one load per channel chunk)
+  const int a_chunk = tall ? p.tall_rows * 128 : S::kABytes;  // A bytes of one K block
+  const int a_stage = stem_direct ? stem_a_bytes(p.a_mode, kbs) : a_chunk * kbs;  // B follows A
   const int b_stage = S::kBBytes * kbs;
   uint8_t* const ring_base = smem + L.resb_bytes;  // stage s at ring_base + s * stage_bytes
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -265,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   trace_cta(p.trace, 0);
   const uint32_t warp = warp_id();
-  constexpr int kTileRows = TAPN ? 120 : kBlockM;  // output rows a tile advances
+  constexpr int kTileRows = tall ? 126 : TAPN ? 120 : kBlockM;  // output rows a tile advances
   constexpr int kAccCols = TAPN ? 3 * BN : BN;      // TMEM columns per accumulator
   constexpr int kTmemCols = 2 * kAccCols <= 32 ? 32 : 2 * kAccCols <= 64 ? 64 : 2 * kAccCols <= 128 ? 128
                           : 2 * kAccCols <= 256 ? 256 : 512;
@@ -363,7 +372,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (p.resb) {
         // resident B (single N tile): every K block's weights, once per CTA
         mbar_arrive_expect_tx(bres, L.resb_bytes);
-        for (int kb = 0; kb < p.num_kb * kbs; ++kb) {  // (stems: kbs K blocks per stage)
+        // (stems: kbs K blocks per stage; tall taps-in-N: kh filter rows per channel chunk)
+        const int n_res = p.num_kb * kbs * (tall ? p.taps / p.kw : 1);
+        for (int kb = 0; kb < n_res; ++kb) {
           uint8_t* sb = smem + kb * S::kBBytes;
           if (TAPN || TS > 1) {
             const int r = kb / p.cchunks;
@@ -416,7 +427,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // taps-in-N: receptive-field origins of the four 32-row quarter loads (per tile)
         int qw[4] = {0, 0, 0, 0}, qh[4] = {0, 0, 0, 0}, qi[4] = {0, 0, 0, 0};
-        if constexpr (TAPN) {
+        if constexpr (tall) {
+          // the tile's first grid position (rows of Ho + kh - 1 per image) at filter row 0
+          const int hwq = (p.Ho + p.taps / p.kw - 1) * p.Wp;
+          const int m0 = tile_m * kTileRows;
+          qi[0] = m0 / hwq;
+          const int rem = m0 - qi[0] * hwq;
+          qh[0] = rem / p.Wp;
+          qw[0] = rem - qh[0] * p.Wp - p.pw;
+          qh[0] -= p.ph;
+        } else if constexpr (TAPN) {
           if constexpr ((TAPN & 4) != 0) {
             // fused 2x2 max-pool: a tile is output rows 2r, 2r+1 x columns [60 sg, 60 sg + 60)
             // of one image; quarters 0/1 = row 2r (30 columns each), 2/3 = row 2r + 1
@@ -485,6 +505,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                   tma_load_im2col_4d_pair(sa + sub * S::kABytes + q * 4096, &map_a, fb, gc * kBlockK,
                                           qw[q], qh[q], qi[q], 0, static_cast<uint16_t>(r));
               }
+            } else if constexpr (tall) {
+              // one load per channel chunk: tall_rows grid positions at filter row 0; filter
+              // row r reads the same rows r * Wp further (B resident)
+              mbar_arrive_expect_tx(&full[stage], kbs * p.tall_rows * 128);
+              for (int sub = 0; sub < kbs; ++sub)
+                tma_load_im2col_4d(sa + sub * a_chunk, &map_a, &full[stage], (kb * kbs + sub) * kBlockK,
+                                   qw[0], qh[0], qi[0], 0, 0);
             } else {
             mbar_arrive_expect_tx(&full[stage], kbs * (4 * 32 * 128 + (p.resb ? 0 : S::kBBytes)));
             for (int sub = 0; sub < kbs; ++sub) {
@@ -685,6 +712,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           } else {
+          if constexpr (tall) {
+            // channel chunk cc's tall tile serves filter row r from r * Wp rows on; B of
+            // (r, cc) is resident tile r * cchunks + cc
+            const uint32_t wp16 = static_cast<uint32_t>(p.Wp) * 8;  // Wp rows of 128 B, 16 B units
+            const uint32_t bres16 = (smem_u32(smem) >> 4) & 0x3FFF;
+            for (int sub = 0; sub < kbs; ++sub) {
+              const int cc = kb * kbs + sub;
+#pragma unroll
+              for (int r = 0; r < 3; ++r) {
+                const uint64_t bt = b_desc_hi + bres16 + (r * p.cchunks + cc) * (S::kBBytes >> 4);
+#pragma unroll
+                for (int k = 0; k < kBlockK / 16; ++k) {
+                  const uint64_t adesc = a0 + sub * (a_chunk >> 4) + r * wp16 + 2 * k;
+                  const uint32_t accum = (kb > kb0 || sub > 0 || r > 0 || k > 0) ? 1u : 0u;
+                  umma_bf16(tmem_d, adesc, bt + 2 * k, idesc, accum);
+                }
+              }
+            }
+          } else
           for (int sub = 0; sub < kbs; ++sub) {  // (kbs > 1: taps-in-N only)
 #pragma unroll
           for (int s2 = 0; s2 < TS; ++s2) {
@@ -783,6 +829,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ow = 60 * sg + 30 * static_cast<int>(quarter & 1) + lane;
         ok = lane < 30 && !(lane & 1) && ow < p.Wo;
         orow = static_cast<size_t>(rowp) * p.Wo2 + (ow >> 1);
+      } else if constexpr (tall) {
+        // 126-row tiles of the (Ho + kh - 1) x Wp grid: every lane of quarters 0-2 and lanes
+        // 0-29 of quarter 3 own a grid position; the 2 extra rows per image are junk
+        const int m = tile_m * kTileRows + static_cast<int>(quarter) * 32 + lane;
+        const int img = fdiv(m, p.fd_img);
+        const int rem = m - img * static_cast<int>(p.fd_img.d);
+        const int oh = fdiv(rem, p.fd_row);
+        const int owp = rem - oh * p.Wp;
+        ok = (quarter < 3 || lane < 30) && m < p.M && oh < p.Ho && owp < p.Wo;
+        orow = (static_cast<size_t>(img) * p.Ho + oh) * p.Wo + owp;
       } else {
         const int m = tile_m * kTileRows + static_cast<int>(quarter) * 30 + lane;
         const int img = fdiv(m, p.fd_img);
@@ -819,7 +875,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // ((D0 + D1') + D2') + bias on fp32 pairs (FADD2), the shifted planes by shuffle
         float2 v2[16];
-        if constexpr (two) {
+        if constexpr (tall) {
+          // rows m+1, m+2 of lanes 31 / 30-31 live in the next quarter's warp: each quarter
+          // above 0 hands its lanes 0-1 of planes 1-2 down through smem (double-buffered by
+          // tile parity; one named barrier per tile and group)
+          float* xb = reinterpret_cast<float*>(smem + L.xch_off) + (half * 2 + ((j >> 1) & 1)) * 3 * 96;
+          if (quarter > 0 && lane < 2) {
+            float4* dst = reinterpret_cast<float4*>(xb + (quarter - 1) * 96);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (lane == 0)
+                dst[i] = make_float4(__uint_as_float(r1[4 * i]), __uint_as_float(r1[4 * i + 1]),
+                                     __uint_as_float(r1[4 * i + 2]), __uint_as_float(r1[4 * i + 3]));
+              dst[8 + 8 * lane + i] = make_float4(__uint_as_float(r2[4 * i]), __uint_as_float(r2[4 * i + 1]),
+                                                  __uint_as_float(r2[4 * i + 2]), __uint_as_float(r2[4 * i + 3]));
+            }
+          }
+          named_bar_sync(2 + half, 128);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            r1[i] = __shfl_down_sync(0xffffffffu, r1[i], 1);
+            r2[i] = __shfl_down_sync(0xffffffffu, r2[i], 2);
+          }
+          if (quarter < 3 && lane >= 30) {
+            const float4* src = reinterpret_cast<const float4*>(xb + quarter * 96);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (lane == 31) {
+                const float4 a = src[i];
+                r1[4 * i] = __float_as_uint(a.x);
+                r1[4 * i + 1] = __float_as_uint(a.y);
+                r1[4 * i + 2] = __float_as_uint(a.z);
+                r1[4 * i + 3] = __float_as_uint(a.w);
+              }
+              const float4 b = src[8 + 8 * (lane - 30) + i];
+              r2[4 * i] = __float_as_uint(b.x);
+              r2[4 * i + 1] = __float_as_uint(b.y);
+              r2[4 * i + 2] = __float_as_uint(b.z);
+              r2[4 * i + 3] = __float_as_uint(b.w);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            v2[i] = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(r0[2 * i]), __uint_as_float(r0[2 * i + 1])),
+                                          make_float2(__uint_as_float(r1[2 * i]), __uint_as_float(r1[2 * i + 1]))),
+                               make_float2(__uint_as_float(r2[2 * i]), __uint_as_float(r2[2 * i + 1])));
+        } else if constexpr (two) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float2 d1 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * i]), 1),
@@ -1337,7 +1438,7 @@ int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
 
 template <int BN, int TS, bool PAIR, int TAPN = 0, bool STEM = false>
 static int stages_of(const ConvParams& p) {
-  return make_layout<ConvSmem<BN, TS, PAIR, TAPN, STEM>>(p.resb, p.num_kb, p.a_mode, p.kbs).stages;
+  return make_layout<ConvSmem<BN, TS, PAIR, TAPN, STEM>>(p).stages;
 }
 int conv_umma_stages(const ConvParams& p, int block_n) {
   const bool ts = p.a_mode == kAModeTapShift;
@@ -1349,6 +1450,7 @@ int conv_umma_stages(const ConvParams& p, int block_n) {
   if (p.a_mode == kAModeTapN) {
     if (p.pair) return block_n == 32 ? stages_of<32, 1, true, 1>(p) : stages_of<64, 1, true, 1>(p);
     // TAPN template value: 1 = three planes, 2 = two (tap 2 folded by the MMA), +4 = fused pool
+    if (p.tall_rows) return block_n == 32 ? stages_of<32, 1, false, 9>(p) : 0;
     const int tv = (p.tapn2 ? 2 : 1) + (p.pool2 ? 4 : 0);
     switch (tv + (block_n == 32 ? 0 : 8)) {
       case 1: return stages_of<32, 1, false, 1>(p);
@@ -1420,6 +1522,9 @@ cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const
     switch (block_n) {
       case 32:
       case 64: {
+        if (p.tall_rows)
+          return block_n == 32 ? launch_bn<32, 1, false, 9>(ma, mb, mo, mr, p, grid, stream)
+                               : cudaErrorInvalidValue;
         const int tv = (p.tapn2 ? 2 : 1) + (p.pool2 ? 4 : 0);
         switch (tv + (block_n == 32 ? 0 : 8)) {
           case 1: return launch_bn<32, 1, false, 1>(ma, mb, mo, mr, p, grid, stream);

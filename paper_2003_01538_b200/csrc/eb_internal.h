@@ -107,6 +107,7 @@ struct ConvParams {
   int stem_tma;              // stem modes: epilogue stores 32-pixel slabs with a clipped 3-D map
   int kbs;                   // stem modes: filter rows (64-wide K blocks) per pipeline stage
   int early_release;         // epilogue frees the accumulator right after its TMEM loads
+  int tall_rows;             // tall taps-in-N: rows of the one A load per channel chunk (0: off)
   int tapn_alt;              // taps-in-N, 64 columns: epilogue groups take alternate tiles
   int tapn2;                 // taps-in-N (unpaired): tap 2 folded into plane 0 by a 2-row A shift
   int pool2;                 // taps-in-N: 2x2/2 max-pool fused (out is the pooled tensor)
@@ -155,7 +156,8 @@ bool encode_tiled_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint6
                           uint32_t b2, std::string* err, int swizzle_bytes = 128);
 bool encode_im2col_bf16(CUtensorMap* map, const void* base, int n, int h, int w, int c, int ldc,
                         int kh, int kw, int sh, int sw, int ph, int pw, int chans_per_pixel,
-                        int pixels, bool swizzle128, std::string* err, int upper_w_extra = 0);
+                        int pixels, bool swizzle128, std::string* err, int upper_w_extra = 0,
+                        int upper_h_extra = 0);
 
 void set_error(const std::string& msg);
 

@@ -141,6 +141,10 @@ bool resb_enabled() {
   static const bool on = env_flag("EB_RESB", true);
   return on;
 }
+bool tall_enabled() {
+  static const bool on = env_flag("EB_TAPN_TALL", true);
+  return on;
+}
 bool tapn_enabled() {
   static const bool on = env_flag("EB_TAPN", true);
   return on;
@@ -216,13 +220,31 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // 3x3 64->64 at 56x56 92 -> 83 us.
   const bool tapn = tap_shift && a.cout <= tapn_max_cout() && a.groups == 1 && !a.pre_scale && a.n_split == 0 &&
                     tapn_enabled();
+  // tall taps-in-N: one A load per channel chunk covers all kh filter rows (filter row r
+  // reads the same buffer r * Wp rows on), over a grid padded to Ho + kh - 1 rows per image
+  // so that the shifted rows stay inside their image; 126-row tiles, neighbouring quarters
+  // exchange their boundary rows in the epilogue.  For 32-column layers with more than one
+  // channel chunk (DenseNet growth convs) whose tall load fits one 256-row TMA box.
+  const int tall_wp = Wo + a.kw - 1;
+  const int tall_rows = (128 + (a.kh - 1) * tall_wp + 7) / 8 * 8;
+  // (not when its extra grid rows would add a wave of tiles: 7x7 images, 135 -> 165 tiles)
+  const int64_t tall_tiles = (static_cast<int64_t>(a.B) * (Ho + a.kh - 1) * tall_wp + 125) / 126;
+  const int64_t tapn_tiles = (static_cast<int64_t>(a.B) * Ho * tall_wp + 119) / 120;
+  // (and only while its resident weights -- kh x chunks x 12 KB -- leave room for two
+  // one-chunk stages: Cin <= 192)
+  const int64_t tall_smem = 3ll * ((a.cin + 63) / 64) * (3 * 32 * 128) + 2ll * tall_rows * 128 + 24 * 1024;
+  const bool tall = tapn && bn_guess == 32 && a.cin > 64 && !a.pool2 && a.kh == 3 && tall_rows <= 256 &&
+                    tall_smem <= 220 * 1024 &&
+                    (tall_tiles + num_sms() - 1) / num_sms() <= (tapn_tiles + num_sms() - 1) / num_sms() &&
+                    tall_enabled();
   // stem rows / planes: x is the padded layout of an 8-channel image (k_stem_relayout)
   const bool stem_direct = a.c8_stem == 2;
   StemGeom sg{};
   if (stem_direct && !stem_geom(a.B, a.H, a.W, a.kh, a.kw, a.sh, a.sw, a.ph, a.pw, &sg))
     EB_FAIL(EB_E_INVALID, "unsupported stem layout geometry");
   const int64_t M64 = stem_direct ? static_cast<int64_t>(a.B) * sg.Mi
-                                  : static_cast<int64_t>(a.B) * Ho * (tap_shift ? Wo + a.kw - 1 : Wo);
+                    : tall     ? static_cast<int64_t>(a.B) * (Ho + a.kh - 1) * tall_wp
+                               : static_cast<int64_t>(a.B) * Ho * (tap_shift ? Wo + a.kw - 1 : Wo);
   if (M64 > (1ll << 31) - 1) EB_FAIL(EB_E_INVALID, "conv M too large");
   const int M = static_cast<int>(M64);
   const int64_t kpad =
@@ -274,7 +296,8 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     // (taps-in-N: four 32-pixel loads); tiles walk the padded grid (Wo + 2 columns per
     // row, the 2 extra are dropped)
     if (!encode_im2col_bf16(&pl.ma, a.x, a.B, a.H, a.W, a.cin, a.ldx, a.kh, a.kw, a.sh, a.sw, a.ph,
-                            a.pw, 64, tapn ? 32 : 136, true, &err, a.kw - 1))
+                            a.pw, 64, tall ? tall_rows : tapn ? 32 : 136, true, &err, a.kw - 1,
+                            tall ? a.kh - 1 : 0))
       EB_FAIL(EB_E_INVALID, err);
     pl.p.a_mode = tapn ? kAModeTapN : kAModeTapShift;
     pl.p.Wp = Wo + a.kw - 1;
@@ -289,8 +312,10 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     EB_FAIL(EB_E_INVALID, err);
   // tap-shift stages cover all kw taps of one filter row; a grouped tile sees BN channels
   const int cin_tile = a.groups > 1 ? bn : a.cin;
-  const int num_kb = tap_shift ? a.kh * ((cin_tile + 63) / 64) : static_cast<int>(kpad / 64);
-  const int mt = (tapn && a.pool2) ? a.B * (Ho / 2) * ((Wo + 59) / 60)
+  const int num_kb = tall ? (cin_tile + 63) / 64
+                   : tap_shift ? a.kh * ((cin_tile + 63) / 64) : static_cast<int>(kpad / 64);
+  const int mt = tall ? (M + 125) / 126
+                 : (tapn && a.pool2) ? a.B * (Ho / 2) * ((Wo + 59) / 60)
                                    : tapn ? (M + 119) / 120 : (M + 127) / 128;
   const int nt = (a.cout + bn - 1) / bn;
   int splits = a.split_k;
@@ -363,7 +388,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     pl.p.fd_img = make_fastdiv(sg.Mi);
     pl.p.fd_row = make_fastdiv(sg.Wg);
   } else if (tap_shift) {
-    pl.p.fd_img = make_fastdiv(static_cast<uint32_t>(Ho) * (Wo + a.kw - 1));
+    pl.p.fd_img = make_fastdiv(static_cast<uint32_t>(tall ? Ho + a.kh - 1 : Ho) * (Wo + a.kw - 1));
     pl.p.fd_row = make_fastdiv(Wo + a.kw - 1);
   }
   static const bool early = env_flag("EB_EARLY_REL", true);
@@ -373,7 +398,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // more K blocks the layer is MMA-issue bound and the extra MMAs cost more.
   // EB_TAPN2: 0 off, 1 auto, 2 always
   static const int tapn2 = getenv("EB_TAPN2") ? atoi(getenv("EB_TAPN2")) : 1;
-  pl.p.tapn2 = (tapn && !pair && (tapn2 == 2 || (tapn2 == 1 && num_kb <= a.kh))) ? 1 : 0;
+  pl.p.tapn2 = (tapn && !tall && !pair && (tapn2 == 2 || (tapn2 == 1 && num_kb <= a.kh))) ? 1 : 0;
   if (a.pool2) {
     // fused max-pool (VGG): taps-in-N tiles re-cut as 2 output rows x 60 columns so that
     // each 2x2 window lies inside one tile
@@ -395,7 +420,21 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   pl.p.tapn_alt = tapn_alt ? 1 : 0;
   static const int dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
   pl.p.dbg = dbg;
-  if (tapn) {
+  if (tall) {
+    // tall: the whole tile (every channel chunk) per stage when two such stages fit beside
+    // the resident weights, else one chunk per stage
+    ConvParams q = pl.p;
+    q.tall_rows = tall_rows;
+    q.resb = 1;
+    q.kbs = num_kb;
+    q.num_kb = q.kb_per_split = 1;
+    if (conv_umma_stages(q, bn) < 2) {
+      q.kbs = 1;
+      q.num_kb = q.kb_per_split = num_kb;
+    }
+    if (conv_umma_stages(q, bn) < 2) EB_FAIL(EB_E_INVALID, "tall taps-in-N does not fit shared memory");
+    pl.p = q;
+  } else if (tapn) {
     // taps-in-N: several K blocks per stage (one 4-MMA K block at N = 3*Cout is only a few
     // hundred cycles of tensor work, less than a stage's fixed sync cost); kbs divides
     // the kh*cchunks K blocks
@@ -446,7 +485,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   }
   // Resident B: with a single N tile every CTA re-streams the same weights per tile; keep
   // them in smem instead when they fit and the A ring stays deep (it gets all the space).
-  if (resb_enabled() && nt == 1 && splits == 1 && !mcast && !stem_whole) {
+  if (resb_enabled() && nt == 1 && splits == 1 && !mcast && !stem_whole && !tall) {
     const int s_stream = conv_umma_stages(pl.p, bn);
     pl.p.resb = 1;
     const int s_res = conv_umma_stages(pl.p, bn);

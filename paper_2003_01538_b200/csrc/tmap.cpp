@@ -98,7 +98,8 @@ bool encode_tiled_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint6
 
 bool encode_im2col_bf16(CUtensorMap* map, const void* base, int n, int h, int w, int c, int ldc,
                         int kh, int kw, int sh, int sw, int ph, int pw, int chans_per_pixel,
-                        int pixels, bool swizzle128, std::string* err, int upper_w_extra) {
+                        int pixels, bool swizzle128, std::string* err, int upper_w_extra,
+                        int upper_h_extra) {
   if (!resolve(err)) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w),
                         static_cast<cuuint64_t>(h), static_cast<cuuint64_t>(n)};
@@ -106,7 +107,8 @@ bool encode_im2col_bf16(CUtensorMap* map, const void* base, int n, int h, int w,
   cuuint64_t strides[3] = {px, px * w, px * w * h};
   int lower[2] = {-pw, -ph};                       // [W, H]
   // upper_w_extra widens the traversal in W (tap-shift mode walks W + 2*pw positions)
-  int upper[2] = {pw - (kw - 1) + upper_w_extra, ph - (kh - 1)};   // [W, H]
+  // (and upper_h_extra in H: tall taps-in-N walks Ho + kh - 1 rows per image)
+  int upper[2] = {pw - (kw - 1) + upper_w_extra, ph - (kh - 1) + upper_h_extra};   // [W, H]
   cuuint32_t estr[4] = {1, static_cast<cuuint32_t>(sw), static_cast<cuuint32_t>(sh), 1};
   CUresult r = g_im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
                         strides, lower, upper, static_cast<cuuint32_t>(chans_per_pixel),

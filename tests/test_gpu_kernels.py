@@ -83,6 +83,14 @@ CASES = [
     ("3x3c24ragged", 2, 9, 11, 40, 24, 3, 3, 1, 1, 1, 1),
     ("1x3c64", 2, 8, 8, 96, 64, 1, 3, 1, 1, 0, 1),
     ("3x3c64big", 4, 30, 30, 64, 64, 3, 3, 1, 1, 1, 1),
+    # tall taps-in-N (Cout 32, Cin > 64, one load per channel chunk): 7x7 tail images,
+    # a ragged second chunk, 4 chunks, and the widest grid one 256-row box covers (Wp = 64)
+    ("tall7", 5, 7, 7, 256, 32, 3, 3, 1, 1, 1, 1),
+    ("tall14c96", 3, 14, 14, 96, 32, 3, 3, 1, 1, 1, 1),
+    ("tall28c256", 2, 28, 28, 256, 32, 3, 3, 1, 1, 1, 1),
+    ("tallWp64", 2, 10, 62, 128, 32, 3, 3, 1, 1, 1, 1),
+    ("tallWp66", 2, 6, 64, 128, 32, 3, 3, 1, 1, 1, 1),
+    ("tallc512", 2, 14, 14, 512, 32, 3, 3, 1, 1, 1, 1),  # weights too large: regular taps-in-N
 ]
 
 
@@ -504,7 +512,15 @@ def test_conv_maxpool2_fused_bit_exact(case):
     assert (b[:guard] == SENT).all() and (b[guard + n:] == SENT).all(), "write outside the tensor"
     yy = y.cpu()
     assert (yy[..., :off].float() == SENT).all() and (yy[..., off + cout:].float() == SENT).all()
-    assert torch.equal(yy[..., off:off + cout], ref.cpu()), "fused pool differs from conv + pool"
+    got = yy[..., off:off + cout]
+    if cin > 64 and cout == 32:
+        # a standalone conv of this class runs the tall taps-in-N mode, whose MMAs sum the
+        # filter rows in another order than the fused kernel's: compare with fp32 instead
+        r = F.max_pool2d(ref_conv(x, cin, w, bias.cpu(), None, True, 3, 3, 1, 1, 1, 1).permute(0, 3, 1, 2), 2)
+        err = (got.float() - r.permute(0, 2, 3, 1)).abs().max().item()
+        assert err <= 0.02 * r.abs().max().item() + 1e-2, err
+    else:
+        assert torch.equal(got, ref.cpu()), "fused pool differs from conv + pool"
 
 
 def test_conv_maxpool2_rejects_unsupported():
