@@ -218,7 +218,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // taps-in-N: small Cout (the MMA would otherwise re-read A from smem per 32 columns).
   // Measured on B200 (B=256): 3x3 128->32 at 56x56 152 -> 105 us, at 28x28 45 -> 32 us;
   // 3x3 64->64 at 56x56 92 -> 83 us.
-  const bool tapn = tap_shift && a.cout <= tapn_max_cout() && a.groups == 1 && !a.pre_scale && a.n_split == 0 &&
+  const bool tapn = tap_shift && a.cout <= std::min(64, tapn_max_cout()) && a.groups == 1 && !a.pre_scale && a.n_split == 0 &&
                     tapn_enabled();
   // tall taps-in-N: one A load per channel chunk covers all kh filter rows (filter row r
   // reads the same buffer r * Wp rows on), over a grid padded to Ho + kh - 1 rows per image
@@ -491,8 +491,13 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     const int s_res = conv_umma_stages(pl.p, bn);
     const int64_t rb = static_cast<int64_t>(pl.p.num_kb) * (pl.p.kbs > 1 ? pl.p.kbs : 1) *
                        (tap_shift ? 3 : 1) * bn * 128;
-    const int min_stages = pl.p.kbs > 1 ? 2 : 4;  // (multi-block stages are long)
-    if (rb > 112 * 1024 || s_res < min_stages || s_res < s_stream) pl.p.resb = 0;
+    // (up to 160 KB of weights when at least three A stages stay: VGG conv2_1, 112x112
+    // 64->128 tap-shift, 147 KB resident, 464 -> 418 us -- streamed, each tile re-read 48 KB
+    // of B per filter row from L2)
+    static const int max_kb = getenv("EB_RESB_MAX_KB") ? atoi(getenv("EB_RESB_MAX_KB")) : 160;
+    static const int min_st = getenv("EB_RESB_MIN_STAGES") ? atoi(getenv("EB_RESB_MIN_STAGES")) : 3;
+    const int min_stages = pl.p.kbs > 1 ? 2 : min_st;  // (multi-block stages are long)
+    if (rb > max_kb * 1024 || s_res < min_stages || s_res < s_stream) pl.p.resb = 0;
   }
   if (mcast) {
     if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn / 2, &err))
