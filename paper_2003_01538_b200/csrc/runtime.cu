@@ -398,7 +398,10 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // more K blocks the layer is MMA-issue bound and the extra MMAs cost more.
   // EB_TAPN2: 0 off, 1 auto, 2 always
   static const int tapn2 = getenv("EB_TAPN2") ? atoi(getenv("EB_TAPN2")) : 1;
-  pl.p.tapn2 = (tapn && !tall && !pair && (tapn2 == 2 || (tapn2 == 1 && num_kb <= a.kh))) ? 1 : 0;
+  // (not with the fused pool, whose epilogue is lighter: three planes measured 999-1021 vs
+  // 1048-1111 us on VGG conv1_2 + pool1 -- the second MMA re-reads A from smem)
+  pl.p.tapn2 = (tapn && !tall && !pair &&
+                (tapn2 == 2 || (tapn2 == 1 && num_kb <= a.kh && !a.pool2))) ? 1 : 0;
   if (a.pool2) {
     // fused max-pool (VGG): taps-in-N tiles re-cut as 2 output rows x 60 columns so that
     // each 2x2 window lies inside one tile
