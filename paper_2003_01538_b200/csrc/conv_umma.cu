@@ -124,10 +124,12 @@ __host__ __device__ inline SmemLayout make_layout(const ConvParams& p) {
   const int bb = S::kBBytes * kbs;  // B bytes of one stage
   L.resb_bytes = p.resb ? p.num_kb * bb * (p.tall_rows ? p.taps / p.kw : 1) : 0;
   L.stage_bytes = (ab ? ab : S::kABytes * kbs) + (p.resb ? 0 : bb);
-  int st = (S::kBudget - S::kEpiBytes - L.resb_bytes) / L.stage_bytes;
+  int st = (S::kBudget - S::kEpiBytes + (p.ring_half ? S::kRingArea / 2 : 0) - L.resb_bytes) / L.stage_bytes;
   L.stages = st > S::kMaxStages ? S::kMaxStages : st;
   L.out_off = L.resb_bytes + L.stages * L.stage_bytes;
-  L.bias_off = L.out_off + S::kRingArea;
+  // (ring_half: plain tiles without a residual keep one chunk buffer per epilogue warp and
+  // give the other half of the ring to the A/B stages)
+  L.bias_off = L.out_off + (p.ring_half ? S::kRingArea / 2 : S::kRingArea);
   L.pre_off = L.bias_off + 8 * S::kBN * 4;
   L.xch_off = L.pre_off + 2 * S::kPreMax * 4;
   L.bar_off = L.xch_off + S::kXchBytes;
@@ -1040,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool alt_tiles = wide && NCH == 1;
     const int c_first = (wide && NCH > 1) ? half : 0;
     const int c_step = (wide && NCH > 1) ? 2 : 1;
-    const int nb = STEM ? 1 : wide ? 2 : 4;  // ring buffers per warp
+    const int nb = (STEM ? 1 : wide ? 2 : 4) >> (p.ring_half ? 1 : 0);  // ring buffers per warp
     uint8_t* ring = smem + L.out_off + ew * nb * S::kStageOutBytes;
     float* bias_s = reinterpret_cast<float*>(smem + L.bias_off) + ew * BN;
     uint64_t* rbar = rfull + ew * nb;
@@ -1220,7 +1222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             if (nb == 1)
               bulk_wait_read<0>();
-            else if (wide)
+            else if (nb == 2)
               bulk_wait_read<1>();
             else
               bulk_wait_read<3>();

@@ -108,6 +108,7 @@ struct ConvParams {
   int kbs;                   // stem modes: filter rows (64-wide K blocks) per pipeline stage
   int early_release;         // epilogue frees the accumulator right after its TMEM loads
   int tall_rows;             // tall taps-in-N: rows of the one A load per channel chunk (0: off)
+  int ring_half;             // plain tiles, no residual: half the epilogue ring (one buffer per warp)
   int tapn_alt;              // taps-in-N, 64 columns: epilogue groups take alternate tiles
   int tapn2;                 // taps-in-N (unpaired): tap 2 folded into plane 0 by a 2-row A shift
   int pool2;                 // taps-in-N: 2x2/2 max-pool fused (out is the pooled tensor)

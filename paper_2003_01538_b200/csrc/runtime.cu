@@ -142,8 +142,7 @@ bool resb_enabled() {
   return on;
 }
 bool tall_enabled() {
-  static const bool on = env_flag("EB_TAPN_TALL", true);
-  return on;
+  return env_flag("EB_TAPN_TALL", true);  // (read per plan: tests pin the mode of a reference conv)
 }
 bool tapn_enabled() {
   static const bool on = env_flag("EB_TAPN", true);
@@ -397,7 +396,8 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // where the epilogue bounds the layer (one 64-channel K block per filter row); with
   // more K blocks the layer is MMA-issue bound and the extra MMAs cost more.
   // EB_TAPN2: 0 off, 1 auto, 2 always
-  static const int tapn2 = getenv("EB_TAPN2") ? atoi(getenv("EB_TAPN2")) : 1;
+  // (read per plan, not cached: tests pin the plane mode of a reference conv)
+  const int tapn2 = getenv("EB_TAPN2") ? atoi(getenv("EB_TAPN2")) : 1;
   // (not with the fused pool, whose epilogue is lighter: three planes measured 999-1021 vs
   // 1048-1111 us on VGG conv1_2 + pool1 -- the second MMA re-reads A from smem)
   pl.p.tapn2 = (tapn && !tall && !pair &&
@@ -419,6 +419,13 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // 64-column taps-in-N: the two epilogue groups take alternate tiles (each warp then has
   // two independent 32-column chunks per tile to overlap) rather than splitting columns:
   // B200, B = 256: 224x224 64->64 (+ fused pool) 1185 -> 1080 us, 56x56 72.6 -> 67.2 us
+  // pre-activation 1x1 convs (DenseNet): one epilogue chunk buffer per warp, the other half
+  // of the ring to the A/B stages (their ring is short -- B streams with A): 56x56 224->128
+  // 109 -> 93 us, 28x28 480->128 54 -> 50 us; plain 1x1 convs without the transform were
+  // measured neutral (BN 128) or slower (BN 64: 81 -> 89 us)
+  static const bool ring_half = env_flag("EB_RING_HALF", true);
+  pl.p.ring_half = (ring_half && a.pre_scale && plain_a && !a.res && !a.out_f32 && a.n_split == 0 &&
+                    !pair && !mcast && bn <= 128) ? 1 : 0;
   static const bool tapn_alt = env_flag("EB_TAPN_ALT", true);
   pl.p.tapn_alt = tapn_alt ? 1 : 0;
   static const int dbg = getenv("EB_DBG") ? atoi(getenv("EB_DBG")) : 0;
