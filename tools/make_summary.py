@@ -47,7 +47,7 @@ L += ["", "Template arguments of `conv_umma_kernel<BN, TS, PAIR, TAPN, STEM>`: N
       "## ncu captures (single layers, `ncu --set full --clock-control none`)", "",
       "| layer | mode | duration | tensor pipe active | UTC HMMA of peak | smem LSU wavefronts of peak | DRAM read / write |",
       "|---|---|---|---|---|---|---|",
-      "| 224², 64→64, 3×3 + 2×2 max-pool (top launch) | taps-in-N, two planes, fused pool, alternate-tile epilogue | 0.97 ms | 40.9 % | 56.1 % | 55.7 % (tensor-core smem reads 65.4 %) | 1.64 / 0.40 GB |",
+      "| 224², 64→64, 3×3 + 2×2 max-pool (top launch) | taps-in-N, three planes, fused pool, alternate-tile epilogue | 0.96 ms | 48.1 % | 58.5 % | 71.3 % (tensor-core smem reads 48.8 %) | 1.70 / 0.40 GB |",
       "| same layer before this round's fusion (conv only, pool separate) | taps-in-N, three planes | 1.07 ms | 39.8 % | 52.9 % | 54.3 % | 2.91 / 1.62 GB |",
       "| 28², 512→512, 3×3 | 2-SM MMA | 0.60 ms | 62.2 % | 85.0 % | 2.8 % | 0.21 / 0.17 GB |", "",
       "Files: `top_224_tapn_pool.ncu-rep` (+ `ncu_top_224_tapn_pool_details.csv`), `top_224_tapn.ncu-rep` "
