@@ -605,6 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (p.a_mode == kAModeStemPlanes)
                 tma_load_2d(sa + r * run + kStemPlaneOff, &map_a, &full[stage], 0, line + stem_plane_lines);
             }
+            trace_ev(p.trace, 0, tr_n, 2);
           } else if (p.a_mode == kAModeTapC8) {
             // filter row kb: tap s brings 128 pixels x 8 channels (16 B) = the K group s
             // column of core matrices (2 KiB, no swizzle); groups s >= kw keep stale
