@@ -108,7 +108,8 @@ class Engine:
         d.shift_off = none if shift_off is None else shift_off
         check(self.lib.eb_add_op(self._h, byref(d)))
         self.n_ops += 1
-        self.op_meta.append(dict(meta or {}, kind=kind, lane=lane, src=src.id, dst=dst.id))
+        self.op_meta.append(dict(meta or {}, kind=kind, lane=lane, src=src.id, dst=dst.id,
+                                 res=res.id if res is not None else -1))
 
     def member(self, kind, logits: TRef, k_off: int, k: int):
         check(self.lib.eb_add_member(self._h, kind, logits.id, k_off, k))

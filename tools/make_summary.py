@@ -54,5 +54,41 @@ L += ["", "Template arguments of `conv_umma_kernel<BN, TS, PAIR, TAPN, STEM>`: N
       "(+ `ncu_top_224_tapn_details.csv`), `ncu_pair_28_512_details.csv`, "
       "`top_launch_ncu.json` (the traffic figure bench.py reports); captures of earlier iterations: "
       "`top_3x3_28.ncu-rep`, `ncu_top_*_details.csv`.", ""]
+# per-layer rooflines from the serialised per-op profile (bench_per_op_profile.json):
+# algorithmic FLOPs and bytes (input + output activations + weights, bf16) per conv launch
+peaks = json.load(open("MEASURED_PEAKS.json")) if Path("MEASURED_PEAKS.json").exists() else {}
+tf_peak = peaks.get("bf16_tflops", 1661.4)  # (burst: each launch is timed alone)
+bw_peak = peaks.get("hbm_gbs", 6533.8)
+ops = json.load(open(R / "bench_per_op_profile.json"))
+B = d["config"]["batch_per_gpu"]
+rows_rl = []
+for o in ops:
+    if o.get("name") != "conv" or not o.get("ms"):
+        continue
+    ho, wo, co, kh, kw, st, ci = o["shape"]
+    hi, wi = ho * st, wo * st
+    byts = 2 * B * (hi * wi * ci + ho * wo * co) + o.get("weight_bytes", 0)
+    if o.get("res", -1) >= 0:  # residual read
+        byts += 2 * B * ho * wo * co
+    fl = o["flops"] * B
+    sec = o["ms"] / 1e3
+    ai = fl / byts
+    ridge = tf_peak * 1e12 / (bw_peak * 1e9)
+    if ai >= ridge:
+        frac, bound, ach = fl / sec / 1e12 / tf_peak, "tensor", f"{fl / sec / 1e12:.0f} TF/s"
+    else:
+        frac, bound, ach = byts / sec / 1e9 / bw_peak, "HBM", f"{byts / sec / 1e9:.0f} GB/s"
+    rows_rl.append((o["ms"], o["lane"], o["shape"], bound, ach, frac))
+rows_rl.sort(key=lambda r: -r[0])
+L += ["## Per-layer rooflines (top 20 conv launches of the per-op profile)", "",
+      f"Bound by arithmetic intensity against the ridge of the measured peaks ({tf_peak} TF/s burst, "
+      f"{bw_peak} GB/s); bytes = input + output activations + weights (bf16), each once. "
+      "Serialised eager launches (no lane overlap), median of 3 runs. VGG conv1_2 writes its "
+      "2×2-pooled output (¼ of the bytes counted here).", "",
+      "| ms | lane | layer (Ho, Wo, Cout, kh, kw, s, Cin) | bound | achieved | fraction of roof |",
+      "|---|---|---|---|---|---|"]
+for ms, lane, shp, bound, ach, frac in rows_rl[:20]:
+    L.append(f"| {ms:.3f} | {lane} | {tuple(shp)} | {bound} | {ach} | {frac:.2f} |")
+L.append("")
 (R / "SUMMARY.md").write_text("\n".join(L) + "\n")
 print("\n".join(L[:30]))
