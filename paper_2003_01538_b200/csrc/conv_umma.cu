@@ -114,13 +114,21 @@ __host__ __device__ inline int stem_a_bytes(int a_mode, int kbs) {
   const int b = stem_run_bytes(a_mode) * (kbs > 0 ? kbs : 1);
   return (b + 1023) / 1024 * 1024;
 }
+// stem stage A bytes: kbs row runs, or (tall stems) one stem_lines-line load per plane
+__host__ __device__ inline int stem_stage_bytes(const ConvParams& p, int kbs) {
+  if (p.stem_lines) {
+    const int b = p.stem_lines * 128 * (p.a_mode == kAModeStemPlanes ? 2 : 1);
+    return (b + 1023) / 1024 * 1024;
+  }
+  return stem_a_bytes(p.a_mode, kbs);
+}
 template <class S>
 __host__ __device__ inline SmemLayout make_layout(const ConvParams& p) {
   SmemLayout L;
   const int kbs = p.kbs > 0 ? p.kbs : 1;
   // A bytes of one stage: stems their row runs; tall taps-in-N one tall_rows-row load per
   // channel chunk (every filter row of it resident, kh B tiles per chunk)
-  const int ab = stem_run_bytes(p.a_mode) ? stem_a_bytes(p.a_mode, kbs) : p.tall_rows * 128 * kbs;
+  const int ab = stem_run_bytes(p.a_mode) ? stem_stage_bytes(p, kbs) : p.tall_rows * 128 * kbs;
   const int bb = S::kBBytes * kbs;  // B bytes of one stage
   L.resb_bytes = p.resb ? p.num_kb * bb * (p.tall_rows ? p.taps / p.kw : 1) : 0;
   L.stage_bytes = (ab ? ab : S::kABytes * kbs) + (p.resb ? 0 : bb);
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kbs = p.kbs > 0 ? p.kbs : 1;  // 64-wide K blocks per stage (stems, taps-in-N)
   constexpr bool tall = (TAPN & 8) != 0;  // tall taps-in-N (one load per channel chunk)
   const int a_chunk = tall ? p.tall_rows * 128 : S::kABytes;  // A bytes of one K block
-  const int a_stage = stem_direct ? stem_a_bytes(p.a_mode, kbs) : a_chunk * kbs;  // B follows A
+  const int a_stage = stem_direct ? stem_stage_bytes(p, kbs) : a_chunk * kbs;  // B follows A
   const int b_stage = S::kBBytes * kbs;
   uint8_t* const ring_base = smem + L.resb_bytes;  // stage s at ring_base + s * stage_bytes
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
@@ -571,6 +579,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t abytes = p.a_mode == kAModeGatherC8 ? 0u
                                     : p.a_mode == kAModeTapC8
                                         ? static_cast<uint32_t>(p.kw * kTapC8Bytes)
+                                    : p.stem_lines ? static_cast<uint32_t>(p.stem_lines * 128 *
+                                                                           (p.a_mode == kAModeStemPlanes ? 2 : 1))
                                     : p.a_mode == kAModeStemRows   ? 2176u * kbs
                                     : p.a_mode == kAModeStemPlanes ? 4352u * kbs
                                                                    : static_cast<uint32_t>(S::kALoadBytes);
@@ -599,6 +609,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             // 8 pixels x 8 channels) of the padded layout; the next filter row is Wq
             // pixels further in both layouts
             const int run = stem_run_bytes(p.a_mode);
+            if (p.stem_lines) {
+              // tall stem: one load per plane covers every filter row of the tile (row r is
+              // Wq pixels = Wq / 8 lines further); the odd plane follows the even one
+              const int line = stem_line0 + kb * kbs * (p.Wq >> 3);
+              tma_load_2d(sa, &map_a, &full[stage], 0, line);
+              if (p.a_mode == kAModeStemPlanes)
+                tma_load_2d(sa + p.stem_lines * 128, &map_a, &full[stage], 0, line + stem_plane_lines);
+            } else
             for (int r = 0; r < kbs; ++r) {
               const int line = stem_line0 + (kb * kbs + r) * (p.Wq >> 3);
               tma_load_2d(sa + r * run, &map_a, &full[stage], 0, line);
@@ -675,8 +693,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ne = ((p.kw + 1) / 2 + 1) / 2;  // even taps -> K groups 0..3
       const int no = (p.kw / 2 + 1) / 2;        // odd taps  -> K groups 4..7
       kmask = ((1u << ne) - 1u) | (((1u << no) - 1u) << 2);
-      a_koff[2] = kStemPlaneOff / 16;
-      a_koff[3] = kStemPlaneOff / 16 + 2;
+      const uint32_t odd16 = p.stem_lines ? static_cast<uint32_t>(p.stem_lines * 8) : kStemPlaneOff / 16;
+      a_koff[2] = odd16;
+      a_koff[3] = odd16 + 2;
     }
     TileWalk tw;
     tw.init(t_first, t_step, nt, mtp);
@@ -704,7 +723,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t b0 = b_desc_hi | ((sb >> 4) & 0x3FFF);
           if constexpr (stem_direct) {
             // kbs filter rows per stage: row block r's run / B tile follow each other
-            const uint32_t run16 = stem_run_bytes(p.a_mode) >> 4;
+            const uint32_t run16 = p.stem_lines ? static_cast<uint32_t>(p.Wq) : stem_run_bytes(p.a_mode) >> 4;
             for (int r = 0; r < kbs; ++r) {
 #pragma unroll
               for (int k = 0; k < kBlockK / 16; ++k) {

@@ -107,6 +107,7 @@ struct ConvParams {
   int stem_tma;              // stem modes: epilogue stores 32-pixel slabs with a clipped 3-D map
   int kbs;                   // stem modes: filter rows (64-wide K blocks) per pipeline stage
   int early_release;         // epilogue frees the accumulator right after its TMEM loads
+  int stem_lines;            // tall stems: lines of the one load per plane (0: a load per filter row)
   int tall_rows;             // tall taps-in-N: rows of the one A load per channel chunk (0: off)
   int ring_half;             // plain tiles, no residual: half the epilogue ring (one buffer per warp)
   int tapn_alt;              // taps-in-N, 64 columns: epilogue groups take alternate tiles

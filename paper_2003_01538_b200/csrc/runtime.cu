@@ -492,6 +492,19 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
       pl.p = q;
       stem_whole = true;
     }
+    // tall stem: the whole filter's rows of a plane as ONE load (17 + (kh-1) * Wq/8 lines)
+    // instead of kh loads of 17 lines -- fewer TMA operations per tile
+    const int lines = 17 + (a.kh - 1) * (sg.Wq >> 3);
+    if (stem_whole && lines <= 256 && env_flag("EB_STEM_TALL", true)) {
+      ConvParams t = pl.p;
+      t.stem_lines = lines;
+      CUtensorMap mt;
+      if (conv_umma_stages(t, bn) >= 2 &&
+          encode_tiled_2d_bf16(&mt, a.x, 64, static_cast<uint64_t>(sg.bytes / 128), 64, 64, lines, &err, 0)) {
+        pl.p = t;
+        pl.ma = mt;
+      }
+    }
   }
   // Resident B: with a single N tile every CTA re-streams the same weights per tile; keep
   // them in smem instead when they fit and the A ring stays deep (it gets all the space).
