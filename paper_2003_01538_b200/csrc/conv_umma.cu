@@ -275,9 +275,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* const ring_base = smem + L.resb_bytes;  // stage s at ring_base + s * stage_bytes
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* empty = full + L.stages;
-  uint64_t* tfull = empty + L.stages;  // [2] accumulator ready
-  uint64_t* tempty = tfull + 2;          // [2] accumulator drained
-  uint64_t* rfull = tempty + 2;          // [4 warps][4] residual chunk landed in ring buffer
+  // TMEM accumulators: four when they fit the 512 columns (the MMA may then run up to three
+  // tiles ahead of a slow epilogue), else two
+  constexpr int kAccCols = TAPN ? 3 * BN : BN;  // TMEM columns per accumulator
+#ifndef EB_MAX_ACC
+#define EB_MAX_ACC 4
+#endif
+  constexpr int kNAcc = (EB_MAX_ACC >= 4 && 4 * kAccCols <= 512) ? 4 : 2;
+  uint64_t* tfull = empty + L.stages;  // [kNAcc] accumulator ready
+  uint64_t* tempty = tfull + kNAcc;      // [kNAcc] accumulator drained
+  uint64_t* rfull = tempty + kNAcc;      // [4 warps][4] residual chunk landed in ring buffer
   uint64_t* xfull = rfull + 16;          // [stages] A tile transformed (pre-activation)
   uint64_t* bres = xfull + L.stages;     // resident B landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
@@ -285,9 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   trace_cta(p.trace, 0);
   const uint32_t warp = warp_id();
   constexpr int kTileRows = tall ? 126 : TAPN ? 120 : kBlockM;  // output rows a tile advances
-  constexpr int kAccCols = TAPN ? 3 * BN : BN;      // TMEM columns per accumulator
-  constexpr int kTmemCols = 2 * kAccCols <= 32 ? 32 : 2 * kAccCols <= 64 ? 64 : 2 * kAccCols <= 128 ? 128
-                          : 2 * kAccCols <= 256 ? 256 : 512;
+  constexpr int kAccAll = kNAcc * kAccCols;
+  constexpr int kTmemCols = kAccAll <= 32 ? 32 : kAccAll <= 64 ? 64 : kAccAll <= 128 ? 128
+                          : kAccAll <= 256 ? 256 : 512;
   const int mt = (p.M + kTileRows - 1) / kTileRows;
   const int nt = (p.N + BN - 1) / BN;
   const int splits = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
@@ -324,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // multicast: both CTAs' MMAs free a slot; PAIR: the leader's MMAs free it in both
       mbar_init(&empty[s], (p.mcast && !PAIR) ? 2 : 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kNAcc; ++a) {
       mbar_init(&tfull[a], 1);
       // arrivals that drain one accumulator: the epilogue warps that read it (8 when the
       // two epilogue groups split each tile's chunks), doubled in PAIR mode where the
@@ -704,9 +711,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int z = tw.z;
       const int kb0 = z * p.kb_per_split;
       const int kb1 = min(kb0 + p.kb_per_split, p.num_kb);
-      const int acc = j & 1;
+      const int acc = j % kNAcc;
       const uint32_t tmem_d = tmem_base + acc * kAccCols;
-      mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      mbar_wait(&tempty[acc], ((j / kNAcc) & 1) ^ 1);
       if (lane_id() == 0) trace_ev(p.trace, 1, tr_n, 10);
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb) {
@@ -839,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         cached_n = tw.tn;
       }
-      const int acc = j & 1;
+      const int acc = j % kNAcc;
       const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
       bool ok;
       size_t orow;
@@ -872,7 +879,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int n_tile0 = tw.tn * BN;
       if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 20);
-      mbar_wait(&tfull[acc], (j >> 1) & 1);
+      mbar_wait(&tfull[acc], (j / kNAcc) & 1);
       if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 21);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * kAccCols + ((quarter * 32) << 16);
@@ -1082,7 +1089,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tile_n = tw.tn;
       const int tile_m = p.mcast ? 2 * tw.pm + static_cast<int>(crank) : tw.pm;
       const int z = tw.z;
-      const int acc = j & 1;
+      const int acc = j % kNAcc;
       const int m = tile_m * kBlockM + row;
       bool row_ok = m < p.M;
       size_t orow = static_cast<size_t>(m);
@@ -1116,7 +1123,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 20);
-      mbar_wait(&tfull[acc], (j >> 1) & 1);
+      mbar_wait(&tfull[acc], (j / kNAcc) & 1);
       if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 21);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + ((quarter * 32) << 16);
