@@ -43,7 +43,9 @@ for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     L.append(f"| `{k}` | {v[0]} | {v[1]:.3f} |")
 L.append(f"| **total** | {sum(v[0] for v in agg.values())} | **{sum(v[1] for v in agg.values()):.3f}** |")
 L += ["", "Template arguments of `conv_umma_kernel<BN, TS, PAIR, TAPN, STEM>`: N tile, taps per stage "
-      "(3 = tap-shift), 2-SM MMA, taps-in-N, stem rows/planes.", "",
+      "(3 = tap-shift), 2-SM MMA, taps-in-N variant (1 = three planes, 2 = two planes with tap 2 "
+      "folded by the MMA, +4 = fused 2×2 max-pool, +8 = tall: one load per channel chunk), "
+      "stem rows/planes.", "",
       "## ncu captures (single layers, `ncu --set full --clock-control none`)", "",
       "| layer | mode | duration | tensor pipe active | UTC HMMA of peak | smem LSU wavefronts of peak | DRAM read / write |",
       "|---|---|---|---|---|---|---|",
