@@ -524,7 +524,16 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
     Vec8 acc;
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc.v[j] = 0.f;
-    // 8 pixels' loads in flight per step (the sum keeps its sequential order)
+    // 8 pixels' loads in flight per step (the sum keeps its sequential order); the BN-ReLU
+    // constants of the thread's 8 channels are loaded once
+    float sc[8], sh[8];
+    if (scale) {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        sc[jj] = __ldg(scale + c + jj);
+        sh[jj] = __ldg(shift + c + jj);
+      }
+    }
     const __nv_bfloat16* xb = x + b * HW * ldx + c;
     for (int p0 = 0; p0 < HW; p0 += 8) {
       uint4 q[8];
@@ -538,7 +547,10 @@ __global__ void gap_kernel(const __nv_bfloat16* __restrict__ x, int ldx,
         Vec8 v;
 #pragma unroll
         for (int j = 0; j < 8; ++j) v.v[j] = __bfloat162float(h[j]);
-        if (scale) bnrelu8(v, scale, shift, c);
+        if (scale) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v.v[j] = fmaxf(fmaf(v.v[j], sc[j], sh[j]), 0.f);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc.v[j] += v.v[j];
       }

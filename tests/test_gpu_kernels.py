@@ -541,3 +541,19 @@ def test_conv_maxpool2_rejects_unsupported():
                                   1, None) != 0
     assert lib.eb_k_conv_maxpool2(_p(x), 1, 7, 7, 64, 64, _p(wp), None, _p(y), 64, 0, 64, 3, 3, 1, 1,
                                   1, None) != 0
+
+
+def test_gap_with_bnrelu_prologue():
+    """Global average pool with the fused BN-ReLU prologue (DenseNet norm5 + relu + pool),
+    against fp32 torch on the same bf16 input."""
+    lib = _lib.load()
+    g = torch.Generator().manual_seed(77)
+    B, H, W, C = 3, 7, 7, 1024
+    x = torch.randn(B, H, W, C, generator=g).to(torch.bfloat16).to(DEV)
+    scale = (torch.rand(C, generator=g) + 0.5).to(DEV)
+    shift = (torch.randn(C, generator=g) * 0.2).to(DEV)
+    y = torch.empty(B, C, device=DEV, dtype=torch.bfloat16)
+    _lib.check(lib.eb_k_gap(_p(x), C, _p(y), B, H * W, C, _p(scale), _p(shift), None))
+    torch.cuda.synchronize()
+    ref = torch.relu(x.float() * scale + shift).mean(dim=(1, 2))
+    assert torch.allclose(y.float(), ref, atol=1e-2, rtol=1e-2)
