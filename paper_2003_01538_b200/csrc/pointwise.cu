@@ -635,11 +635,62 @@ __global__ void splitk_finalize_kernel(const float* __restrict__ ws, int splits,
   }
 }
 
+// 4 columns per thread (float4 partial loads, all slices' loads in flight together),
+// one wave of CTAs striding over the elements: the one-element-per-thread version was
+// bound by launching CTAs (FC 256 x 4096, 4 slices: 14.7 us)
+__global__ void __launch_bounds__(256)
+    splitk_finalize4_kernel(const float4* __restrict__ ws, int splits, int total4, int N4,
+                            const float* __restrict__ bias, int relu, void* out, int ldo,
+                            int out_off, int out_f32) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total4; i += gridDim.x * blockDim.x) {
+    const int m = i / N4;
+    const int n = (i - m * N4) * 4;
+    float4 v = ws[i];
+    for (int z = 1; z < splits; ++z) {
+      const float4 w = ws[static_cast<int64_t>(z) * total4 + i];
+      v.x += w.x;
+      v.y += w.y;
+      v.z += w.z;
+      v.w += w.w;
+    }
+    if (bias) {
+      v.x += bias[n];
+      v.y += bias[n + 1];
+      v.z += bias[n + 2];
+      v.w += bias[n + 3];
+    }
+    if (relu) {
+      v.x = fmaxf(v.x, 0.f);
+      v.y = fmaxf(v.y, 0.f);
+      v.z = fmaxf(v.z, 0.f);
+      v.w = fmaxf(v.w, 0.f);
+    }
+    const int64_t o = static_cast<int64_t>(m) * ldo + out_off + n;
+    if (out_f32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + o) = v;
+    } else {
+      __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&a);
+      u.y = *reinterpret_cast<uint32_t*>(&b);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + o) = u;
+    }
+  }
+}
+
 cudaError_t k_splitk_finalize(const float* ws, int splits, int64_t M, int N, const float* bias,
                               int relu, void* out, int ldo, int out_off, int out_f32,
                               cudaStream_t st) {
   const int64_t total = M * N;
   if (total == 0) return cudaSuccess;
+  if (N % 4 == 0 && ldo % 4 == 0 && out_off % 4 == 0 && total / 4 < (1ll << 31) &&
+      (reinterpret_cast<uintptr_t>(ws) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    const int total4 = static_cast<int>(total / 4);
+    const int grid = std::min((total4 + 255) / 256, 148 * 8);
+    splitk_finalize4_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(ws), splits, total4,
+                                                  N / 4, bias, relu, out, ldo, out_off, out_f32);
+    return cudaGetLastError();
+  }
   splitk_finalize_kernel<<<grid_for(total, 256), 256, 0, st>>>(ws, splits, M, N, bias, relu, out,
                                                                ldo, out_off, out_f32);
   return cudaGetLastError();
