@@ -51,8 +51,9 @@ L += ["", "Template arguments of `conv_umma_kernel<BN, TS, PAIR, TAPN, STEM>`: N
       "|---|---|---|---|---|---|---|",
       "| 224², 64→64, 3×3 + 2×2 max-pool (top launch) | taps-in-N, three planes, fused pool, alternate-tile epilogue | 0.96 ms | 48.1 % | 58.5 % | 71.3 % (tensor-core smem reads 48.8 %) | 1.70 / 0.40 GB |",
       "| same layer before this round's fusion (conv only, pool separate) | taps-in-N, three planes | 1.07 ms | 39.8 % | 52.9 % | 54.3 % | 2.91 / 1.62 GB |",
-      "| 28², 512→512, 3×3 | 2-SM MMA | 0.60 ms | 62.2 % | 85.0 % | 2.8 % | 0.21 / 0.17 GB |", "",
-      "Files: `top_224_tapn_pool.ncu-rep` (+ `ncu_top_224_tapn_pool_details.csv`), `top_224_tapn.ncu-rep` "
+      "| 28², 512→512, 3×3 | 2-SM MMA | 0.60 ms | 62.2 % | 85.0 % | 2.8 % | 0.21 / 0.17 GB |",
+      "| 56², 128→32, 3×3 (DenseNet growth) | tall taps-in-N (one load per channel chunk) | 0.067 ms | 52.6 % (HMMA subpipe) | 47.5 % | 38.3 % (tensor-core smem reads 55.4 %) | 0.21 / 0.04 GB |", "",
+      "Files: `top_224_tapn_pool.ncu-rep` (+ `ncu_top_224_tapn_pool_details.csv`), `growth56_tall.ncu-rep`, `top_224_tapn.ncu-rep` "
       "(+ `ncu_top_224_tapn_details.csv`), `ncu_pair_28_512_details.csv`, "
       "`top_launch_ncu.json` (the traffic figure bench.py reports); captures of earlier iterations: "
       "`top_3x3_28.ncu-rep`, `ncu_top_*_details.csv`.", ""]
