@@ -36,7 +36,9 @@ L = ["# Round 1 — measured evidence (B200, C2 = ResNet-50 + DenseNet-121 + VGG
      f"| reference arm (`--impl reference`) | {ref['value']:.1f} images/s |",
      f"| clocks during the timed region | median {d['clocks']['sm_mhz']} MHz of {d['clocks']['sm_max_mhz']}, reasons {d['clocks']['reasons']} ({d['clocks']['samples']} NVML samples) |",
      "", "The step runs under the B200 power cap (`sw_power_cap`), so its compute-bound layers run at the "
-     "clock the cap allows; box-to-box spread is about ±3 % on the full step.", "",
+     "clock the cap allows; box-to-box spread is about ±3 % on the full step (the same build measured "
+     "19.2k device images/s as the first run on a cool box at a 1942 MHz median, 18.3-18.5k later in "
+     "the same session at 1650-1770 MHz).", "",
      "## Where a step goes (ncu launch list, one step, kernels serialised by ncu)", "",
      "| kernel | launches | ms |", "|---|---|---|"]
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
