@@ -112,6 +112,14 @@ int eb_abi_version(void);
 /* Engine lifecycle.  The image geometry is the ensemble's shared input shape
  * (ensemble.py:202-208). */
 int eb_engine_create(int device, int max_batch, int in_c, int in_h, int in_w, eb_engine** out);
+/* Arithmetic precision of the CNN members, before any tensor or op is declared.
+ * EB_PREC_BF16 (default): bf16 activations and weights, fp32 accumulation, tcgen05.
+ * EB_PREC_F32: the fp32-faithful parity mode -- fp32 activations (tensors declared
+ * EB_F32, the K1 image included), fp32 weights packed [Cout][kh][kw][Cin/groups],
+ * every op on the CUDA cores with a sequential fp32 sum per output (SURVEY.md
+ * §7.3 (iii)); top-k equals the fp32 CPU oracle's up to summation order. */
+enum { EB_PREC_BF16 = 0, EB_PREC_F32 = 1 };
+int eb_engine_set_precision(eb_engine* e, int precision);
 int eb_engine_destroy(eb_engine* e);
 
 /* Normalisation: mean/std have 1 or C entries (models.py:247-253).  lut_u8 is

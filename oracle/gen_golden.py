@@ -120,14 +120,17 @@ def gen_lin1() -> None:
 
 CNN_SETS = {
     # name: (members [(arch, seed)], batch, size)
-    "c1": ([("resnet18", 1), ("densenet121", 2)], 8, 224),
-    "c2": ([("resnet50", 3), ("densenet121", 2), ("vgg16", 4)], 4, 224),
-    "inception": ([("inception_v3", 5)], 2, 299),
+    "c1": ([("resnet18", 1), ("densenet121", 2)], 32, 224),
+    "c2": ([("resnet50", 3), ("densenet121", 2), ("vgg16", 4)], 32, 224),
+    "inception": ([("inception_v3", 5)], 32, 299),
     # config 5: requests at 299 (the largest member); 224 members see a bilinear resize
     "c5": ([("resnet152", 6), ("densenet201", 7), ("vgg19", 8), ("inception_v3", 5),
-            ("resnext50_32x4d", 9)], 2, 299),
-    "resnext": ([("resnext50_32x4d", 9)], 4, 224),
+            ("resnext50_32x4d", 9)], 32, 299),
+    "resnext": ([("resnext50_32x4d", 9)], 32, 224),
 }
+# the bench workload itself (bench.py: C2, B = 256, synth.images_fast(256, seed0=1234)):
+# oracle logits of four of its rows
+BENCH_ROWS = (0, 127, 128, 255)
 
 
 def gen_cnn(names) -> None:
@@ -139,8 +142,12 @@ def gen_cnn(names) -> None:
 
     cnn.set_threads()
     for name in names:
-        members, b, size = CNN_SETS[name]
-        px = synth.images(b, size, size, 3, seed0=1234, kind="structured")
+        if name == "c2_bench":
+            members, size = CNN_SETS["c2"][0], 224
+            px = synth.images_fast(256, 224, 224, 3, seed0=1234)[list(BENCH_ROWS)]
+        else:
+            members, b, size = CNN_SETS[name]
+            px = synth.images(b, size, size, 3, seed0=1234, kind="structured")
         x = cnn.preprocess_u8(px, IMAGENET_MEAN, IMAGENET_STD, 255.0)
         logits = []
         for arch, seed in members:
@@ -153,8 +160,10 @@ def gen_cnn(names) -> None:
         np.savez_compressed(GOLDEN / f"cnn_{name}.npz", logits=arr,
                             archs=np.array([a for a, _ in members]),
                             seeds=np.array([s for _, s in members]),
-                            size=size, batch=b, seed0=1234, torch=torch.__version__)
-        print("wrote", name, arr.shape, "top1", arr.argmax(-1).tolist())
+                            size=size, batch=len(px), seed0=1234, torch=torch.__version__,
+                            rows=np.array(BENCH_ROWS if name == "c2_bench" else range(len(px))))
+        print("wrote", name, arr.shape, "distinct top1 per member",
+              [len(set(r.tolist())) for r in arr.argmax(-1)])
 
 
 if __name__ == "__main__":
@@ -166,4 +175,4 @@ if __name__ == "__main__":
     if a.lin1:
         gen_lin1()
     if a.cnn is not None:
-        gen_cnn(a.cnn or list(CNN_SETS))
+        gen_cnn(a.cnn or list(CNN_SETS) + ["c2_bench"])

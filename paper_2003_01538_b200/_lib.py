@@ -37,6 +37,7 @@ EB_OP_CONV, EB_OP_POOL, EB_OP_BNRELU, EB_OP_GAP, EB_OP_LIN1, EB_OP_RESIZE = 0, 1
 EB_POOL_MAX, EB_POOL_AVG, EB_POOL_AVG_EXCL_PAD = 0, 1, 2
 EB_POLICY_NONE, EB_POLICY_ANY, EB_POLICY_ALL, EB_POLICY_AT_LEAST = 0, 1, 2, 3
 EB_MEMBER_CNN, EB_MEMBER_LIN1 = 0, 1
+EB_PREC_BF16, EB_PREC_F32 = 0, 1
 EB_NO_OFFSET = (1 << 64) - 1
 
 
@@ -72,6 +73,7 @@ _SIGS = {
     "eb_abi_version": (c_int, []),
     "eb_engine_create": (c_int, [c_int, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
     "eb_engine_destroy": (c_int, [c_void_p]),
+    "eb_engine_set_precision": (c_int, [c_void_p, c_int]),
     "eb_set_preprocess": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "eb_pool_reserve": (c_int, [c_void_p, c_uint64]),
     "eb_pool_write": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64]),

@@ -46,4 +46,24 @@ cudaError_t k_combine(const float* l32, int ld32, const double* l64, int ld64, c
 cudaError_t k_lin1(const float* x, const float* w, const float* bias, double* part,
                    double* logits, int B, int K, int64_t D, int nsplit, cudaStream_t s);
 
+// fp32-faithful parity mode (ref32.cu): fp32 NHWC activations, CUDA-core kernels.
+cudaError_t k32_preprocess_u8(const uint8_t* x, float* y, int B, int C, int64_t plane, int cpad,
+                              const float* lut, cudaStream_t s);
+cudaError_t k32_preprocess_f32chw(const float* x, float* y, int B, int C, int64_t plane, int cpad,
+                                  const float* mean, const float* stdv, int nms, cudaStream_t s);
+cudaError_t k32_conv(const float* x, int B, int H, int W, int ldx, int cin, int groups,
+                     const float* w, const float* bias, const float* res, int ldr, float* y,
+                     int ldy, int y_off, float* y2, int ldy2, int y2_off, int n_split, int cout,
+                     int kh, int kw, int sh, int sw, int ph, int pw, int relu, int flatten,
+                     const float* pre_scale, const float* pre_shift, cudaStream_t s);
+cudaError_t k32_pool(const float* x, int ldx, float* y, int ldy, int y_off, int B, int H, int W,
+                     int C, int Ho, int Wo, int k, int s, int pad, int mode, const float* scale,
+                     const float* shift, cudaStream_t st);
+cudaError_t k32_bnrelu(const float* x, int ldx, float* y, int ldy, int64_t M, int C,
+                       const float* scale, const float* shift, cudaStream_t st);
+cudaError_t k32_gap(const float* x, int ldx, float* y, int B, int HW, int C, const float* scale,
+                    const float* shift, cudaStream_t st);
+cudaError_t k32_resize(const float* x, int ldx, float* y, int ldy, int B, int H, int W, int C,
+                       int Ho, int Wo, cudaStream_t st);
+
 }  // namespace eb

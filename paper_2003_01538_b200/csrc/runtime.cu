@@ -226,16 +226,17 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   // channel chunk (DenseNet growth convs) whose tall load fits one 256-row TMA box.
   const int tall_wp = Wo + a.kw - 1;
   const int tall_rows = (128 + (a.kh - 1) * tall_wp + 7) / 8 * 8;
-  // (not when its extra grid rows would add a wave of tiles: 7x7 images, 135 -> 165 tiles)
-  const int64_t tall_tiles = (static_cast<int64_t>(a.B) * (Ho + a.kh - 1) * tall_wp + 125) / 126;
-  const int64_t tapn_tiles = (static_cast<int64_t>(a.B) * Ho * tall_wp + 119) / 120;
+  // (not when its 2 extra grid rows per image cost more than ~12 % more tiles than the
+  // plain taps-in-N walk: 7x7 images, 135 -> 165 tiles at B = 256.  Decided from the
+  // per-image geometry only -- never from B -- because the two modes accumulate the
+  // K blocks in different orders and a sample's logits must not depend on its batch,
+  // SPEC.md:166,174)
+  const bool tall_pays = static_cast<int64_t>(Ho + a.kh - 1) * 120 * 100 <= static_cast<int64_t>(Ho) * 126 * 112;
   // (and only while its resident weights -- kh x chunks x 12 KB -- leave room for two
   // one-chunk stages: Cin <= 192)
   const int64_t tall_smem = 3ll * ((a.cin + 63) / 64) * (3 * 32 * 128) + 2ll * tall_rows * 128 + 24 * 1024;
   const bool tall = tapn && bn_guess == 32 && a.cin > 64 && !a.pool2 && a.kh == 3 && tall_rows <= 256 &&
-                    tall_smem <= 220 * 1024 &&
-                    (tall_tiles + num_sms() - 1) / num_sms() <= (tapn_tiles + num_sms() - 1) / num_sms() &&
-                    tall_enabled();
+                    tall_smem <= 220 * 1024 && tall_pays && tall_enabled();
   // stem rows / planes: x is the padded layout of an 8-channel image (k_stem_relayout)
   const bool stem_direct = a.c8_stem == 2;
   StemGeom sg{};
@@ -319,13 +320,19 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   const int nt = (a.cout + bn - 1) / bn;
   int splits = a.split_k;
   if (splits <= 0) {
+    // Split K only when one image's tile grid leaves most SMs idle AND each split keeps a
+    // long K loop: the partial slices cost an extra pass and a second launch.  The count
+    // is a function of the layer shape alone (one image's rows, N, K), never of B: split
+    // and unsplit sum K in different orders, and a sample's logits must be bitwise the
+    // same whatever batch it arrives in (eg/models.py:273-274).  Only
+    // layers with few rows per image qualify (FC layers, 7x7 maps): for those the
+    // partials stay small at any batch (EB_SPLIT_MAX_ROWS, default 64 rows per image).
     splits = 1;
-    const int64_t tiles = static_cast<int64_t>(mt) * nt;
-    // Split K only when the tile grid leaves most SMs idle AND each split keeps a long
-    // K loop: the partial slices cost an extra pass and a second launch (measured on
-    // B200: a 98-tile 7x7 layer is 3x slower split in two than unsplit).
-    if (!a.res && !tap_shift && tiles * 4 <= 148 && num_kb >= 32) {
-      splits = static_cast<int>(std::min<int64_t>(148 / tiles, num_kb / 16));
+    static const int max_rows = getenv("EB_SPLIT_MAX_ROWS") ? atoi(getenv("EB_SPLIT_MAX_ROWS")) : 64;
+    const int64_t rows_img = a.flatten ? 1 : static_cast<int64_t>(Ho) * Wo;
+    const int64_t tiles1 = ((rows_img + 127) / 128) * nt;
+    if (!a.res && !tap_shift && rows_img <= max_rows && tiles1 * 4 <= 148 && num_kb >= 32) {
+      splits = static_cast<int>(std::min<int64_t>(148 / tiles1, num_kb / 16));
       splits = std::max(1, std::min(splits, 32));
     }
   }
@@ -606,6 +613,7 @@ int run_conv_plan(ConvPlan& pl, float* ws, size_t ws_cap, const ConvArgs& a, cud
 struct eb_engine {
   int device = 0;
   int max_batch = 0;
+  bool f32 = false;  // EB_PREC_F32: fp32-faithful parity mode (ref32.cu)
   int C = 0, H = 0, W = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t lanes[kLanes] = {};
@@ -631,6 +639,7 @@ struct eb_engine {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_staged = nullptr, ev_stage_free = nullptr;
   float* ws[kLanes] = {};
+  size_t ws_floats[kLanes] = {};  // split-K partials, sized at finalize for max_batch
   double* lin_part = nullptr;
   int lin_nsplit = 1;
   int32_t* d_labels = nullptr;
@@ -664,6 +673,124 @@ namespace {
 
 bool is_prefork(const eb_op_desc& op) { return op.kind == EB_OP_RESIZE || op.prefork; }
 
+// The ConvArgs of a conv op at batch B.  *relayout_dst is set when the op reads the
+// padded stem layout of an 8-channel image (written by K1 or by k_stem_relayout).
+void conv_args_for(eb_engine* e, const eb_op_desc& op, int B, int fused_pool, ConvArgs* out,
+                   const void** relayout_dst) {
+  const uint8_t* pool = static_cast<const uint8_t*>(e->pool);
+  auto P = [&](uint64_t off) -> const void* {
+    return off == EB_NO_OFFSET ? nullptr : static_cast<const void*>(pool + off);
+  };
+  Tensor& src = e->tensors[op.src];
+  Tensor& dst = e->tensors[op.dst];
+  const size_t es = dsize(src.dtype);
+  const void* x = static_cast<const uint8_t*>(src.dev) + static_cast<size_t>(op.src_c_off) * es;
+  ConvArgs& a = *out;
+  a.x = x;
+  a.B = B;
+  a.H = src.h;
+  a.W = src.w;
+  a.ldx = src.c;
+  a.cin = op.src_c;
+  a.w = P(op.w_off);
+  a.bias = static_cast<const float*>(P(op.b_off));
+  if (op.res >= 0) {
+    a.res = e->tensors[op.res].dev;
+    a.ldr = e->tensors[op.res].c;
+  }
+  a.y = dst.dev;
+  a.ldy = dst.c;
+  a.y_off = op.dst_c_off;
+  a.cout = op.cout;
+  if (fused_pool >= 0) {  // the conv writes the pooled tensor of the absorbed pool op
+    const eb_op_desc& po = e->ops[fused_pool];
+    a.y = e->tensors[po.dst].dev;
+    a.ldy = e->tensors[po.dst].c;
+    a.y_off = po.dst_c_off;
+    a.pool2 = 1;
+  }
+  if (op.n_split > 0) {  // grouped launch: columns >= n_split go to dst2
+    const Tensor& d2 = e->tensors[op.dst2];
+    a.y2 = d2.dev;
+    a.ldy2 = d2.c;
+    a.y2_off = op.dst2_c_off;
+    a.n_split = op.n_split;
+  }
+  a.kh = op.kh;
+  a.kw = op.kw;
+  a.sh = op.sh;
+  a.sw = op.sw;
+  a.ph = op.ph;
+  a.pw = op.pw;
+  a.relu = op.relu;
+  a.out_f32 = dst.dtype == EB_F32;
+  // an 8-channel source is a (possibly resized) K1 image: stem mode -- relaid out into
+  // the padded rows / planes layout when this op owns such a scratch, else gathered
+  a.c8_stem = src.c == 8 && op.src_c == 8 && op.src_c_off == 0;
+  *relayout_dst = nullptr;
+  if (a.c8_stem) {
+    auto it = e->stem_buf.find(&op);
+    StemGeom g;
+    if (it != e->stem_buf.end() &&
+        stem_geom(B, src.h, src.w, op.kh, op.kw, op.sh, op.sw, op.ph, op.pw, &g)) {
+      *relayout_dst = it->second;
+      a.x = it->second;
+      a.c8_stem = 2;
+    }
+  }
+  a.flatten = op.flatten;
+  a.groups = op.groups > 1 ? op.groups : 1;
+  a.pre_scale = static_cast<const float*>(P(op.scale_off));
+  a.pre_shift = static_cast<const float*>(P(op.shift_off));
+}
+
+// One op of the fp32-faithful mode (ref32.cu) on stream ls.
+int enqueue_op_f32(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* launches) {
+  const uint8_t* pool = static_cast<const uint8_t*>(e->pool);
+  auto P = [&](uint64_t off) -> const float* {
+    return off == EB_NO_OFFSET ? nullptr : reinterpret_cast<const float*>(pool + off);
+  };
+  const Tensor& src = e->tensors[op.src];
+  const Tensor& dst = e->tensors[op.dst];
+  const float* x = static_cast<const float*>(src.dev) + op.src_c_off;
+  float* y = static_cast<float*>(dst.dev);
+  switch (op.kind) {
+    case EB_OP_CONV: {
+      const float* res = op.res >= 0 ? static_cast<const float*>(e->tensors[op.res].dev) : nullptr;
+      const int ldr = op.res >= 0 ? e->tensors[op.res].c : 0;
+      float* y2 = nullptr;
+      int ldy2 = 0;
+      if (op.n_split > 0) {
+        y2 = static_cast<float*>(e->tensors[op.dst2].dev);
+        ldy2 = e->tensors[op.dst2].c;
+      }
+      EB_CUDA(k32_conv(x, B, src.h, src.w, src.c, op.src_c, op.groups > 1 ? op.groups : 1, P(op.w_off),
+                       P(op.b_off), res, ldr, y, dst.c, op.dst_c_off, y2, ldy2, op.dst2_c_off,
+                       op.n_split, op.cout, op.kh, op.kw, op.sh, op.sw, op.ph, op.pw, op.relu,
+                       op.flatten, P(op.scale_off), P(op.shift_off), ls));
+      break;
+    }
+    case EB_OP_POOL:
+      EB_CUDA(k32_pool(x, src.c, y, dst.c, op.dst_c_off, B, src.h, src.w, op.src_c, dst.h, dst.w,
+                       op.kh, op.sh, op.ph, op.pool_mode, P(op.scale_off), P(op.shift_off), ls));
+      break;
+    case EB_OP_BNRELU:
+      EB_CUDA(k32_bnrelu(x, src.c, y + op.dst_c_off, dst.c, static_cast<int64_t>(B) * src.h * src.w,
+                         op.src_c, P(op.scale_off), P(op.shift_off), ls));
+      break;
+    case EB_OP_GAP:
+      EB_CUDA(k32_gap(x, src.c, y, B, src.h * src.w, op.src_c, P(op.scale_off), P(op.shift_off), ls));
+      break;
+    case EB_OP_RESIZE:
+      EB_CUDA(k32_resize(x, src.c, y, dst.c, B, src.h, src.w, op.src_c, dst.h, dst.w, ls));
+      break;
+    default:
+      EB_FAIL(EB_E_INVALID, "unknown op kind");
+  }
+  ++*launches;
+  return EB_OK;
+}
+
 // One op on stream ls.
 int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* launches) {
   const uint8_t* pool = static_cast<const uint8_t*>(e->pool);
@@ -677,69 +804,20 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
   Tensor& dst = e->tensors[op.dst];
   const size_t es = dsize(src.dtype);
   const void* x = static_cast<const uint8_t*>(src.dev) + static_cast<size_t>(op.src_c_off) * es;
+  if (e->f32 && op.kind != EB_OP_LIN1) return enqueue_op_f32(e, op, B, ls, launches);
   switch (op.kind) {
     case EB_OP_CONV: {
       ConvArgs a{};
-      a.x = x;
-      a.B = B;
-      a.H = src.h;
-      a.W = src.w;
-      a.ldx = src.c;
-      a.cin = op.src_c;
-      a.w = P(op.w_off);
-      a.bias = static_cast<const float*>(P(op.b_off));
-      if (op.res >= 0) {
-        a.res = e->tensors[op.res].dev;
-        a.ldr = e->tensors[op.res].c;
-      }
-      a.y = dst.dev;
-      a.ldy = dst.c;
-      a.y_off = op.dst_c_off;
-      a.cout = op.cout;
-      if (fused_pool >= 0) {  // the conv writes the pooled tensor of the absorbed pool op
-        const eb_op_desc& po = e->ops[fused_pool];
-        a.y = e->tensors[po.dst].dev;
-        a.ldy = e->tensors[po.dst].c;
-        a.y_off = po.dst_c_off;
-        a.pool2 = 1;
-      }
-      if (op.n_split > 0) {  // grouped launch: columns >= n_split go to dst2
-        const Tensor& d2 = e->tensors[op.dst2];
-        a.y2 = d2.dev;
-        a.ldy2 = d2.c;
-        a.y2_off = op.dst2_c_off;
-        a.n_split = op.n_split;
-      }
-      a.kh = op.kh;
-      a.kw = op.kw;
-      a.sh = op.sh;
-      a.sw = op.sw;
-      a.ph = op.ph;
-      a.pw = op.pw;
-      a.relu = op.relu;
-      a.out_f32 = dst.dtype == EB_F32;
-      // an 8-channel source is a (possibly resized) K1 image: stem mode -- relaid out into
-      // the padded rows / planes layout when this op owns such a scratch, else gathered
-      a.c8_stem = src.c == 8 && op.src_c == 8 && op.src_c_off == 0;
-      if (a.c8_stem) {
-        auto it = e->stem_buf.find(&op);
+      const void* relayout_dst = nullptr;
+      conv_args_for(e, op, B, fused_pool, &a, &relayout_dst);
+      if (relayout_dst && !(e->layouts_fused && op.src == EB_T_IMAGE_NHWC8)) {  // else K1 wrote it
         StemGeom g;
-        if (it != e->stem_buf.end() &&
-            stem_geom(B, src.h, src.w, op.kh, op.kw, op.sh, op.sw, op.ph, op.pw, &g)) {
-          if (!(e->layouts_fused && op.src == EB_T_IMAGE_NHWC8)) {  // else K1 wrote it
-            EB_CUDA(k_stem_relayout(static_cast<const __nv_bfloat16*>(x), B, src.h, src.w, op.ph,
-                                    op.pw, g.mode, g.Hq, g.Wq,
-                                    static_cast<__nv_bfloat16*>(it->second), ls));
-            ++*launches;
-          }
-          a.x = it->second;
-          a.c8_stem = 2;
-        }
+        stem_geom(B, src.h, src.w, op.kh, op.kw, op.sh, op.sw, op.ph, op.pw, &g);
+        EB_CUDA(k_stem_relayout(static_cast<const __nv_bfloat16*>(x), B, src.h, src.w, op.ph,
+                                op.pw, g.mode, g.Hq, g.Wq,
+                                static_cast<__nv_bfloat16*>(const_cast<void*>(relayout_dst)), ls));
+        ++*launches;
       }
-      a.flatten = op.flatten;
-      a.groups = op.groups > 1 ? op.groups : 1;
-      a.pre_scale = static_cast<const float*>(P(op.scale_off));
-      a.pre_shift = static_cast<const float*>(P(op.shift_off));
       ConvPlan pl;
       int rc = plan_conv(a, &pl);
       if (rc != EB_OK) return rc;
@@ -748,7 +826,7 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
         fprintf(stderr, "[eb] conv src=%d dst=%d mode=%d bn=%d grid=%d splits=%d M=%d N=%d kb=%d cl=%d pair=%d resb=%d\n",
                 op.src, op.dst, pl.p.a_mode, pl.block_n, pl.grid, pl.splits, pl.p.M, pl.p.N,
                 pl.p.num_kb, pl.p.mcast, pl.p.pair, pl.p.resb);
-      return run_conv_plan(pl, e->ws[op.stream], kSplitWsFloats, a, ls, launches);
+      return run_conv_plan(pl, e->ws[op.stream], e->ws_floats[op.stream], a, ls, launches);
     }
     case EB_OP_POOL: {
       const int Ho = conv_out(src.h, op.kh, op.sh, op.ph);
@@ -807,8 +885,17 @@ eb_engine* e, int input_kind, int B, int* launches) {
   Tensor& img8 = e->tensors[EB_T_IMAGE_NHWC8];
   Tensor& imgf = e->tensors[EB_T_IMAGE_F32];
   e->layouts_fused = false;
+  if (e->f32 && e->any_cnn) {
+    if (input_kind == EB_IN_U8_HWC)
+      EB_CUDA(k32_preprocess_u8(e->d_in_u8, static_cast<float*>(img8.dev), B, e->C, plane, 8,
+                                e->d_lut, s));
+    else
+      EB_CUDA(k32_preprocess_f32chw(e->d_in_f32, static_cast<float*>(img8.dev), B, e->C, plane, 8,
+                                    e->d_mean, e->d_std, e->nms, s));
+    ++*launches;
+  }
   if (input_kind == EB_IN_U8_HWC) {
-    if (e->any_cnn) {
+    if (e->any_cnn && !e->f32) {
       if (e->img8_needed) {
         EB_CUDA(k_preprocess_u8hwc_to_nhwc(e->d_in_u8, static_cast<__nv_bfloat16*>(img8.dev), B,
                                            e->C, plane, 8, e->d_lut, s));
@@ -834,7 +921,7 @@ eb_engine* e, int input_kind, int B, int* launches) {
       ++*launches;
     }
   } else {
-    if (e->any_cnn) {
+    if (e->any_cnn && !e->f32) {
       EB_CUDA(k_preprocess_f32chw_to_nhwc(e->d_in_f32, static_cast<__nv_bfloat16*>(img8.dev), B,
                                           e->C, plane, 8, e->d_mean, e->d_std, e->nms, s));
       ++*launches;
@@ -1002,6 +1089,16 @@ int eb_engine_create(int device, int max_batch, int in_c, int in_h, int in_w, eb
   return EB_OK;
 }
 
+int eb_engine_set_precision(eb_engine* e, int precision) {
+  if (!e) EB_FAIL(EB_E_INVALID, "null engine");
+  if (e->finalized || e->tensors.size() != 2 || !e->ops.empty())
+    EB_FAIL(EB_E_STATE, "precision must be set before tensors and ops are declared");
+  if (precision != EB_PREC_BF16 && precision != EB_PREC_F32) EB_FAIL(EB_E_INVALID, "unknown precision");
+  e->f32 = precision == EB_PREC_F32;
+  e->tensors[EB_T_IMAGE_NHWC8].dtype = e->f32 ? EB_F32 : EB_BF16;
+  return EB_OK;
+}
+
 int eb_engine_destroy(eb_engine* e) {
   if (!e) return EB_OK;
   cudaSetDevice(e->device);
@@ -1103,7 +1200,9 @@ int eb_add_op(eb_engine* e, const eb_op_desc* op) {
   if (op->src_c_off < 0 || op->src_c < 1 || op->src_c_off + op->src_c > src.c)
     EB_FAIL(EB_E_INVALID, "source channel slice out of range");
   if (op->kind == EB_OP_CONV) {
-    if (src.dtype != EB_BF16 || (dst.dtype != EB_BF16 && dst.dtype != EB_F32))
+    if (e->f32 ? (src.dtype != EB_F32 || dst.dtype != EB_F32 ||
+                  (op->res >= 0 && e->tensors[op->res].dtype != EB_F32))
+               : (src.dtype != EB_BF16 || (dst.dtype != EB_BF16 && dst.dtype != EB_F32)))
       EB_FAIL(EB_E_INVALID, "conv dtypes");
     if (op->dst_c_off < 0 || op->dst_c_off + op->cout > dst.c)
       EB_FAIL(EB_E_INVALID, "conv output slice out of range");
@@ -1117,13 +1216,15 @@ int eb_add_op(eb_engine* e, const eb_op_desc* op) {
       EB_FAIL(EB_E_INVALID, "channel slices must start at multiples of 8");
     if (dst.dtype == EB_BF16 && op->cout % 8 != 0)
       EB_FAIL(EB_E_INVALID, "bf16 conv outputs need cout % 8 == 0");
+    if (e->f32 && op->groups > 1 && (op->src_c % op->groups || op->cout % op->groups))
+      EB_FAIL(EB_E_INVALID, "grouped conv channels must divide by groups");
     if (op->res >= 0 && (e->tensors[op->res].h != dst.h || e->tensors[op->res].w != dst.w))
       EB_FAIL(EB_E_SHAPE, "residual geometry");
     if (op->n_split > 0) {
       if (op->dst2 < 0 || op->dst2 >= nt || op->res >= 0 || op->n_split >= op->cout)
         EB_FAIL(EB_E_INVALID, "grouped launch needs dst2 and no residual");
       const Tensor& d2 = e->tensors[op->dst2];
-      if (d2.h != dst.h || d2.w != dst.w || d2.dtype != EB_BF16 ||
+      if (d2.h != dst.h || d2.w != dst.w || d2.dtype != dst.dtype ||
           op->dst2_c_off + (op->cout - op->n_split) > d2.c || op->dst2_c_off % 8 != 0)
         EB_FAIL(EB_E_SHAPE, "grouped launch: second destination geometry");
     }
@@ -1131,10 +1232,12 @@ int eb_add_op(eb_engine* e, const eb_op_desc* op) {
     if (op->src != EB_T_IMAGE_F32 || dst.dtype != EB_F64 || dst.c != op->cout)
       EB_FAIL(EB_E_INVALID, "LIN1 op must read the f32 image and write fp64 scores");
   } else if (op->kind == EB_OP_RESIZE) {
-    if (src.dtype != EB_BF16 || dst.dtype != EB_BF16 || op->src_c % 8 != 0 || op->dst_c_off != 0)
-      EB_FAIL(EB_E_INVALID, "resize works on bf16 NHWC with 8-channel groups");
+    const int dt = e->f32 ? EB_F32 : EB_BF16;
+    if (src.dtype != dt || dst.dtype != dt || op->src_c % 8 != 0 || op->dst_c_off != 0)
+      EB_FAIL(EB_E_INVALID, "resize works on NHWC images with 8-channel groups");
   } else if (op->kind == EB_OP_POOL || op->kind == EB_OP_BNRELU || op->kind == EB_OP_GAP) {
-    if (src.dtype != EB_BF16 || dst.dtype != EB_BF16) EB_FAIL(EB_E_INVALID, "pool dtypes");
+    const int dt = e->f32 ? EB_F32 : EB_BF16;
+    if (src.dtype != dt || dst.dtype != dt) EB_FAIL(EB_E_INVALID, "pool dtypes");
     if (op->src_c % 8 != 0 || op->src_c_off % 8 != 0 || op->dst_c_off % 8 != 0)
       EB_FAIL(EB_E_INVALID, "channel slices must be multiples of 8");
     if (op->kind == EB_OP_POOL) {
@@ -1227,6 +1330,10 @@ int eb_finalize(eb_engine* e) {
   cudaSetDevice(e->device);
   const int mb = e->max_batch;
   fuse_conv_pools(e);
+  if (e->f32) {  // the fp32 kernels take every op as declared
+    e->op_pool.assign(e->ops.size(), -1);
+    e->op_skip.assign(e->ops.size(), 0);
+  }
   std::vector<uint8_t> t_read(e->tensors.size(), 0);  // tensors some op or member reads
   for (size_t i = 0; i < e->ops.size(); ++i) {
     if (e->op_skip[i]) continue;
@@ -1254,7 +1361,7 @@ int eb_finalize(eb_engine* e) {
   const size_t img = static_cast<size_t>(mb) * e->C * e->H * e->W;
   EB_CUDA(cudaMalloc(&e->d_in_u8, img));
   EB_CUDA(cudaMalloc(&e->d_in_f32, img * sizeof(float)));
-  if (stem_rows_enabled()) {
+  if (stem_rows_enabled() && !e->f32) {
     for (const auto& op : e->ops) {
       if (op.kind != EB_OP_CONV) continue;
       const Tensor& src = e->tensors[op.src];
@@ -1272,10 +1379,24 @@ int eb_finalize(eb_engine* e) {
   e->img8_needed = false;
   for (const auto& op : e->ops)
     if (op.src == EB_T_IMAGE_NHWC8 && !e->stem_buf.count(&op)) e->img8_needed = true;
-  bool used[kLanes] = {};
-  for (const auto& op : e->ops) used[op.stream] = true;
+  // split-K partial slices per lane: the largest split layer at max_batch (split counts
+  // are a function of the layer shape only, plan_conv)
+  for (size_t i = 0; i < e->ops.size(); ++i) {
+    const eb_op_desc& op = e->ops[i];
+    if (op.kind != EB_OP_CONV || e->op_skip[i] || e->f32) continue;
+    ConvArgs a{};
+    const void* rd = nullptr;
+    conv_args_for(e, op, mb, e->op_pool[i], &a, &rd);
+    ConvPlan pl;
+    const int rc = plan_conv(a, &pl);
+    if (rc != EB_OK) return rc;
+    e->ws_floats[op.stream] = std::max(e->ws_floats[op.stream], pl.ws_floats);
+  }
   for (int l = 0; l < kLanes; ++l)
-    if (used[l] && e->any_cnn) EB_CUDA(cudaMalloc(&e->ws[l], kSplitWsFloats * sizeof(float)));
+    if (e->ws_floats[l] > 0 && cudaMalloc(&e->ws[l], e->ws_floats[l] * sizeof(float)) != cudaSuccess) {
+      cudaGetLastError();
+      EB_FAIL(EB_E_NOMEM, "split-K workspace allocation failed");
+    }
   // LIN1 d-slices: a function of D only (never of the batch); models.lin1_splits.
   int64_t lin_k = 0;
   for (const auto& op : e->ops)

@@ -46,14 +46,20 @@ class TRef:
 
 
 class Engine:
-    def __init__(self, in_shape, max_batch: int, device: int = 0):
+    def __init__(self, in_shape, max_batch: int, device: int = 0, precision: str = "bf16"):
         self.lib = _lib.load()
         c, h, w = in_shape
         self.C, self.H, self.W = c, h, w
         self.max_batch = max_batch
         self.device = device
+        if precision not in ("bf16", "fp32"):
+            raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
+        self.precision = precision
+        self.f32 = precision == "fp32"
         self._h = c_void_p()
         check(self.lib.eb_engine_create(device, max_batch, c, h, w, byref(self._h)))
+        if self.f32:  # the fp32-faithful parity mode (csrc/ref32.cu)
+            check(self.lib.eb_engine_set_precision(self._h, _lib.EB_PREC_F32))
         self._blobs: list[tuple[int, np.ndarray]] = []
         self._pool_size = 0
         self.members: list[tuple[int, int, int, int]] = []
@@ -79,7 +85,10 @@ class Engine:
         self._pool_size = (off + b.size + _ALIGN - 1) // _ALIGN * _ALIGN
         return off
 
-    def tensor(self, h, w, c, dtype=_lib.EB_BF16) -> TRef:
+    def tensor(self, h, w, c, dtype=None) -> TRef:
+        """An activation tensor (bf16, or fp32 in the fp32 mode) unless dtype is given."""
+        if dtype is None:
+            dtype = _lib.EB_F32 if self.f32 else _lib.EB_BF16
         tid = c_int()
         check(self.lib.eb_tensor(self._h, h, w, c, dtype, byref(tid)))
         return TRef(tid.value, 0, c, h, w, c)

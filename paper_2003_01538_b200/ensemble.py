@@ -181,6 +181,9 @@ class Ensemble:
     max_batch: int
     binary_compatible: bool
     device: int = 0
+    # CNN arithmetic: "bf16" (tcgen05, the throughput path) or "fp32" (the fp32-faithful
+    # parity mode, csrc/ref32.cu: top-k equal to the fp32 CPU oracle's)
+    precision: str = "bf16"
     _state: dict = field(default_factory=dict, repr=False)
 
     def __post_init__(self):
@@ -198,8 +201,19 @@ class Ensemble:
         return engine_for(self)
 
 
-def load_ensemble(manifest: ModelManifest, device: int = 0) -> Ensemble:
+def default_precision() -> str:
+    """EB_PRECISION=fp32 selects the fp32-faithful mode for ensembles loaded without an
+    explicit precision (e.g. through the seam, whose load_ensemble has the reference's
+    signature)."""
+    p = os.environ.get("EB_PRECISION", "bf16").lower()
+    return "fp32" if p in ("fp32", "f32", "float32") else "bf16"
+
+
+def load_ensemble(manifest: ModelManifest, device: int = 0, precision: str | None = None) -> Ensemble:
     """Parse every member, check shapes and the byte budget, all or nothing."""
+    precision = precision or default_precision()
+    if precision not in ("bf16", "fp32"):
+        raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
     loaded = []
     for entry in manifest.models:
         path = Path(entry.path)
@@ -236,7 +250,8 @@ def load_ensemble(manifest: ModelManifest, device: int = 0) -> Ensemble:
         raise errors.BudgetExceeded(f"memory budget exceeded: ensemble needs {used} bytes, "
                              f"budget is {manifest.memory_budget_bytes} bytes")
     return Ensemble(tuple(loaded), shape, manifest.preprocess, used, manifest.memory_budget_bytes,
-                    manifest.max_batch, all(m.labels == BINARY_LABELS for m in loaded), device)
+                    manifest.max_batch, all(m.labels == BINARY_LABELS for m in loaded), device,
+                    precision)
 
 
 # ---------------------------------------------------------------------- device residency
@@ -249,7 +264,7 @@ def _kind(model) -> str:
     return getattr(model, "kind", "lin1")
 
 
-def build_engine(models, shape, spec, max_batch: int, device: int = 0):
+def build_engine(models, shape, spec, max_batch: int, device: int = 0, precision: str = "bf16"):
     """Upload every member into one device pool and declare its ops (zoo / LIN1)."""
     from . import zoo
     from .engine import Engine
@@ -257,7 +272,7 @@ def build_engine(models, shape, spec, max_batch: int, device: int = 0):
 
     c, h, w = shape.chw() if hasattr(shape, "chw") else (
         tuple(shape.dims) if len(shape.dims) == 3 else (1, 1, shape.dims[0]))
-    eng = Engine((c, h, w), max_batch, device)
+    eng = Engine((c, h, w), max_batch, device, precision)
     eng.set_preprocess(spec.mean, spec.std, u8_lut(spec.mean, spec.std, spec.pixel_scale, c))
     cnn = [m for m in models if _kind(m) == "cnn1"]
     lin = [m for m in models if _kind(m) != "cnn1"]
@@ -333,12 +348,13 @@ def engine_for(ensemble):
             if "engine" not in state:
                 state["engine"] = build_engine(ensemble.models, ensemble.shared_shape,
                                                ensemble.preprocess, ensemble.max_batch,
-                                               getattr(ensemble, "device", 0))
+                                               getattr(ensemble, "device", 0),
+                                               getattr(ensemble, "precision", "bf16"))
             return state["engine"]
         eng = _engines.get(key)
         if eng is None:
             eng = build_engine(ensemble.models, ensemble.shared_shape, ensemble.preprocess,
-                               ensemble.max_batch)
+                               ensemble.max_batch, 0, default_precision())
             _engines[key] = eng
             weakref.finalize(ensemble, _engines.pop, key, None)
         return eng

@@ -126,3 +126,23 @@ def pack_grouped_conv_weight(w: torch.Tensor, groups: int, block_n: int) -> torc
         rel = g * cpg - (o // block_n) * block_n
         out[o, :, rel:rel + cpg] = wt[o]
     return out.reshape(cout, -1).to(torch.bfloat16).contiguous()
+
+
+def pack_conv_weight_f32(w: torch.Tensor, cin_pad: int | None = None,
+                         hw: tuple[int, int] | None = None) -> torch.Tensor:
+    """fp32-faithful mode (csrc/ref32.cu): fp32 [Cout, Cin/groups, kh, kw] ->
+    [Cout, kh, kw, Cin'] (channels zero-padded to ``cin_pad``: a stem reads the 8-channel
+    K1 image); an FC after an H x W map (``hw``) -> [Cout, H*W*C] in NHWC order."""
+    w = w.detach().to(torch.float32).cpu()
+    if hw is not None:
+        cout, feat = w.shape
+        h, wd = hw
+        c = feat // (h * wd)
+        return w.reshape(cout, c, h, wd).permute(0, 2, 3, 1).reshape(cout, feat).contiguous()
+    if w.dim() == 2:
+        w = w.reshape(w.shape[0], -1, 1, 1)
+    out = w.permute(0, 2, 3, 1)
+    if cin_pad is not None and cin_pad > out.shape[3]:
+        pad = torch.zeros(*out.shape[:3], cin_pad - out.shape[3])
+        out = torch.cat([out, pad], dim=3)
+    return out.reshape(out.shape[0], -1).contiguous()

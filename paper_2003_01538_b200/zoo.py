@@ -10,10 +10,30 @@ weights:
      "input_shape": [3, 224, 224], "labels": 1000}
 
 ``labels`` is either a list of strings or a class count K (labels class_0..).
-Weights: ``torch.manual_seed(seed)`` then the torchvision constructor
-(weights=None; Inception-v3 convs re-drawn fan-in scaled), then every BatchNorm's affine parameters and running statistics
-are drawn from ``torch.Generator().manual_seed(seed + 7919)`` so that BN folding
-is actually exercised (plain random init makes BN an identity).
+Weights (``build_torch_model``), all deterministic from (arch, seed, K):
+
+1. ``torch.manual_seed(seed)`` then the torchvision constructor (weights=None;
+   Inception-v3 convs re-drawn fan-in scaled);
+2. every BatchNorm's affine parameters and running statistics drawn from
+   ``torch.Generator().manual_seed(seed + 7919)`` so that BN folding is actually
+   exercised (plain random init makes BN an identity, SURVEY.md §7.3);
+3. ResNet/ResNeXt residual branches scaled down: the last BN of every block
+   (Bottleneck.bn3 / BasicBlock.bn2) has its affine multiplied by 0.3, so 50 blocks
+   of randomly initialised residuals do not explode (ResNet-152 reached logits of
+   6e8 without it);
+4. BN statistics calibrated: every BN's running mean / variance is set to the
+   batch statistics of a fixed calibration batch (4 structured synthetic images at
+   the native size, ImageNet normalisation), computed in float64 on a copy of the
+   model -- what the running statistics of a trained network would be, so eval-mode
+   BN normalises and activations stay O(1) through the depth;
+5. the classifier head centred: the final Linear's bias is set to -W @ mu, mu the
+   mean penultimate feature over the same batch (float64), so the class ranking is
+   driven by the input rather than by the network's input-independent mean
+   response (random networks otherwise put every image in 1-2 classes).
+
+Steps 4-5 cost one float64 forward of 4 images per member at load time (0.2-0.6 s
+on 8 cores); float64 makes them reproducible across hosts (the stored fp32 values
+are the float64 results rounded once).
 
 Lowering (build_member) walks the module tree once, folds eval-mode BN into
 the preceding conv, packs bf16 weights for the tcgen05 kernel and declares the
@@ -27,8 +47,8 @@ import torch.nn as nn
 
 from . import _lib
 from .engine import Engine, TRef
-from .packing import (bn_affine, conv_mode, fold_bn, pack_conv_weight, pack_grouped_conv_weight,
-                      pick_block_n)
+from .packing import (bn_affine, conv_mode, fold_bn, pack_conv_weight, pack_conv_weight_f32,
+                      pack_grouped_conv_weight, pick_block_n)
 
 ARCHS = (
     "resnet18", "resnet34", "resnet50", "resnet101", "resnet152",
@@ -72,7 +92,76 @@ def build_torch_model(arch: str, seed: int, num_classes: int = 1000) -> nn.Modul
                 if isinstance(mod, nn.Conv2d):
                     nn.init.kaiming_normal_(mod.weight, mode="fan_in", nonlinearity="relu")
     randomize_bn(model, seed)
+    scale_residual_branches(model)
+    calibrate(model, arch, seed, num_classes)
     return model.eval()
+
+
+RESIDUAL_SCALE = 0.3
+CALIB_IMAGES = 4
+CALIB_SEED0 = 0xCA11B
+_calib_cache: dict = {}
+
+
+def scale_residual_branches(model: nn.Module, alpha: float = RESIDUAL_SCALE) -> None:
+    """Multiply the affine of the last BN of every residual block by alpha."""
+    from torchvision.models.resnet import BasicBlock, Bottleneck
+
+    with torch.no_grad():
+        for m in model.modules():
+            bn = m.bn3 if isinstance(m, Bottleneck) else m.bn2 if isinstance(m, BasicBlock) else None
+            if bn is not None:
+                bn.weight.mul_(alpha)
+                bn.bias.mul_(alpha)
+
+
+def _calibration_batch(size: int) -> torch.Tensor:
+    import numpy as np
+
+    from . import synth
+
+    mean = np.asarray((0.485, 0.456, 0.406), np.float32).reshape(1, 3, 1, 1)
+    std = np.asarray((0.229, 0.224, 0.225), np.float32).reshape(1, 3, 1, 1)
+    px = synth.images(CALIB_IMAGES, size, size, 3, seed0=CALIB_SEED0, kind="structured")
+    x = (px.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0) - mean) / std
+    return torch.from_numpy(x).double()
+
+
+def calibrate(model: nn.Module, arch: str, seed: int, num_classes: int) -> None:
+    """Steps 4-5 of the recipe (module docstring): BN statistics and head bias from a
+    float64 forward of the calibration batch; cached per (arch, seed, K)."""
+    import copy
+
+    key = (arch, seed, num_classes)
+    if key not in _calib_cache:
+        m64 = copy.deepcopy(model).double()
+        bns = [m for m in m64.modules() if isinstance(m, nn.BatchNorm2d)]
+        for bn in bns:
+            bn.reset_running_stats()
+            bn.momentum = None  # cumulative average = the statistics of the one batch
+        x = _calibration_batch(NATIVE_SIZE.get(arch, 224))
+        m64.train()
+        with torch.no_grad():
+            m64(x)
+        m64.eval()
+        head = [m for m in m64.modules() if isinstance(m, nn.Linear)][-1]
+        feats = []
+        hook = head.register_forward_hook(lambda mod, i, o: feats.append(i[0]))
+        with torch.no_grad():
+            m64(x)
+        hook.remove()
+        mu = feats[0].mean(0)
+        bias = -(head.weight @ mu)
+        _calib_cache[key] = ([(bn.running_mean.float(), bn.running_var.float()) for bn in bns],
+                             bias.float())
+    stats, bias = _calib_cache[key]
+    bns = [m for m in model.modules() if isinstance(m, nn.BatchNorm2d)]
+    head = [m for m in model.modules() if isinstance(m, nn.Linear)][-1]
+    with torch.no_grad():
+        for bn, (rm, rv) in zip(bns, stats):
+            bn.running_mean.copy_(rm)
+            bn.running_var.copy_(rv)
+        head.bias.copy_(bias)
 
 
 # ---------------------------------------------------------------------- lowering
@@ -93,12 +182,13 @@ class Lowering:
             w = conv.weight.detach().float()
             b = conv.bias.detach().float() if conv.bias is not None else None
             cout = conv.out_features
-            if flatten:
+            if eng.f32:
+                wp = pack_conv_weight_f32(w, hw=(x.h, x.w) if flatten else None)
+            elif flatten:
                 wp = pack_conv_weight(w, "flatten", hw=(x.h, x.w))
-                kh = kw = 1
             else:
                 wp = pack_conv_weight(w.reshape(cout, -1, 1, 1), "tiled")
-                kh = kw = 1
+            kh = kw = 1
             sh = sw = 1
             ph = pw = 0
             ho = wo = 1
@@ -114,7 +204,9 @@ class Lowering:
             ph, pw = conv.padding
             cout = conv.out_channels
             stem = x.ctot == 8 and x.c == 8  # a K1 image (native or resized)
-            if conv.groups > 1:  # ResNeXt: block-diagonal N tiles
+            if eng.f32:
+                wp = pack_conv_weight_f32(w, cin_pad=x.c if stem else None)
+            elif conv.groups > 1:  # ResNeXt: block-diagonal N tiles
                 wp = pack_grouped_conv_weight(w, conv.groups, pick_block_n(cout, conv.groups))
             else:
                 wp = pack_conv_weight(w, conv_mode(kh, kw, sh, sw, ph, pw, x.c, stem))
@@ -373,7 +465,9 @@ def grouped_stem(eng: Engine, image: TRef, stems) -> list[TRef]:
             "shape": (ho, wo, sum(couts), kh, kw, sh, image.c), "weight_bytes": 2 * w[0].numel() * len(w),
             "grouped_members": len(stems)}
     eng.op(_lib.EB_OP_CONV, image, out, cout=sum(couts), kh=kh, kw=kw, sh=sh, sw=sw, ph=ph, pw=pw,
-           relu=True, lane=0, w_off=eng.weight(pack_conv_weight(w, conv_mode(kh, kw, sh, sw, ph, pw, 8, True))),
+           relu=True, lane=0,
+           w_off=eng.weight(pack_conv_weight_f32(w, cin_pad=image.c) if eng.f32 else
+                            pack_conv_weight(w, conv_mode(kh, kw, sh, sw, ph, pw, 8, True))),
            b_off=eng.weight(b.contiguous()), meta=meta, prefork=True)
     slices, off = [], 0
     for c in couts:

@@ -21,27 +21,50 @@ from paper_2003_01538_b200 import synth
 pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).parent / "golden"
 
-# bf16 operands with fp32 accumulation through 50-120 layers: the logit error is
-# bounded by REL_TOL x (the member's max |logit|).
-REL_TOL = 0.03
+# bf16 operands with fp32 accumulation through 16-200 layers: max |dlogit| relative to the
+# member's max |logit|, as measured on B200 over the 32-image golden sets (GPUTEST round 2:
+# ResNet 0.0049-0.0067, ResNeXt 0.0052, DenseNet 0.0062-0.0079, Inception 0.0072, VGG
+# 0.0141-0.0228 -- VGG has no BN and its centred logits are small next to its activations),
+# with 1.5x margin.  The top-k protocol below is checked at these tolerances.
+REL_TOL_BY_FAMILY = {"resnet": 0.010, "resnext": 0.010, "densenet": 0.012, "inception": 0.011,
+                     "vgg": 0.035}
+REL_TOL = 0.035  # (the loosest; used when a member's family is not given)
 TOPK = 5
 
 
-def _check(logits_gpu, logits_ref, name):
-    report = []
+def rel_tol(arch: str) -> float:
+    for fam in ("resnext", "resnet", "densenet", "inception", "vgg"):
+        if str(arch).startswith(fam):
+            return REL_TOL_BY_FAMILY[fam]
+    return REL_TOL
+
+
+def _check(logits_gpu, logits_ref, name, archs):
+    """Returns one report row per member; asserts after printing all of them."""
+    report, fails = [], []
     for m in range(logits_ref.shape[0]):
         ref = logits_ref[m]
         got = logits_gpu[m, :, : ref.shape[-1]]
         scale = float(np.abs(ref).max())
-        tol = REL_TOL * scale
+        tol = rel_tol(archs[m]) * scale
         err = float(np.abs(got - ref).max())
-        assert err <= tol, f"{name} member {m}: max |dlogit| {err:.4g} > tol {tol:.4g}"
-        dec = OC.decisive(ref, TOPK, tol)
-        ok = OC.topk_order(got, TOPK)[dec] == OC.topk_order(ref, TOPK)[dec]
-        assert ok.all(), f"{name} member {m}: top-{TOPK} differs on a decisive sample"
+        dec5 = OC.decisive(ref, TOPK, tol)
         dec1 = OC.decisive(ref, 1, tol)
-        assert (got.argmax(-1)[dec1] == ref.argmax(-1)[dec1]).all()
-        report.append((m, err / scale, int(dec.sum()), ref.shape[0]))
+        top5_ok = OC.topk_order(got, TOPK) == OC.topk_order(ref, TOPK)
+        row = {"member": str(archs[m]), "err/scale": round(err / scale, 6),
+               "tol/scale": rel_tol(archs[m]),
+               "dec5": int(dec5.sum()), "dec1": int(dec1.sum()), "n": ref.shape[0],
+               "top1_equal": int((got.argmax(-1) == ref.argmax(-1)).sum()),
+               "top5_equal": int(top5_ok.all(-1).sum())}
+        report.append(row)
+        if err > tol:
+            fails.append(f"{name} member {m}: max |dlogit| {err:.4g} > tol {tol:.4g}")
+        if not top5_ok[dec5].all():
+            fails.append(f"{name} member {m}: top-{TOPK} differs on a decisive sample")
+        if not (got.argmax(-1)[dec1] == ref.argmax(-1)[dec1]).all():
+            fails.append(f"{name} member {m}: top-1 differs on a decisive sample")
+    print(name, report)
+    assert not fails, fails
     return report
 
 
@@ -55,10 +78,10 @@ def test_members_match_golden_logits(tmp_path, name):
     size, b = int(g["size"]), int(g["batch"])
     docs = [cnn1_doc(f"{a}_{s}", str(a), int(s), NATIVE_SIZE.get(str(a), 224))
             for a, s in zip(g["archs"], g["seeds"])]
-    ens = build(tmp_path, docs, max_batch=16, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    ens = build(tmp_path, docs, max_batch=32, mean=IMAGENET_MEAN, std=IMAGENET_STD)
     px = synth.images(b, size, size, 3, seed0=int(g["seed0"]), kind="structured")
     out, _, res = E.predict_u8(ens, px, topk=TOPK, want_logits=True)
-    print(_check(res["logits"], g["logits"], name))
+    _check(res["logits"], g["logits"], name, g["archs"])
     # top-k indices from the K5 kernel equal the ordering of the returned logits
     assert (res["topk_idx"] == OC.topk_order(res["logits"], TOPK)).all()
     assert [list(r) for r in out.per_model] == res["logits"].argmax(-1).tolist()
@@ -81,16 +104,15 @@ def test_f32_chw_path_matches_u8_path(tmp_path):
 
 
 def test_variable_batch_masking(tmp_path):
-    """Flexible batching: any B (tile padding + masking) gives each sample the same
-    logits as when it is evaluated alone."""
+    """Flexible batching: any B (tile padding + masking) gives each sample bitwise the
+    same logits as in the full batch."""
     docs = [cnn1_doc("r18", "resnet18", 1), cnn1_doc("d121", "densenet121", 2)]
     ens = build(tmp_path, docs, max_batch=40, mean=IMAGENET_MEAN, std=IMAGENET_STD)
     px = synth.images(37, 224, 224, 3, seed0=500)
     _, _, full = E.predict_u8(ens, px, want_logits=True)
     for b in (1, 2, 3, 7, 31, 37):
         _, _, part = E.predict_u8(ens, px[:b], want_logits=True)
-        scale = np.abs(full["logits"]).max()
-        np.testing.assert_allclose(part["logits"], full["logits"][:, :b], rtol=0, atol=0.01 * scale)
+        assert np.array_equal(part["logits"], full["logits"][:, :b]), f"B={b}"
 
 
 def test_variable_batch_masking_vgg_resnet50(tmp_path):
@@ -102,8 +124,7 @@ def test_variable_batch_masking_vgg_resnet50(tmp_path):
     _, _, full = E.predict_u8(ens, px, want_logits=True)
     for b in (1, 5, 33):
         _, _, part = E.predict_u8(ens, px[:b], want_logits=True)
-        scale = np.abs(full["logits"]).max()
-        np.testing.assert_allclose(part["logits"], full["logits"][:, :b], rtol=0, atol=0.01 * scale)
+        assert np.array_equal(part["logits"], full["logits"][:, :b]), f"B={b}"
 
 
 def test_pipelined_batches_equal_single_calls(tmp_path):
@@ -123,3 +144,16 @@ def test_pipelined_batches_equal_single_calls(tmp_path):
     got32 = eng.forward_batches(f32, _lib.EB_IN_F32_CHW)
     for x, lab in zip(f32, got32):
         assert np.array_equal(lab, eng.forward(x, _lib.EB_IN_F32_CHW)["labels"])
+
+
+def test_bench_config_rows_match_oracle(tmp_path):
+    """The bench workload itself (bench.py: C2 at B = 256, synth.images_fast seed 1234):
+    rows 0, 127, 128 and 255 of the 256-image batch against the oracle's logits of
+    those images (tests/golden/cnn_c2_bench.npz)."""
+    g = np.load(GOLDEN / "cnn_c2_bench.npz")
+    docs = [cnn1_doc(f"{a}_{s}", str(a), int(s)) for a, s in zip(g["archs"], g["seeds"])]
+    ens = build(tmp_path, docs, max_batch=256, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    px = synth.images_fast(256, 224, 224, 3, seed0=int(g["seed0"]))
+    _, _, res = E.predict_u8(ens, px, topk=TOPK, want_logits=True)
+    rows = [int(r) for r in g["rows"]]
+    _check(res["logits"][:, rows], g["logits"], "c2_bench", g["archs"])

@@ -1,0 +1,80 @@
+"""The fp32-faithful parity mode (csrc/ref32.cu) against the
+torchvision fp32 CPU oracle: top-5 class indices identical on EVERY golden sample.
+
+The bf16 tcgen05 path (tests/test_gpu_cnn.py) cannot promise that: its logit error is
+0.5-2 % of the logit scale while the oracle's 5th/6th-ranked logits of a 1000-class head
+are often closer than that.  In this mode every conv is a sequential fp32 FFMA chain,
+so the only differences from the oracle are summation order and BN folded into the
+weights -- about 1e-6 of the logit scale.
+"""
+
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from helpers import IMAGENET_MEAN, IMAGENET_STD, cnn1_doc, write_manifest
+from oracle import cnn as OC
+from paper_2003_01538_b200 import ensemble as E
+from paper_2003_01538_b200 import synth
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).parent / "golden"
+TOPK = 5
+# fp32 with a different summation order: measured max |dlogit| / scale is ~1e-6
+F32_REL_TOL = 1e-4
+
+
+def _load_fp32(tmp_path, docs, max_batch):
+    man = write_manifest(tmp_path, docs, max_batch=max_batch, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    return E.load_ensemble(E.load_manifest_file(man), precision="fp32")
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "inception", "resnext", "c5"])
+def test_fp32_mode_top5_equals_oracle_on_every_sample(tmp_path, name):
+    from paper_2003_01538_b200.zoo import NATIVE_SIZE
+
+    g = np.load(GOLDEN / f"cnn_{name}.npz")
+    size, b = int(g["size"]), int(g["batch"])
+    docs = [cnn1_doc(f"{a}_{s}", str(a), int(s), NATIVE_SIZE.get(str(a), 224))
+            for a, s in zip(g["archs"], g["seeds"])]
+    ens = _load_fp32(tmp_path, docs, max_batch=b)
+    assert ens.precision == "fp32"
+    px = synth.images(b, size, size, 3, seed0=int(g["seed0"]), kind="structured")
+    out, _, res = E.predict_u8(ens, px, topk=TOPK, want_logits=True)
+    report = []
+    for m in range(g["logits"].shape[0]):
+        ref = g["logits"][m]
+        got = res["logits"][m, :, : ref.shape[-1]]
+        scale = float(np.abs(ref).max())
+        err = float(np.abs(got - ref).max())
+        same = (OC.topk_order(got, TOPK) == OC.topk_order(ref, TOPK)).all(-1)
+        s = -np.sort(-ref, axis=-1)[:, : TOPK + 1]
+        report.append({"member": str(g["archs"][m]), "err/scale": err / scale,
+                       "min_top6_gap/scale": float((s[:, :-1] - s[:, 1:]).min() / scale),
+                       "top5_equal": f"{int(same.sum())}/{b}"})
+        assert err <= F32_REL_TOL * scale, report[-1]
+        assert same.all(), report[-1]
+    print(name, report)
+    # K5's top-k indices equal the ordering of the returned logits, labels = their argmax
+    assert (res["topk_idx"] == OC.topk_order(res["logits"], TOPK)).all()
+    assert [list(r) for r in out.per_model] == res["logits"].argmax(-1).tolist()
+
+
+def test_fp32_mode_batch_invariant_and_f32_input(tmp_path):
+    """The fp32 mode is batch-invariant too, and the reference-facing f32 CHW input
+    (SampleBatch) gives the same logits as u8 (same fp32 preprocess values)."""
+    from paper_2003_01538_b200 import models as M
+
+    docs = [cnn1_doc("r18", "resnet18", 1), cnn1_doc("d121", "densenet121", 2)]
+    ens = _load_fp32(tmp_path, docs, max_batch=12)
+    px = synth.images(12, 224, 224, 3, seed0=321)
+    _, _, full = E.predict_u8(ens, px, want_logits=True)
+    for lo, hi in ((0, 1), (3, 10)):
+        _, _, part = E.predict_u8(ens, px[lo:hi], want_logits=True)
+        assert np.array_equal(part["logits"], full["logits"][:, lo:hi])
+    f32 = (px.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0)).reshape(12, -1)
+    _, _, r2 = E.predict(ens, M.SampleBatch(ens.shared_shape, f32), want_logits=True)
+    assert np.array_equal(r2["logits"], full["logits"])
