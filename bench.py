@@ -51,10 +51,13 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 
 
 def _event_time(fn, iters: int = 50) -> float:
-    """Mean ms per call of fn() on the current stream (CUDA events, after warm-up)."""
+    """Mean ms per call of fn() on the current stream (CUDA events, after warm-up).
+    EB_PROBE_ITERS=n: n timed calls and one warm-up (short launch lists under ncu)."""
     import torch
 
-    for _ in range(5):
+    if os.environ.get("EB_PROBE_ITERS"):
+        iters = int(os.environ["EB_PROBE_ITERS"])
+    for _ in range(1 if os.environ.get("EB_PROBE_ITERS") else 5):
         fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -200,17 +203,22 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
-def cnn_docs():
-    return [{"format": "cnn1", "id": f"{a}", "arch": a, "seed": s, "input_shape": [3, 224, 224],
-             "labels": 1000} for a, s in MEMBERS]
+def cnn_docs(members=MEMBERS):
+    """cnn1 documents of the members, each at its native input size (Inception-v3: 299;
+    an ensemble mixing sizes takes requests at the largest, zoo.NATIVE_SIZE)."""
+    from paper_2003_01538_b200.zoo import NATIVE_SIZE
+
+    return [{"format": "cnn1", "id": f"{a}", "arch": a, "seed": s,
+             "input_shape": [3, NATIVE_SIZE.get(a, 224), NATIVE_SIZE.get(a, 224)], "labels": 1000}
+            for a, s in members]
 
 
-def build_ensemble(batch: int, device: int):
+def build_ensemble(batch: int, device: int, members=MEMBERS):
     from paper_2003_01538_b200 import ensemble as E
 
     td = Path(tempfile.mkdtemp(prefix="bench_"))
     entries = []
-    for doc in cnn_docs():
+    for doc in cnn_docs(members):
         (td / f"{doc['id']}.json").write_text(json.dumps(doc))
         entries.append({"id": doc["id"], "path": f"{doc['id']}.json"})
     man = {"memory_budget_bytes": 1 << 40, "max_batch": batch,
@@ -220,8 +228,9 @@ def build_ensemble(batch: int, device: int):
     return E.load_ensemble(E.load_manifest_file(td / "manifest.json"), device=device)
 
 
-def cpu_oracle_rate(n_images: int, seconds_cap: float = 30.0) -> dict:
-    """torchvision fp32 eager on all host cores, the same members and inputs."""
+def cpu_oracle_rate(n_images: int = 64, seconds_cap: float = 25.0, chunk: int = 8) -> dict:
+    """torchvision fp32 eager on all host cores, the same members and inputs, in batches
+    of ``chunk`` images until ``seconds_cap``."""
     import torch
 
     from oracle import cnn as OC
@@ -231,24 +240,137 @@ def cpu_oracle_rate(n_images: int, seconds_cap: float = 30.0) -> dict:
     cores = OC.set_threads()
     models = [build_torch_model(a, s) for a, s in MEMBERS]
     px = synth.images_fast(n_images, 224, 224, 3, seed0=4321)
-    x = OC.preprocess_u8(px, MEAN, STD, 255.0)
     with torch.no_grad():
-        for m in models:  # warm-up on one image
-            m(x[:1])
+        x = OC.preprocess_u8(px[:chunk], MEAN, STD, 255.0)
+        for m in models:  # warm-up
+            m(x)
         t0 = time.perf_counter()
         done = 0
-        for i in range(n_images):
-            for m in models:
-                m(x[i:i + 1])
-            done += 1
-            if time.perf_counter() - t0 > seconds_cap:
-                break
+        while done + chunk <= n_images and time.perf_counter() - t0 < seconds_cap:
+            x = OC.preprocess_u8(px[done:done + chunk], MEAN, STD, 255.0)
+            logits = np.stack([m(x).numpy() for m in models])
+            _ = logits.argmax(-1)
+            done += chunk
         dt = time.perf_counter() - t0
     return {"value": done / dt, "unit": "images/s", "cores": cores, "kind": "port",
-            "sample": f"{done} image(s) x {len(MEMBERS)} members, torchvision fp32 eager, batch 1"}
+            "sample": f"{done} images in batches of {chunk} x {len(MEMBERS)} members, torchvision "
+                      "fp32 eager (u8 -> reference fp32 preprocess -> logits -> argmax)"}
+
+
+# ---------------------------------------------------------------------- Track R (LIN1)
+
+TRACK_R = {"members": 3, "shape": (3, 224, 224), "batch": 256}
+
+
+def _lin1_arrays(k: int, d: int, seed: int):
+    rng = np.random.default_rng(seed)
+    w = rng.standard_normal((k, d), dtype=np.float32)
+    b = rng.standard_normal(k, dtype=np.float32)
+    return w, b
+
+
+def track_r_gpu(pk: dict, steps: int = 10) -> dict:
+    """The reference's own member kind on the B200: LIN1 N = 3 at [3, 224, 224], binary and
+    K = 1000, B = 256.  K1 (f32 preprocess) + K6 (fp64 scores) + K5,
+    device-timed with the input resident; GB/s of the path against the HBM peak and
+    K6's fp64 FLOP/s."""
+    import torch
+
+    from paper_2003_01538_b200 import _lib
+    from paper_2003_01538_b200.ensemble import build_engine
+    from paper_2003_01538_b200.models import InputShape, LinearModel, PreprocessSpec
+
+    c, h, w = TRACK_R["shape"]
+    d, B, n = c * h * w, TRACK_R["batch"], TRACK_R["members"]
+    out = {}
+    for name, k in (("binary", 2), ("k1000", 1000)):
+        labels = ("absent", "present") if k == 2 else tuple(f"c{i}" for i in range(k))
+        models = []
+        for i in range(n):
+            wt, bs = _lin1_arrays(k, d, 100 + i)
+            models.append(LinearModel(f"m{i}", InputShape((c, h, w)), labels, wt, bs))
+        eng = build_engine(models, InputShape((c, h, w)), PreprocessSpec(MEAN, STD, 255.0), B)
+        x = np.random.default_rng(7).random((B, d), dtype=np.float32)
+        eng.forward(x, _lib.EB_IN_F32_CHW)  # H2D into the engine's input buffer + warm-up
+        stream = torch.cuda.ExternalStream(eng.stream())
+        for _ in range(3):
+            eng.forward_device(B, _lib.EB_IN_F32_CHW)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for _ in range(steps):
+            eng.forward_device(B, _lib.EB_IN_F32_CHW)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        bytes_ = 4 * B * d * 2 + 4 * n * k * d + 4 * n * k + 4 * n * B  # x in, K1 out/K6 in, W, b, labels
+        flops = 2.0 * B * d * n * k
+        out[name] = {"batch": B, "members": n, "K": k, "D": d, "ms": ms, "images_per_s": B / (ms / 1e3),
+                     "bytes": bytes_, "achieved_gbs": bytes_ / ms / 1e6,
+                     "frac_of_hbm": bytes_ / ms / 1e6 / pk["hbm_gbs"], "fp64_tflops": flops / ms / 1e9}
+        eng.close()
+        del eng
+    out["peak_gbs"] = pk["hbm_gbs"]
+    out["path"] = "K1 f32 preprocess + K6 fp64 scores (fixed d-slices) + K5 argmax, inputs resident"
+    return out
+
+
+def _reference_module():
+    for p in (ROOT / "baseline" / "_ref", Path("/root/reference/pkg/src")):
+        if (p / "ensemblegate").is_dir() and str(p) not in sys.path:
+            sys.path.append(str(p))
+    try:
+        import ensemblegate
+
+        return ensemblegate, "reference"
+    except ImportError:
+        return None, "port"
+
+
+def track_r_cpu(seconds_cap: float = 20.0) -> dict:
+    """The reference's own forward (eg/ensemble.py:232-250: preprocess + fp64 einsum +
+    argmax per member) on the host, same LIN1 configs; the restatement in oracle/lin1.py
+    when the reference package is not importable."""
+    eg, kind = _reference_module()
+    from oracle import lin1 as OL
+
+    c, h, w = TRACK_R["shape"]
+    d, n = c * h * w, TRACK_R["members"]
+    out = {"kind": kind, "cores": 1,
+           "note": "the reference's einsum is single-threaded numpy (SURVEY.md §3.2)"}
+    for name, k, b in (("binary", 2, 64), ("k1000", 1000, 2)):
+        labels = ("absent", "present") if k == 2 else tuple(f"c{i}" for i in range(k))
+        arrays = [_lin1_arrays(k, d, 100 + i) for i in range(n)]
+        x = np.random.default_rng(7).random((b, d), dtype=np.float32)
+        if eg is not None:
+            shape = eg.InputShape((c, h, w))
+            models = tuple(eg.LinearModel(f"m{i}", shape, labels, wt, bs) for i, (wt, bs) in enumerate(arrays))
+            ens = eg.Ensemble(models, shape, eg.PreprocessSpec(MEAN, STD, 255.0),
+                              sum(m.parameter_bytes for m in models), 1 << 40, b, k == 2)
+            run = lambda: eg.forward(ens, eg.SampleBatch(shape, x))  # noqa: E731
+        else:
+            run = lambda: OL.forward(arrays, x, c, MEAN, STD)  # noqa: E731
+        run()
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            run()
+            reps += 1
+            if time.perf_counter() - t0 > seconds_cap / 2 or reps >= 5:
+                break
+        dt = (time.perf_counter() - t0) / reps
+        out[name] = {"batch": b, "members": n, "K": k, "images_per_s": b / dt, "ms_per_call": dt * 1e3}
+    return out
+
+
+# ---------------------------------------------------------------------- reference arm
 
 
 def run_reference(args) -> None:
+    """The reference path's CPU implementation on the host cores (oracle port: torchvision
+    fp32 eager -- the reference has no CNN code), C2's members, a bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -290,16 +412,89 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------- our arm
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) with torchrun
+    and return its exit code (rank 0 prints the line)."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator / transport lines on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py")] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def device_rate(eng, B: int, kind: int, stream, topk: int, iters: int = 10) -> float:
+    """images/s of eng.forward_device(B) (+ K5 with top-k), CUDA events on the engine
+    stream, after warm-up (graph captured)."""
+    import torch
+
+    for _ in range(3):
+        eng.forward_device(B, kind, topk)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        s0.record(stream)
+    for _ in range(iters):
+        eng.forward_device(B, kind, topk)
+    with torch.cuda.stream(stream):
+        s1.record(stream)
+    torch.cuda.synchronize()
+    return B * iters / (s0.elapsed_time(s1) / 1e3)
+
+
+def extra_configs(device: int) -> dict:
+    """C1 (B = 8) and C5 (B = 128 per GPU, its 8-GPU shard size) on this GPU, device-timed;
+    plus bs = 1 latency of each through eb_forward."""
+    import torch
+
+    from paper_2003_01538_b200 import _lib, synth
+    from paper_2003_01538_b200.ensemble import engine_for
+
+    sets = {"C1": ([("resnet18", 1), ("densenet121", 2)], 8, 224),
+            "C5": ([("resnet152", 6), ("densenet201", 7), ("vgg19", 8), ("inception_v3", 5),
+                    ("resnext50_32x4d", 9)], 128, 299)}
+    gflop = {"C1": 9.296, "C5": 90.761}
+    out = {}
+    for name, (members, B, size) in sets.items():
+        ens = build_ensemble(B, device, members=members)
+        eng = engine_for(ens)
+        stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", device))
+        kind = _lib.EB_IN_U8_HWC
+        px = synth.images_fast(B, size, size, 3, seed0=77)
+        eng.forward(px, kind)  # resident input + graph capture
+        rate = device_rate(eng, B, kind, stream, topk=5)
+        lat = []
+        for _ in range(20):
+            t0 = time.perf_counter()
+            eng.forward(px[:1], kind)
+            lat.append((time.perf_counter() - t0) * 1e3)
+        out[name] = {"members": [f"{a}:seed{s}" for a, s in members], "batch": B, "input": size,
+                     "images_per_s": rate, "tflops": rate * gflop[name] / 1e3,
+                     "latency_bs1_p50_ms": statistics.median(lat[5:])}
+        eng.close()
+        del eng, ens
+    return out
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=256)
-    ap.add_argument("--ref-sample", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=256, help="per-GPU batch at N = 1 (C2)")
+    ap.add_argument("--global-batch", type=int, default=4096, help="C4: global batch at N > 1")
+    ap.add_argument("--ref-sample", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also time B in {1,8,32,64,128}")
+    ap.add_argument("--quick", action="store_true",
+                    help="headline only: no batch sweep / Track R / C1 / C5 / drop-in f32 extras")
     ap.add_argument("--profile-json", default="", help="write the per-op profile here")
     ap.add_argument("--minimal", action="store_true",
                     help="timed steps only (for ncu launch lists): no e2e / latency / profile / cpu")
@@ -309,6 +504,8 @@ def main() -> None:
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
 
     import torch
     import torch.distributed as dist
@@ -316,43 +513,49 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun "
+                 f"--nproc-per-node {args.gpus}, or without torchrun to let bench.py spawn the ranks")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2003_01538_b200 import _lib, synth
     from paper_2003_01538_b200.ensemble import engine_for
-    from paper_2003_01538_b200.shard import gather_rows
+    from paper_2003_01538_b200.shard import gather_rows, shard_bounds
 
-    B = args.batch
+    # N = 1: C2 at B = 256 (BASELINE configs[1]); N > 1: C4, a global batch of 4096 split
+    # contiguously (2048 / 1024 / 512 per rank), logits gathered to rank 0 over NCCL.
+    if world > 1:
+        lo, hi = shard_bounds(args.global_batch, rank, world)
+        B, global_b = hi - lo, args.global_batch
+    else:
+        lo, B, global_b = 0, args.batch, args.batch
     ens = build_ensemble(B, local)
     eng = engine_for(ens)
     stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", local))
     kind = _lib.EB_IN_U8_HWC
+    TOPK = 5  # north_star's combine: per-member softmax + top-5, labels, in the timed step
 
-    host = torch.from_numpy(synth.images_fast(B, 224, 224, 3, seed0=1234 + rank * B)).pin_memory()
+    host = torch.from_numpy(synth.images_fast(B, 224, 224, 3, seed0=1234, first_row=lo)).pin_memory()
     dev_in = eng.input_buffer(kind)
     torch.cuda.synchronize()
     # resident input: one copy into the engine's staging buffer
-    from paper_2003_01538_b200.engine import _wrap_device_ptr
+    from paper_2003_01538_b200.engine import TRef, _wrap_device_ptr
 
     staging = _wrap_device_ptr(dev_in, B * 224 * 224 * 3, torch.uint8, local)
     staging.copy_(host.view(-1).cuda())
-    logits_t = None
-    if world > 1:
-        from paper_2003_01538_b200.engine import TRef
-
-        lt = eng.members[0][1]
-        kpad = max(m[2] + m[3] for m in eng.members)
-        logits_t = eng.tensor_view(TRef(lt, 0, kpad, 1, 1, kpad), B).view(B, -1)
+    lt = eng.members[0][1]
+    kpad = max(m[2] + m[3] for m in eng.members)
+    logits_t = eng.tensor_view(TRef(lt, 0, kpad, 1, 1, kpad), B).view(B, -1)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step():
-        eng.forward_device(B, kind)
-        if world > 1:  # logits of every shard to the serving rank, on the engine stream
+        eng.forward_device(B, kind, TOPK)
+        if world > 1:  # every shard's logits to the serving rank, on the engine stream
             with torch.cuda.stream(stream):
-                gather_rows(logits_t, B * world, dst=0)
+                gather_rows(logits_t, global_b, dst=0)
 
     for _ in range(args.warmup):
         step()
@@ -379,12 +582,14 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
         dist.barrier()
-    value = B * world * args.steps / (dev_ms / 1e3)
+    value = global_b * args.steps / (dev_ms / 1e3)
 
     if args.minimal:
         if rank == 0:
             print(json.dumps({"minimal": True, "value": value, "ms_per_step": dev_ms / args.steps,
                               "launches_per_step": n_launch}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
         return
     # ---- e2e through the public C-ABI with pinned host buffers: every step copies its
     # inputs host->device and reads its labels back inside the timed region.
@@ -392,7 +597,7 @@ def main() -> None:
     #             step i's forward) -- the headline e2e;
     #  sequential: one eb_forward call per step (nothing overlaps).
     host_np = host.numpy()
-    host2 = torch.from_numpy(synth.images_fast(B, 224, 224, 3, seed0=9999 + rank * B)).pin_memory().numpy()
+    host2 = torch.from_numpy(synth.images_fast(B, 224, 224, 3, seed0=9999, first_row=lo)).pin_memory().numpy()
     step_inputs = [host_np if i % 2 == 0 else host2 for i in range(args.steps)]
 
     def timed(fn):
@@ -411,15 +616,31 @@ def main() -> None:
         eng.forward(host_np, kind)
     eng.forward_batches(step_inputs[:2], kind)
     # (the headline pipelined run first, right after the device-timed region: under the
-    # power cap a later run sees lower clocks -- tools/e2e_probe.py interleaves the paths
-    # and finds pipelined e2e within 1 % of the device-only throughput)
+    # power cap a later run sees lower clocks)
     pipe_s = timed(lambda: eng.forward_batches(step_inputs, kind))
     seq_s = timed(lambda: [eng.forward(x, kind) for x in step_inputs])
-    e2e = B * world * args.steps / pipe_s
-    e2e_seq = B * world * args.steps / seq_s
+    e2e = global_b * args.steps / pipe_s
+    e2e_seq = global_b * args.steps / seq_s
     n_members = len(eng.members)
 
-    # ---- p50 latency at bs=1 (e2e through eb_forward) and optional batch sweep
+    extras = {}
+    if world == 1 and not args.quick:
+        # the reference-shaped drop-in call: forward(ensemble, SampleBatch) with f32 CHW
+        # samples from ordinary (pageable) numpy memory, 4x the H2D bytes of u8
+        from paper_2003_01538_b200 import ensemble as E
+        from paper_2003_01538_b200 import models as M
+
+        f32 = (host_np.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0)).reshape(B, -1)
+        sb = M.SampleBatch(ens.shared_shape, f32)
+        E.forward(ens, sb)
+        n_f = max(3, args.steps // 4)
+        f_s = timed(lambda: [E.forward(ens, sb) for _ in range(n_f)])
+        extras["dropin_f32_forward"] = {
+            "images_per_s": B * n_f / f_s, "h2d_bytes_per_step": int(f32.nbytes),
+            "path": "ensemble.forward(ensemble, SampleBatch) -- f32 CHW from pageable numpy, labels "
+                    "back as EnsembleOutput (the reference's own call, eg/ensemble.py:232)"}
+
+    # ---- p50 latency at bs=1 (e2e through eb_forward) and the batch sweep
     one = host_np[:1].copy()
     for _ in range(3):
         eng.forward(one, kind)
@@ -429,20 +650,10 @@ def main() -> None:
         eng.forward(one, kind)
         lat.append((time.perf_counter() - t0) * 1e3)
     sweep = {}
-    if args.sweep:
-        for b in (1, 8, 32, 64, 128):
-            for _ in range(3):
-                eng.forward_device(b, kind)
-            torch.cuda.synchronize()
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(stream):
-                s0.record(stream)
-            for _ in range(10):
-                eng.forward_device(b, kind)
-            with torch.cuda.stream(stream):
-                s1.record(stream)
-            torch.cuda.synchronize()
-            sweep[str(b)] = b * 10 / (s0.elapsed_time(s1) / 1e3)
+    if world == 1 and not args.quick:
+        for b in (1, 8, 32, 64, 128, 256):
+            if b <= B:
+                sweep[str(b)] = device_rate(eng, b, kind, stream, TOPK)
 
     # ---- roofline of the tcgen05 conv/GEMM kernel class (serialised per-op profile)
     # per-op median of 3 serialised runs (an eager run's event times absorb any host-side
@@ -460,42 +671,67 @@ def main() -> None:
     achieved = conv_flops / (conv_ms / 1e3) / 1e12
     # DRAM traffic of the top launch from the committed ncu capture of the same layer
     traffic = None
-    tl = ROOT / "profiles" / "round1" / "top_launch_ncu.json"
-    if top is not None and tl.exists():
+    for tl in sorted((ROOT / "profiles").glob("*/top_launch_ncu.json"), reverse=True):
         t = json.loads(tl.read_text())
-        if list(t["shape(ho,wo,cout,kh,kw,s,cin)"]) == list(top[0]["shape"]) and t["batch"] == B:
+        if top is not None and list(t["shape(ho,wo,cout,kh,kw,s,cin)"]) == list(top[0]["shape"]) and t["batch"] == B:
             traffic = {"dram_bytes_per_launch": t["dram_bytes_read"] + t["dram_bytes_write"],
                        "algorithmic_bytes_per_launch": t["algorithmic_bytes"], "source": t["source"]}
+            break
     peak = pk["bf16_tflops_sustained"]
     if args.profile_json and rank == 0:
         Path(args.profile_json).write_text(json.dumps(
             [{"i": i, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in m.items()}, "ms": float(t)}
              for i, (m, t) in enumerate(zip(eng.op_meta, ms))], indent=0))
 
-    hbm = hbm_kernels(B, pk["hbm_gbs"], pk_src) if rank == 0 else None
+    hbm = hbm_kernels(B, pk["hbm_gbs"], pk_src) if rank == 0 and world == 1 else None
+    eng_dev = eng.device
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_oracle_rate(12, seconds_cap=25.0)
+            cpu = cpu_oracle_rate()
         except Exception as exc:  # the baseline is reported, never fatal
             cpu = {"error": str(exc)[:200]}
+    if world == 1 and not args.quick:
+        # free this engine before the extra configurations are built
+        eng.close()
+        del eng, ens, logits_t, staging
+        torch.cuda.empty_cache()
+        try:
+            extras["configs"] = extra_configs(eng_dev)
+        except Exception as exc:
+            extras["configs"] = {"error": str(exc)[:300]}
+        try:
+            tr = {"gpu": track_r_gpu(pk)}
+            if not args.no_cpu_baseline:
+                tr["cpu"] = track_r_cpu()
+            extras["track_r"] = tr
+        except Exception as exc:
+            extras["track_r"] = {"error": str(exc)[:300]}
 
     if rank == 0:
+        c4 = world > 1
         line = {
             "metric": "ensemble images/s (N-model fwd+combine)",
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if c4 else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
             "config": {
-                "workload": "C2 (BASELINE configs[1]): resnet50+densenet121+vgg16 cnn1 members, "
-                            f"{B} synthetic 224x224 RGB u8 images per GPU per step",
-                "batch_per_gpu": B, "global_batch": B * world, "members": [f"{a}:seed{s}" for a, s in MEMBERS],
-                "parallelism": f"replica x{world}, batch-sharded, NCCL logits gather to rank 0" if world > 1 else "single GPU",
+                "workload": (f"C4 (BASELINE configs[3]): resnet50+densenet121+vgg16, global batch "
+                             f"{global_b} of synthetic 224x224 RGB u8 images split contiguously over "
+                             f"{world} GPUs ({B} per rank)") if c4 else
+                            ("C2 (BASELINE configs[1]): resnet50+densenet121+vgg16 cnn1 members, "
+                             f"{B} synthetic 224x224 RGB u8 images per step"),
+                "batch_per_gpu": B, "global_batch": global_b,
+                "members": [f"{a}:seed{s}" for a, s in MEMBERS],
+                "parallelism": (f"dp{world}: a replica per GPU, contiguous shards, NCCL gather of the "
+                                "[B_r, 3000] fp32 logits to rank 0 in every timed step") if c4 else "single GPU",
+                "step": "K1 preprocess + every member's layers + K5 combine (argmax, softmax, top-5)",
                 "l2": "flushed between timed steps (256 MiB write), outside the events",
             },
-            "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(host.numel()),
-                    "d2h_bytes_per_step": int(4 * n_members * B),
+            "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(host.numel()) * world,
+                    "d2h_bytes_per_step": int(4 * n_members * B) * world,
                     "path": "eb_forward_batches (C-ABI): pinned host u8 input copied and labels read "
                             "back every step; step i+1's copy overlaps step i's forward",
                     "sequential_value": e2e_seq,
@@ -508,7 +744,7 @@ def main() -> None:
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{pk_src} bf16_tflops_sustained",
                          "flops_per_step": conv_flops, "kernel_ms_per_step_serialised": conv_ms,
-                         "step_frac_of_peak": GFLOP_PER_IMG * 1e9 * B * world / (dev_ms / args.steps / 1e3) / 1e12 / peak / world,
+                         "step_frac_of_peak": GFLOP_PER_IMG * 1e9 * global_b / (dev_ms / args.steps / 1e3) / 1e12 / peak / world,
                          "top_launch": {"shape(ho,wo,cout,kh,kw,s,cin)": list(top[0]["shape"]), "ms": top[1]} if top else None},
             "clocks": clk.summary(),
             "hbm_kernels": hbm,
@@ -516,6 +752,8 @@ def main() -> None:
         }
         if sweep:
             line["batch_sweep_images_per_s"] = sweep
+        if extras:
+            line["extras"] = extras
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

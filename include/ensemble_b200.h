@@ -120,6 +120,16 @@ int eb_engine_create(int device, int max_batch, int in_c, int in_h, int in_w, eb
  * §7.3 (iii)); top-k equals the fp32 CPU oracle's up to summation order. */
 enum { EB_PREC_BF16 = 0, EB_PREC_F32 = 1 };
 int eb_engine_set_precision(eb_engine* e, int precision);
+/* A second execution context of a finalized engine: same device, ops and weight pool
+ * (shared, freed with the last engine using it), its own activation arena, streams,
+ * split-K workspaces and graph cache.  Concurrent requests lease one context each
+ * (the reference re-enters forward from its worker threads, eg/gateway.py:222-257)
+ * instead of serialising on one engine. */
+int eb_engine_clone(eb_engine* src, eb_engine** out);
+/* Capture the CUDA graphs of every batch-size bucket up to max_b (<= 0: max_batch) so
+ * that no request pays a capture.  Buckets: exact up to 8, then multiples of 16 / 32 /
+ * 64 (runtime.cu bucket_of); a request runs through its bucket's graph. */
+int eb_engine_warmup(eb_engine* e, int input_kind, int max_b);
 int eb_engine_destroy(eb_engine* e);
 
 /* Normalisation: mean/std have 1 or C entries (models.py:247-253).  lut_u8 is

@@ -1,6 +1,7 @@
 """Generate the committed golden fixtures under tests/golden/ (build container only).
 
     PYTHONPATH=/root/reference/pkg/src python -m oracle.gen_golden --lin1
+    python -m oracle.gen_golden --gateway
     python -m oracle.gen_golden --cnn
 
 --lin1 imports the reference itself (/root/reference, read-only) and records
@@ -166,13 +167,48 @@ def gen_cnn(names) -> None:
               [len(set(r.tolist())) for r in arr.argmax(-1)])
 
 
+def gen_gateway() -> None:
+    """Response bytes of the reference's own GatewayApp (eg/gateway.py:76-142) for the
+    request sets of tests/test_gpu_gateway.py, frozen so the GPU tests compare the seam
+    against the reference's output even where only its gateway code is importable."""
+    import base64
+
+    sys.path.insert(0, "/root/reference/pkg/src")
+    sys.path.insert(0, str(ROOT / "tests"))
+    import ensemblegate as eg
+    from ensemblegate.gateway import GatewayApp
+    from test_gpu_gateway import _ensemble_docs, _requests
+
+    from helpers import write_manifest
+
+    out = {"reference": "ensemblegate " + eg.__version__, "cases": []}
+    for binary in (True, False):
+        with tempfile.TemporaryDirectory() as td:
+            d = 96
+            mp = write_manifest(Path(td), _ensemble_docs(d, binary), max_batch=16)
+            reqs = _requests(d, np.random.default_rng(4))
+            app = GatewayApp(eg.load_ensemble(eg.load_manifest_file(mp)))
+            resp = [app.handle("POST", "/v1/predict", r) for r in reqs]
+            models = app.handle("GET", "/v1/models")
+        out["cases"].append({
+            "binary": binary, "d": d, "max_batch": 16,
+            "requests": [base64.b64encode(r).decode() for r in reqs],
+            "responses": [[st, body.decode()] for st, body in resp],
+            "models": [models[0], models[1].decode()]})
+    (GOLDEN / "gateway_bytes.json").write_text(json.dumps(out, indent=0) + "\n")
+    print("wrote", GOLDEN / "gateway_bytes.json")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--lin1", action="store_true")
     ap.add_argument("--cnn", nargs="*")
+    ap.add_argument("--gateway", action="store_true")
     a = ap.parse_args()
     sys.path.insert(0, str(ROOT))
     if a.lin1:
         gen_lin1()
+    if a.gateway:
+        gen_gateway()
     if a.cnn is not None:
         gen_cnn(a.cnn or list(CNN_SETS) + ["c2_bench"])

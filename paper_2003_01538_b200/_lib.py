@@ -74,6 +74,8 @@ _SIGS = {
     "eb_engine_create": (c_int, [c_int, c_int, c_int, c_int, c_int, POINTER(c_void_p)]),
     "eb_engine_destroy": (c_int, [c_void_p]),
     "eb_engine_set_precision": (c_int, [c_void_p, c_int]),
+    "eb_engine_clone": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "eb_engine_warmup": (c_int, [c_void_p, c_int, c_int]),
     "eb_set_preprocess": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "eb_pool_reserve": (c_int, [c_void_p, c_uint64]),
     "eb_pool_write": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64]),

@@ -10,13 +10,14 @@ namespace eb {
 
 // ------------------------------------------------------------------ K5 combine
 //
-// One CTA per sample, one warp per member (looping when N > warps).  Per member:
+// One warp per (sample, member) row.  Per row:
 //   label  = argmax over the member's K logits, lowest index on ties
 //            (np.argmax semantics, eg/models.py:279)
 //   top-k  = indices ordered by (logit desc, index asc), with softmax
 //            probabilities computed in fp32 from the logits
-// Then thread 0 applies the sensitivity policy over the N binary votes
-// (eg/policy.py:66-76): any = max, all = min, at_least = count >= k.
+// Then (policy requests only) a second pass applies the sensitivity policy over the N
+// binary votes of each sample (eg/policy.py:66-76): any = max, all = min, at_least =
+// count >= k.
 
 template <typename T>
 __device__ __forceinline__ bool better(T v, int i, T bv, int bi) {
@@ -59,7 +60,7 @@ __device__ void member_outputs(const T* row, int K, int lane, int mem, int B, in
   warp_argmax_excluding(row, K, false, T(0), 0, &bv, &bi);
   if (lane == 0) {
     labels[static_cast<int64_t>(mem) * B + b] = bi;
-    s_lab[mem] = bi;
+    if (s_lab) s_lab[mem] = bi;
   }
   if (topk > 0) {
     // softmax denominator in fp32, max-subtracted
@@ -134,7 +135,7 @@ __device__ void member_outputs_reg(const float* row, int K, int lane, int mem, i
   warp_best(bv, bi, wv, wi);
   if (lane == 0) {
     labels[static_cast<int64_t>(mem) * B + b] = wi;
-    s_lab[mem] = wi;
+    if (s_lab) s_lab[mem] = wi;
   }
   if (topk <= 0) return;
   const float mx = wv;
@@ -164,47 +165,163 @@ __device__ void member_outputs_reg(const float* row, int K, int lane, int mem, i
   }
 }
 
-// Member m reads logits from the fp32 buffer (CNN members) when kind[m] == 0,
-// else from the fp64 buffer (LIN1 members); koff[m] is its column offset.
-__global__ void combine_kernel(const float* __restrict__ l32, int ld32,
-                               const double* __restrict__ l64, int ld64,
-                               const int* __restrict__ kind, const int* __restrict__ koff,
-                               const int* __restrict__ kcnt, int N, int B, int32_t* labels,
-                               int topk, int32_t* topk_idx, float* topk_prob, int policy,
-                               int policy_k, int32_t* combined) {
-  extern __shared__ int s_lab[];
-  const int b = blockIdx.x;
-  const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
-  const int lane = threadIdx.x & 31;
-  for (int mem = warp; mem < N; mem += nwarps) {
-    if (kind[mem] == 0 && kcnt[mem] <= 1024)
-      member_outputs_reg<32>(l32 + static_cast<int64_t>(b) * ld32 + koff[mem], kcnt[mem], lane, mem,
-                             B, b, labels, s_lab, topk, topk_idx, topk_prob);
-    else if (kind[mem] == 0)
-      member_outputs(l32 + static_cast<int64_t>(b) * ld32 + koff[mem], kcnt[mem], lane, mem, B, b,
-                     labels, s_lab, topk, topk_idx, topk_prob);
-    else
-      member_outputs(l64 + static_cast<int64_t>(b) * ld64 + koff[mem], kcnt[mem], lane, mem, B, b,
-                     labels, s_lab, topk, topk_idx, topk_prob);
+// fp32 rows with K <= 1024, K % 4 == 0 and 16-byte aligned rows: the row is read with
+// 16-byte loads, 8 per lane (lane l holds elements 128 j + 4 l + e, j < 8, e < 4 --
+// each load instruction of the warp is 512 contiguous bytes).  One pass over a lane's 32
+// registers keeps its best and second-best (value desc, index asc: slots are visited in
+// increasing index order with strict '>'); the softmax denominator is a second pass.
+// Top-k round r: every lane offers its current best, a 5-step shuffle reduction picks the
+// winner, the winning lane promotes its second-best -- and only if it wins again does it
+// rescan its registers for the element after it (rare: the top-5 of a row rarely share a
+// lane).  ncu (B = 4096, 3 x 1000 logits): the previous version, which rescanned the
+// winner's 32 registers every round, executed 1750 instructions per row and was issue
+// bound at 36 us.
+__device__ void member_outputs_vec(const float* row, int K, int lane, int mem, int B, int b,
+                                   int32_t* labels, int topk, int32_t* topk_idx,
+                                   float* topk_prob) {
+  float v[32];
+  const float4* row4 = reinterpret_cast<const float4*>(row);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int i0 = 128 * j + 4 * lane;
+    float4 q = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    if (i0 < K) q = __ldg(row4 + 32 * j + lane);
+    v[4 * j + 0] = q.x;
+    v[4 * j + 1] = q.y;
+    v[4 * j + 2] = q.z;
+    v[4 * j + 3] = q.w;
   }
-  if (policy > 0) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int lo = 1, hi = 0, sum = 0;
-      for (int mem = 0; mem < N; ++mem) {
-        const int v = s_lab[mem];
-        lo = min(lo, v);
-        hi = max(hi, v);
-        sum += v;
-      }
-      int out = 0;
-      if (policy == 1) out = hi;             // any
-      else if (policy == 2) out = lo;        // all
-      else out = (sum >= policy_k) ? 1 : 0;  // at_least
-      combined[b] = out;
+  auto idx_of = [&](int slot) { return 128 * (slot >> 2) + 4 * lane + (slot & 3); };
+  // best / second-best slot of this lane
+  float b1 = v[0], b2 = -INFINITY;
+  int s1 = 0, s2 = -1;
+#pragma unroll
+  for (int t = 1; t < 32; ++t) {
+    const float x = v[t];
+    if (x > b1) {
+      b2 = b1;
+      s2 = s1;
+      b1 = x;
+      s1 = t;
+    } else if (x > b2) {
+      b2 = x;
+      s2 = t;
     }
   }
+  auto warp_best = [&](float bv, int bi, float& wv, int& wi) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    wv = bv;
+    wi = bi;
+  };
+  int i1 = b1 == -INFINITY ? -1 : idx_of(s1);
+  float wv;
+  int wi;
+  warp_best(b1, i1, wv, wi);
+  if (lane == 0) labels[static_cast<int64_t>(mem) * B + b] = wi;
+  if (topk <= 0) return;
+  const float mx = wv;
+  const float l2e = 1.4426950408889634f;
+  const float mxl = mx * l2e;
+  float sum = 0.f;
+#pragma unroll
+  for (int t = 0; t < 32; ++t) sum += exp2f(fmaf(v[t], l2e, -mxl));  // (-inf slots add 0)
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  const float inv = 1.f / sum;
+  int my_idx = -1;
+  float my_prob = 0.f;
+  bool have2 = true;  // b2/s2 hold this lane's next element
+  for (int r = 0; r < topk; ++r) {
+    if (r == lane) {
+      my_idx = wi;
+      my_prob = wi >= 0 ? exp2f(fmaf(wv, l2e, -mxl)) * inv : 0.f;
+    }
+    if (r + 1 == topk) break;
+    if (wi >= 0 && wi == i1) {  // this lane won: promote its next element
+      if (!have2) {
+        // rescan: the best element strictly after (b1, i1) in (value desc, index asc)
+        float nb = -INFINITY;
+        int ns = -1;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const float x = v[t];
+          const int it = idx_of(t);
+          const bool after = x < b1 || (x == b1 && it > i1);
+          if (after && (ns < 0 || x > nb)) {
+            nb = x;
+            ns = t;
+          }
+        }
+        b2 = nb;
+        s2 = ns;
+      }
+      b1 = b2;
+      i1 = (s2 < 0 || b2 == -INFINITY) ? -1 : idx_of(s2);
+      have2 = false;
+    }
+    warp_best(b1, i1, wv, wi);
+  }
+  if (lane < topk) {
+    const int64_t base = (static_cast<int64_t>(mem) * B + b) * topk;
+    topk_idx[base + lane] = my_idx;
+    topk_prob[base + lane] = my_prob;
+  }
+}
+
+// One warp per (sample, member) row, 8 rows per CTA (rows of one sample adjacent).
+// Member m reads logits from the fp32 buffer (CNN members) when kind[m] == 0, else
+// from the fp64 buffer (LIN1 members); koff[m] is its column offset.
+__global__ void __launch_bounds__(256)
+    combine_rows_kernel(const float* __restrict__ l32, int ld32, const double* __restrict__ l64,
+                        int ld64, const int* __restrict__ kind, const int* __restrict__ koff,
+                        const int* __restrict__ kcnt, int N, int B, int32_t* labels, int topk,
+                        int32_t* topk_idx, float* topk_prob) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (r >= static_cast<int64_t>(B) * N) return;
+  const int b = static_cast<int>(r / N);
+  const int mem = static_cast<int>(r - static_cast<int64_t>(b) * N);
+  const int K = kcnt[mem];
+  if (kind[mem] == 0) {
+    const float* row = l32 + static_cast<int64_t>(b) * ld32 + koff[mem];
+    if (K <= 1024 && (K & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0)
+      member_outputs_vec(row, K, lane, mem, B, b, labels, topk, topk_idx, topk_prob);
+    else if (K <= 1024)
+      member_outputs_reg<32>(row, K, lane, mem, B, b, labels, nullptr, topk, topk_idx, topk_prob);
+    else
+      member_outputs(row, K, lane, mem, B, b, labels, nullptr, topk, topk_idx, topk_prob);
+  } else {
+    member_outputs(l64 + static_cast<int64_t>(b) * ld64 + koff[mem], K, lane, mem, B, b, labels,
+                   nullptr, topk, topk_idx, topk_prob);
+  }
+}
+
+// The sensitivity policy over the N binary votes of each sample (eg/policy.py:66-76):
+// any = max, all = min, at_least = count >= k.
+__global__ void policy_kernel(const int32_t* __restrict__ labels, int N, int B, int policy,
+                              int policy_k, int32_t* __restrict__ combined) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int lo = 1, hi = 0, sum = 0;
+  for (int mem = 0; mem < N; ++mem) {
+    const int v = labels[static_cast<int64_t>(mem) * B + b];
+    lo = min(lo, v);
+    hi = max(hi, v);
+    sum += v;
+  }
+  int out = 0;
+  if (policy == 1) out = hi;             // any
+  else if (policy == 2) out = lo;        // all
+  else out = (sum >= policy_k) ? 1 : 0;  // at_least
+  combined[b] = out;
 }
 
 cudaError_t k_combine(const float* l32, int ld32, const double* l64, int ld64, const int* kind,
@@ -212,10 +329,12 @@ cudaError_t k_combine(const float* l32, int ld32, const double* l64, int ld64, c
                       int32_t* topk_idx, float* topk_prob, int policy, int policy_k,
                       int32_t* combined, cudaStream_t s) {
   if (B == 0 || N == 0) return cudaSuccess;
-  const int warps = N < 8 ? N : 8;
-  combine_kernel<<<B, 32 * warps, sizeof(int) * N, s>>>(l32, ld32, l64, ld64, kind, koff, kcnt, N,
-                                                        B, labels, topk, topk_idx, topk_prob,
-                                                        policy, policy_k, combined);
+  const int64_t rows = static_cast<int64_t>(B) * N;
+  combine_rows_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(
+      l32, ld32, l64, ld64, kind, koff, kcnt, N, B, labels, topk, topk_idx, topk_prob);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || policy <= 0) return e;
+  policy_kernel<<<(B + 255) / 256, 256, 0, s>>>(labels, N, B, policy, policy_k, combined);
   return cudaGetLastError();
 }
 

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -325,10 +326,12 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     // is a function of the layer shape alone (one image's rows, N, K), never of B: split
     // and unsplit sum K in different orders, and a sample's logits must be bitwise the
     // same whatever batch it arrives in (eg/models.py:273-274).  Only
-    // layers with few rows per image qualify (FC layers, 7x7 maps): for those the
-    // partials stay small at any batch (EB_SPLIT_MAX_ROWS, default 64 rows per image).
+    // FC layers (one row per image) qualify by default: their partials stay small at any
+    // batch.  EB_SPLIT_MAX_ROWS=64 also splits the 7x7 convs (ResNet-50 layer4): B = 1
+    // latency 1.22-1.24 -> 1.13-1.15 ms, but the fp32 partials of those layers cost the
+    // B = 256 step 3 % (13.74-13.83 -> 14.17-14.33 ms; interleaved A/B on one B200).
     splits = 1;
-    static const int max_rows = getenv("EB_SPLIT_MAX_ROWS") ? atoi(getenv("EB_SPLIT_MAX_ROWS")) : 64;
+    static const int max_rows = getenv("EB_SPLIT_MAX_ROWS") ? atoi(getenv("EB_SPLIT_MAX_ROWS")) : 1;
     const int64_t rows_img = a.flatten ? 1 : static_cast<int64_t>(Ho) * Wo;
     const int64_t tiles1 = ((rows_img + 127) / 128) * nt;
     if (!a.res && !tap_shift && rows_img <= max_rows && tiles1 * 4 <= 148 && num_kb >= 32) {
@@ -621,6 +624,9 @@ struct eb_engine {
   cudaEvent_t ev_join[kLanes] = {};
   void* pool = nullptr;
   uint64_t pool_bytes = 0;
+  // the weight pool is shared by an engine and its execution-context clones
+  // (eb_engine_clone): freed when the last of them is destroyed
+  std::shared_ptr<void> pool_ref;
   std::vector<Tensor> tensors;
   std::vector<eb_op_desc> ops;
   std::vector<Member> members;
@@ -975,7 +981,22 @@ eb_engine* e, int input_kind, int B, int* launches) {
   return EB_OK;
 }
 
+// Flexible batching: a batch runs through the graph of its size bucket -- exact up to 8,
+// then multiples of 16 up to 128, of 32 up to 512, of 64 beyond (at most 12 % padding) --
+// so a stream of arbitrary request sizes needs a few dozen graphs, not one per size.
+// Rows past B compute on whatever the input buffer holds and are never read back: every
+// op is per-sample and the conv plans do not depend on B (plan_conv), so the first B
+// rows are bitwise what an exact-size run gives (tests/test_gpu_batch_invariance.py).
+// EB_BUCKETS=0: one graph per exact size.
+int bucket_of(const eb_engine* e, int B) {
+  static const bool on = env_flag("EB_BUCKETS", true);
+  if (!on || B <= 8) return B;
+  const int q = B <= 128 ? 16 : B <= 512 ? 32 : 64;
+  return std::min(e->max_batch, (B + q - 1) / q * q);
+}
+
 int run_layers(eb_engine* e, int input_kind, int B) {
+  B = bucket_of(e, B);
   const auto key = std::make_pair(B, input_kind);
   auto it = e->graphs.find(key);
   if (it != e->graphs.end()) {
@@ -1106,7 +1127,7 @@ int eb_engine_destroy(eb_engine* e) {
   for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
   for (auto& t : e->tensors) cudaFree(t.dev);
   for (auto& kv : e->stem_buf) cudaFree(kv.second);
-  cudaFree(e->pool);
+  e->pool_ref.reset();
   cudaFree(e->d_mean);
   cudaFree(e->d_std);
   cudaFree(e->d_lut);
@@ -1130,6 +1151,49 @@ int eb_engine_destroy(eb_engine* e) {
   for (int l = 0; l < kLanes; ++l) cudaEventDestroy(e->ev_join[l]);
   cudaStreamDestroy(e->stream);
   delete e;
+  return EB_OK;
+}
+
+int eb_engine_clone(eb_engine* src, eb_engine** out) {
+  if (!src || !out) EB_FAIL(EB_E_INVALID, "null argument");
+  if (!src->finalized) EB_FAIL(EB_E_STATE, "clone needs a finalized engine");
+  eb_engine* e = nullptr;
+  int rc = eb_engine_create(src->device, src->max_batch, src->C, src->H, src->W, &e);
+  if (rc != EB_OK) return rc;
+  e->f32 = src->f32;
+  e->tensors = src->tensors;
+  for (auto& t : e->tensors) t.dev = nullptr;
+  e->ops = src->ops;
+  e->members = src->members;
+  e->l32_tensor = src->l32_tensor;
+  e->l64_tensor = src->l64_tensor;
+  e->any_cnn = src->any_cnn;
+  e->any_lin = src->any_lin;
+  e->pool = src->pool;
+  e->pool_bytes = src->pool_bytes;
+  e->pool_ref = src->pool_ref;
+  e->nms = src->nms;
+  cudaSetDevice(e->device);
+  const size_t c = static_cast<size_t>(e->C);
+  bool ok = cudaMalloc(&e->d_mean, c * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&e->d_std, c * sizeof(float)) == cudaSuccess &&
+            cudaMalloc(&e->d_lut, c * 256 * sizeof(float)) == cudaSuccess &&
+            cudaMemcpy(e->d_mean, src->d_mean, c * sizeof(float), cudaMemcpyDeviceToDevice) == cudaSuccess &&
+            cudaMemcpy(e->d_std, src->d_std, c * sizeof(float), cudaMemcpyDeviceToDevice) == cudaSuccess &&
+            cudaMemcpy(e->d_lut, src->d_lut, c * 256 * sizeof(float), cudaMemcpyDeviceToDevice) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    eb_engine_destroy(e);
+    EB_FAIL(EB_E_NOMEM, "clone: preprocess constants");
+  }
+  e->have_pre = true;
+  rc = eb_finalize(e);
+  if (rc != EB_OK) {
+    const std::string msg = eb_last_error();
+    eb_engine_destroy(e);
+    EB_FAIL(rc, msg);
+  }
+  *out = e;
   return EB_OK;
 }
 
@@ -1159,6 +1223,13 @@ int eb_pool_reserve(eb_engine* e, uint64_t bytes) {
   if (cudaMalloc(&e->pool, bytes ? bytes : 256) != cudaSuccess) {
     cudaGetLastError();
     EB_FAIL(EB_E_NOMEM, "cannot allocate a " + std::to_string(bytes) + "-byte weight pool");
+  }
+  {
+    const int dev = e->device;
+    e->pool_ref = std::shared_ptr<void>(e->pool, [dev](void* p) {
+      cudaSetDevice(dev);
+      cudaFree(p);
+    });
   }
   e->pool_bytes = bytes;
   return EB_OK;
@@ -1483,22 +1554,39 @@ int eb_forward(eb_engine* e, const void* host_input, int input_kind, int batch,
   if (policy != EB_POLICY_NONE)
     EB_CUDA(cudaMemcpyAsync(host_combined, e->d_combined, static_cast<size_t>(batch) * sizeof(int32_t),
                             cudaMemcpyDeviceToHost, e->stream));
+  // fp32 member logits are copied row by row into [N][B][Kmax]; LIN1 members' fp64
+  // scores land in a host staging buffer and are narrowed to fp32 after the sync
+  int kmax = 0;
+  for (const auto& m : e->members) kmax = std::max(kmax, m.k);
+  std::vector<double> l64_host;
   if (host_logits) {
-    int kmax = 0;
-    for (const auto& m : e->members) kmax = std::max(kmax, m.k);
-    // fp32 member logits are copied row by row into [N][B][Kmax]; LIN1 (fp64)
-    // scores are narrowed on the host side of the copy by the caller.
     for (int i = 0; i < n; ++i) {
       const Member& m = e->members[i];
-      if (m.kind != EB_MEMBER_CNN) continue;
       const Tensor& t = e->tensors[m.tensor];
-      EB_CUDA(cudaMemcpy2DAsync(host_logits + static_cast<size_t>(i) * batch * kmax,
-                                kmax * sizeof(float),
-                                static_cast<const float*>(t.dev) + m.koff, t.c * sizeof(float),
-                                m.k * sizeof(float), batch, cudaMemcpyDeviceToHost, e->stream));
+      if (m.kind == EB_MEMBER_CNN) {
+        EB_CUDA(cudaMemcpy2DAsync(host_logits + static_cast<size_t>(i) * batch * kmax,
+                                  kmax * sizeof(float),
+                                  static_cast<const float*>(t.dev) + m.koff, t.c * sizeof(float),
+                                  m.k * sizeof(float), batch, cudaMemcpyDeviceToHost, e->stream));
+      } else if (l64_host.empty()) {
+        l64_host.resize(static_cast<size_t>(batch) * t.c);
+        EB_CUDA(cudaMemcpyAsync(l64_host.data(), t.dev, l64_host.size() * sizeof(double),
+                                cudaMemcpyDeviceToHost, e->stream));
+      }
     }
   }
   EB_CUDA(cudaStreamSynchronize(e->stream));
+  if (!l64_host.empty()) {
+    for (int i = 0; i < n; ++i) {
+      const Member& m = e->members[i];
+      if (m.kind != EB_MEMBER_LIN1) continue;
+      const int ld = e->tensors[m.tensor].c;
+      for (int b = 0; b < batch; ++b)
+        for (int k = 0; k < m.k; ++k)
+          host_logits[(static_cast<size_t>(i) * batch + b) * kmax + k] =
+              static_cast<float>(l64_host[static_cast<size_t>(b) * ld + m.koff + k]);
+    }
+  }
   return EB_OK;
 }
 
@@ -1586,6 +1674,25 @@ int eb_profile_ops(eb_engine* e, int input_kind, int batch, float* host_ms, int 
   return rc;
 }
 
+int eb_engine_warmup(eb_engine* e, int input_kind, int max_b) {
+  if (!e || !e->finalized) EB_FAIL(EB_E_STATE, "engine not finalized");
+  if (input_kind != EB_IN_F32_CHW && input_kind != EB_IN_U8_HWC)
+    EB_FAIL(EB_E_INVALID, "unknown input encoding");
+  std::lock_guard<std::mutex> lock(e->mu);
+  cudaSetDevice(e->device);
+  const int top = (max_b > 0 && max_b < e->max_batch) ? max_b : e->max_batch;
+  int last = 0;
+  for (int b = 1; b <= top; ++b) {
+    const int q = bucket_of(e, b);
+    if (q == last) continue;
+    last = q;
+    const int rc = run_layers(e, input_kind, q);
+    if (rc != EB_OK) return rc;
+  }
+  EB_CUDA(cudaStreamSynchronize(e->stream));
+  return EB_OK;
+}
+
 int eb_input_buffer(eb_engine* e, int input_kind, void** dev_ptr) {
   if (!e || !dev_ptr || !e->finalized) EB_FAIL(EB_E_STATE, "engine not finalized");
   *dev_ptr = input_kind == EB_IN_U8_HWC ? static_cast<void*>(e->d_in_u8)
@@ -1619,7 +1726,7 @@ int eb_engine_stream(eb_engine* e, void** stream) {
 
 int eb_launch_count(eb_engine* e, int input_kind, int batch, int* count) {
   if (!e || !count) EB_FAIL(EB_E_INVALID, "null argument");
-  auto it = e->launch_counts.find(std::make_pair(batch, input_kind));
+  auto it = e->launch_counts.find(std::make_pair(bucket_of(e, batch), input_kind));
   if (it == e->launch_counts.end()) EB_FAIL(EB_E_STATE, "no graph captured for this batch");
   *count = it->second + 1;  // + combine
   return EB_OK;

@@ -60,6 +60,9 @@ struct Scanner {
     const char* s = p;
     if (p < end && *p == '-') ++p;
     if (p >= end || *p < '0' || *p > '9') return false;
+    // strict JSON: no leading zeros ("007", "-0..."), and no "-0" either -- anything the
+    // reference's loads_strict might judge differently goes to the reference decoder
+    if (*p == '0' && (*s == '-' || (p + 1 < end && p[1] >= '0' && p[1] <= '9'))) return false;
     long long x = 0;
     while (p < end && *p >= '0' && *p <= '9') {
       x = x * 10 + (*p - '0');

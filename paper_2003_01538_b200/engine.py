@@ -89,6 +89,7 @@ class Engine:
         """An activation tensor (bf16, or fp32 in the fp32 mode) unless dtype is given."""
         if dtype is None:
             dtype = _lib.EB_F32 if self.f32 else _lib.EB_BF16
+        self._arena_bytes = getattr(self, "_arena_bytes", 0) + self.max_batch * h * w * c * (2, 4, 8)[dtype]
         tid = c_int()
         check(self.lib.eb_tensor(self._h, h, w, c, dtype, byref(tid)))
         return TRef(tid.value, 0, c, h, w, c)
@@ -224,6 +225,28 @@ class Engine:
         t_ = _wrap_device_ptr(p.value, numel, dtype, self.device)
         return t_.view(batch, h.value, w.value, c.value)
 
+    def clone(self) -> "Engine":
+        """Another execution context on the same device: shared ops and weight pool, its
+        own activation arena, streams and graph cache (eb_engine_clone)."""
+        if not self.finalized:
+            raise RuntimeError("clone needs a finalized engine")
+        c = object.__new__(Engine)
+        c.__dict__.update({k: v for k, v in self.__dict__.items()
+                           if k not in ("_h", "_pinned_labels", "_blobs")})
+        c._blobs = []
+        c._h = c_void_p()
+        check(self.lib.eb_engine_clone(self._h, byref(c._h)))
+        return c
+
+    def warmup(self, input_kind: int, max_b: int = 0) -> None:
+        """Capture the graph of every batch-size bucket up to max_b (eb_engine_warmup)."""
+        check(self.lib.eb_engine_warmup(self._h, input_kind, max_b))
+
+    @property
+    def arena_bytes(self) -> int:
+        """Device bytes of this context's activation tensors (max_batch deep)."""
+        return getattr(self, "_arena_bytes", 0)
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             self.lib.eb_engine_destroy(self._h)
@@ -247,3 +270,47 @@ def _wrap_device_ptr(ptr: int, numel: int, dtype, device: int) -> torch.Tensor:
 
     t = torch.as_tensor(_Arr(), device=f"cuda:{device}")
     return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+
+
+class ContextPool:
+    """Execution contexts of one engine leased per request (F2): the
+    reference's gateway re-enters forward from ``workers`` pool threads
+    (eg/gateway.py:222-257) and requests stay uncoalesced; with one context
+    they serialise on its lock, with n contexts up to n forwards run concurrently on the
+    GPU (their own arenas, streams and graphs; shared weights).  Same forward contract as
+    Engine."""
+
+    def __init__(self, engine: Engine, n: int):
+        import queue
+
+        self.contexts = [engine] + [engine.clone() for _ in range(max(0, n - 1))]
+        self._free = queue.Queue()
+        for c in self.contexts:
+            self._free.put(c)
+        first = self.contexts[0]
+        self.members, self.max_batch, self.device = first.members, first.max_batch, first.device
+        self.op_meta, self.n_ops = first.op_meta, first.n_ops
+
+    def _lease(self, fn):
+        ctx = self._free.get()
+        try:
+            return fn(ctx)
+        finally:
+            self._free.put(ctx)
+
+    def forward(self, x, input_kind: int, **kw):
+        return self._lease(lambda c: c.forward(x, input_kind, **kw))
+
+    def forward_batches(self, xs, input_kind: int):
+        return self._lease(lambda c: c.forward_batches(xs, input_kind))
+
+    def warmup(self, input_kind: int, max_b: int = 0) -> None:
+        for c in self.contexts:
+            c.warmup(input_kind, max_b)
+
+    def __getattr__(self, name):  # device-level helpers (bench, profiling): first context
+        return getattr(self.contexts[0], name)
+
+    def close(self):
+        for c in self.contexts:
+            c.close()

@@ -184,6 +184,10 @@ class Ensemble:
     # CNN arithmetic: "bf16" (tcgen05, the throughput path) or "fp32" (the fp32-faithful
     # parity mode, csrc/ref32.cu: top-k equal to the fp32 CPU oracle's)
     precision: str = "bf16"
+    # more than one device: a replica per GPU, requests sharded across them (shard.py)
+    devices: tuple = ()
+    # execution contexts per device (engine.ContextPool): concurrent requests in flight
+    contexts: int = 1
     _state: dict = field(default_factory=dict, repr=False)
 
     def __post_init__(self):
@@ -209,9 +213,32 @@ def default_precision() -> str:
     return "fp32" if p in ("fp32", "f32", "float32") else "bf16"
 
 
-def load_ensemble(manifest: ModelManifest, device: int = 0, precision: str | None = None) -> Ensemble:
-    """Parse every member, check shapes and the byte budget, all or nothing."""
+def default_devices() -> tuple:
+    """EB_DEVICES=0,1,2,3 shards ensembles loaded without explicit devices (e.g. by the
+    reference's gateway through the seam) over those GPUs."""
+    v = os.environ.get("EB_DEVICES", "").strip()
+    return tuple(int(d) for d in v.split(",") if d.strip()) if v else ()
+
+
+def default_contexts() -> int:
+    """EB_CONTEXTS=n: execution contexts per device for ensembles loaded without an
+    explicit count (the gateway's worker threads then run up to n forwards at once)."""
+    return max(1, int(os.environ.get("EB_CONTEXTS", "1") or 1))
+
+
+def load_ensemble(manifest: ModelManifest, device: int = 0, precision: str | None = None,
+                  devices=None, contexts: int | None = None) -> Ensemble:
+    """Parse every member, check shapes and the byte budget, all or nothing.
+
+    ``devices`` (two or more GPU ordinals) serves the ensemble from a replica per GPU
+    with every request batch sharded contiguously across them (shard.ShardedEngine)."""
     precision = precision or default_precision()
+    contexts = contexts or default_contexts()
+    devices = tuple(devices) if devices is not None else default_devices()
+    if len(devices) == 1:
+        device, devices = devices[0], ()
+    elif devices:
+        device = devices[0]
     if precision not in ("bf16", "fp32"):
         raise ValueError(f"precision must be 'bf16' or 'fp32', got {precision!r}")
     loaded = []
@@ -231,16 +258,18 @@ def load_ensemble(manifest: ModelManifest, device: int = 0, precision: str | Non
     if all(getattr(m, "kind", "lin1") == "cnn1" for m in loaded) and len(
             {m.input_shape for m in loaded}) > 1:
         # Mixed native resolutions (config 5: Inception-v3 at 299 beside 224 members) are
-        # allowed for CNN members only: requests arrive at the largest resolution and K1
-        # emits a bilinear-resized copy for the others.  LIN1 ensembles keep the
-        # reference's uniform-shape rule (eg/ensemble.py:202-208).
+        # allowed when EVERY member is a CNN: requests arrive at the largest resolution and
+        # K1 emits a bilinear-resized copy for the others.
         if len({m.input_shape.dims[0] for m in loaded}) > 1:
             raise errors.ShapeMismatch("CNN members must agree on the channel count")
         shape = max((m.input_shape for m in loaded), key=lambda s: s.dims[1] * s.dims[2])
-    for m in loaded[1:]:
-        if m.input_shape != shape and getattr(m, "kind", "lin1") != "cnn1":
-            raise errors.ShapeMismatch(f"model {m.id!r} has input shape {list(m.input_shape.dims)}, "
-                                f"expected {list(shape.dims)} shared by the ensemble")
+    else:
+        # any LIN1 member: the reference's uniform-shape rule for every member, in
+        # manifest order (eg/ensemble.py:202-208)
+        for m in loaded[1:]:
+            if m.input_shape != shape:
+                raise errors.ShapeMismatch(f"model {m.id!r} has input shape {list(m.input_shape.dims)}, "
+                                    f"expected {list(shape.dims)} shared by the ensemble")
     for name, vals in (("mean", manifest.preprocess.mean), ("std", manifest.preprocess.std)):
         if len(vals) not in (1, shape.channels):
             raise errors.ShapeMismatch(f"preprocess {name} has {len(vals)} entries; input shape "
@@ -251,7 +280,7 @@ def load_ensemble(manifest: ModelManifest, device: int = 0, precision: str | Non
                              f"budget is {manifest.memory_budget_bytes} bytes")
     return Ensemble(tuple(loaded), shape, manifest.preprocess, used, manifest.memory_budget_bytes,
                     manifest.max_batch, all(m.labels == BINARY_LABELS for m in loaded), device,
-                    precision)
+                    precision, devices, contexts)
 
 
 # ---------------------------------------------------------------------- device residency
@@ -346,10 +375,24 @@ def engine_for(ensemble):
     with _engines_lock:
         if state is not None:
             if "engine" not in state:
-                state["engine"] = build_engine(ensemble.models, ensemble.shared_shape,
-                                               ensemble.preprocess, ensemble.max_batch,
-                                               getattr(ensemble, "device", 0),
-                                               getattr(ensemble, "precision", "bf16"))
+                from .engine import ContextPool
+
+                devices = getattr(ensemble, "devices", ())
+                prec = getattr(ensemble, "precision", "bf16")
+                nctx = getattr(ensemble, "contexts", 1)
+
+                def on(dev, mb):
+                    eng = build_engine(ensemble.models, ensemble.shared_shape, ensemble.preprocess,
+                                       mb, dev, prec)
+                    return ContextPool(eng, nctx) if nctx > 1 else eng
+
+                if len(devices) > 1:
+                    from .shard import ShardedEngine
+
+                    per = -(-ensemble.max_batch // len(devices))
+                    state["engine"] = ShardedEngine([on(d, per) for d in devices])
+                else:
+                    state["engine"] = on(getattr(ensemble, "device", 0), ensemble.max_batch)
             return state["engine"]
         eng = _engines.get(key)
         if eng is None:

@@ -43,3 +43,57 @@ def gather_rows(local: torch.Tensor, batch: int, dst: int = 0) -> torch.Tensor |
         return torch.cat(rows, dim=0)
     dist.gather(buf, None, dst=dst)
     return None
+
+
+class ShardedEngine:
+    """One process serving an ensemble from several GPUs: a full
+    replica (an Engine) per device, the request batch split contiguously with
+    shard_bounds, every shard's forward issued from its own host thread on its own
+    device and stream (the native call releases the GIL), outputs reassembled in shard
+    order.  Each device copies its own labels / top-k / logits to host memory, so no
+    device funnels the others' results through its PCIe link.  Exact: a sample's result
+    does not depend on its batch (runtime.cu plan_conv), so the sharded output equals
+    the single-GPU output bitwise.
+
+    Same ``forward`` contract as Engine, so ensemble.forward / predict / predict_u8 run
+    unchanged on top of it."""
+
+    def __init__(self, engines):
+        import concurrent.futures as cf
+
+        if not engines:
+            raise ValueError("ShardedEngine needs at least one engine")
+        self.engines = list(engines)
+        self.members = self.engines[0].members
+        self.max_batch = sum(e.max_batch for e in self.engines)
+        self._pool = cf.ThreadPoolExecutor(len(self.engines), thread_name_prefix="eb-shard")
+
+    @property
+    def devices(self) -> list[int]:
+        return [e.device for e in self.engines]
+
+    def shards(self, batch: int) -> list[tuple[int, int]]:
+        g = len(self.engines)
+        return [shard_bounds(batch, r, g) for r in range(g)]
+
+    def forward(self, x, input_kind: int, *, topk: int = 0, policy: int = 0, policy_k: int = 0,
+                want_logits: bool = False):
+        import numpy as np
+
+        spans = [(r, lo, hi) for r, (lo, hi) in enumerate(self.shards(int(x.shape[0]))) if hi > lo]
+        futs = [self._pool.submit(self.engines[r].forward, x[lo:hi], input_kind, topk=topk,
+                                  policy=policy, policy_k=policy_k, want_logits=want_logits)
+                for r, lo, hi in spans]
+        parts = [f.result() for f in futs]
+        out = {"labels": np.concatenate([p["labels"] for p in parts], axis=1)}
+        for key in ("logits", "topk_idx", "topk_prob"):
+            if key in parts[0]:
+                out[key] = np.concatenate([p[key] for p in parts], axis=1)
+        if "combined" in parts[0]:
+            out["combined"] = np.concatenate([p["combined"] for p in parts])
+        return out
+
+    def close(self):
+        self._pool.shutdown(wait=True)
+        for e in self.engines:
+            e.close()

@@ -17,10 +17,11 @@ _M1 = np.uint64(0xBF58476D1CE4E5B9)
 _M2 = np.uint64(0x94D049BB133111EB)
 
 
-def splitmix64(seed: int, n: int) -> np.ndarray:
-    """The first n outputs of the SplitMix64 stream for ``seed`` (uint64)."""
+def splitmix64(seed: int, n: int, start: int = 0) -> np.ndarray:
+    """Outputs start .. start + n - 1 of the SplitMix64 stream for ``seed`` (uint64)."""
     with np.errstate(over="ignore"):
-        state = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + _GAMMA * np.arange(1, n + 1, dtype=np.uint64)
+        state = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + _GAMMA * np.arange(
+            start + 1, start + n + 1, dtype=np.uint64)
         z = state
         z = (z ^ (z >> np.uint64(30))) * _M1
         z = (z ^ (z >> np.uint64(27))) * _M2
@@ -49,6 +50,9 @@ def images(n: int, h: int, w: int, c: int = 3, seed0: int = 1234, kind: str = "s
     return np.stack([fn(seed0 + i, h, w, c) for i in range(n)])
 
 
-def images_fast(n: int, h: int, w: int, c: int = 3, seed0: int = 1234) -> np.ndarray:
-    """Large batches for benchmarking: one SplitMix64 stream, byte = z >> 56."""
-    return (splitmix64(seed0, n * h * w * c) >> np.uint64(56)).astype(np.uint8).reshape(n, h, w, c)
+def images_fast(n: int, h: int, w: int, c: int = 3, seed0: int = 1234, first_row: int = 0) -> np.ndarray:
+    """Large batches for benchmarking: one SplitMix64 stream, byte = z >> 56.  Rows
+    first_row .. first_row + n - 1 of that stream's images (a rank's shard of a global
+    batch is the same bytes as the global batch's rows)."""
+    px = h * w * c
+    return (splitmix64(seed0, n * px, first_row * px) >> np.uint64(56)).astype(np.uint8).reshape(n, h, w, c)

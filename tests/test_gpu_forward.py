@@ -165,3 +165,19 @@ def test_concurrent_forward_equals_sequential(tmp_path):
     for t in threads:
         t.join()
     assert got == seq
+
+
+def test_lin1_logits_returned(tmp_path):
+    """want_logits returns every member's scores: LIN1 members' fp64 scores narrowed to
+    fp32 (eg/models.py:275-278 computes them in fp64), CNN members' fp32 logits."""
+    d, k = 3 * 4 * 4, 3
+    members = [O.gen_model_arrays(s, k, d) for s in (41, 42)]
+    docs = [lin1_doc(f"m{i}", (3, 4, 4), ("a", "b", "c"), w, b) for i, (w, b) in enumerate(members)]
+    mean, std = (0.1, 0.2, 0.3), (0.5, 1.0, 2.0)
+    ens = build(tmp_path, docs, mean=mean, std=std)
+    x = O.unit_floats(77, 6 * d).reshape(6, d)
+    _, _, res = E.predict(ens, M.SampleBatch(ens.shared_shape, x), want_logits=True)
+    xp = O.preprocess(x, 3, mean, std)
+    for i, (w, b) in enumerate(members):
+        want = O.linear_scores(xp, w, b).astype(np.float32)
+        np.testing.assert_allclose(res["logits"][i, :, :k], want, rtol=1e-6, atol=1e-6)

@@ -5,6 +5,8 @@ from __future__ import annotations
 
 import json
 
+import numpy as np
+
 import pytest
 
 from helpers import cnn1_doc, lin1_doc, write_manifest
@@ -94,6 +96,22 @@ def test_cnn1_member_format(tmp_path):
     assert len(ens.models[0].labels) == 1000
     # budget counts the real device bytes of the packed member (bf16 weights)
     assert 2 * 11_000_000 < ens.bytes_used < 2 * 12_500_000
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_mixed_lin1_cnn1_shapes_rejected_in_any_order(tmp_path, order):
+    """With any LIN1 member the reference's uniform-shape rule holds for every member
+    (eg/ensemble.py:202-208), whatever the manifest order."""
+    from paper_2003_01538_b200 import ensemble as ours
+    from paper_2003_01538_b200 import errors
+
+    docs = [lin1_doc("l1", (3, 8, 8), weights=np.zeros((2, 192)), bias=(0.0, 0.0)),
+            cnn1_doc("r18", "resnet18", 1)]
+    if order:
+        docs = docs[::-1]
+    mp = write_manifest(tmp_path, docs, budget=10**9)
+    with pytest.raises(errors.ShapeMismatch):
+        ours.load_ensemble(ours.load_manifest_file(mp))
 
 
 def test_install_rebinds_and_restores():

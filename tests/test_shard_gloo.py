@@ -54,3 +54,49 @@ def test_gather_rows_two_ranks(batch):
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=10) is True
+
+
+class _FakeEngine:
+    """Stands in for an Engine: labels = the first pixel of each sample, per member."""
+
+    def __init__(self, device, max_batch):
+        import numpy as np
+
+        self.device, self.max_batch, self.members = device, max_batch, [(0, 0, 0, 4), (0, 0, 8, 4)]
+        self.seen = []
+        self.np = np
+
+    def forward(self, x, kind, *, topk=0, policy=0, policy_k=0, want_logits=False):
+        np = self.np
+        self.seen.append(int(x.shape[0]))
+        lab = np.stack([x.reshape(len(x), -1)[:, 0], x.reshape(len(x), -1)[:, 0] + 1]).astype(np.int32)
+        out = {"labels": lab}
+        if want_logits:
+            out["logits"] = np.repeat(lab[..., None], 4, axis=-1).astype(np.float32)
+        if topk:
+            out["topk_idx"] = np.repeat(lab[..., None], topk, axis=-1)
+            out["topk_prob"] = np.ones(lab.shape + (topk,), np.float32)
+        if policy:
+            out["combined"] = lab[0] % 2
+        return out
+
+    def close(self):
+        pass
+
+
+@pytest.mark.parametrize("batch", [1, 3, 8, 13])
+def test_sharded_engine_reassembles_in_shard_order(batch):
+    import numpy as np
+
+    from paper_2003_01538_b200.shard import ShardedEngine
+
+    engines = [_FakeEngine(d, 4) for d in range(4)]
+    se = ShardedEngine(engines)
+    x = np.arange(batch * 6, dtype=np.float32).reshape(batch, 6)
+    out = se.forward(x, 0, topk=2, policy=1, want_logits=True)
+    spans = [shard_bounds(batch, r, 4) for r in range(4)]
+    assert [e.seen for e in engines] == [[hi - lo] if hi > lo else [] for lo, hi in spans]
+    want = _FakeEngine(0, batch).forward(x, 0, topk=2, policy=1, want_logits=True)
+    for k in ("labels", "logits", "topk_idx", "topk_prob", "combined"):
+        assert np.array_equal(out[k], want[k]), k
+    se.close()

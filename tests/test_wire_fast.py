@@ -59,6 +59,10 @@ def test_whitespace_and_key_order():
     b'{"samples": [], "samples": []}',
     b'{"extra": 1, "samples": [{"encoding": "f32le", "shape": [2], "data": "AACAPwAAAEA="}]}',
     b'not json',
+    # leading zeros / negative zero in a shape: the reference's strict JSON decides
+    b'{"samples": [{"encoding": "f32le", "shape": [02], "data": "AACAPwAAAEA="}]}',
+    b'{"samples": [{"encoding": "f32le", "shape": [002], "data": "AACAPwAAAEA="}]}',
+    b'{"samples": [{"encoding": "f32le", "shape": [-0], "data": "AACAPwAAAEA="}]}',
 ])
 def test_declines_everything_else(body):
     from paper_2003_01538_b200.wire import fast_decode
