@@ -93,6 +93,10 @@ class ShardedEngine:
             out["combined"] = np.concatenate([p["combined"] for p in parts])
         return out
 
+    def warmup(self, input_kind: int, max_b: int = 0) -> None:
+        for f in [self._pool.submit(e.warmup, input_kind, max_b) for e in self.engines]:
+            f.result()
+
     def close(self):
         self._pool.shutdown(wait=True)
         for e in self.engines:
