@@ -305,7 +305,8 @@ def track_r_gpu(pk: dict, steps: int = 10) -> dict:
             e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
-        bytes_ = 4 * B * d * 2 + 4 * n * k * d + 4 * n * k + 4 * n * B  # x in, K1 out/K6 in, W, b, labels
+        # K1: x read + normalised x written; K6: normalised x + W read; bias; labels
+        bytes_ = 4 * B * d * 3 + 4 * n * k * d + 4 * n * k + 4 * n * B
         flops = 2.0 * B * d * n * k
         out[name] = {"batch": B, "members": n, "K": k, "D": d, "ms": ms, "images_per_s": B / (ms / 1e3),
                      "bytes": bytes_, "achieved_gbs": bytes_ / ms / 1e6,
@@ -498,6 +499,8 @@ def main() -> None:
     ap.add_argument("--profile-json", default="", help="write the per-op profile here")
     ap.add_argument("--minimal", action="store_true",
                     help="timed steps only (for ncu launch lists): no e2e / latency / profile / cpu")
+    ap.add_argument("--c4", action="store_true",
+                    help="run the C4 (sharded global batch + NCCL gather) path even at N = 1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -517,7 +520,15 @@ def main() -> None:
         sys.exit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun "
                  f"--nproc-per-node {args.gpus}, or without torchrun to let bench.py spawn the ranks")
     torch.cuda.set_device(local)
-    if world > 1:
+    c4 = world > 1 or args.c4
+    if c4:
+        if "MASTER_ADDR" not in os.environ:  # --c4 at N = 1 without torchrun
+            import socket
+
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(so.getsockname()[1]),
+                                  RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2003_01538_b200 import _lib, synth
@@ -526,7 +537,7 @@ def main() -> None:
 
     # N = 1: C2 at B = 256 (BASELINE configs[1]); N > 1: C4, a global batch of 4096 split
     # contiguously (2048 / 1024 / 512 per rank), logits gathered to rank 0 over NCCL.
-    if world > 1:
+    if c4:
         lo, hi = shard_bounds(args.global_batch, rank, world)
         B, global_b = hi - lo, args.global_batch
     else:
@@ -553,7 +564,7 @@ def main() -> None:
 
     def step():
         eng.forward_device(B, kind, TOPK)
-        if world > 1:  # every shard's logits to the serving rank, on the engine stream
+        if c4:  # every shard's logits to the serving rank, on the engine stream
             with torch.cuda.stream(stream):
                 gather_rows(logits_t, global_b, dst=0)
 
@@ -564,7 +575,7 @@ def main() -> None:
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    if world > 1:
+    if c4:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -577,7 +588,7 @@ def main() -> None:
                 ev[i][1].record(stream)
         torch.cuda.synchronize()
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
-    if world > 1:
+    if c4:
         t = torch.tensor([dev_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_ms = float(t.item())
@@ -588,7 +599,7 @@ def main() -> None:
         if rank == 0:
             print(json.dumps({"minimal": True, "value": value, "ms_per_step": dev_ms / args.steps,
                               "launches_per_step": n_launch}), flush=True)
-        if world > 1:
+        if c4:
             dist.destroy_process_group()
         return
     # ---- e2e through the public C-ABI with pinned host buffers: every step copies its
@@ -601,12 +612,12 @@ def main() -> None:
     step_inputs = [host_np if i % 2 == 0 else host2 for i in range(args.steps)]
 
     def timed(fn):
-        if world > 1:
+        if c4:
             dist.barrier()
         t0 = time.perf_counter()
         fn()
         el = time.perf_counter() - t0
-        if world > 1:
+        if c4:
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
@@ -624,7 +635,7 @@ def main() -> None:
     n_members = len(eng.members)
 
     extras = {}
-    if world == 1 and not args.quick:
+    if not c4 and not args.quick:
         # the reference-shaped drop-in call: forward(ensemble, SampleBatch) with f32 CHW
         # samples from ordinary (pageable) numpy memory, 4x the H2D bytes of u8
         from paper_2003_01538_b200 import ensemble as E
@@ -650,7 +661,7 @@ def main() -> None:
         eng.forward(one, kind)
         lat.append((time.perf_counter() - t0) * 1e3)
     sweep = {}
-    if world == 1 and not args.quick:
+    if not c4 and not args.quick:
         for b in (1, 8, 32, 64, 128, 256):
             if b <= B:
                 sweep[str(b)] = device_rate(eng, b, kind, stream, TOPK)
@@ -683,16 +694,16 @@ def main() -> None:
             [{"i": i, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in m.items()}, "ms": float(t)}
              for i, (m, t) in enumerate(zip(eng.op_meta, ms))], indent=0))
 
-    hbm = hbm_kernels(B, pk["hbm_gbs"], pk_src) if rank == 0 and world == 1 else None
+    hbm = hbm_kernels(B, pk["hbm_gbs"], pk_src) if rank == 0 and not c4 else None
     eng_dev = eng.device
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not c4 and not args.no_cpu_baseline:
         try:
             cpu = cpu_oracle_rate()
         except Exception as exc:  # the baseline is reported, never fatal
             cpu = {"error": str(exc)[:200]}
-    if world == 1 and not args.quick:
+    if not c4 and not args.quick:
         # free this engine before the extra configurations are built
         eng.close()
         del eng, ens, logits_t, staging
@@ -710,7 +721,6 @@ def main() -> None:
             extras["track_r"] = {"error": str(exc)[:300]}
 
     if rank == 0:
-        c4 = world > 1
         line = {
             "metric": "ensemble images/s (N-model fwd+combine)",
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
@@ -755,7 +765,7 @@ def main() -> None:
         if extras:
             line["extras"] = extras
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if c4:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -353,52 +353,148 @@ cudaError_t k_combine(const float* l32, int ld32, const double* l64, int ld64, c
 // logits[b, k] = sum_d f64(x[b, d]) * f64(W[k, d])  (+ bias[k] afterwards),
 // eg/models.py:275-278.  Products of two fp32 values are exact in fp64, so the
 // only rounding is in the summation.  The d range is cut into `nsplit` fixed
-// slices that depend on D only; each slice is summed in ascending d by one
-// thread, and slices are added in ascending order by the reduce kernel.  A
+// slices that depend on D only; each slice is summed in a fixed order (below), and
+// slices are added in ascending order by the reduce kernel.  A
 // sample's logits are therefore bitwise independent of the batch it arrives in
 // (the reference's batch == concatenated singles property, eg/models.py:273-274).
 
-constexpr int kLinTile = 32;
-constexpr int kLinChunk = 32;
-
-__global__ void lin1_partial_kernel(const float* __restrict__ x, const float* __restrict__ w,
-                                    double* __restrict__ part, int B, int K, int64_t D,
-                                    int64_t dslice) {
-  __shared__ float sx[kLinTile][kLinChunk + 1];
-  __shared__ float sw[kLinTile][kLinChunk + 1];
-  const int tx = threadIdx.x & 15;  // k direction
-  const int ty = threadIdx.x >> 4;  // b direction
-  const int b0 = blockIdx.x * kLinTile;
-  const int k0 = blockIdx.y * kLinTile;
-  const int64_t d0 = blockIdx.z * dslice;
-  int64_t d1 = d0 + dslice;
-  if (d1 > D) d1 = D;
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  for (int64_t dc = d0; dc < d1; dc += kLinChunk) {
-    for (int i = threadIdx.x; i < kLinTile * kLinChunk; i += blockDim.x) {
-      const int r = i / kLinChunk;
-      const int c = i % kLinChunk;
-      const int64_t d = dc + c;
-      const bool dok = d < d1;
-      sx[r][c] = (dok && b0 + r < B) ? x[static_cast<int64_t>(b0 + r) * D + d] : 0.f;
-      sw[r][c] = (dok && k0 + r < K) ? w[static_cast<int64_t>(k0 + r) * D + d] : 0.f;
+// Small sum-K (binary members: 2 per member): one warp per sample and d-slice; lane l sums
+// d = d0 + l, d0 + l + 32, ... of the slice in ascending order for every k, then a fixed
+// shuffle tree adds the 32 lane sums (lane 0's result is kept) -- deterministic and a
+// function of D only.  x is read once, coalesced; the 8 warps of a CTA (8 samples) share
+// the slice of W through L1.  KS = sum K is a template value (no predication, the K
+// weight rows' addresses hoisted out of the d loop).
+constexpr int kLinSmallK = 16;
+constexpr int kLinSmallChunk = 256;
+// SPW samples per warp (8 warps: 8 * SPW samples per CTA): each fp64 weight read from
+// shared memory feeds SPW FMAs (B200, B = 256, D = 150528, sum K = 6: SPW 1 / 2 / 4 =
+// 116 / 124 / 113 us -- fp64-FMA bound; the first version without the fp64 weight stage
+// and with predicated K ran 961 us)
+template <int KS, int SPW>
+__global__ void __launch_bounds__(256)
+    lin1_small_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                      double* __restrict__ part, int B, int64_t D, int64_t dslice) {
+  // the slice's weights, converted to fp64 once per CTA (not once per sample), chunk by chunk
+  __shared__ double sw[KS][kLinSmallChunk];
+  const int lane = threadIdx.x & 31;
+  const int bw = (blockIdx.x * 8 + (threadIdx.x >> 5)) * SPW;  // the warp's first sample
+  const int64_t d0 = blockIdx.y * dslice;
+  const int n = static_cast<int>((d0 + dslice < D ? d0 + dslice : D) - d0);
+  double acc[SPW][KS];
+#pragma unroll
+  for (int j = 0; j < SPW; ++j)
+#pragma unroll
+    for (int k = 0; k < KS; ++k) acc[j][k] = 0.0;
+  const float* xb[SPW];
+#pragma unroll
+  for (int j = 0; j < SPW; ++j) xb[j] = x + static_cast<int64_t>(bw + j < B ? bw + j : 0) * D + d0;
+  for (int c0 = 0; c0 < n; c0 += kLinSmallChunk) {
+    const int cn = n - c0 < kLinSmallChunk ? n - c0 : kLinSmallChunk;
+    __syncthreads();
+    for (int t = threadIdx.x; t < KS * kLinSmallChunk; t += 256) {
+      const int k = t / kLinSmallChunk, i = t - k * kLinSmallChunk;
+      sw[k][i] = i < cn ? static_cast<double>(__ldg(w + k * D + d0 + c0 + i)) : 0.0;
     }
     __syncthreads();
-#pragma unroll 8
+    if (bw < B) {
+      // all of the chunk's x loads of this lane in flight at once (8 per sample)
+      float xr[SPW][kLinSmallChunk / 32];
+#pragma unroll
+      for (int q = 0; q < kLinSmallChunk / 32; ++q) {
+        const int i = lane + 32 * q;
+#pragma unroll
+        for (int j = 0; j < SPW; ++j) xr[j][q] = i < cn ? __ldg(xb[j] + c0 + i) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < kLinSmallChunk / 32; ++q) {
+        const int i = lane + 32 * q;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+          const double wv = sw[k][i];
+#pragma unroll
+          for (int j = 0; j < SPW; ++j) acc[j][k] = fma(static_cast<double>(xr[j][q]), wv, acc[j][k]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < SPW; ++j) {
+    if (bw + j >= B) break;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+      double v = acc[j][k];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      if (lane == 0) part[(static_cast<int64_t>(blockIdx.y) * B + bw + j) * KS + k] = v;
+    }
+  }
+}
+
+// Small sum-K reduction: one warp per (b, k); lane l adds slices l, l + 32, ... in
+// ascending order, a fixed shuffle tree adds the lanes, then the bias (after the sum,
+// eg/models.py:278).  The order is a function of the slice count only.
+__global__ void lin1_reduce_warp_kernel(const double* __restrict__ part,
+                                        const float* __restrict__ bias,
+                                        double* __restrict__ logits, int B, int K, int nsplit) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t total = static_cast<int64_t>(B) * K;
+  if (i >= total) return;
+  double s = 0.0;
+  for (int z = lane; z < nsplit; z += 32) s += part[z * total + i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  if (lane == 0) logits[i] = s + static_cast<double>(bias[i % K]);
+}
+
+// Larger sum-K: 64 samples x 64 classes per CTA, 4 x 4 fp64 accumulators per thread, the
+// slice walked in chunks of 16 d staged (transposed) in shared memory so each thread reads
+// its 4 samples and 4 classes with one 16-byte load each.  Each (b, k) of a slice is summed
+// in ascending d by one thread.
+constexpr int kLinTB = 64, kLinTK = 64, kLinChunk = 16;
+__global__ void __launch_bounds__(256)
+    lin1_partial_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                        double* __restrict__ part, int B, int K, int64_t D, int64_t dslice) {
+  __shared__ __align__(16) float sx[kLinChunk][kLinTB + 4];
+  __shared__ __align__(16) float sw[kLinChunk][kLinTK + 4];
+  const int tx = threadIdx.x & 15;  // class quad
+  const int ty = threadIdx.x >> 4;  // sample quad
+  const int b0 = blockIdx.x * kLinTB;
+  const int k0 = blockIdx.y * kLinTK;
+  const int64_t d0 = blockIdx.z * dslice;
+  const int64_t d1 = d0 + dslice < D ? d0 + dslice : D;
+  double acc[4][4] = {};
+  // loader: thread t loads rows t / 16 + 16 i (i < 4), column t % 16 of the chunk
+  const int lc = threadIdx.x & 15, lr = threadIdx.x >> 4;
+  for (int64_t dc = d0; dc < d1; dc += kLinChunk) {
+    const int64_t d = dc + lc;
+    const bool dok = d < d1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = lr + 16 * i;
+      sx[lc][r] = (dok && b0 + r < B) ? __ldg(x + static_cast<int64_t>(b0 + r) * D + d) : 0.f;
+      sw[lc][r] = (dok && k0 + r < K) ? __ldg(w + static_cast<int64_t>(k0 + r) * D + d) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
     for (int c = 0; c < kLinChunk; ++c) {
-      const double xa = sx[ty][c], xb = sx[ty + 16][c];
-      const double wa = sw[tx][c], wb = sw[tx + 16][c];
-      acc[0][0] = fma(xa, wa, acc[0][0]);
-      acc[0][1] = fma(xa, wb, acc[0][1]);
-      acc[1][0] = fma(xb, wa, acc[1][0]);
-      acc[1][1] = fma(xb, wb, acc[1][1]);
+      const float4 xa = *reinterpret_cast<const float4*>(&sx[c][4 * ty]);
+      const float4 wa = *reinterpret_cast<const float4*>(&sw[c][4 * tx]);
+      const double xv[4] = {xa.x, xa.y, xa.z, xa.w};
+      const double wv[4] = {wa.x, wa.y, wa.z, wa.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(xv[i], wv[j], acc[i][j]);
     }
     __syncthreads();
   }
-  for (int i = 0; i < 2; ++i)
-    for (int j = 0; j < 2; ++j) {
-      const int b = b0 + ty + 16 * i;
-      const int k = k0 + tx + 16 * j;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int b = b0 + 4 * ty + i;
+      const int k = k0 + 4 * tx + j;
       if (b < B && k < K) part[(static_cast<int64_t>(blockIdx.z) * B + b) * K + k] = acc[i][j];
     }
 }
@@ -418,8 +514,29 @@ cudaError_t k_lin1(const float* x, const float* w, const float* bias, double* pa
                    double* logits, int B, int K, int64_t D, int nsplit, cudaStream_t s) {
   if (B == 0 || K == 0) return cudaSuccess;
   const int64_t dslice = (D + nsplit - 1) / nsplit;
-  dim3 grid((B + kLinTile - 1) / kLinTile, (K + kLinTile - 1) / kLinTile, nsplit);
-  lin1_partial_kernel<<<grid, 256, 0, s>>>(x, w, part, B, K, D, dslice);
+  if (K <= kLinSmallK) {
+    switch (K) {
+#define EB_LIN_SMALL(k, spw)                                                              \
+  case k:                                                                                 \
+    lin1_small_kernel<k, spw><<<dim3((B + 8 * spw - 1) / (8 * spw), nsplit), 256, 0, s>>>( \
+        x, w, part, B, D, dslice);                                                        \
+    break;
+      EB_LIN_SMALL(1, 1) EB_LIN_SMALL(2, 1) EB_LIN_SMALL(3, 1) EB_LIN_SMALL(4, 1)
+      EB_LIN_SMALL(5, 1) EB_LIN_SMALL(6, 1) EB_LIN_SMALL(7, 1) EB_LIN_SMALL(8, 1)
+      EB_LIN_SMALL(9, 1) EB_LIN_SMALL(10, 1) EB_LIN_SMALL(11, 1) EB_LIN_SMALL(12, 1)
+      EB_LIN_SMALL(13, 1) EB_LIN_SMALL(14, 1) EB_LIN_SMALL(15, 1) EB_LIN_SMALL(16, 1)
+#undef EB_LIN_SMALL
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t warps = static_cast<int64_t>(B) * K;
+    lin1_reduce_warp_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(part, bias, logits,
+                                                                                  B, K, nsplit);
+    return cudaGetLastError();
+  } else {
+    dim3 grid((B + kLinTB - 1) / kLinTB, (K + kLinTK - 1) / kLinTK, nsplit);
+    lin1_partial_kernel<<<grid, 256, 0, s>>>(x, w, part, B, K, D, dslice);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t total = static_cast<int64_t>(B) * K;

@@ -86,7 +86,27 @@ struct ConvArgs {
   const float* pre_scale = nullptr;  // pre-activation on A (tiled mode only)
   const float* pre_shift = nullptr;
   int pool2 = 0;  // fused 2x2/2 max-pool: y is the pooled (Ho/2 x Wo/2) tensor
+  int max_ctas = 0;  // persistent grid cap (0 = every SM): the SM share of the op's lane
 };
+
+// EB_LANE_SMS=a,b,c,d: the persistent conv grids of lane l use at most that many SMs, so
+// members on different lanes run side by side on disjoint SM sets (one CTA per SM) instead
+// of each grid taking the whole GPU in turn.  Unset / 0: every lane uses every SM.
+int lane_sms(int lane) {
+  static int v[4] = {-1, -1, -1, -1};
+  if (v[0] < 0) {
+    for (int& x : v) x = 0;
+    if (const char* e = getenv("EB_LANE_SMS")) {
+      int i = 0;
+      for (const char* q = e; *q && i < 4; ++i) {
+        v[i] = atoi(q);
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+    }
+  }
+  return (lane >= 0 && lane < 4) ? v[lane] : 0;
+}
 
 int conv_out(int in, int k, int s, int p) { return (in + 2 * p - k) / s + 1; }
 
@@ -535,11 +555,13 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   if (mcast) {
     if (!encode_tiled_2d_bf16(&pl.mb, a.w, kpad, a.cout, kpad, 64, bn / 2, &err))
       EB_FAIL(EB_E_INVALID, err);
+    const int sms = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
     const int64_t pairs = static_cast<int64_t>((mt + 1) / 2) * nt;
-    pl.grid = 2 * static_cast<int>(std::min<int64_t>(pairs, num_sms() / 2));
+    pl.grid = 2 * static_cast<int>(std::min<int64_t>(pairs, std::max(1, sms / 2)));
   } else {
+    const int sms = a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms();
     const int64_t total = static_cast<int64_t>(mt) * nt * splits;
-    pl.grid = static_cast<int>(std::min<int64_t>(total, num_sms()));
+    pl.grid = static_cast<int>(std::min<int64_t>(total, sms));
   }
   if (tap_shift && splits != 1) EB_FAIL(EB_E_INVALID, "tap-shift mode does not split K");
   if (a.n_split > 0 && (a.res || a.out_f32 || splits != 1 || tap_shift ||
@@ -748,6 +770,7 @@ void conv_args_for(eb_engine* e, const eb_op_desc& op, int B, int fused_pool, Co
   a.groups = op.groups > 1 ? op.groups : 1;
   a.pre_scale = static_cast<const float*>(P(op.scale_off));
   a.pre_shift = static_cast<const float*>(P(op.shift_off));
+  a.max_ctas = is_prefork(op) ? 0 : lane_sms(op.stream);
 }
 
 // One op of the fp32-faithful mode (ref32.cu) on stream ls.

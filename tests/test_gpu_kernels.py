@@ -351,10 +351,13 @@ def test_combine_argmax_topk_policy():
     assert torch.allclose(tp.cpu()[0, 0], p.flip(0)[:3], atol=1e-5)
 
 
-def test_lin1_f64_scores():
+@pytest.mark.parametrize("B,K", [(7, 5), (70, 16), (9, 40), (70, 130)])
+def test_lin1_f64_scores(B, K):
+    """K6 (both the small-K warp kernel and the 64 x 64 tiled one) against the fp64 einsum
+    of eg/models.py:275-278; each sample's scores are bitwise the same alone."""
     lib = _lib.load()
     rng = np.random.default_rng(2)
-    B, K, D, ns = 7, 5, 3000, 3
+    D, ns = 3000, 3
     x = rng.standard_normal((B, D)).astype(np.float32)
     w = rng.standard_normal((K, D)).astype(np.float32)
     b = rng.standard_normal(K).astype(np.float32)
@@ -367,6 +370,10 @@ def test_lin1_f64_scores():
     got = out.cpu().numpy()
     assert np.allclose(got, ref, rtol=1e-12, atol=1e-9)
     assert (got.argmax(1) == ref.argmax(1)).all()
+    one = torch.empty(1, K, dtype=torch.float64, device=DEV)
+    _lib.check(lib.eb_k_lin1(_p(dx[B - 1:]), _p(dw), _p(db), _p(part), _p(one), 1, K, D, ns, None))
+    torch.cuda.synchronize()
+    assert np.array_equal(one.cpu().numpy()[0], got[B - 1])
 
 
 def test_conv_pre_activation_bnrelu():
