@@ -595,6 +595,35 @@ def main() -> None:
         dist.barrier()
     value = global_b * args.steps / (dev_ms / 1e3)
 
+    # ---- roofline of the tcgen05 conv/GEMM kernel class (serialised per-op profile, taken
+    # right after the timed region so that it runs at the same power-capped clocks)
+    # per-op median of 3 serialised runs (an eager run's event times absorb any host-side
+    # launch hiccup of the op that follows it)
+    ms = np.median(np.stack([eng.profile(B, kind) for _ in range(3)]), axis=0) if not args.minimal else np.zeros(eng.n_ops)
+    conv_ms = conv_flops = 0.0
+    top = None
+    for m, t in zip(eng.op_meta, ms):
+        if m.get("name") == "conv":
+            conv_ms += float(t)
+            conv_flops += m["flops"] * B
+            if top is None or t > top[1]:
+                top = (m, float(t))
+    pk, pk_src = peaks()
+    achieved = conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
+    # DRAM traffic of the top launch from the committed ncu capture of the same layer
+    traffic = None
+    for tl in sorted((ROOT / "profiles").glob("*/top_launch_ncu.json"), reverse=True):
+        t = json.loads(tl.read_text())
+        if top is not None and list(t["shape(ho,wo,cout,kh,kw,s,cin)"]) == list(top[0]["shape"]) and t["batch"] == B:
+            traffic = {"dram_bytes_per_launch": t["dram_bytes_read"] + t["dram_bytes_write"],
+                       "algorithmic_bytes_per_launch": t["algorithmic_bytes"], "source": t["source"]}
+            break
+    peak = pk["bf16_tflops_sustained"]
+    if args.profile_json and rank == 0:
+        Path(args.profile_json).write_text(json.dumps(
+            [{"i": i, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in m.items()}, "ms": float(t)}
+             for i, (m, t) in enumerate(zip(eng.op_meta, ms))], indent=0))
+
     if args.minimal:
         if rank == 0:
             print(json.dumps({"minimal": True, "value": value, "ms_per_step": dev_ms / args.steps,
@@ -665,34 +694,6 @@ def main() -> None:
         for b in (1, 8, 32, 64, 128, 256):
             if b <= B:
                 sweep[str(b)] = device_rate(eng, b, kind, stream, TOPK)
-
-    # ---- roofline of the tcgen05 conv/GEMM kernel class (serialised per-op profile)
-    # per-op median of 3 serialised runs (an eager run's event times absorb any host-side
-    # launch hiccup of the op that follows it)
-    ms = np.median(np.stack([eng.profile(B, kind) for _ in range(3)]), axis=0)
-    conv_ms = conv_flops = 0.0
-    top = None
-    for m, t in zip(eng.op_meta, ms):
-        if m.get("name") == "conv":
-            conv_ms += float(t)
-            conv_flops += m["flops"] * B
-            if top is None or t > top[1]:
-                top = (m, float(t))
-    pk, pk_src = peaks()
-    achieved = conv_flops / (conv_ms / 1e3) / 1e12
-    # DRAM traffic of the top launch from the committed ncu capture of the same layer
-    traffic = None
-    for tl in sorted((ROOT / "profiles").glob("*/top_launch_ncu.json"), reverse=True):
-        t = json.loads(tl.read_text())
-        if top is not None and list(t["shape(ho,wo,cout,kh,kw,s,cin)"]) == list(top[0]["shape"]) and t["batch"] == B:
-            traffic = {"dram_bytes_per_launch": t["dram_bytes_read"] + t["dram_bytes_write"],
-                       "algorithmic_bytes_per_launch": t["algorithmic_bytes"], "source": t["source"]}
-            break
-    peak = pk["bf16_tflops_sustained"]
-    if args.profile_json and rank == 0:
-        Path(args.profile_json).write_text(json.dumps(
-            [{"i": i, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in m.items()}, "ms": float(t)}
-             for i, (m, t) in enumerate(zip(eng.op_meta, ms))], indent=0))
 
     hbm = hbm_kernels(B, pk["hbm_gbs"], pk_src) if rank == 0 and not c4 else None
     eng_dev = eng.device

@@ -48,6 +48,9 @@ constexpr int kThreads = 384;
 #endif
 constexpr int kXformThreads = EB_XFORM_THREADS;  // pre-activation transform: the last warps
 constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels x 8 bf16
+#ifndef EB_STEM_NB
+#define EB_STEM_NB 1  // stems: epilogue chunk buffers per warp (1 or 2)
+#endif
 
 // TS = filter taps consumed per pipeline stage: 1 (one TMA im2col load per tap)
 // or 3 (tap-shift mode: one 136-row load per filter row serves its 3 horizontal taps).
@@ -78,8 +81,9 @@ struct ConvSmem {
   // instead stage 32 rows x 32 columns per warp for coalesced row stores
   static constexpr int kRowStageBytes = 32 * 32 * 2;
   // (stems: one chunk buffer per warp -- their whole-filter stages need the space)
-  static constexpr int kRingArea = STEM ? (8 * kStageOutBytes > 8 * kRowStageBytes ? 8 * kStageOutBytes
-                                                                                    : 8 * kRowStageBytes)
+  static constexpr int kRingArea = STEM ? (8 * EB_STEM_NB * kStageOutBytes > 8 * kRowStageBytes
+                                              ? 8 * EB_STEM_NB * kStageOutBytes
+                                              : 8 * kRowStageBytes)
                                    : (TS == 1 && !TAPN) ? 16 * kStageOutBytes
                                                         : 8 * kRowStageBytes;
   // tall taps-in-N: per epilogue group, two tile-parity buffers of the boundary rows three
@@ -1069,7 +1073,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool alt_tiles = wide && NCH == 1;
     const int c_first = (wide && NCH > 1) ? half : 0;
     const int c_step = (wide && NCH > 1) ? 2 : 1;
-    const int nb = (STEM ? 1 : wide ? 2 : 4) >> (p.ring_half ? 1 : 0);  // ring buffers per warp
+    const int nb = (STEM ? EB_STEM_NB : wide ? 2 : 4) >> (p.ring_half ? 1 : 0);  // ring buffers per warp
     uint8_t* ring = smem + L.out_off + ew * nb * S::kStageOutBytes;
     float* bias_s = reinterpret_cast<float*>(smem + L.bias_off) + ew * BN;
     uint64_t* rbar = rfull + ew * nb;
