@@ -28,6 +28,9 @@ enum AMode : int {
 //   rows   (stride 1): buffer [B][Hq][Wq][8], padded pixel (ih + ph, iw + pw); Wg = Wq
 //   planes (stride 2): buffer [2][B][Hq][Wq][8], plane q holds padded columns 2j + q;
 //                      Wg = 128 * ceil(Wo / 128)
+#ifndef EB_STEM_ALIGN
+#define EB_STEM_ALIGN 8  // rows mode: padded row width multiple (128: a tile never straddles rows)
+#endif
 struct StemGeom {
   int mode;        // kAModeStemRows / kAModeStemPlanes
   int Hq, Wq, Wg;  // padded rows / width per image, output grid width
@@ -46,7 +49,7 @@ inline bool stem_geom(int B, int H, int W, int kh, int kw, int sh, int sw, int p
     // a multiple of 8: an epilogue warp's 32-row slab meets at most one grid-row boundary,
     // at an 8-row-aligned offset (the second part is stored in 8-row boxes); taps >= kw
     // meet zero weights
-    g->Wq = (W + 2 * pw + 7) / 8 * 8;
+    g->Wq = (W + 2 * pw + EB_STEM_ALIGN - 1) / EB_STEM_ALIGN * EB_STEM_ALIGN;
     g->Wg = g->Wq;
     g->Mi = (Ho * g->Wg + 127) / 128 * 128;
     // the last tile's loads reach Mi - 1 + 7 + (kh - 1) * Wq
