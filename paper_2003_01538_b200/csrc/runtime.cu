@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -17,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ensemble_b200.h"
@@ -660,6 +662,10 @@ struct eb_engine {
   int nms = 1;
   uint8_t* d_in_u8 = nullptr;
   float* d_in_f32 = nullptr;
+  // eb_forward with pageable host input: pinned staging slots filled by host threads
+  // while the previous slot's DMA runs (upload_pageable)
+  uint8_t* h_slot[2] = {nullptr, nullptr};
+  cudaEvent_t ev_slot[2] = {nullptr, nullptr};
   // eb_forward_batches: a staging buffer filled on a copy stream while the previous
   // batch computes
   void* d_stage = nullptr;
@@ -1094,6 +1100,68 @@ int enqueue_combine(eb_engine* e, int B, int topk, int policy, int policy_k) {
 
 }  // namespace
 
+// Host -> device copy of a request from ordinary (pageable) memory.  The driver stages
+// pageable copies through its own small pinned buffers with one thread (~12 GB/s for the
+// reference's f32 samples, 154 MB per 256 images); here kHostCopyThreads threads copy
+// kSlotBytes chunks into two pinned slots while the previous slot's DMA runs (B200 box,
+// C2 B = 256, f32: drop-in forward 9.9k -> 12.5k images/s with 4 threads).
+constexpr size_t kSlotBytes = 16u << 20;
+constexpr int kMaxHostCopyThreads = 16;
+int host_copy_threads() {  // EB_HOST_COPY_THREADS (default 4)
+  static const int n = [] {
+    const char* v = getenv("EB_HOST_COPY_THREADS");
+    const int k = (v && *v) ? atoi(v) : 4;
+    return std::max(1, std::min(k, kMaxHostCopyThreads));
+  }();
+  return n;
+}
+
+static bool is_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+static int upload_pageable(eb_engine* e, void* dst, const void* src, size_t bytes) {
+  for (int i = 0; i < 2; ++i) {
+    if (!e->h_slot[i]) {
+      if (cudaHostAlloc(reinterpret_cast<void**>(&e->h_slot[i]), kSlotBytes, cudaHostAllocDefault) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        e->h_slot[i] = nullptr;
+        EB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, e->stream));  // plain path
+        return EB_OK;
+      }
+      EB_CUDA(cudaEventCreateWithFlags(&e->ev_slot[i], cudaEventDisableTiming));
+    }
+  }
+  const uint8_t* s = static_cast<const uint8_t*>(src);
+  uint8_t* d = static_cast<uint8_t*>(dst);
+  int slot = 0;
+  bool used[2] = {false, false};
+  for (size_t off = 0; off < bytes; off += kSlotBytes, slot ^= 1) {
+    const size_t n = std::min(kSlotBytes, bytes - off);
+    if (used[slot]) EB_CUDA(cudaEventSynchronize(e->ev_slot[slot]));  // its last DMA is done
+    uint8_t* h = e->h_slot[slot];
+    const int nt = host_copy_threads();
+    const size_t part = (n / nt + 63) / 64 * 64;
+    std::thread th[kMaxHostCopyThreads];
+    for (int t = 1; t < nt; ++t) {
+      const size_t a = std::min(n, t * part), b = std::min(n, (t + 1) * part);
+      th[t] = std::thread([=] { if (b > a) memcpy(h + a, s + off + a, b - a); });
+    }
+    memcpy(h, s + off, std::min(n, part));
+    for (int t = 1; t < nt; ++t) th[t].join();
+    EB_CUDA(cudaMemcpyAsync(d + off, h, n, cudaMemcpyHostToDevice, e->stream));
+    EB_CUDA(cudaEventRecord(e->ev_slot[slot], e->stream));
+    used[slot] = true;
+  }
+  return EB_OK;
+}
+
 // ====================================================================== C ABI
 
 extern "C" {
@@ -1158,6 +1226,10 @@ int eb_engine_destroy(eb_engine* e) {
   cudaFree(e->d_in_f32);
   cudaFree(e->d_stage);
   if (e->copy_stream) cudaStreamDestroy(e->copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (e->h_slot[i]) cudaFreeHost(e->h_slot[i]);
+    if (e->ev_slot[i]) cudaEventDestroy(e->ev_slot[i]);
+  }
   if (e->ev_staged) cudaEventDestroy(e->ev_staged);
   if (e->ev_stage_free) cudaEventDestroy(e->ev_stage_free);
   for (int l = 0; l < kLanes; ++l) cudaFree(e->ws[l]);
@@ -1553,13 +1625,16 @@ int eb_forward(eb_engine* e, const void* host_input, int input_kind, int batch,
   std::lock_guard<std::mutex> lock(e->mu);
   cudaSetDevice(e->device);
   const size_t px = static_cast<size_t>(batch) * e->C * e->H * e->W;
-  if (input_kind == EB_IN_U8_HWC) {
-    EB_CUDA(cudaMemcpyAsync(e->d_in_u8, host_input, px, cudaMemcpyHostToDevice, e->stream));
-  } else if (input_kind == EB_IN_F32_CHW) {
-    EB_CUDA(cudaMemcpyAsync(e->d_in_f32, host_input, px * sizeof(float), cudaMemcpyHostToDevice,
-                            e->stream));
-  } else {
+  if (input_kind != EB_IN_U8_HWC && input_kind != EB_IN_F32_CHW)
     EB_FAIL(EB_E_INVALID, "unknown input encoding");
+  void* d_in = input_kind == EB_IN_U8_HWC ? static_cast<void*>(e->d_in_u8) : static_cast<void*>(e->d_in_f32);
+  const size_t in_bytes = input_kind == EB_IN_U8_HWC ? px : px * sizeof(float);
+  static const bool staged_up = env_flag("EB_PAGEABLE_STAGING", true);
+  if (staged_up && in_bytes >= (4u << 20) && is_pageable(host_input)) {
+    rc = upload_pageable(e, d_in, host_input, in_bytes);
+    if (rc != EB_OK) return rc;
+  } else {
+    EB_CUDA(cudaMemcpyAsync(d_in, host_input, in_bytes, cudaMemcpyHostToDevice, e->stream));
   }
   rc = eb_forward_device(e, input_kind, batch, topk, policy, policy_k);
   if (rc != EB_OK) return rc;

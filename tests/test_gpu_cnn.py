@@ -157,3 +157,18 @@ def test_bench_config_rows_match_oracle(tmp_path):
     _, _, res = E.predict_u8(ens, px, topk=TOPK, want_logits=True)
     rows = [int(r) for r in g["rows"]]
     _check(res["logits"][:, rows], g["logits"], "c2_bench", g["archs"])
+
+
+def test_f32_pageable_staged_upload_equals_u8(tmp_path):
+    """A large f32 SampleBatch from ordinary numpy memory goes through the pinned staging
+    slots (runtime.cu upload_pageable, >= 4 MB, 16 MB chunks): same logits as u8."""
+    from paper_2003_01538_b200 import models as M
+
+    docs = [cnn1_doc("r18", "resnet18", 1)]
+    ens = build(tmp_path, docs, max_batch=48, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    px = synth.images_fast(48, 224, 224, 3, seed0=5)
+    f32 = (px.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0)).reshape(48, -1)
+    assert f32.nbytes > 16 << 20  # several chunks
+    _, _, r = E.predict_u8(ens, px, want_logits=True)
+    _, _, r2 = E.predict(ens, M.SampleBatch(ens.shared_shape, f32), want_logits=True)
+    assert np.array_equal(r["logits"], r2["logits"])
