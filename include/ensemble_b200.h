@@ -190,6 +190,12 @@ int eb_launch_count(eb_engine* e, int input_kind, int batch, int* count);
 int eb_decode_request(const char* body, uint64_t len, const int32_t* dims, int ndims,
                       float* host_out, int max_samples, int* n_samples, uint64_t* policy_off,
                       uint64_t* policy_len);
+/* As eb_decode_request, and also the "pgm" encoding (eg/wire.py:60-72) when
+ * pixel_scale > 0 and dims = [1, H, W]: P5 parsed as eg/pgm.py:16-59, raster /
+ * pixel_scale in fp32 (eg/wire.py:71). */
+int eb_decode_request2(const char* body, uint64_t len, const int32_t* dims, int ndims,
+                       float pixel_scale, float* out, int max_samples, int* n_samples,
+                       uint64_t* policy_off, uint64_t* policy_len);
 
 /* Kernel-level entry points on caller-owned device memory (used by the parity
  * tests; `stream` is a cudaStream_t, NULL = legacy default stream). */

@@ -7,7 +7,9 @@
 //   {"samples": [{"encoding": "f32le", "shape": [...], "data": "<base64>"}, ...],
 //    "policy": {...}}                               (keys in any order, any whitespace)
 //
-// and base64-decodes every sample straight into one caller-provided (pinned) buffer,
+// (and, given the ensemble's pixel scale, the "pgm" encoding of a [1, H, W] shape: the
+// P5 header parsed as eg/pgm.py does, raster / pixel_scale in fp32) and base64-decodes
+// every sample straight into one caller-provided (pinned) buffer,
 // in parallel across samples, checking finiteness.  Anything else -- another
 // encoding, an unexpected key, a duplicate key, an escape sequence, a shape or length
 // mismatch, invalid base64, a non-finite value -- returns EB_E_INVALID and the caller
@@ -142,13 +144,67 @@ bool b64_decode(const char* s, size_t len, uint8_t* out, size_t n_out) {
 struct Sample {
   const char* data_b;
   const char* data_e;
+  bool pgm;  // "encoding": "pgm" (eg/wire.py:60-72): P5 raster / pixel_scale, shape [1, H, W]
 };
 
+// The reference's parse_pgm (eg/pgm.py:16-59) on a decoded P5 document, then
+// u8 / pixel_scale in fp32 (eg/wire.py:71).  false for anything it would reject (or
+// anything this restatement is unsure about: very long header tokens) -- the caller then
+// falls back to the reference decoder for the exact error.
+bool is_pgm_ws(uint8_t c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == 0x0b || c == 0x0c; }
+bool pgm_to_f32(const uint8_t* d, size_t n, int h_want, int w_want, float pixel_scale, float* out) {
+  size_t pos = 0;
+  auto token = [&](size_t* b, size_t* e) {
+    while (pos < n && is_pgm_ws(d[pos])) ++pos;
+    *b = pos;
+    while (pos < n && !is_pgm_ws(d[pos])) ++pos;
+    *e = pos;
+    return *e > *b;
+  };
+  size_t b, e;
+  if (!token(&b, &e) || e - b != 2 || d[b] != 'P' || d[b + 1] != '5') return false;
+  long long v[3];
+  for (int i = 0; i < 3; ++i) {
+    if (!token(&b, &e) || e - b > 9) return false;
+    long long x = 0;
+    for (size_t k = b; k < e; ++k) {
+      if (d[k] < '0' || d[k] > '9') return false;
+      x = x * 10 + (d[k] - '0');
+    }
+    v[i] = x;
+  }
+  const long long width = v[0], height = v[1], maxval = v[2];
+  if (width < 1 || height < 1 || maxval < 1 || maxval > 255) return false;
+  if (pos >= n || !is_pgm_ws(d[pos])) return false;
+  ++pos;
+  if (width != w_want || height != h_want || static_cast<long long>(n - pos) != width * height) return false;
+  const uint8_t* px = d + pos;
+  const int64_t np = width * height;
+  for (int64_t k = 0; k < np; ++k) {
+    if (px[k] > maxval) return false;
+    out[k] = static_cast<float>(px[k]) / pixel_scale;
+  }
+  return true;
+}
+
 }  // namespace
+
+extern "C" int eb_decode_request2(const char* body, uint64_t len, const int32_t* dims, int ndims,
+                                  float pixel_scale, float* out, int max_samples, int* n_samples,
+                                  uint64_t* policy_off, uint64_t* policy_len);
 
 extern "C" int eb_decode_request(const char* body, uint64_t len, const int32_t* dims, int ndims,
                                  float* out, int max_samples, int* n_samples,
                                  uint64_t* policy_off, uint64_t* policy_len) {
+  return eb_decode_request2(body, len, dims, ndims, 0.f, out, max_samples, n_samples, policy_off,
+                            policy_len);
+}
+
+extern "C" int eb_decode_request2(const char* body, uint64_t len, const int32_t* dims, int ndims,
+                                  float pixel_scale, float* out, int max_samples, int* n_samples,
+                                  uint64_t* policy_off, uint64_t* policy_len) {
+  // pgm samples only with a pixel scale and a [1, H, W] ensemble shape
+  const bool pgm_ok = pixel_scale > 0.f && ndims == 3 && dims[0] == 1;
   if (!body || !dims || !out || !n_samples || ndims < 1 || ndims > 3) return EB_E_INVALID;
   int64_t D = 1;
   for (int i = 0; i < ndims; ++i) D *= dims[i];
@@ -176,7 +232,11 @@ extern "C" int eb_decode_request(const char* body, uint64_t len, const int32_t* 
             if (!sc.str(&fb, &fe) || !sc.lit(':')) return EB_E_INVALID;
             if (key_is(fb, fe, "encoding")) {
               const char *vb, *ve;
-              if (h_enc || !sc.str(&vb, &ve) || !key_is(vb, ve, "f32le")) return EB_E_INVALID;
+              if (h_enc || !sc.str(&vb, &ve)) return EB_E_INVALID;
+              if (key_is(vb, ve, "pgm") && pgm_ok)
+                smp.pgm = true;
+              else if (!key_is(vb, ve, "f32le"))
+                return EB_E_INVALID;
               h_enc = true;
             } else if (key_is(fb, fe, "shape")) {
               if (h_shape || !sc.lit('[')) return EB_E_INVALID;
@@ -197,7 +257,8 @@ extern "C" int eb_decode_request(const char* body, uint64_t len, const int32_t* 
             if (!sc.lit('}')) return EB_E_INVALID;
             break;
           }
-          if (!(h_enc && h_shape && h_data)) return EB_E_INVALID;
+          // f32le: encoding, shape, data; pgm: encoding, data (eg/wire.py:26-27)
+          if (!(h_enc && h_data) || h_shape == smp.pgm) return EB_E_INVALID;
           samples.push_back(smp);
           if (static_cast<int>(samples.size()) > max_samples) return EB_E_TOO_LARGE;
           if (sc.lit(',')) continue;
@@ -227,8 +288,23 @@ extern "C" int eb_decode_request(const char* body, uint64_t len, const int32_t* 
   const size_t nbytes = static_cast<size_t>(D) * 4;
   std::vector<char> bad(n, 0);
   auto work = [&](int lo, int hi) {
+    std::vector<uint8_t> doc;
     for (int i = lo; i < hi; ++i) {
       float* dst = out + static_cast<size_t>(i) * D;
+      if (samples[i].pgm) {
+        const size_t l = samples[i].data_e - samples[i].data_b;
+        if (l % 4 != 0 || l == 0) {
+          bad[i] = 1;
+          continue;
+        }
+        const char* q = samples[i].data_b;
+        const size_t pad = (q[l - 1] == '=') + (l >= 2 && q[l - 2] == '=');
+        doc.resize(l / 4 * 3 - pad);
+        if (!b64_decode(q, l, doc.data(), doc.size()) ||
+            !pgm_to_f32(doc.data(), doc.size(), dims[1], dims[2], pixel_scale, dst))
+          bad[i] = 1;
+        continue;
+      }
       if (!b64_decode(samples[i].data_b, samples[i].data_e - samples[i].data_b,
                       reinterpret_cast<uint8_t*>(dst), nbytes)) {
         bad[i] = 1;

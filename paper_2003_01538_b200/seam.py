@@ -86,7 +86,8 @@ def install() -> None:
 
             from .wire import fast_decode
 
-            got = fast_decode(body, ensemble.shared_shape.dims, ensemble.max_batch)
+            got = fast_decode(body, ensemble.shared_shape.dims, ensemble.max_batch,
+                              pixel_scale=float(ensemble.preprocess.pixel_scale))
             if got is None:
                 return None
             data, policy_raw = got

@@ -35,8 +35,9 @@ def _buffer(n_floats: int, pinned: bool) -> np.ndarray:
     return buf
 
 
-def fast_decode(body: bytes, dims, max_batch: int, pinned: bool = True):
-    """(data (B, D) float32 view, policy bytes or None), or None when not accepted."""
+def fast_decode(body: bytes, dims, max_batch: int, pinned: bool = True, pixel_scale: float = 0.0):
+    """(data (B, D) float32 view, policy bytes or None), or None when not accepted.
+    pixel_scale > 0 also accepts "pgm" samples for a [1, H, W] shape."""
     lib = _lib.load()
     dims = tuple(int(d) for d in dims)
     d = int(np.prod(dims))
@@ -44,8 +45,8 @@ def fast_decode(body: bytes, dims, max_batch: int, pinned: bool = True):
     dims_arr = (ctypes.c_int32 * len(dims))(*dims)
     n = c_int(0)
     poff, plen = c_uint64(0), c_uint64(0)
-    rc = lib.eb_decode_request(body, len(body), dims_arr, len(dims), out.ctypes.data, max_batch,
-                               byref(n), byref(poff), byref(plen))
+    rc = lib.eb_decode_request2(body, len(body), dims_arr, len(dims), float(pixel_scale),
+                                out.ctypes.data, max_batch, byref(n), byref(poff), byref(plen))
     if rc != _lib.EB_OK:
         return None
     data = out[: n.value * d].reshape(n.value, d)

@@ -179,3 +179,39 @@ def test_gateway_bytes_match_frozen_reference_output(tmp_path):
             assert app.handle("GET", "/v1/models") == (st, body.encode())
     finally:
         seam.uninstall()
+
+
+def test_pgm_requests_bytes_match_reference(tmp_path):
+    """Grayscale [1, H, W] ensembles take "pgm" samples (eg/wire.py:60-72); with the seam
+    they go through the native decoder (P5 parsed as eg/pgm.py does) -- same bytes as the
+    reference's own gateway, including its errors for malformed documents."""
+    from ensemblegate.gateway import GatewayApp
+
+    from paper_2003_01538_b200 import seam
+
+    h, w = 6, 9
+    docs = []
+    for s in (51, 52):
+        wt, b = O.gen_model_arrays(s, 2, h * w)
+        docs.append(lin1_doc(f"g{s}", (1, h, w), ("absent", "present"), wt, b))
+    mp = write_manifest(tmp_path, docs, max_batch=16, mean=(0.5,), std=(0.25,), pixel_scale=200.0)
+    rng = np.random.default_rng(8)
+
+    def body(docs_):
+        return json.dumps({"samples": [{"encoding": "pgm", "data": base64.b64encode(d).decode()}
+                                       for d in docs_]}).encode()
+
+    good = [b"P5\n%d %d\n255\n" % (w, h) + rng.integers(0, 256, h * w, dtype=np.uint8).tobytes()
+            for _ in range(12)]
+    reqs = [body(good[:b]) for b in (1, 3, 12)]
+    reqs.append(body([b"P5\n%d %d\n9\n" % (w, h) + bytes([10] * (h * w))]))  # pixel > maxval
+    reqs.append(body([b"P5\n%d %d\n255\n" % (w + 1, h) + bytes((w + 1) * h)]))  # other shape
+    ref_app = GatewayApp(eg.load_ensemble(eg.load_manifest_file(mp)))
+    expected = [ref_app.handle("POST", "/v1/predict", r) for r in reqs]
+    assert [e[0] for e in expected[:3]] == [200, 200, 200]
+    seam.install()
+    try:
+        app = GatewayApp(eg.gateway.load_ensemble(eg.load_manifest_file(mp)))
+        assert [app.handle("POST", "/v1/predict", r) for r in reqs] == expected
+    finally:
+        seam.uninstall()

@@ -84,3 +84,54 @@ def test_decode_speed_64_rgb():
     dt = time.perf_counter() - t
     assert got is not None and np.array_equal(got[0], x)
     assert dt < 0.5, dt  # the reference takes ~0.4 s on 8 cores for this body
+
+
+def _pgm_body(docs):
+    import base64
+
+    return json.dumps({"samples": [{"encoding": "pgm", "data": base64.b64encode(d).decode()}
+                                   for d in docs]}).encode()
+
+
+def _p5(h, w, px, maxval=255, header=None):
+    head = header if header is not None else f"P5\n{w} {h}\n{maxval}\n".encode()
+    return head + bytes(px)
+
+
+@pytest.mark.parametrize("scale", [255.0, 100.0, 7.0])
+def test_pgm_matches_reference_decode(scale):
+    """eg/wire.py:60-72 + eg/pgm.py:16-59: P5 raster / pixel_scale, shape [1, H, W]."""
+    from ensemblegate.wire import decode_request
+
+    from paper_2003_01538_b200.wire import fast_decode
+
+    rng = np.random.default_rng(3)
+    docs = [_p5(5, 7, rng.integers(0, 256, 35, dtype=np.uint8)) for _ in range(4)]
+    docs.append(_p5(5, 7, rng.integers(0, 100, 35, dtype=np.uint8), maxval=99))
+    docs.append(_p5(5, 7, [3] * 35, header=b"P5 \t7\r\n5\x0b\x0c255 "))  # any header whitespace
+    docs.append(_p5(5, 7, [9] * 35, header=b"P5\n007 05\n0255\n"))  # leading zeros: int() accepts
+    body = _pgm_body(docs)
+    got = fast_decode(body, (1, 5, 7), 16, pinned=False, pixel_scale=scale)
+    assert got is not None
+    ref, _ = decode_request(body, pixel_scale=scale)
+    assert np.array_equal(got[0].view(np.uint32), ref.data.view(np.uint32))
+    # without a pixel scale (the f32le-only entry point) pgm is declined
+    assert fast_decode(body, (1, 5, 7), 16, pinned=False) is None
+
+
+@pytest.mark.parametrize("doc", [
+    b"P2\n7 5\n255\n" + bytes(35),               # ASCII PGM
+    b"P5\n7 5\n0\n" + bytes(35),                 # maxval 0
+    b"P5\n7 5\n256\n" + bytes(35),               # maxval > 255
+    b"P5\n7 5\n10\n" + bytes([11] * 35),         # pixel > maxval
+    b"P5\n7 5\n255\n\n" + bytes(35),             # two whitespace bytes before the raster
+    b"P5\n7 5\n255\n" + bytes(34),               # short raster
+    b"P5\n7 5\n255" + bytes(35),                 # no separator
+    b"P5\n+7 5\n255\n" + bytes(35),              # non-digit token
+    b"P5\n7 6\n255\n" + bytes(42),               # other shape than the ensemble's
+    b"P5\n7 5\n255\n",                           # no raster
+])
+def test_pgm_declines_what_the_reference_rejects(doc):
+    from paper_2003_01538_b200.wire import fast_decode
+
+    assert fast_decode(_pgm_body([doc]), (1, 5, 7), 16, pinned=False, pixel_scale=255.0) is None
