@@ -242,7 +242,9 @@ __device__ __forceinline__ void trace_cta(long long* tr, int which) {
 }
 
 // EB_DBG timing probes (trace build only): 2 = MMA does not wait for the stem gather,
-// 3 = no pre-activation transform.  Results are wrong under a probe; timing only.
+// 3 = no pre-activation transform, 5 = no TMA output stores, 6 = epilogue loads TMEM
+// and releases it, nothing else.  Results are wrong under a
+// probe; timing only.
 __device__ __forceinline__ bool dbg_probe(const ConvParams& p, int which) {
 #ifdef EB_ENABLE_TRACE
   return p.dbg == which;
@@ -1160,6 +1162,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 23);
         if (ci == last_ci && p.early_release) release();
+        if (dbg_probe(p, 6)) {  // (probe 6: TMEM load + release only, timing only)
+          ++seq;
+          continue;
+        }
         if (p.out_mode != kOutBF16) {
           // fp32 logits or a split-K partial slice: direct stores (small outputs)
           if (row_ok) {
@@ -1269,7 +1275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 27);
-        if (lane == 0) {
+        if (lane == 0 && !dbg_probe(p, 5)) {  // (probe 5: no output stores, timing only)
           // a grouped launch (members sharing a stem) writes its second column range
           // to another tensor through the residual map slot
           if (stem_direct) {

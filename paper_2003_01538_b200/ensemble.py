@@ -338,12 +338,25 @@ def build_engine(models, shape, spec, max_batch: int, device: int = 0, precision
     stem_out: dict = {}
     if grouped_stems_enabled():
         for key, group in stem_groups.items():
-            if len(group) < 2:
-                continue
-            img = zoo.resized_image(eng, key[0][1:], images)
-            outs = zoo.grouped_stem(eng, img, [zoo.stem_of(g.arch, torch_models[g.id]) for g in group])
-            for g, o in zip(group, outs):
-                stem_out[g.id] = o
+            # launches of at most 128 output channels: a wider stem is two N tiles whose
+            # 7-row filter no longer fits resident in shared memory beside the A stages
+            # (B200, B = 128: 192 channels in one launch 684 us; 128 + 64 in two, 150 + 114)
+            chunks, cur, width = [], [], 0
+            for g in group:
+                cout = zoo.stem_of(g.arch, torch_models[g.id])[0].out_channels
+                if cur and width + cout > 128:
+                    chunks.append(cur)
+                    cur, width = [], 0
+                cur.append(g)
+                width += cout
+            chunks.append(cur)
+            for chunk in chunks:
+                if len(chunk) < 2:
+                    continue
+                img = zoo.resized_image(eng, key[0][1:], images)
+                outs = zoo.grouped_stem(eng, img, [zoo.stem_of(g.arch, torch_models[g.id]) for g in chunk])
+                for g, o in zip(chunk, outs):
+                    stem_out[g.id] = o
     for m in models:
         k = len(m.labels)
         if _kind(m) == "cnn1":
