@@ -243,7 +243,7 @@ __device__ __forceinline__ void trace_cta(long long* tr, int which) {
 
 // EB_DBG timing probes (trace build only): 2 = MMA does not wait for the stem gather,
 // 3 = no pre-activation transform, 5 = no TMA output stores, 6 = epilogue loads TMEM
-// and releases it, nothing else.  Results are wrong under a
+// and releases it, nothing else, 7 = stems: no A loads.  Results are wrong under a
 // probe; timing only.
 __device__ __forceinline__ bool dbg_probe(const ConvParams& p, int which) {
 #ifdef EB_ENABLE_TRACE
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     : p.a_mode == kAModeStemPlanes ? 4352u * kbs
                                                                    : static_cast<uint32_t>(S::kALoadBytes);
             // (gather mode with resident B: this stage only waits for the cp.async arrivals)
-            mbar_arrive_expect_tx(&full[stage], abytes + bbytes);
+            mbar_arrive_expect_tx(&full[stage], dbg_probe(p, 7) && stem_direct ? bbytes : abytes + bbytes);
           }
           if (TS > 1) {
             // filter row r, channel chunk cc: 136 consecutive padded-grid pixels at tap (r, 0);
@@ -622,7 +622,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             // 8 pixels x 8 channels) of the padded layout; the next filter row is Wq
             // pixels further in both layouts
             const int run = stem_run_bytes(p.a_mode);
-            if (p.stem_lines) {
+            if (dbg_probe(p, 7)) {
+              // (probe 7: no A loads -- the MMAs read stale smem; timing only)
+            } else if (p.stem_lines) {
               // tall stem: one load per plane covers every filter row of the tile (row r is
               // Wq pixels = Wq / 8 lines further); the odd plane follows the even one
               const int line = stem_line0 + kb * kbs * (p.Wq >> 3);

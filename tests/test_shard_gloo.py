@@ -100,3 +100,41 @@ def test_sharded_engine_reassembles_in_shard_order(batch):
     for k in ("labels", "logits", "topk_idx", "topk_prob", "combined"):
         assert np.array_equal(out[k], want[k]), k
     se.close()
+
+
+def test_bench_spawns_ranks_for_multi_gpu(monkeypatch):
+    """`bench.py --gpus N` outside torchrun launches N ranks through torch.distributed.run
+    (one per GPU, rendezvous on 127.0.0.1) with NCCL's init log on, and returns its exit
+    code; under torchrun a --gpus / WORLD_SIZE mismatch is an error, not a silent N = 1."""
+    import subprocess
+    import sys
+
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
+    import bench
+
+    seen = {}
+
+    def fake_run(cmd, env=None, **kw):
+        seen["cmd"], seen["env"] = cmd, env
+        return subprocess.CompletedProcess(cmd, 0)
+
+    monkeypatch.setattr(bench.subprocess, "run", fake_run)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert ex.value.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"]
+    assert seen["env"]["NCCL_DEBUG"] == "INFO"
+    # torchrun already set WORLD_SIZE = 2 but --gpus 4: refuse
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(bench, "__name__", "bench")
+    import torch
+
+    monkeypatch.setattr(torch.cuda, "set_device", lambda *_: None)
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert "WORLD_SIZE=2" in str(ex.value.code)
