@@ -196,6 +196,15 @@ int eb_decode_request(const char* body, uint64_t len, const int32_t* dims, int n
 int eb_decode_request2(const char* body, uint64_t len, const int32_t* dims, int ndims,
                        float pixel_scale, float* out, int max_samples, int* n_samples,
                        uint64_t* policy_off, uint64_t* policy_len);
+/* F4: the /v1/predict response body, byte-identical to the reference's
+ * dumps_canonical(render_prediction(...)) (eg/wire.py:136-143, eg/jsonio.py:28-36).
+ * key_json: the JSON-encoded keys in sorted order; key_kind[i] = -1 "_batch_size",
+ * -2 "_combined", m >= 0 model m; label_json[m] + label_off[m][v] .. [v + 1]: model m's
+ * label v JSON-encoded.  EB_E_TOO_LARGE (with *out_len set) when cap is too small. */
+int eb_render_prediction(const int32_t* labels, int n_models, int batch, const int32_t* combined,
+                         const char* const* key_json, const int32_t* key_kind, int n_keys,
+                         const char* const* label_json, const int64_t* const* label_off,
+                         const int32_t* n_labels, char* out, uint64_t cap, uint64_t* out_len);
 
 /* Kernel-level entry points on caller-owned device memory (used by the parity
  * tests; `stream` is a cudaStream_t, NULL = legacy default stream). */

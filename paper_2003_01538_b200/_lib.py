@@ -98,6 +98,9 @@ _SIGS = {
     "eb_profile_ops": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int]),
     "eb_decode_request2": (c_int, [c_char_p, c_uint64, c_void_p, c_int, c_float, c_void_p, c_int,
                                    POINTER(c_int), POINTER(c_uint64), POINTER(c_uint64)]),
+    "eb_render_prediction": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_int,
+                                     c_void_p, c_void_p, c_void_p, c_void_p, c_uint64,
+                                     POINTER(c_uint64)]),
     "eb_decode_request": (c_int, [c_char_p, c_uint64, c_void_p, c_int, c_void_p, c_int,
                                   POINTER(c_int), POINTER(c_uint64), POINTER(c_uint64)]),
     "eb_k_preprocess_f32": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int64, c_void_p, c_void_p,

@@ -332,3 +332,59 @@ extern "C" int eb_decode_request2(const char* body, uint64_t len, const int32_t*
   *n_samples = n;
   return EB_OK;
 }
+
+// ---------------------------------------------------------------------------------------
+// F4: the response body of /v1/predict, byte-identical to
+//   dumps_canonical(render_prediction(ensemble, output, combined))   (eg/wire.py:136-143,
+//   eg/jsonio.py:28-36: sorted keys, compact separators, ensure_ascii)
+// The caller passes every key already JSON-encoded, in sorted order, and every model's
+// labels JSON-encoded (json.dumps(label, ensure_ascii=True) on the host, once per
+// ensemble); key_kind[i] = -1: "_batch_size", -2: "_combined", m >= 0: model m.
+extern "C" int eb_render_prediction(const int32_t* labels, int n_models, int batch,
+                                    const int32_t* combined, const char* const* key_json,
+                                    const int32_t* key_kind, int n_keys,
+                                    const char* const* label_json, const int64_t* const* label_off,
+                                    const int32_t* n_labels, char* out, uint64_t cap,
+                                    uint64_t* out_len) {
+  if (!labels || !key_json || !key_kind || !out_len || n_models < 0 || batch < 0) return EB_E_INVALID;
+  static const char* kBin[2] = {"\"absent\"", "\"present\""};
+  std::string s;
+  s.reserve(64 + static_cast<size_t>(batch) * (n_models + 1) * 12);
+  s.push_back('{');
+  for (int i = 0; i < n_keys; ++i) {
+    if (i) s.push_back(',');
+    s.append(key_json[i]);
+    s.push_back(':');
+    const int k = key_kind[i];
+    if (k == -1) {
+      s.append(std::to_string(batch));
+    } else if (k == -2) {
+      if (!combined) return EB_E_INVALID;
+      s.push_back('[');
+      for (int b = 0; b < batch; ++b) {
+        if (b) s.push_back(',');
+        const int v = combined[b];
+        if (v < 0 || v > 1) return EB_E_INVALID;
+        s.append(kBin[v]);
+      }
+      s.push_back(']');
+    } else if (k >= 0 && k < n_models) {
+      const int32_t* row = labels + static_cast<int64_t>(k) * batch;
+      s.push_back('[');
+      for (int b = 0; b < batch; ++b) {
+        if (b) s.push_back(',');
+        const int v = row[b];
+        if (v < 0 || v >= n_labels[k]) return EB_E_INVALID;
+        s.append(label_json[k] + label_off[k][v], label_json[k] + label_off[k][v + 1]);
+      }
+      s.push_back(']');
+    } else {
+      return EB_E_INVALID;
+    }
+  }
+  s.push_back('}');
+  *out_len = s.size();
+  if (!out || s.size() > cap) return EB_E_TOO_LARGE;
+  memcpy(out, s.data(), s.size());
+  return EB_OK;
+}

@@ -78,8 +78,19 @@ def install() -> None:
                 batch, policy = eg_gw.decode_request(body, pixel_scale=ensemble.preprocess.pixel_scale)
             else:
                 batch, policy = decoded
-            output, combined, _ = ours.predict(ensemble, batch, policy)
-            return 200, eg_gw.dumps_canonical(eg_gw.render_prediction(ensemble, output, combined))
+            output, combined, res = ours.predict(ensemble, batch, policy)
+            return 200, _renderer(ensemble).render(res["labels"], combined)
+
+        def _renderer(ensemble):
+            # F4: the native renderer, prepared once per ensemble (immutable)
+            from .wire import Renderer
+
+            state = getattr(ensemble, "_state", None)
+            if state is None:
+                return Renderer(ensemble)
+            if "renderer" not in state:
+                state["renderer"] = Renderer(ensemble)
+            return state["renderer"]
 
         def _fast_path(ensemble, body):
             from types import SimpleNamespace

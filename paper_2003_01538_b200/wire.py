@@ -52,3 +52,55 @@ def fast_decode(body: bytes, dims, max_batch: int, pinned: bool = True, pixel_sc
     data = out[: n.value * d].reshape(n.value, d)
     policy = body[poff.value: poff.value + plen.value] if plen.value else None
     return data, policy
+
+
+class Renderer:
+    """F4: native response bodies (eb_render_prediction) for one ensemble -- the keys'
+    sorted order and every label's JSON encoding are prepared once, with the reference's
+    own json.dumps(ensure_ascii=True), so the bytes equal
+    dumps_canonical(render_prediction(ensemble, output, combined)) (eg/wire.py:136-143)."""
+
+    def __init__(self, ensemble):
+        import json
+
+        self.lib = _lib.load()
+        models = list(ensemble.models)
+        self.n = len(models)
+        self._label_bufs, offs = [], []
+        for m in models:
+            enc = [json.dumps(lab, ensure_ascii=True).encode() for lab in m.labels]
+            self._label_bufs.append(ctypes.create_string_buffer(b"".join(enc), sum(map(len, enc)) + 1))
+            offs.append(np.concatenate([[0], np.cumsum([len(e) for e in enc])]).astype(np.int64))
+        self._offs = offs
+        self._label_ptrs = (ctypes.c_char_p * self.n)(*[ctypes.cast(b, ctypes.c_char_p) for b in self._label_bufs])
+        self._off_ptrs = (ctypes.c_void_p * self.n)(*[o.ctypes.data for o in offs])
+        self._nlab = (ctypes.c_int32 * self.n)(*[len(m.labels) for m in models])
+        self._keys = {}
+        for with_comb in (False, True):
+            entries = [("_batch_size", -1)] + [(m.id, i) for i, m in enumerate(models)]
+            if with_comb:
+                entries.append(("_combined", -2))
+            entries.sort(key=lambda e: e[0])
+            kj = [json.dumps(k, ensure_ascii=True).encode() for k, _ in entries]
+            self._keys[with_comb] = ((ctypes.c_char_p * len(kj))(*kj),
+                                     (ctypes.c_int32 * len(kj))(*[k for _, k in entries]), len(kj), kj)
+
+    def render(self, labels: np.ndarray, combined=None) -> bytes:
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        b = int(labels.shape[1]) if labels.ndim == 2 else 0
+        keys, kinds, nk, _ = self._keys[combined is not None]
+        comb = None if combined is None else np.ascontiguousarray(np.asarray(combined, dtype=np.int32))
+        cap = 64 + b * (self.n + 1) * 32
+        for _ in range(2):
+            out = ctypes.create_string_buffer(cap)
+            n = c_uint64(0)
+            rc = self.lib.eb_render_prediction(labels.ctypes.data, self.n, b,
+                                               comb.ctypes.data if comb is not None else None,
+                                               keys, kinds, nk, self._label_ptrs, self._off_ptrs,
+                                               self._nlab, out, cap, byref(n))
+            if rc == _lib.EB_OK:
+                return out.raw[: n.value]
+            if rc != _lib.EB_E_TOO_LARGE:
+                _lib.check(rc)
+            cap = n.value
+        raise RuntimeError("render buffer sizing failed")

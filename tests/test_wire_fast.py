@@ -135,3 +135,29 @@ def test_pgm_declines_what_the_reference_rejects(doc):
     from paper_2003_01538_b200.wire import fast_decode
 
     assert fast_decode(_pgm_body([doc]), (1, 5, 7), 16, pinned=False, pixel_scale=255.0) is None
+
+
+@pytest.mark.parametrize("with_policy", [False, True])
+def test_native_render_matches_reference_bytes(with_policy):
+    """F4: eb_render_prediction == dumps_canonical(render_prediction(...)) byte for byte,
+    including label escaping (quotes, backslashes, control and non-ASCII characters) and
+    key order around the reserved "_batch_size" / "_combined" keys."""
+    from types import SimpleNamespace
+
+    from ensemblegate.jsonio import dumps_canonical
+    from ensemblegate.wire import render_prediction
+
+    from paper_2003_01538_b200.wire import Renderer
+
+    labels_a = ("absent", "present")
+    labels_b = ('say "hi"', "back\\slash", "tab\there", "café", "\U0001f600", "ctl\x01", "plain")
+    models = [SimpleNamespace(id=i, labels=l) for i, l in
+              (("zeta", labels_b), ("A1", labels_a), ("m.2", labels_b), ("_x"[1:], labels_a))]
+    ens = SimpleNamespace(models=tuple(models))
+    rng = np.random.default_rng(5)
+    r = Renderer(ens)
+    for b in (1, 3, 40):
+        idx = np.stack([rng.integers(0, len(m.labels), b) for m in models]).astype(np.int32)
+        out = SimpleNamespace(batch_size=b, per_model=tuple(tuple(int(v) for v in row) for row in idx))
+        comb = [int(v) for v in rng.integers(0, 2, b)] if with_policy else None
+        assert r.render(idx, comb) == dumps_canonical(render_prediction(ens, out, comb))
