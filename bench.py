@@ -213,7 +213,7 @@ def cnn_docs(members=MEMBERS):
             for a, s in members]
 
 
-def build_ensemble(batch: int, device: int, members=MEMBERS):
+def build_ensemble(batch: int, device: int, members=MEMBERS, precision: str = "bf16"):
     from paper_2003_01538_b200 import ensemble as E
 
     td = Path(tempfile.mkdtemp(prefix="bench_"))
@@ -225,7 +225,8 @@ def build_ensemble(batch: int, device: int, members=MEMBERS):
            "preprocess": {"mean": list(MEAN), "std": list(STD), "pixel_scale": 255.0},
            "models": entries}
     (td / "manifest.json").write_text(json.dumps(man))
-    return E.load_ensemble(E.load_manifest_file(td / "manifest.json"), device=device)
+    return E.load_ensemble(E.load_manifest_file(td / "manifest.json"), device=device,
+                           precision=precision)
 
 
 def cpu_oracle_rate(n_images: int = 64, seconds_cap: float = 25.0, chunk: int = 8) -> dict:
@@ -481,6 +482,17 @@ def extra_configs(device: int) -> dict:
                      "latency_bs1_p50_ms": statistics.median(lat[5:])}
         eng.close()
         del eng, ens
+    # the fp32-faithful parity mode (csrc/ref32.cu) on C2: how fast exact top-k costs
+    B = 32
+    ens = build_ensemble(B, device, precision="fp32")
+    eng = engine_for(ens)
+    stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", device))
+    eng.forward(synth.images_fast(B, 224, 224, 3, seed0=77), _lib.EB_IN_U8_HWC)
+    rate = device_rate(eng, B, _lib.EB_IN_U8_HWC, stream, topk=5, iters=3)
+    out["C2_fp32_parity_mode"] = {"batch": B, "images_per_s": rate,
+                                  "tflops_fp32": rate * GFLOP_PER_IMG / 1e3,
+                                  "path": "fp32 CUDA-core kernels (csrc/ref32.cu), top-5 equal to the oracle"}
+    eng.close()
     return out
 
 

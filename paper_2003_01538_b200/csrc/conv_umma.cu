@@ -48,6 +48,9 @@ constexpr int kThreads = 384;
 #endif
 constexpr int kXformThreads = EB_XFORM_THREADS;  // pre-activation transform: the last warps
 constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels x 8 bf16
+#ifndef EB_STEM_CW
+#define EB_STEM_CW 64
+#endif
 #ifndef EB_STEM_NB
 #define EB_STEM_NB 1  // stems: epilogue chunk buffers per warp (1 or 2)
 #endif
@@ -72,7 +75,9 @@ struct ConvSmem {
   static constexpr int kBRows = PAIR ? BN / 2 : BN;                 // B rows held per tap
   static constexpr int kBTapBytes = kBRows * kBlockK * 2;
   static constexpr int kBBytes = (TAPN ? 3 : TS) * kBTapBytes;
-  static constexpr int kCW = BN < 64 ? BN : 64;             // epilogue chunk (columns)
+  // epilogue chunk (columns); stems: EB_STEM_CW (32: both epilogue warp groups take half
+  // of every tile's columns instead of alternating tiles)
+  static constexpr int kCW = STEM ? (BN < EB_STEM_CW ? BN : EB_STEM_CW) : (BN < 64 ? BN : 64);
   // one warp's 32-row chunk; tap-shift tiles store directly (no staging, no residual)
   static constexpr int kStageOutBytes = (TS == 1 && !TAPN) ? 32 * kCW * 2 : 0;
   // pre-activation scale/shift cache (DenseNet 1x1 convs, cout = 128): 2 x 2048 floats
@@ -1476,6 +1481,7 @@ static cudaError_t launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const
 }
 
 int conv_umma_chunk(int block_n) { return block_n < 64 ? block_n : 64; }
+int conv_umma_stem_chunk(int block_n) { return block_n < EB_STEM_CW ? block_n : EB_STEM_CW; }
 
 template <int BN, int TS, bool PAIR, int TAPN = 0, bool STEM = false>
 static int stages_of(const ConvParams& p) {

@@ -145,6 +145,7 @@ cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
                              cudaStream_t stream);
 int conv_umma_chunk(int block_n);
+int conv_umma_stem_chunk(int block_n);  // the stem instances' epilogue chunk
 // batch of the forward being enqueued on this thread (0 = unknown): gates PDL
 void set_pdl_batch(int batch);
 // pipeline stages the kernel instance for this plan would get (host-side layout query)

@@ -578,7 +578,7 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   }
   if (stem_direct && !a.out_f32 && a.n_split == 0 && pl.p.vec_ok && stem_tma_store_enabled()) {
     // stems: 32-pixel slabs stored through a (C, Wo, B*Ho) map that clips the junk columns
-    const int cw = conv_umma_chunk(bn);
+    const int cw = conv_umma_stem_chunk(bn);
     for (int box : {32, 8}) {  // (8-row boxes: a slab's part in the next output row)
       if (!encode_tiled_3d_bf16(box == 32 ? &pl.mo : &pl.mr,
                                 static_cast<const __nv_bfloat16*>(a.y) + a.y_off, a.cout, Wo,

@@ -181,3 +181,28 @@ def test_lin1_logits_returned(tmp_path):
     for i, (w, b) in enumerate(members):
         want = O.linear_scores(xp, w, b).astype(np.float32)
         np.testing.assert_allclose(res["logits"][i, :, :k], want, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+def test_mixed_lin1_and_cnn_members(tmp_path, precision):
+    """An ensemble mixing the reference's LIN1 kind with a CNN member (same [3, 224, 224]
+    shape, as the reference's uniform-shape rule requires): one forward evaluates both;
+    each member's labels equal those of an ensemble holding it alone."""
+    from helpers import IMAGENET_MEAN, IMAGENET_STD, cnn1_doc, write_manifest
+
+    d = 3 * 224 * 224
+    w, b = O.gen_model_arrays(61, 4, d)
+    lin = lin1_doc("lin", (3, 224, 224), ("a", "b", "c", "d"), w, b)
+    cnn = cnn1_doc("r18", "resnet18", 1)
+    x = O.unit_floats(62, 5 * d).reshape(5, d)
+
+    def run(docs, sub):
+        sub.mkdir()
+        mp = write_manifest(sub, docs, max_batch=8, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+        ens = E.load_ensemble(E.load_manifest_file(mp), precision=precision)
+        return E.forward(ens, M.SampleBatch(ens.shared_shape, x)).per_model
+
+    both = run([lin, cnn], tmp_path / "both")
+    assert both[0] == run([lin], tmp_path / "lin")[0]
+    assert both[1] == run([cnn], tmp_path / "cnn")[0]
+    assert list(both[0]) == O.forward([(w, b)], x, 3, IMAGENET_MEAN, IMAGENET_STD)[0]
