@@ -611,7 +611,9 @@ def main() -> None:
     # right after the timed region so that it runs at the same power-capped clocks)
     # per-op median of 3 serialised runs (an eager run's event times absorb any host-side
     # launch hiccup of the op that follows it)
-    ms = np.median(np.stack([eng.profile(B, kind) for _ in range(3)]), axis=0) if not args.minimal else np.zeros(eng.n_ops)
+    # (each op launched 5 times back to back per run: its own duration, not the host's
+    # launch latency between serialised eager launches)
+    ms = np.median(np.stack([eng.profile(B, kind, repeat=5) for _ in range(3)]), axis=0) if not args.minimal else np.zeros(eng.n_ops)
     conv_ms = conv_flops = 0.0
     top = None
     for m, t in zip(eng.op_meta, ms):

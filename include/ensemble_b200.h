@@ -179,6 +179,10 @@ int eb_engine_stream(eb_engine* e, void** stream);
  * (CUDA events around every op on one stream); host_ms holds one float per op
  * in eb_add_op order.  Used for the roofline of each kernel class. */
 int eb_profile_ops(eb_engine* e, int input_kind, int batch, float* host_ms, int n_ops);
+/* As eb_profile_ops with every op launched `repeat` times back to back (1..100); host_ms
+ * gets the mean per launch, so short ops are timed without the host's launch latency. */
+int eb_profile_ops_repeat(eb_engine* e, int input_kind, int batch, float* host_ms, int n_ops,
+                          int repeat);
 /* Number of kernels one eb_forward_device launches for this batch size. */
 int eb_launch_count(eb_engine* e, int input_kind, int batch, int* count);
 

@@ -96,6 +96,7 @@ _SIGS = {
     "eb_engine_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "eb_launch_count": (c_int, [c_void_p, c_int, c_int, POINTER(c_int)]),
     "eb_profile_ops": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int]),
+    "eb_profile_ops_repeat": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int, c_int]),
     "eb_decode_request2": (c_int, [c_char_p, c_uint64, c_void_p, c_int, c_float, c_void_p, c_int,
                                    POINTER(c_int), POINTER(c_uint64), POINTER(c_uint64)]),
     "eb_render_prediction": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_int,

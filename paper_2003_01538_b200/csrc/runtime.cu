@@ -691,6 +691,7 @@ struct eb_engine {
   std::mutex mu;
   // profiling: when set, every op runs on the main stream bracketed by events
   std::vector<cudaEvent_t>* prof = nullptr;
+  int prof_repeat = 1;
   // stem convs reading an 8-channel image: padded-layout scratch (stem rows / planes modes)
   std::map<const eb_op_desc*, void*> stem_buf;
   // u8 input: stems reading the preprocessed image get their layout straight from K1;
@@ -970,13 +971,18 @@ eb_engine* e, int input_kind, int B, int* launches) {
   if (e->prof) {
     // profiling: every op serialised on the main stream in declaration order,
     // bracketed by events (one elapsed time per op)
+    // (prof_repeat > 1: each op launched that many times back to back -- every op is a
+    // pure function of tensors it does not write -- so a short op's time is its own, not
+    // the host's launch latency; the caller divides)
     for (const auto& op : e->ops) {
       cudaEvent_t ev;
       EB_CUDA(cudaEventCreate(&ev));
       e->prof->push_back(ev);
       EB_CUDA(cudaEventRecord(ev, s));
-      const int rc = enqueue_op(e, op, B, s, launches);
-      if (rc != EB_OK) return rc;
+      for (int r = 0; r < e->prof_repeat; ++r) {
+        const int rc = enqueue_op(e, op, B, s, launches);
+        if (rc != EB_OK) return rc;
+      }
     }
     cudaEvent_t ev;
     EB_CUDA(cudaEventCreate(&ev));
@@ -1748,25 +1754,35 @@ int eb_forward_batches(eb_engine* e, const void* const* host_inputs, int n_batch
 }
 
 int eb_profile_ops(eb_engine* e, int input_kind, int batch, float* host_ms, int n_ops) {
+  return eb_profile_ops_repeat(e, input_kind, batch, host_ms, n_ops, 1);
+}
+
+int eb_profile_ops_repeat(eb_engine* e, int input_kind, int batch, float* host_ms, int n_ops,
+                          int repeat) {
   int rc = check_batch(e, batch);
   if (rc != EB_OK) return rc;
   if (!host_ms || n_ops != static_cast<int>(e->ops.size()))
     EB_FAIL(EB_E_INVALID, "host_ms must hold one float per op");
+  if (repeat < 1 || repeat > 100) EB_FAIL(EB_E_INVALID, "repeat must be 1..100");
   std::lock_guard<std::mutex> lock(e->mu);
   cudaSetDevice(e->device);
   std::vector<cudaEvent_t> evs;
   e->prof = &evs;
+  e->prof_repeat = repeat;
   int launches = 0;
   rc = enqueue_layers(e, input_kind, batch, &launches);
   e->prof = nullptr;
+  e->prof_repeat = 1;
   cudaError_t ce = cudaStreamSynchronize(e->stream);
   if (rc == EB_OK && ce != cudaSuccess) {
     set_error(std::string("profile run: ") + cudaGetErrorString(ce));
     rc = EB_E_CUDA;
   }
   if (rc == EB_OK) {
-    for (int i = 0; i < n_ops && i + 1 < static_cast<int>(evs.size()); ++i)
+    for (int i = 0; i < n_ops && i + 1 < static_cast<int>(evs.size()); ++i) {
       cudaEventElapsedTime(&host_ms[i], evs[i], evs[i + 1]);
+      host_ms[i] /= static_cast<float>(repeat);
+    }
   }
   for (auto ev : evs) cudaEventDestroy(ev);
   return rc;

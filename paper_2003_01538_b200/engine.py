@@ -204,10 +204,13 @@ class Engine:
         check(self.lib.eb_engine_stream(self._h, byref(p)))
         return p.value
 
-    def profile(self, batch: int, input_kind: int) -> np.ndarray:
-        """Per-op device ms of one serialised eager run (eb_profile_ops)."""
+    def profile(self, batch: int, input_kind: int, repeat: int = 1) -> np.ndarray:
+        """Per-op device ms of one serialised eager run; with repeat > 1 each op is
+        launched that many times back to back and the mean per launch is returned
+        (eb_profile_ops_repeat)."""
         ms = np.zeros(self.n_ops, dtype=np.float32)
-        check(self.lib.eb_profile_ops(self._h, input_kind, batch, ms.ctypes.data, self.n_ops))
+        check(self.lib.eb_profile_ops_repeat(self._h, input_kind, batch, ms.ctypes.data,
+                                             self.n_ops, repeat))
         return ms
 
     def launch_count(self, input_kind: int, batch: int) -> int:
