@@ -225,8 +225,9 @@ def build_ensemble(batch: int, device: int, members=MEMBERS, precision: str = "b
            "preprocess": {"mean": list(MEAN), "std": list(STD), "pixel_scale": 255.0},
            "models": entries}
     (td / "manifest.json").write_text(json.dumps(man))
+    # one engine on this GPU, one execution context (whatever EB_DEVICES / EB_CONTEXTS say)
     return E.load_ensemble(E.load_manifest_file(td / "manifest.json"), device=device,
-                           precision=precision)
+                           precision=precision, devices=(device,), contexts=1)
 
 
 def cpu_oracle_rate(n_images: int = 64, seconds_cap: float = 25.0, chunk: int = 8) -> dict:
@@ -684,15 +685,19 @@ def main() -> None:
         from paper_2003_01538_b200 import ensemble as E
         from paper_2003_01538_b200 import models as M
 
-        f32 = (host_np.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0)).reshape(B, -1)
-        sb = M.SampleBatch(ens.shared_shape, f32)
-        E.forward(ens, sb)
-        n_f = max(3, args.steps // 4)
-        f_s = timed(lambda: [E.forward(ens, sb) for _ in range(n_f)])
-        extras["dropin_f32_forward"] = {
-            "images_per_s": B * n_f / f_s, "h2d_bytes_per_step": int(f32.nbytes),
-            "path": "ensemble.forward(ensemble, SampleBatch) -- f32 CHW from pageable numpy, labels "
-                    "back as EnsembleOutput (the reference's own call, eg/ensemble.py:232)"}
+        try:
+            f32 = (host_np.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0)).reshape(B, -1)
+            sb = M.SampleBatch(ens.shared_shape, f32)
+            E.forward(ens, sb)
+            n_f = max(3, args.steps // 4)
+            f_s = timed(lambda: [E.forward(ens, sb) for _ in range(n_f)])
+            extras["dropin_f32_forward"] = {
+                "images_per_s": B * n_f / f_s, "h2d_bytes_per_step": int(f32.nbytes),
+                "path": "ensemble.forward(ensemble, SampleBatch) -- f32 CHW from pageable numpy "
+                        "(pinned staging slots), labels back as EnsembleOutput (the reference's own "
+                        "call, eg/ensemble.py:232)"}
+        except Exception as exc:  # an extra, never fatal
+            extras["dropin_f32_forward"] = {"error": str(exc)[:200]}
 
     # ---- p50 latency at bs=1 (e2e through eb_forward) and the batch sweep
     one = host_np[:1].copy()

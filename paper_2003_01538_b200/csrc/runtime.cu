@@ -356,9 +356,11 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     static const int max_rows = getenv("EB_SPLIT_MAX_ROWS") ? atoi(getenv("EB_SPLIT_MAX_ROWS")) : 1;
     const int64_t rows_img = a.flatten ? 1 : static_cast<int64_t>(Ho) * Wo;
     const int64_t tiles1 = ((rows_img + 127) / 128) * nt;
+    static const int cap = getenv("EB_SPLIT_CAP") ? atoi(getenv("EB_SPLIT_CAP")) : 32;
     if (!a.res && !tap_shift && rows_img <= max_rows && tiles1 * 4 <= 148 && num_kb >= 32) {
       splits = static_cast<int>(std::min<int64_t>(148 / tiles1, num_kb / 16));
-      splits = std::max(1, std::min(splits, 32));
+      // (conv layers -- several rows per image -- at most EB_SPLIT_CAP slices)
+      splits = std::max(1, std::min(splits, rows_img > 1 ? cap : 32));
     }
   }
   if (splits > num_kb) splits = num_kb;
