@@ -234,7 +234,9 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
         a.c8_stem || a.flatten || a.res)
       EB_FAIL(EB_E_INVALID, "unsupported grouped convolution geometry");
   }
-  const bool tap_shift = !tiled && !a.c8_stem && !a.flatten && a.kw == 3 && a.pw == 1 &&
+  // (pw 0 or 1: the padded grid is Wo + 2 columns wide either way -- W + 2 or W; the
+  // im2col map's traversal box covers it, unpadded Inception convs included)
+  const bool tap_shift = !tiled && !a.c8_stem && !a.flatten && a.kw == 3 && (a.pw == 1 || a.pw == 0) &&
                          a.sh == 1 && a.sw == 1 && !a.res && !a.out_f32 && bn_guess <= 128 &&
                          tap_shift_enabled();
   // taps-in-N: small Cout (the MMA would otherwise re-read A from smem per 32 columns).

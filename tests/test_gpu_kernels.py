@@ -91,6 +91,11 @@ CASES = [
     ("tallWp64", 2, 10, 62, 128, 32, 3, 3, 1, 1, 1, 1),
     ("tallWp66", 2, 6, 64, 128, 32, 3, 3, 1, 1, 1, 1),
     ("tallc512", 2, 14, 14, 512, 32, 3, 3, 1, 1, 1, 1),  # weights too large: regular taps-in-N
+    # unpadded 3x3 stride-1 (Inception-v3 Conv2d_2a / 4a): padded-grid modes with Wp = W
+    ("valid3x3c32", 2, 37, 37, 32, 32, 3, 3, 1, 1, 0, 0),
+    ("valid3x3c192", 2, 19, 19, 80, 192, 3, 3, 1, 1, 0, 0),
+    ("valid3x3c64", 3, 21, 17, 64, 64, 3, 3, 1, 1, 0, 0),
+    ("valid3x3tall", 2, 16, 16, 128, 32, 3, 3, 1, 1, 0, 0),
 ]
 
 
