@@ -223,8 +223,13 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
   const int Ho = a.flatten ? 1 : conv_out(a.H, a.kh, a.sh, a.ph);
   const int Wo = a.flatten ? 1 : conv_out(a.W, a.kw, a.sw, a.pw);
   if (Ho <= 0 || Wo <= 0) EB_FAIL(EB_E_SHAPE, "conv output would be empty");
+  // grouped convs (block-diagonal N tiles): 64-wide tiles whenever a group fits -- a
+  // tile's K window is its own channel block, so the zero off-diagonal blocks shrink with
+  // the tile (B200, ResNeXt-50 at B = 128: 3x3 grouped 94.7 -> 80.3 us at 56x56, 24.1 ->
+  // 18.7 us at 7x7 against 128-wide tiles; 32-wide tiles are slower again)
   const int bn_guess = a.block_n ? a.block_n
-                                 : (a.groups > 1 ? std::min(128, pick_block_n(a.cout))
+                                 : (a.groups > 1 ? (a.cout / a.groups <= 64 ? std::min(64, pick_block_n(a.cout))
+                                                                            : std::min(128, pick_block_n(a.cout)))
                                                  : pick_block_n(a.cout));
   if (a.groups > 1) {
     // block-diagonal grouped conv: an N tile of BN outputs reads the BN input channels of

@@ -103,7 +103,9 @@ def u8_lut(mean, std, pixel_scale: float, channels: int) -> np.ndarray:
 def pick_block_n(cout: int, groups: int = 1) -> int:
     """The N-tile width the native planner uses (runtime.cu pick_block_n)."""
     bn = 32 if cout <= 32 else 64 if cout <= 64 else 128 if cout <= 128 else (256 if cout % 256 == 0 else 128)
-    return min(bn, 128) if groups > 1 else bn
+    if groups > 1:  # (runtime.cu plan_conv: 64-wide block-diagonal tiles when a group fits)
+        return min(bn, 64) if cout // groups <= 64 else min(bn, 128)
+    return bn
 
 
 def pack_grouped_conv_weight(w: torch.Tensor, groups: int, block_n: int) -> torch.Tensor:
