@@ -78,3 +78,20 @@ def test_fp32_mode_batch_invariant_and_f32_input(tmp_path):
     f32 = (px.transpose(0, 3, 1, 2).astype(np.float32) / np.float32(255.0)).reshape(12, -1)
     _, _, r2 = E.predict(ens, M.SampleBatch(ens.shared_shape, f32), want_logits=True)
     assert np.array_equal(r2["logits"], full["logits"])
+
+
+def test_fp32_mode_bench_config_rows(tmp_path):
+    """The bench workload itself (C2 at B = 256, synth.images_fast seed 1234) in the fp32
+    mode: rows 0, 127, 128 and 255 of the 256-image batch have the oracle's top-5."""
+    g = np.load(GOLDEN / "cnn_c2_bench.npz")
+    docs = [cnn1_doc(f"{a}_{s}", str(a), int(s)) for a, s in zip(g["archs"], g["seeds"])]
+    ens = _load_fp32(tmp_path, docs, max_batch=256)
+    px = synth.images_fast(256, 224, 224, 3, seed0=int(g["seed0"]))
+    _, _, res = E.predict_u8(ens, px, topk=TOPK, want_logits=True)
+    rows = [int(r) for r in g["rows"]]
+    for m in range(g["logits"].shape[0]):
+        ref = g["logits"][m]
+        got = res["logits"][m][rows, : ref.shape[-1]]
+        assert np.abs(got - ref).max() <= F32_REL_TOL * np.abs(ref).max()
+        assert (OC.topk_order(got, TOPK) == OC.topk_order(ref, TOPK)).all()
+        assert (res["topk_idx"][m][rows] == OC.topk_order(ref, TOPK)).all()
