@@ -11,4 +11,8 @@ ncu -i $O/k1_k5.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__
 # K6 (Track R)
 ncu --set full --clock-control none -k regex:"lin1" -c 4 -o $O/k6_lin1 -f python tools/lin1_probe.py 6 3000 > /dev/null 2>&1
 ncu -i $O/k6_lin1.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum > $O/k6_lin1_raw.csv 2>/dev/null
+# tensor-pipe utilisation / DRAM bytes of every kernel of the timed step (last 2 steps)
+ncu --clock-control none --csv --log-file $O/step_kernels_ncu.csv \
+    --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed \
+    python bench.py --minimal --steps 2 --warmup 3 > /dev/null 2>&1
 echo done
