@@ -500,7 +500,8 @@ int plan_conv(const ConvArgs& a, ConvPlan* out) {
     q.kb_per_split = q.num_kb;
     // 2-SM taps-in-N: the MMA re-reads the stacked 3-tap B for every K step; a CTA pair
     // halves that per SM.  Requires resident B (each CTA keeps its half).
-    bool tp = pair_tapn_enabled() && splits == 1 && mt >= 2 && nt == 1 && resb_enabled();
+    bool tp = pair_tapn_enabled() && splits == 1 && mt >= 2 && nt == 1 && resb_enabled() &&
+              !a.pool2;  // (the fused pool's tile re-cut has no 2-SM form)
     if (tp) {
       q.pair = 1;
       q.mcast = 1;
