@@ -48,6 +48,9 @@ constexpr int kThreads = 384;
 #endif
 constexpr int kXformThreads = EB_XFORM_THREADS;  // pre-activation transform: the last warps
 constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels x 8 bf16
+#ifndef EB_MAX_ACC
+#define EB_MAX_ACC 4  // TMEM accumulators per CTA at most (8: measured no gain on the stems)
+#endif
 #ifndef EB_STEM_CW
 #define EB_STEM_CW 64
 #endif
@@ -98,7 +101,8 @@ struct ConvSmem {
   static constexpr int kEpiBytes = kRingArea + 8 * BN * 4 + 2 * kPreMax * 4 + kXchBytes;
   // dynamic smem: everything (one CTA per SM); 1 KiB alignment slack + barrier block
   static constexpr int kBytes = 232448;
-  static constexpr int kBarBytes = 1024;
+  // up to 32 stages x 3 + 2 x 4 accumulators + 16 + 2 mbarriers (EB_MAX_ACC=8 needs 1088)
+  static constexpr int kBarBytes = EB_MAX_ACC >= 8 ? 1088 : 1024;
   static constexpr int kBudget = kBytes - 1024 - kBarBytes;
   // barrier block: 3 x 32 + 21 mbarriers + TMEM slot; small stages (stems) run deep rings
   static constexpr int kMaxStages = 32;
@@ -289,10 +293,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // TMEM accumulators: four when they fit the 512 columns (the MMA may then run up to three
   // tiles ahead of a slow epilogue), else two
   constexpr int kAccCols = TAPN ? 3 * BN : BN;  // TMEM columns per accumulator
-#ifndef EB_MAX_ACC
-#define EB_MAX_ACC 4
-#endif
-  constexpr int kNAcc = (EB_MAX_ACC >= 4 && 4 * kAccCols <= 512) ? 4 : 2;
+  constexpr int kNAcc = (EB_MAX_ACC >= 8 && 8 * kAccCols <= 512)   ? 8
+                        : (EB_MAX_ACC >= 4 && 4 * kAccCols <= 512) ? 4
+                                                                    : 2;
   uint64_t* tfull = empty + L.stages;  // [kNAcc] accumulator ready
   uint64_t* tempty = tfull + kNAcc;      // [kNAcc] accumulator drained
   uint64_t* rfull = tempty + kNAcc;      // [4 warps][4] residual chunk landed in ring buffer
