@@ -69,7 +69,14 @@ def install() -> None:
         _set(eg_gw, "load_ensemble", ours.load_ensemble)
         _set(eg_gw, "apply_policy", our_policy.apply_policy)
 
+        reference_predict = eg_gw.GatewayApp._predict
+
         def _predict(self, body: bytes):
+            if eg_gw.forward is not ours.forward:
+                # someone rebound the gateway's forward after install (the reference's own
+                # tests monkeypatch it, tests/test_gateway.py:109-118): honour it through the
+                # reference's unfused _predict, which calls gateway.forward
+                return reference_predict(self, body)
             ensemble = self._require_ensemble()
             if ensemble is None:
                 return 503, eg_gw._error_body("loading", "ensemble is still loading")
