@@ -17,12 +17,16 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def test_reference_suite_passes_through_the_seam():
+@pytest.mark.parametrize("contexts", ["1", "3"])
+def test_reference_suite_passes_through_the_seam(contexts):
+    """(contexts = 3: three execution contexts per engine, so the suite's concurrent
+    gateway tests run forwards in parallel on the GPU)"""
     suite = ROOT / "baseline" / "_ref_tests"
     ref = ROOT / "baseline" / "_ref"
     if not (suite / "conftest.py").exists() or not (ref / "ensemblegate").is_dir():
         pytest.fail("baseline/_ref(_tests) missing: run __graft_entry__.build() in the build container")
-    env = dict(os.environ, PYTHONPATH=f"{ROOT}{os.pathsep}{ref}", PYTHONDONTWRITEBYTECODE="1")
+    env = dict(os.environ, PYTHONPATH=f"{ROOT}{os.pathsep}{ref}", PYTHONDONTWRITEBYTECODE="1",
+               EB_CONTEXTS=contexts)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
                         "-p", "paper_2003_01538_b200.seam", str(suite)],
                        cwd=str(ROOT), env=env, capture_output=True, text=True, timeout=900)
