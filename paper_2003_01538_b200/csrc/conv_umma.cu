@@ -252,7 +252,7 @@ __device__ __forceinline__ void trace_cta(long long* tr, int which) {
 
 // EB_DBG timing probes (trace build only): 2 = MMA does not wait for the stem gather,
 // 3 = no pre-activation transform, 5 = no TMA output stores, 6 = epilogue loads TMEM
-// and releases it, nothing else, 7 = stems: no A loads.  Results are wrong under a
+// and releases it, nothing else, 7 = stems: no A loads, 8 = 6 and 7.  Results are wrong under a
 // probe; timing only.
 __device__ __forceinline__ bool dbg_probe(const ConvParams& p, int which) {
 #ifdef EB_ENABLE_TRACE
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     : p.a_mode == kAModeStemPlanes ? 4352u * kbs
                                                                    : static_cast<uint32_t>(S::kALoadBytes);
             // (gather mode with resident B: this stage only waits for the cp.async arrivals)
-            mbar_arrive_expect_tx(&full[stage], dbg_probe(p, 7) && stem_direct ? bbytes : abytes + bbytes);
+            mbar_arrive_expect_tx(&full[stage], (dbg_probe(p, 7) || dbg_probe(p, 8)) && stem_direct ? bbytes : abytes + bbytes);
           }
           if (TS > 1) {
             // filter row r, channel chunk cc: 136 consecutive padded-grid pixels at tap (r, 0);
@@ -630,8 +630,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // 8 pixels x 8 channels) of the padded layout; the next filter row is Wq
             // pixels further in both layouts
             const int run = stem_run_bytes(p.a_mode);
-            if (dbg_probe(p, 7)) {
-              // (probe 7: no A loads -- the MMAs read stale smem; timing only)
+            if (dbg_probe(p, 7) || dbg_probe(p, 8)) {
+              // (probe 7/8: no A loads -- the MMAs read stale smem; timing only)
             } else if (p.stem_lines) {
               // tall stem: one load per plane covers every filter row of the tile (row r is
               // Wq pixels = Wq / 8 lines further); the odd plane follows the even one
@@ -1172,7 +1172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         if (warp == 2 && lane == 0) trace_ev(p.trace, 2, tr_n, 23);
         if (ci == last_ci && p.early_release) release();
-        if (dbg_probe(p, 6)) {  // (probe 6: TMEM load + release only, timing only)
+        if (dbg_probe(p, 6) || dbg_probe(p, 8)) {  // (probe 6/8: TMEM load + release only)
           ++seq;
           continue;
         }
