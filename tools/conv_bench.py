@@ -26,6 +26,7 @@ ap.add_argument("--groups", type=int, default=1)
 ap.add_argument("--relayout", action="store_true", help="stem: padded rows / planes layout (c8_stem=2)")
 ap.add_argument("--pool", action="store_true", help="fused 2x2/2 max-pool (eb_k_conv_maxpool2)")
 ap.add_argument("--then-pool", action="store_true", help="conv then a separate eb_k_pool (2x2/2 max)")
+ap.add_argument("--graph", action="store_true", help="time a CUDA graph of --iters launches (no host cost)")
 a = ap.parse_args()
 lib = _lib.load()
 P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
@@ -69,22 +70,40 @@ if a.pool or a.then_pool:
     yp = torch.empty(a.B, Ho // 2, Wo // 2, a.COUT, device="cuda", dtype=torch.bfloat16)
 
 
+def stream_arg():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
 def run():
     if a.pool:
         _lib.check(lib.eb_k_conv_maxpool2(P(src), a.B, a.H, a.W, LD, LD, P(wp), P(bias), P(yp), a.COUT, 0,
-                                          a.COUT, a.KH, a.KW, a.P, a.P, 1, None))
+                                          a.COUT, a.KH, a.KW, a.P, a.P, 1, stream_arg()))
         return
     _lib.check(lib.eb_k_conv(P(src), a.B, a.H, a.W, LD, LD, P(wp), P(bias), P(res),
                              a.COUT if res is not None else 0, P(y), a.COUT, 0, a.COUT, a.KH, a.KW,
-                             a.S, a.S, a.P, a.P, 1, 0, STEM, a.split, a.block_n, a.groups, P(ws), P(pre_s), P(pre_t), None))
+                             a.S, a.S, a.P, a.P, 1, 0, STEM, a.split, a.block_n, a.groups, P(ws), P(pre_s), P(pre_t),
+                             stream_arg()))
     if a.then_pool:
         _lib.check(lib.eb_k_pool(P(y), a.COUT, P(yp), a.COUT, 0, a.B, Ho, Wo, a.COUT, 2, 2, 0, 0,
-                                 None, None, None))
+                                 None, None, stream_arg()))
 
 
 for _ in range(3):
     run()
 torch.cuda.synchronize()
+if a.graph:
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(a.iters):
+            run()
+    torch.cuda.synchronize()
+    body = run
+
+    def run():  # noqa: F811  (one replay = --iters launches; timed per launch below)
+        g.replay()
+
+    a_iters = a.iters
+    a.iters = 1
 # L2 flush buffer (inputs of the big layers exceed L2 anyway; small ones should not hit)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device="cuda")
 times = []
@@ -96,7 +115,7 @@ for _ in range(5):
         run()
     e1.record()
     torch.cuda.synchronize()
-    times.append(e0.elapsed_time(e1) / a.iters)
+    times.append(e0.elapsed_time(e1) / a.iters / (a_iters if a.graph else 1))
 ms = sorted(times)[len(times) // 2]  # median of 5 repeats
 flops = 2 * a.B * Ho * Wo * a.COUT * a.CIN * a.KH * a.KW
 bytes_ = 2 * (x.numel() + y.numel() + (res.numel() if res is not None else 0) + wp.numel())
