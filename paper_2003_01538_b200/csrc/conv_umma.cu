@@ -252,7 +252,7 @@ __device__ __forceinline__ void trace_cta(long long* tr, int which) {
 
 // EB_DBG timing probes (trace build only): 2 = MMA does not wait for the stem gather,
 // 3 = no pre-activation transform, 5 = no TMA output stores, 6 = epilogue loads TMEM
-// and releases it, nothing else, 7 = stems: no A loads, 8 = 6 and 7.  Results are wrong under a
+// and releases it, nothing else, 7 = stems: no A loads, 8 = 6 and 7, 9 = return at entry.  Results are wrong under a
 // probe; timing only.
 __device__ __forceinline__ bool dbg_probe(const ConvParams& p, int which) {
 #ifdef EB_ENABLE_TRACE
@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   trace_cta(p.trace, 0);
+  if (dbg_probe(p, 9)) return;  // (probe 9: launch cost only)
   const uint32_t warp = warp_id();
   constexpr int kTileRows = tall ? 126 : TAPN ? 120 : kBlockM;  // output rows a tile advances
   constexpr int kAccAll = kNAcc * kAccCols;
