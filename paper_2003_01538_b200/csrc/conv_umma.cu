@@ -819,6 +819,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();
+        if (lane_id() == 0) trace_ev(p.trace, 1, tr_n, 12);
         if (++stage == L.stages) {
           stage = 0;
           phase ^= 1;

@@ -2,6 +2,8 @@
 //   v0: loop, descriptors rebuilt per MMA (as a generic loop would)
 //   v1: unrolled groups of 12 MMAs, descriptors = base + compile-time offsets
 //   v2: like v1 but two warps issue, each into its own accumulator
+//   v3: groups of 6 MMAs (the VGG stem's tile), one commit to an mbarrier after each group
+//   v4: groups of 6 MMAs, two commits per group (the stage slot and the accumulator)
 // cycles per MMA over ITER MMAs per issuing warp, one CTA per SM.
 #include <cuda_runtime.h>
 
@@ -19,7 +21,7 @@ __global__ void __launch_bounds__(128, 1) issue_bench(long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bar[2];
-  for (int i = threadIdx.x; i < 98304 / 16; i += blockDim.x)
+  for (int i = threadIdx.x; i < 196608 / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0, 0);
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -47,6 +49,16 @@ __global__ void __launch_bounds__(128, 1) issue_bench(long long* out) {
         const uint64_t bd = umma_desc_sw128(smem_u32(smem + 65536) + r * 8192) + 2 * k;
         umma_bf16(td, ad, bd, idesc, i ? 1u : 0u);
       }
+    } else if (V == 3 || V == 4) {
+      for (int i = 0; i < ITER; i += 6) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const int r = j / 2, k = j & 1;
+          umma_bf16(td, a0 + r * 264 + 2 * k, b0 + r * 512 + 2 * k, idesc, (i | j) ? 1u : 0u);
+        }
+        umma_commit(&bar[1]);
+        if (V == 4) umma_commit(&bar[1]);
+      }
     } else {
       for (int i = 0; i < ITER; i += 12) {
 #pragma unroll
@@ -69,7 +81,7 @@ __global__ void __launch_bounds__(128, 1) issue_bench(long long* out) {
 
 template <int V, int N>
 void run(long long* d) {
-  const int smem = 98304;
+  const int smem = 196608;
   cudaFuncSetAttribute(issue_bench<V, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   issue_bench<V, N><<<148, 128, smem>>>(d);
   long long c = 0;
@@ -91,5 +103,8 @@ int main() {
   run<1, 192>(d);
   run<2, 192>(d);
   run<1, 256>(d);
+  run<3, 64>(d);
+  run<4, 64>(d);
+  run<3, 128>(d);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
