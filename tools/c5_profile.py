@@ -19,7 +19,7 @@ ens = bench.build_ensemble(B, 0, members=members)
 eng = engine_for(ens)
 px = synth.images_fast(B, 299, 299, 3, seed0=77)
 eng.forward(px, _lib.EB_IN_U8_HWC)
-ms = np.median(np.stack([eng.profile(B, _lib.EB_IN_U8_HWC) for _ in range(3)]), axis=0)
+ms = np.median(np.stack([eng.profile(B, _lib.EB_IN_U8_HWC, repeat=5) for _ in range(3)]), axis=0)
 lanes = collections.defaultdict(float)
 rows = []
 for m, t in zip(eng.op_meta, ms):
@@ -32,3 +32,7 @@ for r in sorted(rows, key=lambda r: -r[0])[:40]:
     print(round(r[0], 3), r[1], r[2], "lane", r[3], "TF/s", round(r[4]))
 json.dump([{"ms": float(r[0]), "name": r[1], "shape": r[2], "lane": r[3], "tflops": float(r[4])} for r in rows],
           open(ROOT / "gpurun_out" / "c5_profile.json", "w"))
+# the bench.py --profile-json format (tools/ops_roofline.py reads it)
+json.dump([{"i": i, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in m.items()}, "ms": float(t)}
+           for i, (m, t) in enumerate(zip(eng.op_meta, ms))],
+          open(ROOT / "gpurun_out" / "c5_per_op_profile.json", "w"), indent=0)

@@ -11,6 +11,7 @@ whole-step lower bounds:
 Non-conv ops (pool, GAP, ...) count at their measured time in both.
 
     python tools/ops_roofline.py profiles/round2/bench_per_op_profile.json [B] [--burst]
+        [--names=ResNet-50,DenseNet-121,VGG-16]   (member name of each lane; default C2's)
 
 The tensor bound uses the sustained bf16 peak of MEASURED_PEAKS.json (what a long step
 sees, as bench.py's roofline does); --burst uses the burst peak instead (each op of the
@@ -30,7 +31,9 @@ peaks = json.load(open(ROOT / "MEASURED_PEAKS.json")) if (ROOT / "MEASURED_PEAKS
 TC = (peaks.get("bf16_tflops", 1616.7) if "--burst" in sys.argv
       else peaks.get("bf16_tflops_sustained", 1363.1)) * 1e12
 HBM = peaks.get("hbm_gbs", 6536.4) * 1e9
-LANES = {0: "ResNet-50", 1: "DenseNet-121", 2: "VGG-16"}
+_names = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--names=")),
+              "ResNet-50,DenseNet-121,VGG-16")
+LANES = dict(enumerate(_names.split(",")))
 
 rows, other_ms, tot_flops, tot_bytes = [], 0.0, 0.0, 0.0
 for o in ops:
