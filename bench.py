@@ -131,6 +131,26 @@ def hbm_kernels(B: int, hbm_peak: float, src: str) -> dict:
     return out
 
 
+def op_bounds(op_meta, ms, B: int, tc_peak_tflops: float, hbm_gbs: float) -> list:
+    """Per conv/FC launch: its roofline bound max(algorithmic flops / tensor peak,
+    algorithmic bytes / HBM) in ms beside its measured ms.  Bytes = the input read once
+    (a stem's 3 image channels, not the 8-channel padding) + the output written once (+ the
+    residual read) + the weights.  (tools/ops_roofline.py prints the breakdown.)"""
+    out = []
+    for m, t in zip(op_meta, ms):
+        if m.get("name") != "conv":
+            continue
+        ho, wo, co, kh, kw, s, ci = m["shape"]
+        cin = 3 if ci == 8 else ci
+        nbytes = B * 2 * (ho * s * wo * s * cin + ho * wo * co * (2 if m.get("res", -1) >= 0 else 1)) \
+            + m.get("weight_bytes", 0)
+        t_tc = m["flops"] * B / (tc_peak_tflops * 1e12) * 1e3
+        t_hbm = nbytes / (hbm_gbs * 1e9) * 1e3
+        out.append({"meta": m, "ms": float(t), "tensor_ms": t_tc, "hbm_ms": t_hbm,
+                    "bound_ms": max(t_tc, t_hbm), "bytes": nbytes})
+    return out
+
+
 def peaks() -> tuple[dict, str]:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -634,6 +654,7 @@ def main() -> None:
                        "algorithmic_bytes_per_launch": t["algorithmic_bytes"], "source": t["source"]}
             break
     peak = pk["bf16_tflops_sustained"]
+    bound_ms = sum(r["bound_ms"] for r in op_bounds(eng.op_meta, ms, B, peak, pk["hbm_gbs"]))
     if args.profile_json and rank == 0:
         Path(args.profile_json).write_text(json.dumps(
             [{"i": i, **{k: (list(v) if isinstance(v, tuple) else v) for k, v in m.items()}, "ms": float(t)}
@@ -775,7 +796,9 @@ def main() -> None:
                          "peak_source": f"{pk_src} bf16_tflops_sustained",
                          "flops_per_step": conv_flops, "kernel_ms_per_step_serialised": conv_ms,
                          "step_frac_of_peak": GFLOP_PER_IMG * 1e9 * global_b / (dev_ms / args.steps / 1e3) / 1e12 / peak / world,
-                         "top_launch": {"shape(ho,wo,cout,kh,kw,s,cin)": list(top[0]["shape"]), "ms": top[1]} if top else None},
+                         "top_launch": {"shape(ho,wo,cout,kh,kw,s,cin)": list(top[0]["shape"]), "ms": top[1]} if top else None,
+                         # each conv/FC launch against its own roofline bound (tensor or HBM)
+                         "per_op_bound_ms": bound_ms, "per_op_bound_frac": bound_ms / conv_ms if conv_ms else None},
             "clocks": clk.summary(),
             "hbm_kernels": hbm,
             "cpu_baseline": cpu,

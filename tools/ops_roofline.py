@@ -35,21 +35,14 @@ _names = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--names="))
               "ResNet-50,DenseNet-121,VGG-16")
 LANES = dict(enumerate(_names.split(",")))
 
-rows, other_ms, tot_flops, tot_bytes = [], 0.0, 0.0, 0.0
-for o in ops:
-    if o.get("name") != "conv":
-        other_ms += o["ms"]
-        continue
-    ho, wo, co, kh, kw, s, ci = o["shape"]
-    hi, wi = ho * s, wo * s
-    cin = 3 if ci == 8 else ci  # stems: the image's 3 channels (the layout pads them to 8)
-    # (a grouped stem launch reads its shared input once and writes every member's columns)
-    nbytes = B * 2 * (hi * wi * cin + ho * wo * co * (2 if o["res"] >= 0 else 1)) + o["weight_bytes"]
-    flops = o["flops"] * B
-    t_tc, t_hbm = flops / TC * 1e3, nbytes / HBM * 1e3
-    rows.append(dict(o=o, ms=o["ms"], tc=t_tc, hbm=t_hbm, bound=max(t_tc, t_hbm)))
-    tot_flops += flops
-    tot_bytes += nbytes
+sys.path.insert(0, str(ROOT))
+from bench import op_bounds  # noqa: E402  (the same bound bench.py reports)
+
+bounds = op_bounds(ops, [o["ms"] for o in ops], B, TC / 1e12, HBM / 1e9)
+rows = [dict(o=r["meta"], ms=r["ms"], tc=r["tensor_ms"], hbm=r["hbm_ms"], bound=r["bound_ms"]) for r in bounds]
+other_ms = sum(o["ms"] for o in ops if o.get("name") != "conv")
+tot_flops = sum(r["o"]["flops"] * B for r in rows)
+tot_bytes = sum(r["bytes"] for r in bounds)
 
 conv_ms = sum(r["ms"] for r in rows)
 sum_bound = sum(r["bound"] for r in rows)
