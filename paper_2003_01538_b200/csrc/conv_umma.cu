@@ -372,6 +372,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.mcast) cluster_sync();  // the peer's barriers exist before we multicast into it
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (warp == 0 && elect_one()) {
+    // resident weights: no earlier kernel of the graph writes them, so they are fetched
+    // before the PDL wait and land while the previous layer drains
+    if (p.resb && PAIR) {
+      // 2-SM taps-in-N: each CTA keeps its half of the stacked [tap0; tap1; tap2] rows
+      // (rows 1.5*BN*crank .. +1.5*BN, as three BN/2-row boxes); both halves complete
+      // on the leader's barrier
+      const uint32_t rb = mapa_shared(smem_u32(bres), 0);
+      if (crank == 0) mbar_arrive_expect_tx(bres, 2u * L.resb_bytes);
+      for (int kb = 0; kb < p.num_kb * kbs; ++kb) {
+        uint8_t* sb = smem + kb * S::kBBytes;
+        const int r = kb / p.cchunks;
+        const int cc = kb - r * p.cchunks;
+        for (int box = 0; box < 3; ++box) {
+          const int R = (3 * static_cast<int>(crank) + box) * (BN / 2);  // stacked row
+          const int tap = R / BN;
+          tma_load_2d_pair(sb + box * S::kBTapBytes, &map_b, rb,
+                           ((r * p.kw + tap) * p.cchunks + cc) * kBlockK, R - tap * BN);
+        }
+      }
+    } else if (p.resb) {
+      // resident B (single N tile): every K block's weights, once per CTA
+      mbar_arrive_expect_tx(bres, L.resb_bytes);
+      // (stems: kbs K blocks per stage; tall taps-in-N: kh filter rows per channel chunk)
+      const int n_res = p.num_kb * kbs * (tall ? p.taps / p.kw : 1);
+      for (int kb = 0; kb < n_res; ++kb) {
+        uint8_t* sb = smem + kb * S::kBBytes;
+        if (TAPN || TS > 1) {
+          const int r = kb / p.cchunks;
+          const int cc = kb - r * p.cchunks;
+          for (int s2 = 0; s2 < (TAPN ? 3 : TS); ++s2)
+            tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, bres,
+                        ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, 0);
+        } else {
+          tma_load_2d(sb, &map_b, bres, kb * kBlockK, 0);
+        }
+      }
+    }
+  }
   // PDL: everything above overlapped the previous layer's tail; from here on we read
   // its output.  Let the next layer's CTAs start their own prologue as SMs free up.
   pdl_wait();
@@ -384,41 +423,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int tr_n = 0;
-      if (p.resb && PAIR) {
-        // 2-SM taps-in-N: each CTA keeps its half of the stacked [tap0; tap1; tap2] rows
-        // (rows 1.5*BN*crank .. +1.5*BN, as three BN/2-row boxes); both halves complete
-        // on the leader's barrier
-        const uint32_t rb = mapa_shared(smem_u32(bres), 0);
-        if (crank == 0) mbar_arrive_expect_tx(bres, 2u * L.resb_bytes);
-        for (int kb = 0; kb < p.num_kb * kbs; ++kb) {
-          uint8_t* sb = smem + kb * S::kBBytes;
-          const int r = kb / p.cchunks;
-          const int cc = kb - r * p.cchunks;
-          for (int box = 0; box < 3; ++box) {
-            const int R = (3 * static_cast<int>(crank) + box) * (BN / 2);  // stacked row
-            const int tap = R / BN;
-            tma_load_2d_pair(sb + box * S::kBTapBytes, &map_b, rb,
-                             ((r * p.kw + tap) * p.cchunks + cc) * kBlockK, R - tap * BN);
-          }
-        }
-      } else if (p.resb) {
-        // resident B (single N tile): every K block's weights, once per CTA
-        mbar_arrive_expect_tx(bres, L.resb_bytes);
-        // (stems: kbs K blocks per stage; tall taps-in-N: kh filter rows per channel chunk)
-        const int n_res = p.num_kb * kbs * (tall ? p.taps / p.kw : 1);
-        for (int kb = 0; kb < n_res; ++kb) {
-          uint8_t* sb = smem + kb * S::kBBytes;
-          if (TAPN || TS > 1) {
-            const int r = kb / p.cchunks;
-            const int cc = kb - r * p.cchunks;
-            for (int s2 = 0; s2 < (TAPN ? 3 : TS); ++s2)
-              tma_load_2d(sb + s2 * S::kBTapBytes, &map_b, bres,
-                          ((r * p.kw + s2) * p.cchunks + cc) * kBlockK, 0);
-          } else {
-            tma_load_2d(sb, &map_b, bres, kb * kBlockK, 0);
-          }
-        }
-      }
       TileWalk tw;
       tw.init(t_first, t_step, nt, mtp);
       for (int t = t_first; t < total; t += t_step, tw.next()) {
