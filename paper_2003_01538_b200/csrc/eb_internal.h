@@ -141,6 +141,21 @@ struct ConvParams {
   const float* pre_shift;
 };
 
+// VGG block 1 fused (block1.cu): conv3x3(3->64)+ReLU, conv3x3(64->64)+ReLU, 2x2/2 max-pool;
+// input = the stem rows layout ([B][Hq][Wq][8], padding 1), output pooled NHWC
+struct Block1Params {
+  int H, W, Hq;                // image (= both convs' output) size; padded rows per image
+  int bh, nbands, nseg;        // strips: image x band of bh rows x 120-column segment
+  int strips;
+  const float* bias1;          // conv1_1 bias [64]
+  const float* bias2;          // conv1_2 bias [64]
+  __nv_bfloat16* out;          // pooled [B][H/2][W/2][ldo] at channel offset out_off
+  int ldo, out_off;
+};
+cudaError_t block1_launch(const CUtensorMap& mx, const CUtensorMap& mw1, const CUtensorMap& mw2,
+                          const Block1Params& p, int grid, cudaStream_t stream);
+bool pdl_enabled();
+
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
                              cudaStream_t stream);

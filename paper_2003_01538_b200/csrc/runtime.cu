@@ -712,6 +712,12 @@ struct eb_engine {
   // output conv i writes directly (-1 if none); op_skip marks the absorbed pool ops
   std::vector<int> op_pool;
   std::vector<uint8_t> op_skip;
+  // VGG block 1 fused at finalize (block1.cu): op_block1[i] = the stem conv whose output
+  // conv i (3x3 64->64 + fused pool) computes itself; block1_stem marks that stem op.  The
+  // fused kernel runs at batch sizes with enough strips (block1_bh); below, both ops run
+  // as declared.
+  std::vector<int> op_block1;
+  std::vector<uint8_t> block1_stem;
 };
 
 namespace {
@@ -838,6 +844,68 @@ int enqueue_op_f32(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, i
 }
 
 // One op on stream ls.
+// Band height of the fused VGG block 1 at batch B (0: run the two convs unfused).  The
+// fused and unfused paths compute bitwise the same values, so this may depend on B.
+int block1_bh(int B, int H, int W) {
+  const int nseg = (W + 119) / 120;
+  for (int bh : {112, 56, 28}) {
+    if (H % bh || bh % 2) continue;
+    if (static_cast<int64_t>(B) * (H / bh) * nseg >= 2 * num_sms()) return bh;
+  }
+  if (H % 28 == 0 && static_cast<int64_t>(B) * (H / 28) * nseg >= num_sms()) return 28;
+  return 0;
+}
+
+// The fused VGG block 1 (block1.cu) for stem conv sop -> conv c (+ its fused pool).
+int enqueue_block1(eb_engine* e, const eb_op_desc& sop, const eb_op_desc& c, int fused_pool, int B,
+                   int bh, cudaStream_t ls, int* launches) {
+  ConvArgs as{}, ac{};
+  const void* rd = nullptr;
+  const void* rd_c = nullptr;
+  conv_args_for(e, sop, B, -1, &as, &rd);
+  conv_args_for(e, c, B, fused_pool, &ac, &rd_c);
+  const Tensor& src = e->tensors[sop.src];
+  StemGeom g;
+  if (!rd || !stem_geom(B, src.h, src.w, 3, 3, 1, 1, 1, 1, &g) || g.mode != kAModeStemRows)
+    EB_FAIL(EB_E_STATE, "fused VGG block 1 needs the stem rows layout");
+  if (!(e->layouts_fused && sop.src == EB_T_IMAGE_NHWC8)) {  // else K1 wrote the layout
+    const void* x = static_cast<const uint8_t*>(src.dev) + static_cast<size_t>(sop.src_c_off) * 2;
+    EB_CUDA(k_stem_relayout(static_cast<const __nv_bfloat16*>(x), B, src.h, src.w, 1, 1, g.mode, g.Hq,
+                            g.Wq, static_cast<__nv_bfloat16*>(const_cast<void*>(rd)), ls));
+    ++*launches;
+  }
+  ConvPlan ps, pc;
+  int rc = plan_conv(as, &ps);
+  if (rc != EB_OK) return rc;
+  rc = plan_conv(ac, &pc);
+  if (rc != EB_OK) return rc;
+  if (ps.p.a_mode != kAModeStemRows || ps.block_n != 64 || ps.p.kbs != 3 || pc.p.a_mode != kAModeTapN ||
+      !pc.p.pool2 || pc.block_n != 64 || pc.p.tapn2 || pc.p.tall_rows || pc.p.pair)
+    EB_FAIL(EB_E_STATE, "fused VGG block 1: unexpected conv plans");
+  CUtensorMap mx;
+  std::string err;
+  // the padded image rows: (8 channels, Wq pixels, B * Hq rows), 136-pixel runs, zero fill
+  if (!encode_tiled_3d_bf16(&mx, rd, 8, g.Wq, static_cast<uint64_t>(B) * g.Hq, 8,
+                            static_cast<uint64_t>(g.Wq) * 8, 8, 136, 1, &err, 0))
+    EB_FAIL(EB_E_INVALID, err);
+  Block1Params p{};
+  p.H = src.h;
+  p.W = src.w;
+  p.Hq = g.Hq;
+  p.bh = bh;
+  p.nbands = src.h / bh;
+  p.nseg = (src.w + 119) / 120;
+  p.strips = B * p.nbands * p.nseg;
+  p.bias1 = as.bias;
+  p.bias2 = ac.bias;
+  p.out = static_cast<__nv_bfloat16*>(ac.y);
+  p.ldo = ac.ldy;
+  p.out_off = ac.y_off;
+  EB_CUDA(block1_launch(mx, ps.mb, pc.mb, p, std::min(p.strips, num_sms()), ls));
+  ++*launches;
+  return EB_OK;
+}
+
 int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* launches) {
   const uint8_t* pool = static_cast<const uint8_t*>(e->pool);
   auto P = [&](uint64_t off) -> const void* {
@@ -845,7 +913,14 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
   };
   const size_t op_idx = static_cast<size_t>(&op - e->ops.data());
   if (op_idx < e->op_skip.size() && e->op_skip[op_idx]) return EB_OK;  // fused into its conv
+  if (op_idx < e->block1_stem.size() && e->block1_stem[op_idx] &&
+      block1_bh(B, e->tensors[op.dst].h, e->tensors[op.dst].w) > 0)
+    return EB_OK;  // computed inside the next op's fused VGG block-1 kernel
   const int fused_pool = op_idx < e->op_pool.size() ? e->op_pool[op_idx] : -1;
+  if (op_idx < e->op_block1.size() && e->op_block1[op_idx] >= 0 && !e->f32) {
+    const int bh = block1_bh(B, e->tensors[op.src].h, e->tensors[op.src].w);
+    if (bh > 0) return enqueue_block1(e, e->ops[e->op_block1[op_idx]], op, fused_pool, B, bh, ls, launches);
+  }
   Tensor& src = e->tensors[op.src];
   Tensor& dst = e->tensors[op.dst];
   const size_t es = dsize(src.dtype);
@@ -1503,6 +1578,43 @@ void fuse_conv_pools(eb_engine* e) {
     ++i;
   }
 }
+
+// Peephole at finalize, after fuse_conv_pools: a stem conv (3x3/s1/p1 over the 8-channel
+// image in the rows layout, 64 outputs, ReLU) whose only reader is the next op on its
+// lane, a taps-in-N 3x3 64->64 conv with a fused 2x2 max-pool, becomes one kernel
+// (block1.cu).  EB_BLOCK1=0 keeps them apart (read per finalize: tests compare both).
+void fuse_block1(eb_engine* e) {
+  const size_t n = e->ops.size();
+  e->op_block1.assign(n, -1);
+  e->block1_stem.assign(n, 0);
+  if (!env_flag("EB_BLOCK1", true) || !stem_rows_enabled() || e->f32) return;
+  for (size_t i = 0; i + 1 < n; ++i) {
+    const eb_op_desc& sop = e->ops[i];
+    const eb_op_desc& c = e->ops[i + 1];
+    if (sop.kind != EB_OP_CONV || c.kind != EB_OP_CONV || e->op_skip[i] || e->op_pool[i] >= 0 ||
+        e->op_pool[i + 1] < 0 || c.src != sop.dst || c.stream != sop.stream || is_prefork(sop))
+      continue;
+    const Tensor& src = e->tensors[sop.src];
+    const Tensor& mid = e->tensors[sop.dst];
+    if (!(src.c == 8 && sop.src_c == 8 && sop.src_c_off == 0) || sop.kh != 3 || sop.kw != 3 ||
+        sop.sh != 1 || sop.sw != 1 || sop.ph != 1 || sop.pw != 1 || sop.cout != 64 || !sop.relu ||
+        sop.res >= 0 || sop.groups > 1 || sop.n_split || sop.flatten || sop.scale_off != EB_NO_OFFSET ||
+        sop.b_off == EB_NO_OFFSET || sop.dst_c_off != 0 || mid.c != 64 || mid.dtype != EB_BF16)
+      continue;
+    if (c.cout != 64 || c.src_c != 64 || c.src_c_off != 0 || !c.relu || c.b_off == EB_NO_OFFSET ||
+        mid.h % 2 || mid.w % 2 || mid.h < 28)
+      continue;
+    bool other = false;  // the conv1_1 output has no other reader
+    for (size_t k = 0; k < n; ++k)
+      if (k != i + 1 && (e->ops[k].src == sop.dst || e->ops[k].res == sop.dst)) other = true;
+    for (const auto& m : e->members)
+      if (m.tensor == sop.dst) other = true;
+    if (other) continue;
+    e->op_block1[i + 1] = static_cast<int>(i);
+    e->block1_stem[i] = 1;
+    ++i;
+  }
+}
 }  // namespace
 
 int eb_finalize(eb_engine* e) {
@@ -1516,6 +1628,7 @@ int eb_finalize(eb_engine* e) {
     e->op_pool.assign(e->ops.size(), -1);
     e->op_skip.assign(e->ops.size(), 0);
   }
+  fuse_block1(e);
   std::vector<uint8_t> t_read(e->tensors.size(), 0);  // tensors some op or member reads
   for (size_t i = 0; i < e->ops.size(); ++i) {
     if (e->op_skip[i]) continue;

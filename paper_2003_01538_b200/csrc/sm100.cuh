@@ -72,6 +72,13 @@ EB_DEVICE void tma_load_2d(void* dst, const void* map, uint64_t* bar, int c0, in
 }
 // Multicast tile load: the box lands at the same smem offset in every CTA of the
 // cluster named in cta_mask and completes tx bytes on each CTA's mbarrier there.
+EB_DEVICE void tma_load_3d(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 EB_DEVICE void tma_load_2d_mcast(void* dst, const void* map, uint64_t* bar, int c0, int c1,
                                  uint16_t cta_mask) {
   asm volatile(
