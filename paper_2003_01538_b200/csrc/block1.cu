@@ -15,19 +15,25 @@
 // taps-in-N + fused pool), so the pooled output is bitwise the same.
 //
 // Roles: warp 0 TMA producer (stem input runs; resident weights), warp 1 MMA issuer,
-// warps 2-9 epilogue (quarter = warp & 3 owns TMEM lanes 32q..32q+31; the two groups
-// take channels 0-31 / 32-63 of both the stem and the conv1_2 accumulators).
+// warps 2-9 conv1_2 epilogue (quarter = warp & 3 owns TMEM lanes 32q..32q+31; the two
+// groups take channels 0-31 / 32-63), warps 10-13 stem epilogue (one per lane quarter,
+// all 64 channels) -- the two epilogues run side by side.
 // Job order (identical in all roles): before conv1_2 tile t of the CTA's tile sequence,
-// every ring job (conv1_1 row) up to tile t's third row + 1 -- one row of look-ahead,
-// which also reaches into the next strip at the end of a strip.
+// every ring job (conv1_1 row) up to tile t's third row + kLook -- the stem epilogue
+// then has kLook tiles of MMA time to deliver a row; the look-ahead also reaches into the
+// next strip at the end of a strip.
 #include "eb_internal.h"
 #include "sm100.cuh"
 
 namespace eb {
 
 namespace {
-constexpr int kThreads1 = 384;
-constexpr int kRing = 5;                     // conv1_1 row slots: 3 read + 1 written ahead + 1 slack
+constexpr int kThreads1 = 448;  // producer, MMA, 8 conv1_2-epilogue warps, 4 stem-epilogue warps
+#ifndef EB_B1_LOOK
+#define EB_B1_LOOK 2
+#endif
+constexpr int kLook = EB_B1_LOOK;            // conv1_1 rows computed ahead of the tile that reads them
+constexpr int kRing = 3 + kLook + 1;         // conv1_1 row slots: 3 read + kLook written ahead + 1
 constexpr int kSlotBytes = 128 * 128;        // 128 grid rows x 64 channels bf16 (SW128 K-major)
 constexpr int kRunBytes = 136 * 16;          // one filter row's run: 136 padded pixels x 8 ch
 constexpr int kStemStage = 3 * kRunBytes;    // the 3 filter rows of one conv1_1 row segment
@@ -96,12 +102,12 @@ __global__ void __launch_bounds__(kThreads1, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&afull[i], 1);
-      mbar_init(&aempty[i], 8);
+      mbar_init(&aempty[i], 4);
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 8);
     }
     for (int i = 0; i < kRing; ++i) {
-      mbar_init(&rfull[i], 8);
+      mbar_init(&rfull[i], 4);
       mbar_init(&rempty[i], 1);
     }
     mbar_init(bres, 1);
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     for (int g = 0; g < ntile; ++g) {
       const int i = g / p.bh;
       const int t = g - i * p.bh;
-      const int need = min(i * rj + t + 3, nring - 1);
+      const int need = min(i * rj + t + 2 + kLook, nring - 1);
       for (; next <= need; ++next) on_ring(next);
       on_tile(i, t);
     }
@@ -233,121 +239,149 @@ __global__ void __launch_bounds__(kThreads1, 1)
           __syncwarp();
           ++tj;
         });
-  } else if (warp < 10) {
-    // ---------------------------------------------------------------- epilogue
+  } else if (warp >= 10) {
+    // ---------------------------------------------------------------- stem epilogue
     const uint32_t quarter = warp & 3;
-    const int half = (static_cast<int>(warp) - 2) >> 2;  // channels 32 * half .. + 31
     const int m = static_cast<int>(quarter) * 32 + lane;  // TMEM lane = grid position
     const uint32_t lane_off = (quarter * 32) << 16;
-    int sj = 0, tj = 0;
-    float2 keep[16];  // an even conv1_2 row's horizontally pooled values (fp32, pre-bias)
+    float2 bias_r[32];  // in registers: shared-memory bandwidth is what bounds this kernel
 #pragma unroll
-    for (int i = 0; i < 16; ++i) keep[i] = make_float2(0.f, 0.f);
+    for (int i = 0; i < 32; ++i) bias_r[i] = make_float2(bias1[2 * i], bias1[2 * i + 1]);
+    int sj = 0;
     walk(
         [&](int j) {
           int b, k, x0;
           ring_job(j, b, k, x0);
           const int slot = j % kRing;
           if (j >= kRing) mbar_wait(&rempty[slot], ((j / kRing) - 1) & 1);
-          uint32_t pk[16];
-          if (k >= 0 && k < p.H) {
-            const int a = sj & 1;
+          const bool live = k >= 0 && k < p.H;
+          const int col = x0 - 1 + m;  // conv1_1 column; outside the image it is padding
+          const bool inside = live && col >= 0 && col < p.W;
+          const int a = sj & 1;
+          if (live) {
             mbar_wait(&afull[a], (sj >> 1) & 1);
             tc_fence_after();
-            uint32_t r[32];
-            tmem_ld32(tmem_base + lane_off + kStemAcc0 + a * 64 + 32 * half, r);
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&aempty[a]);
-            const int col = x0 - 1 + m;  // conv1_1 column; outside the image it is padding
-            const bool inside = col >= 0 && col < p.W;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float2 v = __fadd2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
-                                          make_float2(bias1[32 * half + 2 * i], bias1[32 * half + 2 * i + 1]));
-              pk[i] = inside ? pack_bf16x2_relu(v.x, v.y) : 0u;
-            }
-            ++sj;
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = 0u;
           }
-          // grid position m is A row m + 2q of every quarter q it belongs to (quarter q
-          // covers positions 30q .. 30q + 31: the taps-in-N rows overlap by two)
           uint8_t* sb = ring + slot * kSlotBytes;
           const int qh = m / 30;
 #pragma unroll
-          for (int d = 0; d < 2; ++d) {
-            const int q = qh - d;
-            if (q < 0 || q > 3 || m - 30 * q > 31) continue;
-            const int R = m + 2 * q;
-            uint8_t* rowp = sb + (R >> 3) * 1024 + (R & 7) * 128;
+          for (int half = 0; half < 2; ++half) {  // channels 32 * half .. + 31
+            uint32_t pk[16];
+            if (live) {
+              uint32_t r[32];
+              tmem_ld32(tmem_base + lane_off + kStemAcc0 + a * 64 + 32 * half, r);
+              tmem_ld_wait();
+              if (half == 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&aempty[a]);
+              }
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-              const int chunk = 4 * half + c4;  // 16-byte chunk (8 channels) of the 128-byte row
-              *reinterpret_cast<uint4*>(rowp + ((chunk ^ (R & 7)) << 4)) =
-                  make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]);
+              for (int i = 0; i < 16; ++i) {
+                const float2 v = __fadd2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])),
+                                            bias_r[16 * half + i]);
+                pk[i] = inside ? pack_bf16x2_relu(v.x, v.y) : 0u;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = 0u;
+            }
+            // grid position m is A row m + 2q of every quarter q it belongs to (quarter q
+            // covers positions 30q .. 30q + 31: the taps-in-N rows overlap by two)
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+              const int q = qh - d;
+              if (q < 0 || q > 3 || m - 30 * q > 31) continue;
+              const int R = m + 2 * q;
+              uint8_t* rowp = sb + (R >> 3) * 1024 + (R & 7) * 128;
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) {
+                const int chunk = 4 * half + c4;  // 16-byte chunk (8 channels) of the 128-byte row
+                *reinterpret_cast<uint4*>(rowp + ((chunk ^ (R & 7)) << 4)) =
+                    make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]);
+              }
             }
           }
+          if (live) ++sj;
           fence_proxy_async_smem();  // generic-proxy writes, read by the MMAs (async proxy)
           __syncwarp();
           if (lane == 0) mbar_arrive(&rfull[slot]);
         },
+        [&](int, int) {});
+  } else if (warp >= 2) {
+    // ---------------------------------------------------------------- conv1_2 epilogue
+    const uint32_t quarter = warp & 3;
+    const int half = (static_cast<int>(warp) - 2) >> 2;  // channels 32 * half .. + 31
+    const uint32_t lane_off = (quarter * 32) << 16;
+    int tj = 0;
+    float2 bias_r[16];  // this group's 32 channels, in registers
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bias_r[i] = make_float2(bias2[32 * half + 2 * i], bias2[32 * half + 2 * i + 1]);
+    float2 keep[16];  // an even conv1_2 row's tap-combined values (fp32, pre-bias)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) keep[i] = make_float2(0.f, 0.f);
+    walk(
+        [&](int) {},
         [&](int i, int t) {
           const int a = tj & 1;
           mbar_wait(&tfull[a], (tj >> 1) & 1);
           tc_fence_after();
-          uint32_t r0[32], r1[32], r2[32];
           const uint32_t tb = tmem_base + lane_off + a * kConvAcc + 32 * half;
-          tmem_ld32(tb, r0);
-          tmem_ld32(tb + 64, r1);
-          tmem_ld32(tb + 128, r2);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[a]);
-          // out[m] = (D0[m] + D1[m+1]) + D2[m+2], then the horizontal max of lanes (2k, 2k+1)
-          float2 v2[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float2 d1 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * q]), 1),
-                                          __shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * q + 1]), 1));
-            const float2 d2 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r2[2 * q]), 2),
-                                          __shfl_down_sync(0xffffffffu, __uint_as_float(r2[2 * q + 1]), 2));
-            v2[q] = __fadd2_rn(__fadd2_rn(make_float2(__uint_as_float(r0[2 * q]), __uint_as_float(r0[2 * q + 1])), d1),
-                               d2);
+          const int s = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+          const int b = s / per_img;
+          const int rem = s - b * per_img;
+          const int band = rem / p.nseg;
+          const int x = 120 * (rem - band * p.nseg) + 30 * static_cast<int>(quarter) + lane;
+          const int y = band * p.bh + t;
+          const bool store = (t & 1) && !(lane & 1) && lane < 30 && x < p.W;
+          uint4* o4 = nullptr;
+          if (store) {
+            const size_t orow = (static_cast<size_t>(b) * (p.H >> 1) + (y >> 1)) * (p.W >> 1) + (x >> 1);
+            o4 = reinterpret_cast<uint4*>(p.out + orow * p.ldo + p.out_off + 32 * half);
           }
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            v2[q].x = fmaxf(v2[q].x, __shfl_down_sync(0xffffffffu, v2[q].x, 1));
-            v2[q].y = fmaxf(v2[q].y, __shfl_down_sync(0xffffffffu, v2[q].y, 1));
-          }
-          if ((t & 1) == 0) {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) keep[q] = v2[q];
-          } else {
-            // vertical max (even row first, as the unfused kernel's fmaxf(row 0, row 1)),
-            // then bias, ReLU, rounding
-            uint32_t pk[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              float2 w = make_float2(fmaxf(keep[q].x, v2[q].x), fmaxf(keep[q].y, v2[q].y));
-              w = __fadd2_rn(w, make_float2(bias2[32 * half + 2 * q], bias2[32 * half + 2 * q + 1]));
-              pk[q] = pack_bf16x2_relu(w.x, w.y);
+          for (int sub = 0; sub < 2; ++sub) {  // 16 channels at a time (register budget)
+            uint32_t r0[16], r1[16], r2[16];
+            tmem_ld16(tb + 16 * sub, r0);
+            tmem_ld16(tb + 64 + 16 * sub, r1);
+            tmem_ld16(tb + 128 + 16 * sub, r2);
+            tmem_ld_wait();
+            if (sub == 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[a]);
             }
-            const int s = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
-            const int b = s / per_img;
-            const int rem = s - b * per_img;
-            const int band = rem / p.nseg;
-            const int x = 120 * (rem - band * p.nseg) + 30 * static_cast<int>(quarter) + lane;
-            const int y = band * p.bh + t;  // odd
-            if (!(lane & 1) && lane < 30 && x < p.W) {
-              const size_t orow = (static_cast<size_t>(b) * (p.H >> 1) + (y >> 1)) * (p.W >> 1) + (x >> 1);
-              uint4* o4 = reinterpret_cast<uint4*>(p.out + orow * p.ldo + p.out_off + 32 * half);
+            // out[m] = (D0[m] + D1[m+1]) + D2[m+2]
+            float2 v2[8];
 #pragma unroll
-              for (int c4 = 0; c4 < 4; ++c4)
-                o4[c4] = make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]);
+            for (int q = 0; q < 8; ++q) {
+              const float2 d1 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * q]), 1),
+                                            __shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * q + 1]), 1));
+              const float2 d2 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r2[2 * q]), 2),
+                                            __shfl_down_sync(0xffffffffu, __uint_as_float(r2[2 * q + 1]), 2));
+              v2[q] = __fadd2_rn(
+                  __fadd2_rn(make_float2(__uint_as_float(r0[2 * q]), __uint_as_float(r0[2 * q + 1])), d1), d2);
+            }
+            if ((t & 1) == 0) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q) keep[8 * sub + q] = v2[q];
+            } else {
+              // the 2x2 max (vertical, then lanes (2k, 2k+1): max is exact in any order, the
+              // unfused kernel's horizontal-first order gives the same value), then bias,
+              // ReLU, rounding -- the shuffle runs once per row pair
+              uint32_t pk[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                float2 w = make_float2(fmaxf(keep[8 * sub + q].x, v2[q].x), fmaxf(keep[8 * sub + q].y, v2[q].y));
+                w.x = fmaxf(w.x, __shfl_down_sync(0xffffffffu, w.x, 1));
+                w.y = fmaxf(w.y, __shfl_down_sync(0xffffffffu, w.y, 1));
+                w = __fadd2_rn(w, bias_r[8 * sub + q]);
+                pk[q] = pack_bf16x2_relu(w.x, w.y);
+              }
+              if (store) {
+                o4[2 * sub] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                o4[2 * sub + 1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+              }
             }
           }
           ++tj;
