@@ -790,7 +790,7 @@ def main() -> None:
             "latency_bs1_ms": {"p50": statistics.median(lat), "p99": sorted(lat)[int(0.99 * (len(lat) - 1))],
                                "path": "eb_forward, B=1, host buffers"},
             "gpu_launches": int(n_launch * args.steps),
-            "roofline": {"bound": "tensor", "kernel": "conv_umma_kernel (all conv/FC launches)",
+            "roofline": {"bound": "tensor", "kernel": "conv_umma_kernel + block1_kernel (all conv/FC launches)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": f"{pk_src} bf16_tflops_sustained",
