@@ -31,7 +31,7 @@ if os.environ.get("EB_BUILD_TRACE"):
     BUILD = ROOT / "build_trace"
     LIB = ROOT / "tools" / "_ab" / "libtrace.so"
 
-SOURCES = ["conv_umma.cu", "block1.cu", "pointwise.cu", "combine.cu", "ref32.cu", "runtime.cu", "tmap.cpp",
+SOURCES = ["conv_umma.cu", "block1.cu", "stem_pool.cu", "pointwise.cu", "combine.cu", "ref32.cu", "runtime.cu", "tmap.cpp",
            "wire_decode.cpp"]
 
 

@@ -156,6 +156,23 @@ cudaError_t block1_launch(const CUtensorMap& mx, const CUtensorMap& mw1, const C
                           const Block1Params& p, int grid, cudaStream_t stream);
 bool pdl_enabled();
 
+// Grouped 7x7/2 stem of two members + both 3x3/2 (pad 1) max-pools (stem_pool.cu); input =
+// the stem planes layout with the tall-box line map, output = the two pooled tensors
+struct StemPoolParams {
+  int Ho, Wo;                  // stem output size (Wo <= 128: one planes tile per row)
+  int Hq, Wq;                  // padded rows per image / plane width of the planes layout
+  long long plane_px;          // pixels per plane
+  int lines;                   // 128-byte lines of one tall box (7 filter rows of a plane)
+  int pb, nbands, strips;      // strips: image x band of pb pooled rows
+  const float* bias;           // [128]: member 0's 64, then member 1's
+  __nv_bfloat16* out0;         // member 0 pooled [B][Ho/2][Wo/2][ld0] at off0
+  int ld0, off0;
+  __nv_bfloat16* out1;         // member 1 pooled
+  int ld1, off1;
+};
+cudaError_t stem_pool_launch(const CUtensorMap& ma, const CUtensorMap& mb, const StemPoolParams& p,
+                             int grid, cudaStream_t stream);
+
 cudaError_t conv_umma_launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                              const CUtensorMap& mr, const ConvParams& p, int block_n, int grid,
                              cudaStream_t stream);

@@ -718,6 +718,10 @@ struct eb_engine {
   // as declared.
   std::vector<int> op_block1;
   std::vector<uint8_t> block1_stem;
+  // grouped 7x7/2 stem + both members' 3x3/2 max-pools fused (stem_pool.cu): for the stem
+  // op, the indices of the two absorbed pool ops (-1: none); stempool_pool marks them
+  std::vector<std::pair<int, int>> op_stempool;
+  std::vector<uint8_t> stempool_pool;
 };
 
 namespace {
@@ -856,6 +860,62 @@ int block1_bh(int B, int H, int W) {
   return 0;
 }
 
+// Pooled rows per strip of the fused stem + pools at batch B (0: unfused).  Bitwise the
+// same values either way, so this may depend on B.
+int stempool_pb(int B, int Hp) {
+  for (int pb : {14, 7}) {
+    if (Hp % pb) continue;
+    if (static_cast<int64_t>(B) * (Hp / pb) >= num_sms()) return pb;
+  }
+  return 0;
+}
+
+int enqueue_stem_pool(eb_engine* e, const eb_op_desc& g, int B, int pb, cudaStream_t ls, int* launches) {
+  const auto pools = e->op_stempool[static_cast<size_t>(&g - e->ops.data())];
+  ConvArgs a{};
+  const void* rd = nullptr;
+  conv_args_for(e, g, B, -1, &a, &rd);
+  const Tensor& src = e->tensors[g.src];
+  StemGeom sg;
+  if (!rd || !stem_geom(B, src.h, src.w, 7, 7, 2, 2, 3, 3, &sg) || sg.mode != kAModeStemPlanes)
+    EB_FAIL(EB_E_STATE, "fused stem + pools needs the stem planes layout");
+  if (!(e->layouts_fused && g.src == EB_T_IMAGE_NHWC8)) {  // else K1 wrote the layout
+    const void* x = static_cast<const uint8_t*>(src.dev) + static_cast<size_t>(g.src_c_off) * 2;
+    EB_CUDA(k_stem_relayout(static_cast<const __nv_bfloat16*>(x), B, src.h, src.w, 3, 3, sg.mode, sg.Hq,
+                            sg.Wq, static_cast<__nv_bfloat16*>(const_cast<void*>(rd)), ls));
+    ++*launches;
+  }
+  ConvPlan pl;
+  const int rc = plan_conv(a, &pl);
+  if (rc != EB_OK) return rc;
+  if (pl.p.a_mode != kAModeStemPlanes || pl.block_n != 128 || pl.p.stem_lines <= 0 || pl.p.kbs != 7)
+    EB_FAIL(EB_E_STATE, "fused stem + pools: unexpected stem plan");
+  const eb_op_desc& q0 = e->ops[pools.first];
+  const eb_op_desc& q1 = e->ops[pools.second];
+  const Tensor& d0 = e->tensors[q0.dst];
+  const Tensor& d1 = e->tensors[q1.dst];
+  StemPoolParams p{};
+  p.Ho = e->tensors[g.dst].h;
+  p.Wo = e->tensors[g.dst].w;
+  p.Hq = sg.Hq;
+  p.Wq = sg.Wq;
+  p.plane_px = sg.plane_px;
+  p.lines = pl.p.stem_lines;
+  p.pb = pb;
+  p.nbands = (p.Ho / 2) / pb;
+  p.strips = B * p.nbands;
+  p.bias = a.bias;
+  p.out0 = static_cast<__nv_bfloat16*>(d0.dev);
+  p.ld0 = d0.c;
+  p.off0 = q0.dst_c_off;
+  p.out1 = static_cast<__nv_bfloat16*>(d1.dev);
+  p.ld1 = d1.c;
+  p.off1 = q1.dst_c_off;
+  EB_CUDA(stem_pool_launch(pl.ma, pl.mb, p, std::min(p.strips, num_sms()), ls));
+  ++*launches;
+  return EB_OK;
+}
+
 // The fused VGG block 1 (block1.cu) for stem conv sop -> conv c (+ its fused pool).
 int enqueue_block1(eb_engine* e, const eb_op_desc& sop, const eb_op_desc& c, int fused_pool, int B,
                    int bh, cudaStream_t ls, int* launches) {
@@ -916,6 +976,13 @@ int enqueue_op(eb_engine* e, const eb_op_desc& op, int B, cudaStream_t ls, int* 
   if (op_idx < e->block1_stem.size() && e->block1_stem[op_idx] &&
       block1_bh(B, e->tensors[op.dst].h, e->tensors[op.dst].w) > 0)
     return EB_OK;  // computed inside the next op's fused VGG block-1 kernel
+  if (op_idx < e->stempool_pool.size() && e->stempool_pool[op_idx] &&
+      stempool_pb(B, e->tensors[op.dst].h) > 0)
+    return EB_OK;  // pooled inside the fused stem launch
+  if (op_idx < e->op_stempool.size() && e->op_stempool[op_idx].first >= 0 && !e->f32) {
+    const int pb = stempool_pb(B, e->tensors[op.dst].h / 2);
+    if (pb > 0) return enqueue_stem_pool(e, op, B, pb, ls, launches);
+  }
   const int fused_pool = op_idx < e->op_pool.size() ? e->op_pool[op_idx] : -1;
   if (op_idx < e->op_block1.size() && e->op_block1[op_idx] >= 0 && !e->f32) {
     const int bh = block1_bh(B, e->tensors[op.src].h, e->tensors[op.src].w);
@@ -1583,6 +1650,51 @@ void fuse_conv_pools(eb_engine* e) {
 // image in the rows layout, 64 outputs, ReLU) whose only reader is the next op on its
 // lane, a taps-in-N 3x3 64->64 conv with a fused 2x2 max-pool, becomes one kernel
 // (block1.cu).  EB_BLOCK1=0 keeps them apart (read per finalize: tests compare both).
+// Peephole at finalize: a grouped stem launch of two members (7x7/2/p3 over the 8-channel
+// image in the planes layout, 64 + 64 output channels of one tensor, ReLU) whose two
+// channel halves are read only by one 3x3/2/p1 max-pool each becomes one kernel that writes
+// the pooled tensors (stem_pool.cu).  EB_STEM_POOL=0 keeps them apart (read per finalize).
+void fuse_stem_pools(eb_engine* e) {
+  const size_t n = e->ops.size();
+  e->op_stempool.assign(n, {-1, -1});
+  e->stempool_pool.assign(n, 0);
+  if (!env_flag("EB_STEM_POOL", true) || !stem_rows_enabled() || e->f32) return;
+  for (size_t i = 0; i < n; ++i) {
+    const eb_op_desc& g = e->ops[i];
+    if (g.kind != EB_OP_CONV || !g.prefork || g.n_split != 0 || g.cout != 128 || g.kh != 7 ||
+        g.kw != 7 || g.sh != 2 || g.sw != 2 || g.ph != 3 || g.pw != 3 || !g.relu || g.res >= 0 ||
+        g.groups > 1 || g.flatten || g.b_off == EB_NO_OFFSET || g.scale_off != EB_NO_OFFSET ||
+        g.dst_c_off != 0 || e->op_pool[i] >= 0 || e->op_skip[i])
+      continue;
+    const Tensor& src = e->tensors[g.src];
+    const Tensor& t = e->tensors[g.dst];
+    if (!(src.c == 8 && g.src_c == 8 && g.src_c_off == 0) || t.c != 128 || t.dtype != EB_BF16 ||
+        t.h % 2 || t.w % 2 || t.w > 128)
+      continue;
+    int pool_of[2] = {-1, -1};
+    bool ok = true;
+    for (size_t k = 0; k < n && ok; ++k) {
+      const eb_op_desc& o = e->ops[k];
+      if (k == i || (o.src != g.dst && o.res != g.dst)) continue;
+      const int half = o.src_c_off == 0 ? 0 : o.src_c_off == 64 ? 1 : -1;
+      const Tensor& d = e->tensors[o.dst];
+      if (o.kind != EB_OP_POOL || o.res == g.dst || half < 0 || o.src_c != 64 || pool_of[half] >= 0 ||
+          o.pool_mode != EB_POOL_MAX || o.kh != 3 || o.kw != 3 || o.sh != 2 || o.sw != 2 || o.ph != 1 ||
+          o.pw != 1 || o.scale_off != EB_NO_OFFSET || e->op_skip[k] || d.dtype != EB_BF16 || d.c % 8 ||
+          o.dst_c_off % 8)
+        ok = false;
+      else
+        pool_of[half] = static_cast<int>(k);
+    }
+    for (const auto& m : e->members)
+      if (m.tensor == g.dst) ok = false;
+    if (!ok || pool_of[0] < 0 || pool_of[1] < 0) continue;
+    e->op_stempool[i] = {pool_of[0], pool_of[1]};
+    e->stempool_pool[pool_of[0]] = 1;
+    e->stempool_pool[pool_of[1]] = 1;
+  }
+}
+
 void fuse_block1(eb_engine* e) {
   const size_t n = e->ops.size();
   e->op_block1.assign(n, -1);
@@ -1629,6 +1741,7 @@ int eb_finalize(eb_engine* e) {
     e->op_skip.assign(e->ops.size(), 0);
   }
   fuse_block1(e);
+  fuse_stem_pools(e);
   std::vector<uint8_t> t_read(e->tensors.size(), 0);  // tensors some op or member reads
   for (size_t i = 0; i < e->ops.size(); ++i) {
     if (e->op_skip[i]) continue;

@@ -1,0 +1,271 @@
+// stem_pool.cu -- the grouped 7x7/2 stem of two members (ResNet / ResNeXt / DenseNet:
+// conv 3->64 + bias + ReLU each, N = 128 concatenated) with both members' 3x3/2 (pad 1)
+// max-pools in one kernel: the 112 x 112 x 128 stem output (822 MB per 256 images) is
+// pooled in registers and never written.
+//
+// Work unit ("strip"): one image, a band of pb pooled rows (conv rows 2 p0 - 1 .. 2 p1 - 1;
+// the first band starts at conv row 0).  A conv row is one stem tile exactly (the planes
+// grid is 128 wide, Wo = 112), computed with the stem planes mode's descriptors: two tall
+// TMA boxes (even / odd column planes, all 7 filter rows) and 28 MMAs (K16 steps: even taps
+// 0-2, 4-6 then odd taps 1-3, 5-(7); N = 128).  The epilogue (8 warps: lane quarter x member)
+// rounds each value exactly as the stem kernel does (bias, ReLU, bf16), takes the max of
+// positions (2x-1, 2x, 2x+1) -- lane shuffles, and one smem hand-over of lane 31 to the
+// next quarter -- and runs the vertical max over conv rows (2y-1, 2y, 2y+1) in registers.
+// Max is exact in any order, so the pooled tensors are bitwise the unfused pair's.
+#include "eb_internal.h"
+#include "sm100.cuh"
+
+namespace eb {
+
+namespace {
+constexpr int kThreadsSP = 320;       // producer, MMA, 8 epilogue warps
+constexpr int kSPStages = 3;
+constexpr int kSPBRow = 128 * 128;    // weights of one filter row: 128 N x 64 K bf16 (SW128)
+constexpr int kSPB = 7 * kSPBRow;     // resident
+constexpr int kSPAcc = 4;             // TMEM accumulators (128 columns each)
+constexpr int kSPMaxStage = 31 * 1024;  // two tall boxes of <= 124 lines, 1024-aligned
+constexpr int kOffSPB = 0;
+constexpr int kOffSPStage = kOffSPB + kSPB;
+constexpr int kOffSPBias = kOffSPStage + kSPStages * kSPMaxStage;
+constexpr int kOffSPXch = kOffSPBias + 128 * 4;              // [member][quarter][parity] 128 B
+constexpr int kOffSPBar = kOffSPXch + 2 * 4 * 2 * 128;
+constexpr int kSPBars = 2 * kSPStages + 2 * kSPAcc + 1;
+constexpr int kSPSmem = kOffSPBar + kSPBars * 8 + 16 + 1024;
+static_assert(kSPSmem <= 232448, "stem_pool shared memory");
+}  // namespace
+
+__global__ void __launch_bounds__(kThreadsSP, 1)
+    stem_pool_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                     const StemPoolParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* bres_s = smem + kOffSPB;
+  uint8_t* stage_s = smem + kOffSPStage;
+  float* bias = reinterpret_cast<float*>(smem + kOffSPBias);
+  uint32_t* xch = reinterpret_cast<uint32_t*>(smem + kOffSPXch);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffSPBar);
+  uint64_t* empty = full + kSPStages;
+  uint64_t* tfull = empty + kSPStages;
+  uint64_t* tempty = tfull + kSPAcc;
+  uint64_t* bres = tempty + kSPAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+
+  const uint32_t warp = warp_id();
+  const int lane = static_cast<int>(lane_id());
+  const int ns = (p.strips - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                 static_cast<int>(gridDim.x);
+  const int Hp = p.Ho >> 1;  // pooled rows (3x3/2, pad 1, even Ho)
+  // strip i of this CTA -> image, first and last conv row
+  auto strip = [&](int i, int& b, int& y0, int& y1) {
+    const int s = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+    b = s / p.nbands;
+    const int band = s - b * p.nbands;
+    const int p0 = band * p.pb;
+    y0 = p0 > 0 ? 2 * p0 - 1 : 0;
+    y1 = 2 * (p0 + p.pb) - 1;
+  };
+
+  if (threadIdx.x < 128) bias[threadIdx.x] = p.bias[threadIdx.x];
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int i = 0; i < kSPStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < kSPAcc; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);
+    }
+    mbar_init(bres, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (warp == 0 && elect_one()) {  // weights: never written inside the graph
+    mbar_arrive_expect_tx(bres, kSPB);
+    for (int r = 0; r < 7; ++r) tma_load_2d(bres_s + r * kSPBRow, &map_b, bres, r * 64, 0);
+  }
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer
+    if (elect_one()) {
+      int st = 0;
+      uint32_t ph = 0;
+      const int plane_lines = static_cast<int>(p.plane_px >> 3);
+      for (int i = 0; i < ns; ++i) {
+        int b, y0, y1;
+        strip(i, b, y0, y1);
+        for (int y = y0; y <= y1; ++y) {
+          mbar_wait(&empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&full[st], 2 * p.lines * 128);
+          // padded row 2y (filter row 0) .. 2y + 6 of both column planes, whole rows
+          const int line = ((b * p.Hq + 2 * y) * p.Wq) >> 3;
+          uint8_t* dst = stage_s + st * kSPMaxStage;
+          tma_load_2d(dst, &map_a, &full[st], 0, line);
+          tma_load_2d(dst + p.lines * 128, &map_a, &full[st], 0, line + plane_lines);
+          if (++st == kSPStages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(128, 128);
+    const uint64_t b0 = umma_desc_sw128(smem_u32(bres_s));
+    const uint32_t odd16 = static_cast<uint32_t>(p.lines * 8);  // the odd plane's box
+    const uint32_t koff[4] = {0u, 2u, odd16, odd16 + 2u};
+    int st = 0, j = 0;
+    uint32_t ph = 0;
+    mbar_wait(bres, 0);
+    for (int i = 0; i < ns; ++i) {
+      int b, y0, y1;
+      strip(i, b, y0, y1);
+      for (int y = y0; y <= y1; ++y, ++j) {
+        const int a = j % kSPAcc;
+        mbar_wait(&tempty[a], ((j / kSPAcc) & 1) ^ 1);
+        mbar_wait(&full[st], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t a0 = umma_desc(smem_u32(stage_s + st * kSPMaxStage), 16, 128, 0);
+          for (int r = 0; r < 7; ++r)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_bf16(tmem_base + a * 128, a0 + r * static_cast<uint32_t>(p.Wq) + koff[k],
+                        b0 + r * (kSPBRow >> 4) + 2 * k, idesc, (r | k) ? 1u : 0u);
+          umma_commit(&empty[st]);
+          umma_commit(&tfull[a]);
+        }
+        __syncwarp();
+        if (++st == kSPStages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const uint32_t quarter = warp & 3;
+    const int member = (static_cast<int>(warp) - 2) >> 2;  // columns 64 * member .. + 63
+    const int pos = static_cast<int>(quarter) * 32 + lane;  // output column of the conv row
+    const uint32_t lane_off = (quarter * 32) << 16;
+    const float2* bias2 = reinterpret_cast<const float2*>(bias + 64 * member);
+    __nv_bfloat16* out = member ? p.out1 : p.out0;
+    const int ldo = member ? p.ld1 : p.ld0;
+    const int ooff = member ? p.off1 : p.off0;
+    uint32_t prev[32], acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) prev[i] = acc[i] = 0u;
+    int j = 0;
+    for (int i = 0; i < ns; ++i) {
+      int b, y0, y1;
+      strip(i, b, y0, y1);
+      for (int y = y0; y <= y1; ++y, ++j) {
+        const int a = j % kSPAcc;
+        mbar_wait(&tfull[a], (j / kSPAcc) & 1);
+        tc_fence_after();
+        uint32_t h[32];  // this position's 64 channels, rounded as the stem kernel stores them
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {  // 16 channels at a time (register budget)
+          uint32_t r[16];
+          tmem_ld16(tmem_base + lane_off + a * 128 + 64 * member + 16 * qd, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float2 v = __fadd2_rn(make_float2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1])),
+                                        bias2[8 * qd + q]);
+            h[8 * qd + q] = pack_bf16x2_relu(v.x, v.y);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[a]);
+        // horizontal: max of positions pos - 1, pos, pos + 1 (even pos); position -1 is
+        // padding, positions >= Wo never enter an even position's window (Wo even)
+        uint32_t* xw = xch + ((member * 4 + static_cast<int>(quarter)) * 2 + (j & 1)) * 32;
+        if (lane == 31 && quarter < 3) {
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            reinterpret_cast<uint4*>(xw)[c4] = make_uint4(h[4 * c4], h[4 * c4 + 1], h[4 * c4 + 2], h[4 * c4 + 3]);
+        }
+        named_bar_sync(1 + member, 128);
+        uint32_t* hm = h;  // (in place: each channel pair's shuffles precede its update)
+        const uint32_t* xr = xch + ((member * 4 + static_cast<int>(quarter) - 1) * 2 + (j & 1)) * 32;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          uint32_t up = __shfl_up_sync(0xffffffffu, h[c], 1);
+          const uint32_t dn = __shfl_down_sync(0xffffffffu, h[c], 1);
+          if (lane == 0) up = quarter > 0 ? xr[c] : h[c];
+          __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&up),
+                                      *reinterpret_cast<const __nv_bfloat162*>(&h[c]));
+          m2 = __hmax2(m2, *reinterpret_cast<const __nv_bfloat162*>(&dn));
+          hm[c] = *reinterpret_cast<uint32_t*>(&m2);
+        }
+        // vertical: pooled row py = max(conv rows 2py - 1, 2py, 2py + 1)
+        if ((y & 1) == 0) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            if (y == 0) {
+              acc[c] = hm[c];
+            } else {
+              __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&prev[c]),
+                                          *reinterpret_cast<const __nv_bfloat162*>(&hm[c]));
+              acc[c] = *reinterpret_cast<uint32_t*>(&m2);
+            }
+          }
+        } else {
+          if (y != y0 && !(lane & 1) && pos < p.Wo) {  // (a band's first odd row only primes prev)
+            uint32_t o[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&acc[c]),
+                                          *reinterpret_cast<const __nv_bfloat162*>(&hm[c]));
+              o[c] = *reinterpret_cast<uint32_t*>(&m2);
+            }
+            const size_t orow = (static_cast<size_t>(b) * Hp + (y >> 1)) * (p.Wo >> 1) + (pos >> 1);
+            uint4* o4 = reinterpret_cast<uint4*>(out + orow * ldo + ooff);
+#pragma unroll
+            for (int c4 = 0; c4 < 8; ++c4) o4[c4] = make_uint4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
+          }
+#pragma unroll
+          for (int c = 0; c < 32; ++c) prev[c] = hm[c];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, 512);
+}
+
+cudaError_t stem_pool_launch(const CUtensorMap& ma, const CUtensorMap& mb, const StemPoolParams& p,
+                             int grid, cudaStream_t stream) {
+  if (2 * p.lines * 128 > kSPMaxStage) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(stem_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSPSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreadsSP);
+  cfg.dynamicSmemBytes = kSPSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, stem_pool_kernel, ma, mb, p);
+}
+
+}  // namespace eb
