@@ -14,8 +14,8 @@
 // max-before-bias pooling, rounding) is the unfused pair's (conv_umma.cu stem rows mode,
 // taps-in-N + fused pool), so the pooled output is bitwise the same.
 //
-// Roles: warp 0 TMA producer (stem input runs; resident weights), warp 1 MMA issuer,
-// warps 2-9 conv1_2 epilogue (quarter = warp & 3 owns TMEM lanes 32q..32q+31; the two
+// Roles: warp 0 TMA producer (stem input runs; resident weights), warp 1 conv1_2 MMA
+// issuer, warp 14 stem MMA issuer, warps 2-9 conv1_2 epilogue (quarter = warp & 3 owns TMEM lanes 32q..32q+31; the two
 // groups take channels 0-31 / 32-63), warps 10-13 stem epilogue (one per lane quarter,
 // all 64 channels) -- the two epilogues run side by side.
 // Job order (identical in all roles): before conv1_2 tile t of the CTA's tile sequence,
@@ -28,11 +28,15 @@
 namespace eb {
 
 namespace {
-constexpr int kThreads1 = 448;  // producer, MMA, 8 conv1_2-epilogue warps, 4 stem-epilogue warps
+constexpr int kThreads1 = 480;  // producer, conv MMA, 8 conv1_2-epilogue, 4 stem-epilogue, stem MMA warps
 #ifndef EB_B1_LOOK
 #define EB_B1_LOOK 2
 #endif
-constexpr int kLook = EB_B1_LOOK;            // conv1_1 rows computed ahead of the tile that reads them
+constexpr int kLook = EB_B1_LOOK;
+#ifndef EB_B1_DBG
+#define EB_B1_DBG 0  // timing probes (variant builds only; results wrong): 1 no tap shuffles, 2 no ring stores,
+                   // 4 conv planes 1-2 not loaded from TMEM, 8 epilogues hand-shake only
+#endif            // conv1_1 rows computed ahead of the tile that reads them
 constexpr int kRing = 3 + kLook + 1;         // conv1_1 row slots: 3 read + kLook written ahead + 1
 constexpr int kSlotBytes = 128 * 128;        // 128 grid rows x 64 channels bf16 (SW128 K-major)
 constexpr int kRunBytes = 136 * 16;          // one filter row's run: 136 padded pixels x 8 ch
@@ -177,8 +181,11 @@ __global__ void __launch_bounds__(kThreads1, 1)
           },
           [&](int, int) {});
     }
-  } else if (warp == 1) {
-    // ---------------------------------------------------------------- MMA issuer
+  } else if (warp == 1 || warp == 14) {
+    // ---------------------------------------------------------------- MMA issuers
+    // (two: warp 14 the stem MMAs, warp 1 the conv1_2 MMAs -- one issuing thread cannot
+    // keep the tensor core fed through the hand-shakes and descriptor math of both)
+    const bool stem_issuer = warp == 14;
     constexpr uint32_t idesc1 = umma_idesc_bf16(128, 64);
     constexpr uint32_t idesc2 = umma_idesc_bf16(128, 192);
     const uint64_t bstem_d = umma_desc_sw128(smem_u32(bstem));
@@ -188,6 +195,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     mbar_wait(bres, 0);
     walk(
         [&](int j) {
+          if (!stem_issuer) return;
           int b, k, x0;
           ring_job(j, b, k, x0);
           if (k < 0 || k >= p.H) return;
@@ -215,6 +223,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
           }
         },
         [&](int i, int t) {
+          if (stem_issuer) return;
           const int a = tj & 1;
           const int j0 = i * rj + t;  // the tile's conv1_1 rows are ring jobs j0 .. j0 + 2
           mbar_wait(&tempty[a], ((tj >> 1) & 1) ^ 1);
@@ -239,7 +248,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
           __syncwarp();
           ++tj;
         });
-  } else if (warp >= 10) {
+  } else if (warp >= 10) {  // (10 .. 13)
     // ---------------------------------------------------------------- stem epilogue
     const uint32_t quarter = warp & 3;
     const int m = static_cast<int>(quarter) * 32 + lane;  // TMEM lane = grid position
@@ -261,6 +270,16 @@ __global__ void __launch_bounds__(kThreads1, 1)
           if (live) {
             mbar_wait(&afull[a], (sj >> 1) & 1);
             tc_fence_after();
+          }
+          if (EB_B1_DBG & 8) {  // (probe: hand-shakes only)
+            if (live) {
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&aempty[a]);
+              ++sj;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rfull[slot]);
+            return;
           }
           uint8_t* sb = ring + slot * kSlotBytes;
           const int qh = m / 30;
@@ -297,8 +316,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
 #pragma unroll
               for (int c4 = 0; c4 < 4; ++c4) {
                 const int chunk = 4 * half + c4;  // 16-byte chunk (8 channels) of the 128-byte row
-                *reinterpret_cast<uint4*>(rowp + ((chunk ^ (R & 7)) << 4)) =
-                    make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]);
+                if (!(EB_B1_DBG & 2))
+                  *reinterpret_cast<uint4*>(rowp + ((chunk ^ (R & 7)) << 4)) =
+                      make_uint4(pk[4 * c4], pk[4 * c4 + 1], pk[4 * c4 + 2], pk[4 * c4 + 3]);
               }
             }
           }
@@ -326,6 +346,12 @@ __global__ void __launch_bounds__(kThreads1, 1)
           const int a = tj & 1;
           mbar_wait(&tfull[a], (tj >> 1) & 1);
           tc_fence_after();
+          if (EB_B1_DBG & 8) {  // (probe: hand-shakes only)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+            ++tj;
+            return;
+          }
           const uint32_t tb = tmem_base + lane_off + a * kConvAcc + 32 * half;
           const int s = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
           const int b = s / per_img;
@@ -343,8 +369,13 @@ __global__ void __launch_bounds__(kThreads1, 1)
           for (int sub = 0; sub < 2; ++sub) {  // 16 channels at a time (register budget)
             uint32_t r0[16], r1[16], r2[16];
             tmem_ld16(tb + 16 * sub, r0);
+#if EB_B1_DBG & 4  // (probe: planes 1-2 not read -- TMEM read bandwidth)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) r1[q] = r2[q] = r0[q];
+#else
             tmem_ld16(tb + 64 + 16 * sub, r1);
             tmem_ld16(tb + 128 + 16 * sub, r2);
+#endif
             tmem_ld_wait();
             if (sub == 1) {
               tc_fence_before();
@@ -355,10 +386,15 @@ __global__ void __launch_bounds__(kThreads1, 1)
             float2 v2[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
+#if EB_B1_DBG & 1
+              const float2 d1 = make_float2(__uint_as_float(r1[2 * q]), __uint_as_float(r1[2 * q + 1]));
+              const float2 d2 = make_float2(__uint_as_float(r2[2 * q]), __uint_as_float(r2[2 * q + 1]));
+#else
               const float2 d1 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * q]), 1),
                                             __shfl_down_sync(0xffffffffu, __uint_as_float(r1[2 * q + 1]), 1));
               const float2 d2 = make_float2(__shfl_down_sync(0xffffffffu, __uint_as_float(r2[2 * q]), 2),
                                             __shfl_down_sync(0xffffffffu, __uint_as_float(r2[2 * q + 1]), 2));
+#endif
               v2[q] = __fadd2_rn(
                   __fadd2_rn(make_float2(__uint_as_float(r0[2 * q]), __uint_as_float(r0[2 * q + 1])), d1), d2);
             }

@@ -4,6 +4,9 @@
 //   v2: like v1 but two warps issue, each into its own accumulator
 //   v3: groups of 6 MMAs (the VGG stem's tile), one commit to an mbarrier after each group
 //   v4: groups of 6 MMAs, two commits per group (the stage slot and the accumulator)
+//   v5: the fused VGG block-1 conv pattern: per row 3 SW128 A slots x 4 K16 steps, N = 192,
+//       alternating accumulators, one commit per row -- random operand data
+//   v6: v5 with zero operand data (data-dependence check)
 // cycles per MMA over ITER MMAs per issuing warp, one CTA per SM.
 #include <cuda_runtime.h>
 
@@ -21,8 +24,20 @@ __global__ void __launch_bounds__(128, 1) issue_bench(long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tmem_slot;
   __shared__ __align__(8) uint64_t bar[2];
-  for (int i = threadIdx.x; i < 196608 / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0, 0);
+  for (int i = threadIdx.x; i < 196608 / 16; i += blockDim.x) {
+    if (V == 5) {  // pseudo-random bf16 in [-1, 1)
+      uint32_t h = (i * 2654435761u) ^ 0x9e3779b9u, q[4];
+      for (int e = 0; e < 4; ++e) {
+        h = h * 1664525u + 1013904223u;
+        const uint32_t lo = 0x3f80u | ((h >> 9) & 0x7fu) | ((h & 1u) << 15);
+        const uint32_t hi = 0x3f00u | ((h >> 17) & 0x7fu) | ((h & 2u) << 14);
+        q[e] = lo | (hi << 16);
+      }
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(q[0], q[1], q[2], q[3]);
+    } else {
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(V == 6 ? 0u : 0x3f803f80u, 0, 0, 0);
+    }
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -48,6 +63,19 @@ __global__ void __launch_bounds__(128, 1) issue_bench(long long* out) {
         const uint64_t ad = umma_desc(smem_u32(smem) + r * 4224, 16, 128, 0) + 2 * k;
         const uint64_t bd = umma_desc_sw128(smem_u32(smem + 65536) + r * 8192) + 2 * k;
         umma_bf16(td, ad, bd, idesc, i ? 1u : 0u);
+      }
+    } else if (V == 5 || V == 6) {
+      // rows of 12 MMAs: A = 3 SW128 slots (16 KB) x K16 steps, B = 3 x 24 KB at 64 KB
+      for (int i = 0; i < ITER; i += 12) {
+        const uint32_t acc = tmem + ((i / 12) & 1) * 192;
+#pragma unroll
+        for (int j = 0; j < 12; ++j) {
+          const int r = j / 4, k = j & 3;
+          const uint64_t ad = umma_desc_sw128(smem_u32(smem) + r * 16384) + 2 * k;
+          const uint64_t bd = umma_desc_sw128(smem_u32(smem + 65536) + r * 24576) + 2 * k;
+          umma_bf16(acc, ad, bd, idesc, j ? 1u : 0u);
+        }
+        umma_commit(&bar[1]);
       }
     } else if (V == 3 || V == 4) {
       for (int i = 0; i < ITER; i += 6) {
@@ -106,5 +134,8 @@ int main() {
   run<3, 64>(d);
   run<4, 64>(d);
   run<3, 128>(d);
+  run<5, 192>(d);
+  run<6, 192>(d);
+  run<1, 192>(d);
   printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
