@@ -7,9 +7,9 @@
 // the first band starts at conv row 0).  A conv row is one stem tile exactly (the planes
 // grid is 128 wide, Wo = 112), computed with the stem planes mode's descriptors: two tall
 // TMA boxes (even / odd column planes, all 7 filter rows) and 28 MMAs (K16 steps: even taps
-// 0-2, 4-6 then odd taps 1-3, 5-(7); N = 128).  The epilogue (8 warps: lane quarter x member)
-// rounds each value exactly as the stem kernel does (bias, ReLU, bf16), takes the max of
-// positions (2x-1, 2x, 2x+1) -- lane shuffles, and one smem hand-over of lane 31 to the
+// 0-2, 4-6 then odd taps 1-3, 5-(7); N = 128).  The epilogue (16 warps: lane quarter x
+// 32-channel group) rounds each value exactly as the stem kernel does (bias, ReLU, bf16),
+// takes the max of positions (2x-1, 2x, 2x+1) -- lane shuffles, and one smem hand-over of lane 31 to the
 // next quarter -- and runs the vertical max over conv rows (2y-1, 2y, 2y+1) in registers.
 // Max is exact in any order, so the pooled tensors are bitwise the unfused pair's.
 #include "eb_internal.h"
@@ -17,8 +17,17 @@
 
 namespace eb {
 
+#ifndef EB_SP_DBG
+#define EB_SP_DBG 0  // timing probe (variant builds only; results wrong): 1 epilogue hand-shakes only
+#endif
 namespace {
-constexpr int kThreadsSP = 320;       // producer, MMA, 8 epilogue warps
+#ifndef EB_SP_EPI
+#define EB_SP_EPI 16  // epilogue warps: 8 (64 channels each) or 16 (32 each)
+#endif
+constexpr int kEpiW = EB_SP_EPI;
+constexpr int kCh = 128 / (kEpiW / 4);  // channels per epilogue warp
+constexpr int kWords = kCh / 2;         // bf16x2 words per lane
+constexpr int kThreadsSP = 64 + 32 * kEpiW;  // producer, MMA, epilogue warps
 constexpr int kSPStages = 3;
 constexpr int kSPBRow = 128 * 128;    // weights of one filter row: 128 N x 64 K bf16 (SW128)
 constexpr int kSPB = 7 * kSPBRow;     // resident
@@ -27,8 +36,8 @@ constexpr int kSPMaxStage = 31 * 1024;  // two tall boxes of <= 124 lines, 1024-
 constexpr int kOffSPB = 0;
 constexpr int kOffSPStage = kOffSPB + kSPB;
 constexpr int kOffSPBias = kOffSPStage + kSPStages * kSPMaxStage;
-constexpr int kOffSPXch = kOffSPBias + 128 * 4;              // [member][quarter][parity] 128 B
-constexpr int kOffSPBar = kOffSPXch + 2 * 4 * 2 * 128;
+constexpr int kOffSPXch = kOffSPBias + 128 * 4;              // [group][quarter][parity] kCh * 2 B
+constexpr int kOffSPBar = kOffSPXch + (kEpiW / 4) * 4 * 2 * kCh * 2;
 constexpr int kSPBars = 2 * kSPStages + 2 * kSPAcc + 1;
 constexpr int kSPSmem = kOffSPBar + kSPBars * 8 + 16 + 1024;
 static_assert(kSPSmem <= 232448, "stem_pool shared memory");
@@ -75,7 +84,7 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
     }
     for (int i = 0; i < kSPAcc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 8);
+      mbar_init(&tempty[i], kEpiW);
     }
     mbar_init(bres, 1);
     fence_mbar_init();
@@ -118,18 +127,20 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
+    // (a second issuer taking alternate rows measured no faster: 0.317 vs 0.314 ms)
     constexpr uint32_t idesc = umma_idesc_bf16(128, 128);
     const uint64_t b0 = umma_desc_sw128(smem_u32(bres_s));
     const uint32_t odd16 = static_cast<uint32_t>(p.lines * 8);  // the odd plane's box
     const uint32_t koff[4] = {0u, 2u, odd16, odd16 + 2u};
-    int st = 0, j = 0;
-    uint32_t ph = 0;
+    int j = 0;
     mbar_wait(bres, 0);
     for (int i = 0; i < ns; ++i) {
       int b, y0, y1;
       strip(i, b, y0, y1);
       for (int y = y0; y <= y1; ++y, ++j) {
         const int a = j % kSPAcc;
+        const int st = j % kSPStages;
+        const uint32_t ph = static_cast<uint32_t>((j / kSPStages) & 1);
         mbar_wait(&tempty[a], ((j / kSPAcc) & 1) ^ 1);
         mbar_wait(&full[st], ph);
         tc_fence_after();
@@ -144,25 +155,23 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
           umma_commit(&tfull[a]);
         }
         __syncwarp();
-        if (++st == kSPStages) {
-          st = 0;
-          ph ^= 1;
-        }
       }
     }
   } else {
     // ---------------------------------------------------------------- epilogue
     const uint32_t quarter = warp & 3;
-    const int member = (static_cast<int>(warp) - 2) >> 2;  // columns 64 * member .. + 63
+    const int grp = (static_cast<int>(warp) - 2) >> 2;  // channels kCh * grp .. + kCh - 1
+    const int col0 = kCh * grp;
+    const int member = col0 >> 6;
     const int pos = static_cast<int>(quarter) * 32 + lane;  // output column of the conv row
     const uint32_t lane_off = (quarter * 32) << 16;
-    const float2* bias2 = reinterpret_cast<const float2*>(bias + 64 * member);
+    const float2* bias2 = reinterpret_cast<const float2*>(bias + col0);
     __nv_bfloat16* out = member ? p.out1 : p.out0;
     const int ldo = member ? p.ld1 : p.ld0;
-    const int ooff = member ? p.off1 : p.off0;
-    uint32_t prev[32], acc[32];
+    const int ooff = (member ? p.off1 : p.off0) + (col0 & 63);
+    uint32_t prev[kWords], acc[kWords];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) prev[i] = acc[i] = 0u;
+    for (int i = 0; i < kWords; ++i) prev[i] = acc[i] = 0u;
     int j = 0;
     for (int i = 0; i < ns; ++i) {
       int b, y0, y1;
@@ -171,11 +180,16 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
         const int a = j % kSPAcc;
         mbar_wait(&tfull[a], (j / kSPAcc) & 1);
         tc_fence_after();
-        uint32_t h[32];  // this position's 64 channels, rounded as the stem kernel stores them
+        if (EB_SP_DBG & 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[a]);
+          continue;
+        }
+        uint32_t h[kWords];  // this position's channels, rounded as the stem kernel stores them
 #pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {  // 16 channels at a time (register budget)
+        for (int qd = 0; qd < kCh / 16; ++qd) {  // 16 channels at a time (register budget)
           uint32_t r[16];
-          tmem_ld16(tmem_base + lane_off + a * 128 + 64 * member + 16 * qd, r);
+          tmem_ld16(tmem_base + lane_off + a * 128 + col0 + 16 * qd, r);
           tmem_ld_wait();
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -189,17 +203,17 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
         if (lane == 0) mbar_arrive(&tempty[a]);
         // horizontal: max of positions pos - 1, pos, pos + 1 (even pos); position -1 is
         // padding, positions >= Wo never enter an even position's window (Wo even)
-        uint32_t* xw = xch + ((member * 4 + static_cast<int>(quarter)) * 2 + (j & 1)) * 32;
+        uint32_t* xw = xch + ((grp * 4 + static_cast<int>(quarter)) * 2 + (j & 1)) * kWords;
         if (lane == 31 && quarter < 3) {
 #pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4)
+          for (int c4 = 0; c4 < kWords / 4; ++c4)
             reinterpret_cast<uint4*>(xw)[c4] = make_uint4(h[4 * c4], h[4 * c4 + 1], h[4 * c4 + 2], h[4 * c4 + 3]);
         }
-        named_bar_sync(1 + member, 128);
+        named_bar_sync(1 + grp, 128);
         uint32_t* hm = h;  // (in place: each channel pair's shuffles precede its update)
-        const uint32_t* xr = xch + ((member * 4 + static_cast<int>(quarter) - 1) * 2 + (j & 1)) * 32;
+        const uint32_t* xr = xch + ((grp * 4 + static_cast<int>(quarter) - 1) * 2 + (j & 1)) * kWords;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < kWords; ++c) {
           uint32_t up = __shfl_up_sync(0xffffffffu, h[c], 1);
           const uint32_t dn = __shfl_down_sync(0xffffffffu, h[c], 1);
           if (lane == 0) up = quarter > 0 ? xr[c] : h[c];
@@ -211,7 +225,7 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
         // vertical: pooled row py = max(conv rows 2py - 1, 2py, 2py + 1)
         if ((y & 1) == 0) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
+          for (int c = 0; c < kWords; ++c) {
             if (y == 0) {
               acc[c] = hm[c];
             } else {
@@ -222,9 +236,9 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
           }
         } else {
           if (y != y0 && !(lane & 1) && pos < p.Wo) {  // (a band's first odd row only primes prev)
-            uint32_t o[32];
+            uint32_t o[kWords];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
+            for (int c = 0; c < kWords; ++c) {
               __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&acc[c]),
                                           *reinterpret_cast<const __nv_bfloat162*>(&hm[c]));
               o[c] = *reinterpret_cast<uint32_t*>(&m2);
@@ -232,10 +246,11 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
             const size_t orow = (static_cast<size_t>(b) * Hp + (y >> 1)) * (p.Wo >> 1) + (pos >> 1);
             uint4* o4 = reinterpret_cast<uint4*>(out + orow * ldo + ooff);
 #pragma unroll
-            for (int c4 = 0; c4 < 8; ++c4) o4[c4] = make_uint4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
+            for (int c4 = 0; c4 < kWords / 4; ++c4)
+              o4[c4] = make_uint4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
           }
 #pragma unroll
-          for (int c = 0; c < 32; ++c) prev[c] = hm[c];
+          for (int c = 0; c < kWords; ++c) prev[c] = hm[c];
         }
       }
     }
