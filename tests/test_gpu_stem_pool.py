@@ -52,3 +52,34 @@ def test_fused_stem_pools_bitwise_equal_unfused(tmp_path):
     # one stem launch either way; the two pool launches are gone
     assert ef.launch_count(_lib.EB_IN_U8_HWC, 64) == eu.launch_count(_lib.EB_IN_U8_HWC, 64) - 2
     assert ef.launch_count(_lib.EB_IN_U8_HWC, 4) == eu.launch_count(_lib.EB_IN_U8_HWC, 4)
+
+
+def test_fusions_bitwise_in_the_c5_mix(tmp_path):
+    """C5's mix (ResNet-152 + DenseNet-201 share a fused stem + pools, VGG-19 runs the fused
+    block 1, ResNeXt-50's stem and Inception-v3 at 299 stay unfused) with both fusions on
+    and off: the same logits, bit for bit, at a batch where both fusions run."""
+    docs = [cnn1_doc("resnet152_6", "resnet152", 6), cnn1_doc("densenet201_7", "densenet201", 7),
+            cnn1_doc("vgg19_8", "vgg19", 8), cnn1_doc("inception_v3_5", "inception_v3", 5, size=299),
+            cnn1_doc("resnext50_32x4d_9", "resnext50_32x4d", 9)]
+    ens = {}
+    for flag in ("1", "0"):
+        saved = {k: os.environ.get(k) for k in ("EB_STEM_POOL", "EB_BLOCK1")}
+        os.environ["EB_STEM_POOL"] = os.environ["EB_BLOCK1"] = flag
+        try:
+            d = tmp_path / f"c5_{flag}"
+            d.mkdir()
+            ens[flag] = build(d, docs, max_batch=32, mean=IMAGENET_MEAN, std=IMAGENET_STD)
+            engine_for(ens[flag])
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+    px = synth.images_fast(32, 299, 299, 3, seed0=5151)
+    _, _, f = E.predict_u8(ens["1"], px, topk=5, want_logits=True)
+    _, _, u = E.predict_u8(ens["0"], px, topk=5, want_logits=True)
+    assert np.array_equal(f["logits"], u["logits"])
+    kind = _lib.EB_IN_U8_HWC
+    # the fused C5 step: one stem launch, two pools and one VGG conv fewer
+    assert engine_for(ens["1"]).launch_count(kind, 32) == engine_for(ens["0"]).launch_count(kind, 32) - 3
