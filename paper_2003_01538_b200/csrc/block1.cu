@@ -36,6 +36,7 @@ constexpr int kLook = EB_B1_LOOK;
 #ifndef EB_B1_DBG
 #define EB_B1_DBG 0  // timing probes (variant builds only; results wrong): 1 no tap shuffles, 2 no ring stores,
                    // 4 conv planes 1-2 not loaded from TMEM, 8 epilogues hand-shake only
+                   // (16 the stem epilogue only, 32 the conv epilogue only)
 #endif            // conv1_1 rows computed ahead of the tile that reads them
 constexpr int kRing = 3 + kLook + 1;         // conv1_1 row slots: 3 read + kLook written ahead + 1
 constexpr int kSlotBytes = 128 * 128;        // 128 grid rows x 64 channels bf16 (SW128 K-major)
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
             mbar_wait(&afull[a], (sj >> 1) & 1);
             tc_fence_after();
           }
-          if (EB_B1_DBG & 8) {  // (probe: hand-shakes only)
+          if (EB_B1_DBG & (8 | 16)) {  // (probe: hand-shakes only)
             if (live) {
               __syncwarp();
               if (lane == 0) mbar_arrive(&aempty[a]);
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
           const int a = tj & 1;
           mbar_wait(&tfull[a], (tj >> 1) & 1);
           tc_fence_after();
-          if (EB_B1_DBG & 8) {  // (probe: hand-shakes only)
+          if (EB_B1_DBG & (8 | 32)) {  // (probe: hand-shakes only)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[a]);
             ++tj;
