@@ -9,9 +9,9 @@
 // TMA boxes (even / odd column planes, all 7 filter rows) and 28 MMAs (K16 steps: even taps
 // 0-2, 4-6 then odd taps 1-3, 5-(7); N = 128).  The epilogue (16 warps: lane quarter x
 // 32-channel group) rounds each value exactly as the stem kernel does (bias, ReLU, bf16),
-// takes the max of positions (2x-1, 2x, 2x+1) -- lane shuffles, and one smem hand-over of lane 31 to the
-// next quarter -- and runs the vertical max over conv rows (2y-1, 2y, 2y+1) in registers.
-// Max is exact in any order, so the pooled tensors are bitwise the unfused pair's.
+// runs the vertical max over conv rows (2y-1, 2y, 2y+1) in registers and then the max of
+// positions (2x-1, 2x, 2x+1) once per pooled row -- lane shuffles, and one smem hand-over
+// of lane 31 to the next quarter.  Max is exact in any order, so the pooled tensors are bitwise the unfused pair's.
 #include "eb_internal.h"
 #include "sm100.cuh"
 
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
     uint32_t prev[kWords], acc[kWords];
 #pragma unroll
     for (int i = 0; i < kWords; ++i) prev[i] = acc[i] = 0u;
-    int j = 0;
+    int j = 0, xn = 0;
     for (int i = 0; i < ns; ++i) {
       int b, y0, y1;
       strip(i, b, y0, y1);
@@ -201,56 +201,63 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[a]);
-        // horizontal: max of positions pos - 1, pos, pos + 1 (even pos); position -1 is
-        // padding, positions >= Wo never enter an even position's window (Wo even)
-        uint32_t* xw = xch + ((grp * 4 + static_cast<int>(quarter)) * 2 + (j & 1)) * kWords;
-        if (lane == 31 && quarter < 3) {
-#pragma unroll
-          for (int c4 = 0; c4 < kWords / 4; ++c4)
-            reinterpret_cast<uint4*>(xw)[c4] = make_uint4(h[4 * c4], h[4 * c4 + 1], h[4 * c4 + 2], h[4 * c4 + 3]);
-        }
-        named_bar_sync(1 + grp, 128);
-        uint32_t* hm = h;  // (in place: each channel pair's shuffles precede its update)
-        const uint32_t* xr = xch + ((grp * 4 + static_cast<int>(quarter) - 1) * 2 + (j & 1)) * kWords;
-#pragma unroll
-        for (int c = 0; c < kWords; ++c) {
-          uint32_t up = __shfl_up_sync(0xffffffffu, h[c], 1);
-          const uint32_t dn = __shfl_down_sync(0xffffffffu, h[c], 1);
-          if (lane == 0) up = quarter > 0 ? xr[c] : h[c];
-          __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&up),
-                                      *reinterpret_cast<const __nv_bfloat162*>(&h[c]));
-          m2 = __hmax2(m2, *reinterpret_cast<const __nv_bfloat162*>(&dn));
-          hm[c] = *reinterpret_cast<uint32_t*>(&m2);
-        }
-        // vertical: pooled row py = max(conv rows 2py - 1, 2py, 2py + 1)
+        // vertical first, per lane: pooled row py = max(conv rows 2py - 1, 2py, 2py + 1)
+        // (max is exact in any order); the horizontal window then runs once per pooled row
         if ((y & 1) == 0) {
 #pragma unroll
           for (int c = 0; c < kWords; ++c) {
             if (y == 0) {
-              acc[c] = hm[c];
+              acc[c] = h[c];
             } else {
               __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&prev[c]),
-                                          *reinterpret_cast<const __nv_bfloat162*>(&hm[c]));
+                                          *reinterpret_cast<const __nv_bfloat162*>(&h[c]));
               acc[c] = *reinterpret_cast<uint32_t*>(&m2);
             }
           }
-        } else {
-          if (y != y0 && !(lane & 1) && pos < p.Wo) {  // (a band's first odd row only primes prev)
-            uint32_t o[kWords];
+          continue;
+        }
+        if (y == y0) {  // a band's first (odd) row only primes the next pooled row
 #pragma unroll
-            for (int c = 0; c < kWords; ++c) {
-              __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&acc[c]),
-                                          *reinterpret_cast<const __nv_bfloat162*>(&hm[c]));
-              o[c] = *reinterpret_cast<uint32_t*>(&m2);
-            }
-            const size_t orow = (static_cast<size_t>(b) * Hp + (y >> 1)) * (p.Wo >> 1) + (pos >> 1);
-            uint4* o4 = reinterpret_cast<uint4*>(out + orow * ldo + ooff);
+          for (int c = 0; c < kWords; ++c) prev[c] = h[c];
+          continue;
+        }
+        uint32_t v[kWords];
 #pragma unroll
-            for (int c4 = 0; c4 < kWords / 4; ++c4)
-              o4[c4] = make_uint4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
-          }
+        for (int c = 0; c < kWords; ++c) {
+          __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&acc[c]),
+                                      *reinterpret_cast<const __nv_bfloat162*>(&h[c]));
+          v[c] = *reinterpret_cast<uint32_t*>(&m2);
+          prev[c] = h[c];
+        }
+        // horizontal: max of positions pos - 1, pos, pos + 1 (even pos); position -1 is
+        // padding, positions >= Wo never enter an even position's window (Wo even); lane 31
+        // hands its column to the next quarter's lane 0 through shared memory
+        uint32_t* xw = xch + ((grp * 4 + static_cast<int>(quarter)) * 2 + (xn & 1)) * kWords;
+        if (lane == 31 && quarter < 3) {
 #pragma unroll
-          for (int c = 0; c < kWords; ++c) prev[c] = hm[c];
+          for (int c4 = 0; c4 < kWords / 4; ++c4)
+            reinterpret_cast<uint4*>(xw)[c4] = make_uint4(v[4 * c4], v[4 * c4 + 1], v[4 * c4 + 2], v[4 * c4 + 3]);
+        }
+        named_bar_sync(1 + grp, 128);
+        const uint32_t* xr = xch + ((grp * 4 + static_cast<int>(quarter) - 1) * 2 + (xn & 1)) * kWords;
+        ++xn;
+        uint32_t o[kWords];
+#pragma unroll
+        for (int c = 0; c < kWords; ++c) {
+          uint32_t up = __shfl_up_sync(0xffffffffu, v[c], 1);
+          const uint32_t dn = __shfl_down_sync(0xffffffffu, v[c], 1);
+          if (lane == 0) up = quarter > 0 ? xr[c] : v[c];
+          __nv_bfloat162 m2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&up),
+                                      *reinterpret_cast<const __nv_bfloat162*>(&v[c]));
+          m2 = __hmax2(m2, *reinterpret_cast<const __nv_bfloat162*>(&dn));
+          o[c] = *reinterpret_cast<uint32_t*>(&m2);
+        }
+        if (!(lane & 1) && pos < p.Wo) {
+          const size_t orow = (static_cast<size_t>(b) * Hp + (y >> 1)) * (p.Wo >> 1) + (pos >> 1);
+          uint4* o4 = reinterpret_cast<uint4*>(out + orow * ldo + ooff);
+#pragma unroll
+          for (int c4 = 0; c4 < kWords / 4; ++c4)
+            o4[c4] = make_uint4(o[4 * c4], o[4 * c4 + 1], o[4 * c4 + 2], o[4 * c4 + 3]);
         }
       }
     }
