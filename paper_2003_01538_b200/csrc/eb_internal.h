@@ -156,9 +156,10 @@ cudaError_t block1_launch(const CUtensorMap& mx, const CUtensorMap& mw1, const C
                           const Block1Params& p, int grid, cudaStream_t stream);
 bool pdl_enabled();
 
-// Grouped 7x7/2 stem of two members + both 3x3/2 (pad 1) max-pools (stem_pool.cu); input =
+// 7x7/2 stem of one member or two (grouped) + the 3x3/2 (pad 1) max-pools (stem_pool.cu); input =
 // the stem planes layout with the tall-box line map, output = the two pooled tensors
 struct StemPoolParams {
+  int ncol;                    // 64 (one member) or 128 (two)
   int Ho, Wo;                  // stem output size (Wo <= 128: one planes tile per row)
   int Hq, Wq;                  // padded rows per image / plane width of the planes layout
   long long plane_px;          // pixels per plane

@@ -888,13 +888,14 @@ int enqueue_stem_pool(eb_engine* e, const eb_op_desc& g, int B, int pb, cudaStre
   ConvPlan pl;
   const int rc = plan_conv(a, &pl);
   if (rc != EB_OK) return rc;
-  if (pl.p.a_mode != kAModeStemPlanes || pl.block_n != 128 || pl.p.stem_lines <= 0 || pl.p.kbs != 7)
+  if (pl.p.a_mode != kAModeStemPlanes || pl.block_n != g.cout || pl.p.stem_lines <= 0 || pl.p.kbs != 7)
     EB_FAIL(EB_E_STATE, "fused stem + pools: unexpected stem plan");
   const eb_op_desc& q0 = e->ops[pools.first];
-  const eb_op_desc& q1 = e->ops[pools.second];
+  const eb_op_desc& q1 = e->ops[pools.second >= 0 ? pools.second : pools.first];
   const Tensor& d0 = e->tensors[q0.dst];
   const Tensor& d1 = e->tensors[q1.dst];
   StemPoolParams p{};
+  p.ncol = g.cout;
   p.Ho = e->tensors[g.dst].h;
   p.Wo = e->tensors[g.dst].w;
   p.Hq = sg.Hq;
@@ -1650,10 +1651,11 @@ void fuse_conv_pools(eb_engine* e) {
 // image in the rows layout, 64 outputs, ReLU) whose only reader is the next op on its
 // lane, a taps-in-N 3x3 64->64 conv with a fused 2x2 max-pool, becomes one kernel
 // (block1.cu).  EB_BLOCK1=0 keeps them apart (read per finalize: tests compare both).
-// Peephole at finalize: a grouped stem launch of two members (7x7/2/p3 over the 8-channel
-// image in the planes layout, 64 + 64 output channels of one tensor, ReLU) whose two
-// channel halves are read only by one 3x3/2/p1 max-pool each becomes one kernel that writes
-// the pooled tensors (stem_pool.cu).  EB_STEM_POOL=0 keeps them apart (read per finalize).
+// Peephole at finalize: a 7x7/2/p3 stem over the 8-channel image in the planes layout with
+// ReLU -- a member's own (64 outputs) or a grouped launch of two members (64 + 64 channels
+// of one tensor) -- each 64-channel part of whose output is read only by one 3x3/2/p1
+// max-pool becomes one kernel that writes the pooled tensors (stem_pool.cu).
+// EB_STEM_POOL=0 keeps them apart (read per finalize).
 void fuse_stem_pools(eb_engine* e) {
   const size_t n = e->ops.size();
   e->op_stempool.assign(n, {-1, -1});
@@ -1661,16 +1663,18 @@ void fuse_stem_pools(eb_engine* e) {
   if (!env_flag("EB_STEM_POOL", true) || !stem_rows_enabled() || e->f32) return;
   for (size_t i = 0; i < n; ++i) {
     const eb_op_desc& g = e->ops[i];
-    if (g.kind != EB_OP_CONV || !g.prefork || g.n_split != 0 || g.cout != 128 || g.kh != 7 ||
-        g.kw != 7 || g.sh != 2 || g.sw != 2 || g.ph != 3 || g.pw != 3 || !g.relu || g.res >= 0 ||
-        g.groups > 1 || g.flatten || g.b_off == EB_NO_OFFSET || g.scale_off != EB_NO_OFFSET ||
-        g.dst_c_off != 0 || e->op_pool[i] >= 0 || e->op_skip[i])
+    if (g.kind != EB_OP_CONV || g.n_split != 0 || (g.cout != 128 && g.cout != 64) ||
+        (g.cout == 128 && !g.prefork) || g.kh != 7 || g.kw != 7 || g.sh != 2 || g.sw != 2 ||
+        g.ph != 3 || g.pw != 3 || !g.relu || g.res >= 0 || g.groups > 1 || g.flatten ||
+        g.b_off == EB_NO_OFFSET || g.scale_off != EB_NO_OFFSET || g.dst_c_off != 0 ||
+        e->op_pool[i] >= 0 || e->op_skip[i])
       continue;
     const Tensor& src = e->tensors[g.src];
     const Tensor& t = e->tensors[g.dst];
-    if (!(src.c == 8 && g.src_c == 8 && g.src_c_off == 0) || t.c != 128 || t.dtype != EB_BF16 ||
+    if (!(src.c == 8 && g.src_c == 8 && g.src_c_off == 0) || t.c != g.cout || t.dtype != EB_BF16 ||
         t.h % 2 || t.w % 2 || t.w > 128)
       continue;
+    const int parts = g.cout / 64;
     int pool_of[2] = {-1, -1};
     bool ok = true;
     for (size_t k = 0; k < n && ok; ++k) {
@@ -1678,20 +1682,19 @@ void fuse_stem_pools(eb_engine* e) {
       if (k == i || (o.src != g.dst && o.res != g.dst)) continue;
       const int half = o.src_c_off == 0 ? 0 : o.src_c_off == 64 ? 1 : -1;
       const Tensor& d = e->tensors[o.dst];
-      if (o.kind != EB_OP_POOL || o.res == g.dst || half < 0 || o.src_c != 64 || pool_of[half] >= 0 ||
-          o.pool_mode != EB_POOL_MAX || o.kh != 3 || o.kw != 3 || o.sh != 2 || o.sw != 2 || o.ph != 1 ||
-          o.pw != 1 || o.scale_off != EB_NO_OFFSET || e->op_skip[k] || d.dtype != EB_BF16 || d.c % 8 ||
-          o.dst_c_off % 8)
+      if (o.kind != EB_OP_POOL || o.res == g.dst || half < 0 || half >= parts || o.src_c != 64 ||
+          pool_of[half] >= 0 || o.pool_mode != EB_POOL_MAX || o.kh != 3 || o.kw != 3 || o.sh != 2 ||
+          o.sw != 2 || o.ph != 1 || o.pw != 1 || o.scale_off != EB_NO_OFFSET || e->op_skip[k] ||
+          d.dtype != EB_BF16 || d.c % 8 || o.dst_c_off % 8)
         ok = false;
       else
         pool_of[half] = static_cast<int>(k);
     }
     for (const auto& m : e->members)
       if (m.tensor == g.dst) ok = false;
-    if (!ok || pool_of[0] < 0 || pool_of[1] < 0) continue;
+    if (!ok || pool_of[0] < 0 || (parts == 2 && pool_of[1] < 0)) continue;
     e->op_stempool[i] = {pool_of[0], pool_of[1]};
-    e->stempool_pool[pool_of[0]] = 1;
-    e->stempool_pool[pool_of[1]] = 1;
+    for (int h = 0; h < parts; ++h) e->stempool_pool[pool_of[h]] = 1;
   }
 }
 

@@ -1,7 +1,7 @@
-// stem_pool.cu -- the grouped 7x7/2 stem of two members (ResNet / ResNeXt / DenseNet:
-// conv 3->64 + bias + ReLU each, N = 128 concatenated) with both members' 3x3/2 (pad 1)
-// max-pools in one kernel: the 112 x 112 x 128 stem output (822 MB per 256 images) is
-// pooled in registers and never written.
+// stem_pool.cu -- the 7x7/2 stem of one member, or the grouped stem of two (ResNet / ResNeXt
+// / DenseNet: conv 3->64 + bias + ReLU each, N = 64 or 128 concatenated), with the members'
+// 3x3/2 (pad 1) max-pools in one kernel: the 112 x 112 stem output (411 MB per member and
+// 256 images) is pooled in registers and never written.
 //
 // Work unit ("strip"): one image, a band of pb pooled rows (conv rows 2 p0 - 1 .. 2 p1 - 1;
 // the first band starts at conv row 0).  A conv row is one stem tile exactly (the planes
@@ -22,37 +22,48 @@ namespace eb {
 #endif
 namespace {
 #ifndef EB_SP_EPI
-#define EB_SP_EPI 16  // epilogue warps: 8 (64 channels each) or 16 (32 each)
+#define EB_SP_EPI 16  // epilogue warps: 8 or 16
 #endif
 constexpr int kEpiW = EB_SP_EPI;
-constexpr int kCh = 128 / (kEpiW / 4);  // channels per epilogue warp
-constexpr int kWords = kCh / 2;         // bf16x2 words per lane
 constexpr int kThreadsSP = 64 + 32 * kEpiW;  // producer, MMA, epilogue warps
 constexpr int kSPStages = 3;
-constexpr int kSPBRow = 128 * 128;    // weights of one filter row: 128 N x 64 K bf16 (SW128)
-constexpr int kSPB = 7 * kSPBRow;     // resident
-constexpr int kSPAcc = 4;             // TMEM accumulators (128 columns each)
+constexpr int kSPAcc = 4;             // TMEM accumulators (NCOL columns each)
 constexpr int kSPMaxStage = 31 * 1024;  // two tall boxes of <= 124 lines, 1024-aligned
-constexpr int kOffSPB = 0;
-constexpr int kOffSPStage = kOffSPB + kSPB;
-constexpr int kOffSPBias = kOffSPStage + kSPStages * kSPMaxStage;
-constexpr int kOffSPXch = kOffSPBias + 128 * 4;              // [group][quarter][parity] kCh * 2 B
-constexpr int kOffSPBar = kOffSPXch + (kEpiW / 4) * 4 * 2 * kCh * 2;
-constexpr int kSPBars = 2 * kSPStages + 2 * kSPAcc + 1;
-constexpr int kSPSmem = kOffSPBar + kSPBars * 8 + 16 + 1024;
-static_assert(kSPSmem <= 232448, "stem_pool shared memory");
+// NCOL = 64 * members (one or two members' stems)
+template <int NCOL>
+struct SPCfg {
+  static constexpr int kCh = NCOL / (kEpiW / 4);  // channels per epilogue warp
+  static constexpr int kWords = kCh / 2;          // bf16x2 words per lane
+  static constexpr int kBRow = NCOL * 128;        // weights of one filter row: NCOL N x 64 K (SW128)
+  static constexpr int kB = 7 * kBRow;            // resident
+  static constexpr int kOffB = 0;
+  static constexpr int kOffStage = kOffB + kB;
+  static constexpr int kOffBias = kOffStage + kSPStages * kSPMaxStage;
+  static constexpr int kOffXch = kOffBias + 128 * 4;  // [group][quarter][parity] kCh * 2 B
+  static constexpr int kOffBar = kOffXch + (kEpiW / 4) * 4 * 2 * kCh * 2;
+  static constexpr int kBars = 2 * kSPStages + 2 * kSPAcc + 1;
+  static constexpr int kSmem = kOffBar + kBars * 8 + 16 + 1024;
+  static_assert(kSmem <= 232448, "stem_pool shared memory");
+  static_assert(kCh % 16 == 0, "epilogue channel groups of 16");
+};
 }  // namespace
 
+template <int NCOL>
 __global__ void __launch_bounds__(kThreadsSP, 1)
     stem_pool_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const StemPoolParams p) {
+  using C = SPCfg<NCOL>;
+  constexpr int kCh = C::kCh;
+  constexpr int kWords = C::kWords;
+  constexpr int kSPBRow = C::kBRow;
+  constexpr int kSPB = C::kB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* bres_s = smem + kOffSPB;
-  uint8_t* stage_s = smem + kOffSPStage;
-  float* bias = reinterpret_cast<float*>(smem + kOffSPBias);
-  uint32_t* xch = reinterpret_cast<uint32_t*>(smem + kOffSPXch);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffSPBar);
+  uint8_t* bres_s = smem + C::kOffB;
+  uint8_t* stage_s = smem + C::kOffStage;
+  float* bias = reinterpret_cast<float*>(smem + C::kOffBias);
+  uint32_t* xch = reinterpret_cast<uint32_t*>(smem + C::kOffXch);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* empty = full + kSPStages;
   uint64_t* tfull = empty + kSPStages;
   uint64_t* tempty = tfull + kSPAcc;
@@ -74,7 +85,7 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
     y1 = 2 * (p0 + p.pb) - 1;
   };
 
-  if (threadIdx.x < 128) bias[threadIdx.x] = p.bias[threadIdx.x];
+  if (threadIdx.x < NCOL) bias[threadIdx.x] = p.bias[threadIdx.x];
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     // (a second issuer taking alternate rows measured no faster: 0.317 vs 0.314 ms)
-    constexpr uint32_t idesc = umma_idesc_bf16(128, 128);
+    constexpr uint32_t idesc = umma_idesc_bf16(128, NCOL);
     const uint64_t b0 = umma_desc_sw128(smem_u32(bres_s));
     const uint32_t odd16 = static_cast<uint32_t>(p.lines * 8);  // the odd plane's box
     const uint32_t koff[4] = {0u, 2u, odd16, odd16 + 2u};
@@ -149,7 +160,7 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
           for (int r = 0; r < 7; ++r)
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              umma_bf16(tmem_base + a * 128, a0 + r * static_cast<uint32_t>(p.Wq) + koff[k],
+              umma_bf16(tmem_base + a * NCOL, a0 + r * static_cast<uint32_t>(p.Wq) + koff[k],
                         b0 + r * (kSPBRow >> 4) + 2 * k, idesc, (r | k) ? 1u : 0u);
           umma_commit(&empty[st]);
           umma_commit(&tfull[a]);
@@ -189,7 +200,7 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
 #pragma unroll
         for (int qd = 0; qd < kCh / 16; ++qd) {  // 16 channels at a time (register budget)
           uint32_t r[16];
-          tmem_ld16(tmem_base + lane_off + a * 128 + col0 + 16 * qd, r);
+          tmem_ld16(tmem_base + lane_off + a * NCOL + col0 + 16 * qd, r);
           tmem_ld_wait();
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -267,27 +278,35 @@ __global__ void __launch_bounds__(kThreadsSP, 1)
   if (warp == 1) tmem_dealloc(tmem_base, 512);
 }
 
-cudaError_t stem_pool_launch(const CUtensorMap& ma, const CUtensorMap& mb, const StemPoolParams& p,
-                             int grid, cudaStream_t stream) {
-  if (2 * p.lines * 128 > kSPMaxStage) return cudaErrorInvalidValue;
+template <int NCOL>
+static cudaError_t launch_sp(const CUtensorMap& ma, const CUtensorMap& mb, const StemPoolParams& p, int grid,
+                             cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(stem_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSPSmem);
+    const cudaError_t e = cudaFuncSetAttribute(stem_pool_kernel<NCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               SPCfg<NCOL>::kSmem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreadsSP);
-  cfg.dynamicSmemBytes = kSPSmem;
+  cfg.dynamicSmemBytes = SPCfg<NCOL>::kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, stem_pool_kernel, ma, mb, p);
+  return cudaLaunchKernelEx(&cfg, stem_pool_kernel<NCOL>, ma, mb, p);
+}
+
+cudaError_t stem_pool_launch(const CUtensorMap& ma, const CUtensorMap& mb, const StemPoolParams& p,
+                             int grid, cudaStream_t stream) {
+  if (2 * p.lines * 128 > kSPMaxStage) return cudaErrorInvalidValue;
+  if (p.ncol == 128) return launch_sp<128>(ma, mb, p, grid, stream);
+  if (p.ncol == 64) return launch_sp<64>(ma, mb, p, grid, stream);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace eb

@@ -55,8 +55,8 @@ def test_fused_stem_pools_bitwise_equal_unfused(tmp_path):
 
 
 def test_fusions_bitwise_in_the_c5_mix(tmp_path):
-    """C5's mix (ResNet-152 + DenseNet-201 share a fused stem + pools, VGG-19 runs the fused
-    block 1, ResNeXt-50's stem and Inception-v3 at 299 stay unfused) with both fusions on
+    """C5's mix (ResNet-152 + DenseNet-201 share a fused stem + pools, ResNeXt-50's own stem
+    + pool is fused too, VGG-19 runs the fused block 1, Inception-v3 at 299 stays unfused) with both fusions on
     and off: the same logits, bit for bit, at a batch where both fusions run."""
     docs = [cnn1_doc("resnet152_6", "resnet152", 6), cnn1_doc("densenet201_7", "densenet201", 7),
             cnn1_doc("vgg19_8", "vgg19", 8), cnn1_doc("inception_v3_5", "inception_v3", 5, size=299),
@@ -81,5 +81,32 @@ def test_fusions_bitwise_in_the_c5_mix(tmp_path):
     _, _, u = E.predict_u8(ens["0"], px, topk=5, want_logits=True)
     assert np.array_equal(f["logits"], u["logits"])
     kind = _lib.EB_IN_U8_HWC
-    # the fused C5 step: one stem launch, two pools and one VGG conv fewer
-    assert engine_for(ens["1"]).launch_count(kind, 32) == engine_for(ens["0"]).launch_count(kind, 32) - 3
+    # the fused C5 step: three pools (the grouped pair's two, ResNeXt's own) and one VGG conv fewer
+    assert engine_for(ens["1"]).launch_count(kind, 32) == engine_for(ens["0"]).launch_count(kind, 32) - 4
+
+
+def test_single_member_stem_pool_bitwise(tmp_path):
+    """A lone ResNet-50 (its own 64-channel stem, no grouped launch) with the stem + pool
+    fusion on and off."""
+    ens = {}
+    for flag in ("1", "0"):
+        saved = os.environ.get("EB_STEM_POOL")
+        os.environ["EB_STEM_POOL"] = flag
+        try:
+            d = tmp_path / f"r50_{flag}"
+            d.mkdir()
+            ens[flag] = build(d, [cnn1_doc("resnet50_3", "resnet50", 3)], max_batch=64, mean=IMAGENET_MEAN,
+                              std=IMAGENET_STD)
+            engine_for(ens[flag])
+        finally:
+            if saved is None:
+                os.environ.pop("EB_STEM_POOL", None)
+            else:
+                os.environ["EB_STEM_POOL"] = saved
+    px = synth.images_fast(64, 224, 224, 3, seed0=6262)
+    for b in (4, 40, 64):
+        _, _, f = E.predict_u8(ens["1"], px[:b], topk=5, want_logits=True)
+        _, _, u = E.predict_u8(ens["0"], px[:b], topk=5, want_logits=True)
+        assert np.array_equal(f["logits"], u["logits"]), f"B={b}"
+    kind = _lib.EB_IN_U8_HWC
+    assert engine_for(ens["1"]).launch_count(kind, 64) == engine_for(ens["0"]).launch_count(kind, 64) - 1
