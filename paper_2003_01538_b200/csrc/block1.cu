@@ -15,9 +15,9 @@
 // taps-in-N + fused pool), so the pooled output is bitwise the same.
 //
 // Roles: warp 0 TMA producer (stem input runs; resident weights), warp 1 conv1_2 MMA
-// issuer, warp 14 stem MMA issuer, warps 2-9 conv1_2 epilogue (quarter = warp & 3 owns TMEM lanes 32q..32q+31; the two
-// groups take channels 0-31 / 32-63), warps 10-13 stem epilogue (one per lane quarter,
-// all 64 channels) -- the two epilogues run side by side.
+// issuer, warp 14 stem MMA issuer, warps 2-9 conv1_2 epilogue (quarter = warp & 3 owns
+// TMEM lanes 32q..32q+31; the two groups take channels 0-31 / 32-63), warps 10-13 stem
+// epilogue (one per lane quarter, all 64 channels) -- the two epilogues run side by side.
 // Job order (identical in all roles): before conv1_2 tile t of the CTA's tile sequence,
 // every ring job (conv1_1 row) up to tile t's third row + kLook -- the stem epilogue
 // then has kLook tiles of MMA time to deliver a row; the look-ahead also reaches into the
@@ -32,12 +32,13 @@ constexpr int kThreads1 = 480;  // producer, conv MMA, 8 conv1_2-epilogue, 4 ste
 #ifndef EB_B1_LOOK
 #define EB_B1_LOOK 2
 #endif
-constexpr int kLook = EB_B1_LOOK;
+constexpr int kLook = EB_B1_LOOK;  // conv1_1 rows computed ahead of the tile that reads them
+// EB_B1_DBG: timing probes (variant builds only; results wrong): 1 no tap shuffles, 2 no
+// ring stores, 4 conv planes 1-2 not loaded from TMEM, 8 epilogues hand-shake only (16 the
+// stem epilogue only, 32 the conv epilogue only)
 #ifndef EB_B1_DBG
-#define EB_B1_DBG 0  // timing probes (variant builds only; results wrong): 1 no tap shuffles, 2 no ring stores,
-                   // 4 conv planes 1-2 not loaded from TMEM, 8 epilogues hand-shake only
-                   // (16 the stem epilogue only, 32 the conv epilogue only)
-#endif            // conv1_1 rows computed ahead of the tile that reads them
+#define EB_B1_DBG 0
+#endif
 constexpr int kRing = 3 + kLook + 1;         // conv1_1 row slots: 3 read + kLook written ahead + 1
 constexpr int kSlotBytes = 128 * 128;        // 128 grid rows x 64 channels bf16 (SW128 K-major)
 constexpr int kRunBytes = 136 * 16;          // one filter row's run: 136 padded pixels x 8 ch
