@@ -47,6 +47,9 @@ constexpr int kThreads = 384;
 #define EB_XFORM_THREADS 64
 #endif
 constexpr int kXformThreads = EB_XFORM_THREADS;  // pre-activation transform: the last warps
+// (128 -- four transform warps beside a four-warp epilogue -- hangs on B200 as of round 2's
+// end; only the 64-thread configuration is maintained)
+static_assert(EB_XFORM_THREADS == 64, "EB_XFORM_THREADS: only 64 is maintained");
 constexpr int kTapC8Bytes = kBlockM * 16;  // tap-C8 mode: one tap = 128 pixels x 8 bf16
 #ifndef EB_MAX_ACC
 #define EB_MAX_ACC 4  // TMEM accumulators per CTA at most (8: measured no gain on the stems)
